@@ -1,0 +1,171 @@
+/*
+ * rlfc_b200.h -- C ABI of the B200-native RLFC decode / render hot path.
+ *
+ * The reference's plugin API for this path is the `rlfc.kernels` module
+ * (/root/reference/pkg/src/rlfc/kernels.py), selected at import time
+ * (kernels.py:22-44) and called by rlfc.decoder / rlfc.renderer.  Each entry
+ * point below replaces one of those calls; the Python host layer
+ * (paper_1805_06019_b200/decoder.py, renderer.py) keeps the reference's
+ * public signatures and binds these symbols with ctypes.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes; every data pointer is DEVICE memory owned by
+ *     the caller (torch tensors in the Python host layer); nothing here
+ *     allocates output memory;
+ *   - `stream` is a cudaStream_t passed as void*; work is enqueued on it and
+ *     the call returns without synchronising;
+ *   - the return value is RLFC_OK or RLFC_ERR_ARGUMENT / RLFC_ERR_CUDA for
+ *     launch problems.  Stream-format errors are DATA-dependent and are
+ *     reported asynchronously through a device status word (below);
+ *   - thread-safe: the field descriptor is read-only.
+ *
+ * Device status word (uint64, caller zero-initialises): 0 = ok.  Otherwise
+ *   status = ((RLFC_KEY_MAX - key) << 2) | code
+ * where code is 1 (corrupt coded pack) or 2 (descriptor outside range table),
+ * mirroring kernels.py:165-171, and key orders failures exactly as the
+ * reference encounters them (decoder.py:187-210 image -> channel, then
+ * kernels.py:227-237 block row -> block column).  The largest status word is
+ * the failure the reference would raise first; decoder._raise_status
+ * (decoder.py:66-70) maps the code to its FormatError.
+ */
+#ifndef RLFC_B200_H
+#define RLFC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLFC_OK 0
+#define RLFC_ERR_CORRUPT_PACK 1
+#define RLFC_ERR_BAD_DESCRIPTOR 2
+#define RLFC_ERR_ARGUMENT 3
+#define RLFC_ERR_CUDA 4
+
+#define RLFC_MAX_LEVELS 32
+#define RLFC_KEY_MAX (1ull << 60)
+
+/* One parsed stream resident in device memory (decoder.py:20-28
+ * DecoderState).  Geometry follows container.py:59-145; the SRV sections
+ * are the stream's unmodified bytes (container.py:394-399) copied to HBM
+ * with >= 16 zero bytes of tail padding; offsets are the u64 block offset
+ * arrays (container.py:382-391); roots are the decoded, unbiased root planes
+ * (container.py:355-379), stored (rsx, rsy, 3, hp, wp) as int16 when every
+ * sample fits, else int32. */
+typedef struct rlfc_field {
+    int32_t s_count, t_count, width, height;
+    int32_t block, tree_height, quant_shift, m_nodes;
+    int32_t wp, hp, wb, hb, rsx, rsy;
+    int32_t roots_i16; /* 1: roots are int16, 0: int32 */
+    int32_t bitmap_bytes;
+    /* BFS geometry (container.py:102-145): level l (0..h-1) holds
+     * level_sx[l] x level_sy[l] nodes starting at serial index level_base[l]. */
+    int32_t level_base[RLFC_MAX_LEVELS];
+    int32_t level_sx[RLFC_MAX_LEVELS];
+    int32_t level_sy[RLFC_MAX_LEVELS];
+    const uint8_t *srv[3];
+    const uint64_t *offsets[3];
+    uint64_t srv_len[3];
+    const void *roots;
+} rlfc_field;
+
+/* Random-access block decode, batched.  Replaces kernels.decode_chain_core
+ * (kernels.py:162-216) as called by decoder.decode_block_progressive
+ * (decoder.py:81-106).  req: n x 6 int32 (s, t, bx, by, channel, stop_level),
+ * already range-checked by the host (decoder.py:51-63).  out: n x B*B int32
+ * (root block + dequantised chain residuals).  status: n int32 per-request
+ * codes (0 / 1 / 2). */
+int rlfc_decode_blocks(const rlfc_field *f, const int32_t *req, int32_t n,
+                       int32_t *out, int32_t *status, void *stream);
+
+/* Whole padded planes.  Replaces kernels.decode_plane_core
+ * (kernels.py:219-242) as called by decoder.decode_plane (decoder.py:165-184).
+ * planes: n x 3 int32 (s, t, channel); out: n x hp x wp int32.  Failure key =
+ * (request index, block row, block column). */
+int rlfc_decode_planes(const rlfc_field *f, int32_t stop_level,
+                       const int32_t *planes, int32_t n, int32_t *out,
+                       uint64_t *status, void *stream);
+
+/* Fused full-field decode: every (s, t) image with image_slots[s*T + t] >= 0
+ * (image_slots NULL = all images, slot = s*T + t), block rows
+ * [by_lo, by_hi), all three channels: tree traversal + YCoCg-R inverse +
+ * clamp + RGB8 store (decoder.py:187-210 decode_image / decode_all with
+ * colorspace.py:27-56).  Output pixel (s, t, y, x) goes to
+ *   rgb + slot(s, t) * img_stride + (y - by_lo*B) * row_stride + 3*x
+ * for y < height, x < width (the true-dims crop).  Failure key =
+ * ((image*3 + channel)*hb + by)*wb + bx with image = s*T + t. */
+int rlfc_decode_field(const rlfc_field *f, int32_t stop_level,
+                      const int32_t *image_slots, int32_t by_lo, int32_t by_hi,
+                      uint8_t *rgb, int64_t img_stride, int64_t row_stride,
+                      uint64_t *status, void *stream);
+
+/* Same contract as rlfc_decode_field, computed by the simple per-(image,
+ * block) kernel that walks every record once per image exactly like
+ * kernels.decode_plane_core.  Kept as the always-applicable path and as the
+ * in-library cross-check of the fused kernel. */
+int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
+                             const int32_t *image_slots, int32_t by_lo,
+                             int32_t by_hi, uint8_t *rgb, int64_t img_stride,
+                             int64_t row_stride, uint64_t *status,
+                             void *stream);
+
+/* BISE payload decode, batched.  Replaces kernels.bise_decode_core
+ * (kernels.py:128-159) / bise.bise_decode (bise.py:108-118).  payload i
+ * starts at data + offs[i], has descriptor descs[i] and `count` values;
+ * out: n x count uint32; status: n int32 (0 ok / 1 corrupt pack /
+ * 2 bad descriptor).  `data` must be readable 8 bytes past every payload. */
+int rlfc_bise_decode(const uint8_t *data, const int64_t *offs,
+                     const uint8_t *descs, int32_t n, int32_t count,
+                     uint32_t *out, int32_t *status, void *stream);
+
+/* Slab-pose rendering (renderer.py:233-276 _render_slab), batched.
+ * rgb_field: decoded RGB8 camera images at the stop level, camera (s, t) at
+ * rgb_field + slots[s*T + t] * H*W*3 (slots NULL = s*T + t); only the tap
+ * cameras of each pose are read.  poses: n x 4 doubles
+ * (s, t, has_focal, focal_z); geoms: n plane geometries
+ * (lightfield.py:24-43).  out: n x oh x ow x 3 uint8.
+ * bg: n x 3 uint8 backgrounds.  IEEE double, reference operation order, no
+ * FMA contraction: bit-exact with the reference. */
+typedef struct rlfc_render_geom {
+    double cam_z, img_z, x0, y0, x1, y1;
+} rlfc_render_geom;
+
+int rlfc_render_slab(const uint8_t *rgb_field, const int32_t *slots,
+                     int32_t S, int32_t T, int32_t W, int32_t H,
+                     const double *poses,
+                     const rlfc_render_geom *geoms, const uint8_t *bg,
+                     int32_t n, int32_t ow, int32_t oh, uint8_t *out,
+                     void *stream);
+
+/* Pinhole-pose rendering (renderer.py:279-305 with ray_to_lf_coords
+ * renderer.py:87-116 and sample_quadrilinear renderer.py:147-169).
+ * frames: n x 14 doubles (eye[3], look[3], right[3], down[3], half, aspect)
+ * as computed by the reference's per-frame numpy code
+ * (renderer.py:190-209); rgb_field / slots as for rlfc_render_slab.  status: n int32 (0, or -2 when a ray is parallel
+ * to the slab planes -- ValueError in renderer.py:97-98). */
+int rlfc_render_pinhole(const uint8_t *rgb_field, const int32_t *slots,
+                        int32_t S, int32_t T, int32_t W, int32_t H,
+                        const double *frames,
+                        const rlfc_render_geom *geoms, const uint8_t *bg,
+                        int32_t n, int32_t ow, int32_t oh, uint8_t *out,
+                        int32_t *status, void *stream);
+
+/* Camera-need marking for pinhole batches: sets need[s*T + t] = 1 for every
+ * tap camera any pixel of the n frames samples (same arithmetic as
+ * rlfc_render_pinhole).  need: S*T bytes, caller zero-initialises. */
+int rlfc_render_pinhole_needs(int32_t S, int32_t T, int32_t W, int32_t H,
+                              const double *frames,
+                              const rlfc_render_geom *geoms, int32_t n,
+                              int32_t ow, int32_t oh, uint8_t *need,
+                              void *stream);
+
+/* Library identification: returns the number of kernels this build exposes
+ * and writes a short version string. */
+int rlfc_version(char *buf, int32_t len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RLFC_B200_H */

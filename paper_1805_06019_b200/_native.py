@@ -1,0 +1,107 @@
+"""ctypes binding of librlfc_b200.so (the C ABI in include/rlfc_b200.h).
+
+The product path has no CPU fallback: if the CUDA library is missing, fails
+to load, or no CUDA device is visible, every decode / render call raises
+NativeUnavailable.
+"""
+
+import ctypes
+import os
+
+from ._build import CUDA_LIB
+
+RLFC_OK = 0
+RLFC_ERR_CORRUPT_PACK = 1
+RLFC_ERR_BAD_DESCRIPTOR = 2
+RLFC_ERR_ARGUMENT = 3
+RLFC_ERR_CUDA = 4
+MAX_LEVELS = 32
+KEY_MAX = 1 << 60
+
+
+class NativeUnavailable(RuntimeError):
+    """The sm_100a extension (librlfc_b200.so) or a CUDA device is missing."""
+
+
+class RlfcField(ctypes.Structure):
+    """Mirror of `rlfc_field` (include/rlfc_b200.h)."""
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "s_count", "t_count", "width", "height", "block", "tree_height",
+        "quant_shift", "m_nodes", "wp", "hp", "wb", "hb", "rsx", "rsy",
+        "roots_i16", "bitmap_bytes")] + [
+        ("level_base", ctypes.c_int32 * MAX_LEVELS),
+        ("level_sx", ctypes.c_int32 * MAX_LEVELS),
+        ("level_sy", ctypes.c_int32 * MAX_LEVELS),
+        ("srv", ctypes.c_void_p * 3),
+        ("offsets", ctypes.c_void_p * 3),
+        ("srv_len", ctypes.c_uint64 * 3),
+        ("roots", ctypes.c_void_p)]
+
+
+class RenderGeom(ctypes.Structure):
+    """Mirror of `rlfc_render_geom`."""
+    _fields_ = [(n, ctypes.c_double) for n in
+                ("cam_z", "img_z", "x0", "y0", "x1", "y1")]
+
+
+_lib = None
+_SIGS = {
+    "rlfc_decode_blocks": ["p", "p", "i", "p", "p", "p"],
+    "rlfc_decode_planes": ["p", "i", "p", "i", "p", "p", "p"],
+    "rlfc_decode_field": ["p", "i", "p", "i", "i", "p", "q", "q", "p", "p"],
+    "rlfc_decode_field_simple": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
+                                 "p"],
+    "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
+    "rlfc_render_slab": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
+                         "i", "i", "p", "p"],
+    "rlfc_render_pinhole": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
+                            "i", "i", "p", "p", "p"],
+    "rlfc_render_pinhole_needs": ["i", "i", "i", "i", "p", "p", "i", "i", "i",
+                                  "p", "p"],
+    "rlfc_version": ["p", "i"],
+}
+_CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64}
+EXPORTS = tuple(_SIGS)
+
+
+def load_library(path=CUDA_LIB):
+    """dlopen the library and declare every exported entry point."""
+    if not os.path.exists(path):
+        raise NativeUnavailable(
+            f"{path} not built: run `python -m paper_1805_06019_b200._build` "
+            "(nvcc, sm_100a)")
+    try:
+        L = ctypes.CDLL(path)
+    except OSError as exc:
+        raise NativeUnavailable(f"cannot load {path}: {exc}") from exc
+    for name, sig in _SIGS.items():
+        fn = getattr(L, name)
+        fn.restype = ctypes.c_int
+        fn.argtypes = [_CT[c] for c in sig]
+    return L
+
+
+def lib():
+    """The loaded library; requires a visible CUDA device."""
+    global _lib
+    if _lib is None:
+        import torch
+        if not torch.cuda.is_available():
+            raise NativeUnavailable(
+                "no CUDA device visible: the RLFC B200 path has no CPU "
+                "fallback")
+        _lib = load_library()
+    return _lib
+
+
+def check(rc, what):
+    if rc != RLFC_OK:
+        raise RuntimeError(f"{what} failed with status {rc}")
+
+
+def decode_status_word(word):
+    """(key, code) of a device status word, or None for success."""
+    word = int(word)
+    if word == 0:
+        return None
+    return KEY_MAX - (word >> 2), word & 3

@@ -1,0 +1,334 @@
+"""Stream container: header, sections, BFS node geometry, random-access locate.
+
+The wire format is the reference's, unchanged (reference container.py:1-27,
+SPEC.md:381-403):
+
+    header (64 bytes, little-endian)
+    per channel (Y, Co, Cg):
+        root stream   per root view (y outer, x inner): u32 length + blob
+        offset array  u64 per spatial block, relative to the SRV stream
+        SRV stream    one record per spatial block, row-major
+
+Everything here is host-side, init-time parsing; the per-block work runs on
+the GPU (decoder.py).
+"""
+
+import io
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from .bise import RANGE_TABLE, payload_bytes_table
+from .errors import FormatError, UnsupportedCodecError
+
+MAGIC = b"RLFC"
+VERSION = 1
+HEADER_SIZE = 64
+HEADER_FORMAT = "<4sBBBBHHHHBBHHI2x9I"     # container.py:46
+assert struct.calcsize(HEADER_FORMAT) == HEADER_SIZE
+
+CODEC_RAW, CODEC_PNG, CODEC_JPEG2000 = 0, 1, 2
+CODEC_IDS = {"raw": CODEC_RAW, "png": CODEC_PNG, "jpeg2000": CODEC_JPEG2000}
+CODEC_NAMES = {v: k for k, v in CODEC_IDS.items()}
+FILTER_IDS = {"uniform": 0, "gaussian": 1}
+FILTER_NAMES = {v: k for k, v in FILTER_IDS.items()}
+VALID_BLOCK_SIZES = (2, 4, 8, 16)
+CHANNEL_BIAS = (0, 256, 256)
+
+
+def padded_dims(width, height, block_size):
+    return -(-width // block_size) * block_size, \
+        -(-height // block_size) * block_size
+
+
+@dataclass(frozen=True)
+class RlfcHeader:
+    """Decoded 64-byte header (fields as reference container.py:59-95)."""
+    s_count: int
+    t_count: int
+    width: int
+    height: int
+    tree_height: int
+    block_size: int
+    quant_shift: int
+    pixel_threshold: int
+    block_threshold: int
+    filter_kind: str
+    sigma_fp: int
+    root_codec_id: int
+    section_lengths: tuple
+
+    @property
+    def padded_dims(self):
+        return padded_dims(self.width, self.height, self.block_size)
+
+    @property
+    def block_grid(self):
+        wp, hp = self.padded_dims
+        return wp // self.block_size, hp // self.block_size
+
+    def params(self):
+        from .encoder import EncodingParams, FilterSpec
+        sigma = self.sigma_fp / 256.0 if self.filter_kind == "gaussian" \
+            else 0.7
+        return EncodingParams(
+            tree_height=self.tree_height, block_size=self.block_size,
+            pixel_threshold=self.pixel_threshold,
+            block_threshold=self.block_threshold,
+            quant_shift=self.quant_shift,
+            filter=FilterSpec(kind=self.filter_kind, sigma=sigma),
+            root_codec=CODEC_NAMES[self.root_codec_id])
+
+
+# --- BFS tree geometry (container.py:102-145) --------------------------------
+
+def level_dims(s_count, t_count, level):
+    """Camera-grid dims at a tree level: repeated ceil-halving."""
+    return -(-s_count >> level), -(-t_count >> level)
+
+
+def level_node_counts(s_count, t_count, tree_height):
+    return [level_dims(s_count, t_count, l)[0] *
+            level_dims(s_count, t_count, l)[1] for l in range(tree_height)]
+
+
+def total_srv_nodes(s_count, t_count, tree_height):
+    return int(sum(level_node_counts(s_count, t_count, tree_height)))
+
+
+def level_bases(s_count, t_count, tree_height):
+    """Serial index of the first node of each level (level h-1 is first)."""
+    counts = level_node_counts(s_count, t_count, tree_height)
+    bases, acc = [0] * tree_height, 0
+    for l in range(tree_height - 1, -1, -1):
+        bases[l] = acc
+        acc += counts[l]
+    return bases
+
+
+def bfs_index(level, x, y, s_count, t_count, tree_height):
+    if not 0 <= level < tree_height:
+        raise ValueError(f"level {level} outside SRV tree")
+    sx, sy = level_dims(s_count, t_count, level)
+    if not (0 <= x < sx and 0 <= y < sy):
+        raise ValueError(f"node ({x}, {y}) outside level-{level} grid")
+    return level_bases(s_count, t_count, tree_height)[level] + y * sx + x
+
+
+def ancestors(s, t, s_count, t_count, tree_height):
+    """[(level, x, y)] from level h-1 down to 0, plus the root cell."""
+    if not (0 <= s < s_count and 0 <= t < t_count):
+        raise ValueError(f"image index ({s}, {t}) outside grid")
+    return ([(l, s >> l, t >> l) for l in range(tree_height - 1, -1, -1)],
+            (s >> tree_height, t >> tree_height))
+
+
+def chain_node_indices(s, t, s_count, t_count, tree_height):
+    chain, _ = ancestors(s, t, s_count, t_count, tree_height)
+    return np.asarray([bfs_index(l, x, y, s_count, t_count, tree_height)
+                       for l, x, y in chain], dtype=np.int64)
+
+
+def all_chains(s_count, t_count, tree_height):
+    """chains[s, t, :] for every image, vectorised (decoder.py:40-44)."""
+    bases = level_bases(s_count, t_count, tree_height)
+    s = np.arange(s_count)[:, None, None]
+    t = np.arange(t_count)[None, :, None]
+    lv = np.arange(tree_height - 1, -1, -1)[None, None, :]
+    sx = np.array([level_dims(s_count, t_count, l)[0]
+                   for l in range(tree_height)])
+    base = np.array(bases)
+    return (base[lv] + (t >> lv) * sx[lv] + (s >> lv)).astype(np.int64)
+
+
+# --- header -------------------------------------------------------------------
+
+def pack_header(header: RlfcHeader) -> bytes:
+    flat = [int(v) for sec in header.section_lengths for v in sec]
+    return struct.pack(
+        HEADER_FORMAT, MAGIC, VERSION, header.root_codec_id,
+        header.block_size, header.tree_height, header.s_count,
+        header.t_count, header.width, header.height, header.quant_shift,
+        FILTER_IDS[header.filter_kind], header.sigma_fp,
+        header.pixel_threshold, header.block_threshold, *flat)
+
+
+def parse_header(data) -> RlfcHeader:
+    """Validate and decode the header (same checks as container.py:214-243)."""
+    if len(data) < HEADER_SIZE:
+        raise FormatError(f"stream too short for header: {len(data)} bytes")
+    (magic, version, codec, block, height_tree, s_count, t_count, width,
+     height, shift, filt, sigma_fp, p_thr, b_thr, *flat) = struct.unpack(
+        HEADER_FORMAT, bytes(data[:HEADER_SIZE]))
+    if magic != MAGIC:
+        raise FormatError(f"bad magic {magic!r}")
+    if version != VERSION:
+        raise FormatError(f"unsupported version {version}")
+    if codec not in CODEC_NAMES:
+        raise UnsupportedCodecError(f"unknown root codec id {codec}")
+    if block not in VALID_BLOCK_SIZES:
+        raise FormatError(f"invalid block size {block}")
+    if height_tree < 1:
+        raise FormatError("tree height must be >= 1")
+    if filt not in FILTER_NAMES:
+        raise FormatError(f"invalid filter kind {filt}")
+    if min(s_count, t_count, width, height) < 1:
+        raise FormatError("grid and image dims must be >= 1")
+    return RlfcHeader(
+        s_count=s_count, t_count=t_count, width=width, height=height,
+        tree_height=height_tree, block_size=block, quant_shift=shift,
+        pixel_threshold=p_thr, block_threshold=b_thr,
+        filter_kind=FILTER_NAMES[filt], sigma_fp=sigma_fp,
+        root_codec_id=codec,
+        section_lengths=tuple(tuple(flat[3 * c:3 * c + 3]) for c in range(3)))
+
+
+def section_offsets(header: RlfcHeader):
+    """Absolute (root, offsets, srv) starts per channel, and the stream end."""
+    starts, pos = [], HEADER_SIZE
+    for root_len, off_len, srv_len in header.section_lengths:
+        starts.append((pos, pos + root_len, pos + root_len + off_len))
+        pos += root_len + off_len + srv_len
+    return starts, pos
+
+
+def check_stream_length(header: RlfcHeader, data):
+    _, end = section_offsets(header)
+    if len(data) < end:
+        raise FormatError(f"stream truncated: {len(data)} < {end} bytes")
+    if len(data) > end:
+        raise FormatError(
+            f"{len(data) - end} trailing bytes after the last section")
+
+
+# --- root views -----------------------------------------------------------------
+
+def decode_root(blob, codec_id, width, height):
+    """One lossless 16-bit root plane (container.py:175-195 semantics)."""
+    if codec_id == CODEC_RAW:
+        if len(blob) != width * height * 2:
+            raise FormatError(
+                f"raw root length {len(blob)} != {width * height * 2}")
+        return np.frombuffer(blob, dtype="<u2").reshape(height, width) \
+            .astype(np.int64)
+    if codec_id in (CODEC_PNG, CODEC_JPEG2000):
+        from PIL import Image
+        try:
+            with Image.open(io.BytesIO(blob)) as im:
+                arr = np.asarray(im)
+        except Exception as exc:
+            raise FormatError(f"root image decode failed: {exc}") from exc
+        if arr.ndim != 2:
+            raise FormatError("root image is not single-channel")
+        if arr.shape != (height, width):
+            raise FormatError(
+                f"root dims {arr.shape[::-1]} != header {(width, height)}")
+        return arr.astype(np.int64)
+    raise UnsupportedCodecError(f"unknown root codec id {codec_id}")
+
+
+def encode_root(plane, codec_id) -> bytes:
+    arr = np.asarray(plane)
+    if arr.min() < 0 or arr.max() > 0xFFFF:
+        raise ValueError("root plane out of unsigned 16-bit range")
+    arr = arr.astype(np.uint16)
+    if codec_id == CODEC_RAW:
+        return arr.astype("<u2").tobytes()
+    from PIL import Image
+    buf = io.BytesIO()
+    if codec_id == CODEC_PNG:
+        Image.fromarray(arr).save(buf, format="PNG")
+    elif codec_id == CODEC_JPEG2000:
+        try:
+            Image.fromarray(arr).save(buf, format="JPEG2000",
+                                      irreversible=False)
+        except Exception as exc:
+            raise UnsupportedCodecError(
+                f"jpeg2000 encoding unavailable: {exc}") from exc
+    else:
+        raise UnsupportedCodecError(f"unknown root codec id {codec_id}")
+    return buf.getvalue()
+
+
+def parse_roots(data, header: RlfcHeader):
+    """All root planes, (rsx, rsy, 3, Hp, Wp) int32 with the bias removed."""
+    wp, hp = header.padded_dims
+    rsx, rsy = level_dims(header.s_count, header.t_count, header.tree_height)
+    starts, _ = section_offsets(header)
+    out = np.zeros((rsx, rsy, 3, hp, wp), dtype=np.int32)
+    for c in range(3):
+        pos = starts[c][0]
+        end = pos + header.section_lengths[c][0]
+        for y in range(rsy):
+            for x in range(rsx):
+                if pos + 4 > end:
+                    raise FormatError("root stream truncated")
+                (n,) = struct.unpack_from("<I", data, pos)
+                pos += 4
+                if pos + n > end:
+                    raise FormatError("root stream truncated")
+                out[x, y, c] = decode_root(bytes(data[pos:pos + n]),
+                                           header.root_codec_id, wp, hp) \
+                    - CHANNEL_BIAS[c]
+                pos += n
+        if pos != end:
+            raise FormatError("trailing bytes in root stream")
+    return out
+
+
+def parse_offsets(data, header: RlfcHeader, channel):
+    wb, hb = header.block_grid
+    starts, _ = section_offsets(header)
+    length = header.section_lengths[channel][1]
+    if length != wb * hb * 8:
+        raise FormatError(f"offset array length {length} != {wb * hb * 8}")
+    return np.frombuffer(data, dtype="<u8", count=wb * hb,
+                         offset=starts[channel][1])
+
+
+def srv_section(data, header: RlfcHeader, channel):
+    starts, _ = section_offsets(header)
+    return np.frombuffer(data, dtype=np.uint8,
+                         count=header.section_lengths[channel][2],
+                         offset=starts[channel][2])
+
+
+def locate_block(data, header: RlfcHeader, channel, blk_index, node_index):
+    """(payload_start, payload_end, descriptor) of one node, or None.
+
+    Host-side random-access locate (container.py:402-445 semantics): touches
+    the record's bitmap and the descriptors of earlier present nodes only.
+    """
+    wb, hb = header.block_grid
+    if not 0 <= blk_index < wb * hb:
+        raise ValueError(f"block index {blk_index} outside grid")
+    m = total_srv_nodes(header.s_count, header.t_count, header.tree_height)
+    if not 0 <= node_index < m:
+        raise ValueError(f"node index {node_index} outside tree")
+    starts, _ = section_offsets(header)
+    srv_start = starts[channel][2]
+    srv_end = srv_start + header.section_lengths[channel][2]
+    rec = srv_start + int(parse_offsets(data, header, channel)[blk_index])
+    nbm = (m + 7) >> 3
+    if rec + nbm > srv_end:
+        raise FormatError("record offset past section end")
+    bitmap = np.unpackbits(np.frombuffer(bytes(data[rec:rec + nbm]),
+                                         np.uint8), bitorder="little")
+    if not bitmap[node_index]:
+        return None
+    pbytes = payload_bytes_table(header.block_size ** 2)
+    cursor = rec + nbm
+    for node in np.flatnonzero(bitmap[:node_index + 1]):
+        if cursor >= srv_end:
+            raise FormatError("record truncated mid-scan")
+        desc = data[cursor]
+        if desc >= len(RANGE_TABLE):
+            raise FormatError(f"descriptor {desc} outside range table")
+        if node == node_index:
+            end = cursor + 1 + int(pbytes[desc])
+            if end > srv_end:
+                raise FormatError("payload past section end")
+            return cursor + 1, end, desc
+        cursor += 1 + int(pbytes[desc])
+    raise AssertionError("unreachable")

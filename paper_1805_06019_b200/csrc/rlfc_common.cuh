@@ -1,0 +1,225 @@
+// rlfc_common.cuh -- device helpers shared by the RLFC decode / render kernels.
+//
+// Everything here is integer-only and bit-exact with the reference kernels
+// (/root/reference/pkg/src/rlfc/kernels.py).  Payload bits are LSB-first
+// across bytes (kernels.py:1-11); every value of a BISE payload has a
+// closed-form bit offset because all groups but the last are full
+// (SURVEY.md Appendix A), so no per-value prefix sum is needed.
+#pragma once
+
+#include <cstdint>
+#include "../../include/rlfc_b200.h"
+
+namespace rlfc {
+
+constexpr int MODE_BITS = 0;   // kernels.py:17-19
+constexpr int MODE_TRIT = 1;
+constexpr int MODE_QUINT = 2;
+constexpr int NUM_DESC = 30;   // bise.py:22-25
+
+// bise.py:22-60 RANGE_TABLE factored into (mode, low bits) per descriptor
+// (TABLE_MODE / TABLE_BITS, bise.py:59-60).
+__host__ __device__ constexpr int desc_mode(int d) {
+    constexpr int8_t M[30] = {0, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0,
+                              2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0};
+    return M[d];
+}
+__host__ __device__ constexpr int desc_bits(int d) {
+    constexpr int8_t Bt[30] = {1, 0, 2, 0, 1, 3, 1, 2, 4, 2, 3, 5, 3, 4, 6,
+                               4, 5, 7, 5, 6, 8, 6, 7, 9, 7, 8, 10, 8, 9, 11};
+    return Bt[d];
+}
+
+// kernels.py:63-70 payload_bits
+__host__ __device__ constexpr int payload_bits(int mode, int bits, int count) {
+    return mode == MODE_BITS ? count * bits
+         : mode == MODE_TRIT ? 8 * ((count + 4) / 5) + count * bits
+                             : 7 * ((count + 2) / 3) + count * bits;
+}
+__host__ __device__ constexpr int payload_bytes(int d, int count) {
+    return (payload_bits(desc_mode(d), desc_bits(d), count) + 7) >> 3;
+}
+
+// Bytes occupied by one present node (descriptor + padded payload) for
+// descriptor d at B*B values; index 30 = invalid descriptor sentinel.
+struct NodeBytes {
+    uint16_t v[32];
+};
+template <int BSQ>
+__host__ __device__ constexpr NodeBytes make_node_bytes() {
+    NodeBytes nb{};
+    for (int d = 0; d < NUM_DESC; ++d) nb.v[d] = (uint16_t)(1 + payload_bytes(d, BSQ));
+    nb.v[30] = 0;
+    nb.v[31] = 0;
+    return nb;
+}
+
+// Packed base-3 / base-5 digit tables (kernels.py:47-60 TRIT_DIGITS /
+// QUINT_DIGITS): trit digit i of pack p = (TRIT[p] >> 2i) & 3, quint digit i
+// = (QUINT[p] >> 3i) & 7.
+struct DigitLut {
+    uint16_t trit[243];
+    uint16_t quint[125];
+};
+__host__ __device__ constexpr DigitLut make_digit_lut() {
+    DigitLut L{};
+    for (int p = 0; p < 243; ++p) {
+        int r = p, v = 0;
+        for (int i = 0; i < 5; ++i) { v |= (r % 3) << (2 * i); r /= 3; }
+        L.trit[p] = (uint16_t)v;
+    }
+    for (int p = 0; p < 125; ++p) {
+        int r = p, v = 0;
+        for (int i = 0; i < 3; ++i) { v |= (r % 5) << (3 * i); r /= 5; }
+        L.quint[p] = (uint16_t)v;
+    }
+    return L;
+}
+
+// 32 bits starting at absolute bit position `bitpos` of byte array `base`.
+// Reads the two aligned 32-bit words covering the position; the buffer must
+// be readable 8 bytes past the last payload byte (device SRV copies carry
+// >= 16 bytes of zero padding).
+__device__ __forceinline__ uint32_t load_bits32(const uint8_t* base, uint64_t bitpos) {
+    uintptr_t a = reinterpret_cast<uintptr_t>(base) + (bitpos >> 3);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    uint32_t sh = (uint32_t)((a & 3) << 3) + (uint32_t)(bitpos & 7);
+    uint32_t lo = __ldg(w), hi = __ldg(w + 1);
+    return __funnelshift_r(lo, hi, sh);
+}
+__device__ __forceinline__ uint32_t get_bits(const uint8_t* base, uint64_t bitpos, int nbits) {
+    return load_bits32(base, bitpos) & ((1u << nbits) - 1u);
+}
+
+// Dequantise one zigzag code (bise.py:69-72 unzigzag + hierarchy.py:232-237
+// dequantize, inlined exactly as kernels.py:202-211).  The reference adds in
+// int64 and stores into an int32 accumulator; the 32-bit wrap below is the
+// same result.
+__device__ __forceinline__ int32_t dequant(uint32_t z, int shift) {
+    if (z == 0) return 0;
+    int64_t half = (int64_t(1) << shift) >> 1;
+    int64_t mag = (int64_t)((z + 1) >> 1) << shift;
+    int64_t v = (z & 1) ? -(mag + half) : (mag + half);
+    return (int32_t)(uint32_t)(uint64_t)v;
+}
+
+// kernels.py:128-159 bise_decode_core for one payload, accumulating the
+// dequantised values into acc[0..BSQ).  Returns 0 or 1 (corrupt pack).  The
+// whole payload is validated before any value is added, as the reference
+// decodes into tmp first.
+template <int BSQ>
+__device__ int decode_payload_acc(const uint8_t* p, int desc, int shift, int32_t* acc,
+                                  const DigitLut& lut) {
+    const int mode = desc_mode(desc), b = desc_bits(desc);
+    if (mode != MODE_BITS) {
+        const int G = mode == MODE_TRIT ? 5 : 3;
+        const int PB = mode == MODE_TRIT ? 8 : 7;
+        const uint32_t PMAX = mode == MODE_TRIT ? 242u : 124u;
+        const int gbits = PB + G * b;
+        for (int g = 0; g * G < BSQ; ++g)
+            if (get_bits(p, (uint64_t)g * gbits, PB) > PMAX) return 1;
+    }
+    for (int k = 0; k < BSQ; ++k) {
+        uint32_t z;
+        if (mode == MODE_BITS) {
+            z = get_bits(p, (uint64_t)k * b, b);
+        } else if (mode == MODE_TRIT) {
+            int g = k / 5, i = k - 5 * g;
+            uint64_t gp = (uint64_t)g * (8 + 5 * b);
+            uint32_t pack = get_bits(p, gp, 8);
+            uint32_t digit = (lut.trit[pack] >> (2 * i)) & 3u;
+            uint32_t low = b ? get_bits(p, gp + 8 + i * b, b) : 0u;
+            z = (digit << b) | low;
+        } else {
+            int g = k / 3, i = k - 3 * g;
+            uint64_t gp = (uint64_t)g * (7 + 3 * b);
+            uint32_t pack = get_bits(p, gp, 7);
+            uint32_t digit = (lut.quint[pack] >> (3 * i)) & 7u;
+            uint32_t low = b ? get_bits(p, gp + 7 + i * b, b) : 0u;
+            z = (digit << b) | low;
+        }
+        acc[k] += dequant(z, shift);
+    }
+    return 0;
+}
+
+// 32 presence bits of nodes [n0, n0+32) of a record's bitmap (bit i of the
+// record = byte i>>3 bit i&7, kernels.py:181-183), n0 a multiple of 32.
+__device__ __forceinline__ uint32_t bitmap_word(const uint8_t* rec, int n0) {
+    return load_bits32(rec, (uint64_t)n0);
+}
+
+// Serial index of image (s, t)'s level-l ancestor (container.py:122-145).
+__device__ __forceinline__ int chain_node(const rlfc_field& f, int l, int s, int t) {
+    return f.level_base[l] + (t >> l) * f.level_sx[l] + (s >> l);
+}
+
+// kernels.py:162-216 decode_chain_core: walk one record up to the image's
+// last target (levels h-1 .. stop_level), decoding target payloads into acc
+// (pre-filled with the root block).  Present nodes are visited with
+// find-first-set over the bitmap, so the walk costs one step per PRESENT
+// node; the result and the status (0 / 1 / 2) are identical to the
+// reference's node-by-node loop.
+template <int BSQ>
+__device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t, int stop_level,
+                          int32_t* acc, const DigitLut& lut, const NodeBytes& nb) {
+    const int h = f.tree_height;
+    const int nt = h - stop_level;
+    if (nt <= 0) return 0;
+    int ti = 0;                                  // next target, level h-1-ti
+    int target = chain_node(f, h - 1, s, t);
+    const int last = chain_node(f, stop_level, s, t);
+    uint64_t cursor = (uint64_t)f.bitmap_bytes;  // relative to rec
+    for (int n0 = 0; n0 <= last; n0 += 32) {
+        uint32_t bits = bitmap_word(rec, n0);
+        int span = last - n0 + 1;                // nodes n0..last
+        if (span < 32) bits &= (1u << span) - 1u;
+        while (bits) {
+            int node = n0 + __ffs(bits) - 1;
+            bits &= bits - 1u;
+            while (target < node) {              // absent targets contribute 0
+                if (++ti == nt) return 0;
+                target = chain_node(f, h - 1 - ti, s, t);
+            }
+            int desc = rec[cursor];
+            if (desc >= NUM_DESC) return 2;
+            if (target == node) {
+                int st = decode_payload_acc<BSQ>(rec + cursor + 1, desc, f.quant_shift, acc, lut);
+                if (st) return st;
+                if (++ti == nt) return 0;
+                target = chain_node(f, h - 1 - ti, s, t);
+            }
+            cursor += nb.v[desc];
+        }
+    }
+    return 0;
+}
+
+__device__ __forceinline__ int32_t root_sample(const rlfc_field& f, int s, int t, int c, int y, int x) {
+    const int h = f.tree_height;
+    int64_t idx = ((((int64_t)(s >> h) * f.rsy + (t >> h)) * 3 + c) * f.hp + y) * f.wp + x;
+    return f.roots_i16 ? (int32_t)reinterpret_cast<const int16_t*>(f.roots)[idx]
+                       : reinterpret_cast<const int32_t*>(f.roots)[idx];
+}
+
+// colorspace.py:27-36 ycocgr_to_rgb (arithmetic shifts = floor halves)
+// followed by colorspace.py:46-56 clip to [0, 255].
+__device__ __forceinline__ uint32_t clamp8(int32_t v) { return (uint32_t)min(max(v, 0), 255); }
+__device__ __forceinline__ void ycocg_to_rgb8(int32_t y, int32_t co, int32_t cg, uint32_t& r,
+                                              uint32_t& g, uint32_t& b) {
+    int32_t t = y - (cg >> 1);
+    int32_t gg = cg + t;
+    int32_t bb = t - (co >> 1);
+    int32_t rr = bb + co;
+    r = clamp8(rr);
+    g = clamp8(gg);
+    b = clamp8(bb);
+}
+
+// Failure word for the device status (see rlfc_b200.h).
+__device__ __forceinline__ void report(uint64_t* status, uint64_t key, int code) {
+    if (code) atomicMax((unsigned long long*)status,
+                        (unsigned long long)(((RLFC_KEY_MAX - key) << 2) | (uint64_t)code));
+}
+
+}  // namespace rlfc

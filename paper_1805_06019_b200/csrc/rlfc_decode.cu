@@ -1,0 +1,256 @@
+// rlfc_decode.cu -- random-access and per-(image, block) decode kernels plus
+// the C-ABI entry points of librlfc_b200.so (include/rlfc_b200.h).
+//
+// The fused full-field kernel lives in rlfc_field.cu; this file holds the
+// always-applicable kernels that follow the reference's block-at-a-time
+// structure (kernels.py:162-242) one CUDA thread per block request.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+
+#include "rlfc_common.cuh"
+#include "rlfc_field.cuh"
+
+namespace rlfc {
+
+__constant__ DigitLut c_lut = make_digit_lut();
+
+template <int B>
+__constant__ NodeBytes c_nb = make_node_bytes<B * B>();
+
+// One thread per request: root block + dequantised chain (decoder.py:81-106).
+template <int B>
+__global__ void k_decode_blocks(const rlfc_field f, const int32_t* __restrict__ req, int n,
+                                int32_t* __restrict__ out, int32_t* __restrict__ status) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = req[6 * i], t = req[6 * i + 1], bx = req[6 * i + 2], by = req[6 * i + 3];
+    const int c = req[6 * i + 4], k = req[6 * i + 5];
+    int32_t acc[B * B];
+#pragma unroll
+    for (int yy = 0; yy < B; ++yy)
+#pragma unroll
+        for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+    const uint8_t* rec = f.srv[c] + f.offsets[c][by * f.wb + bx];
+    int st = walk_chain<B * B>(f, rec, s, t, k, acc, c_lut, c_nb<B>);
+    status[i] = st;
+    int32_t* o = out + (int64_t)i * B * B;
+#pragma unroll
+    for (int j = 0; j < B * B; ++j) o[j] = acc[j];
+}
+
+// One thread per (plane request, block): kernels.py:219-242 decode_plane_core.
+template <int B>
+__global__ void k_decode_planes(const rlfc_field f, int stop_level, const int32_t* __restrict__ planes,
+                                int n, int32_t* __restrict__ out, uint64_t* status) {
+    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    if (gid >= nblk * n) return;
+    const int r = (int)(gid / nblk);
+    const int blk = (int)(gid - (int64_t)r * nblk);
+    const int bx = blk % f.wb, by = blk / f.wb;
+    const int s = planes[3 * r], t = planes[3 * r + 1], c = planes[3 * r + 2];
+    int32_t acc[B * B];
+#pragma unroll
+    for (int yy = 0; yy < B; ++yy)
+#pragma unroll
+        for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+    const uint8_t* rec = f.srv[c] + f.offsets[c][blk];
+    int st = walk_chain<B * B>(f, rec, s, t, stop_level, acc, c_lut, c_nb<B>);
+    if (st) report(status, (uint64_t)r * nblk + blk, st);
+    int32_t* o = out + (int64_t)r * f.hp * f.wp;
+#pragma unroll
+    for (int yy = 0; yy < B; ++yy)
+#pragma unroll
+        for (int xx = 0; xx < B; ++xx) o[(int64_t)(by * B + yy) * f.wp + bx * B + xx] = acc[yy * B + xx];
+}
+
+// One thread per (image, block) of a band: three channel chains, inverse lift,
+// clamp, RGB8 store of the true-dims crop (decoder.py:187-194).
+template <int B>
+__global__ void k_decode_field_simple(const rlfc_field f, int stop_level, const int32_t* __restrict__ slots,
+                                      int by_lo, int by_hi, uint8_t* __restrict__ rgb, int64_t img_stride,
+                                      int64_t row_stride, uint64_t* status) {
+    const int64_t nblk = (int64_t)f.wb * (by_hi - by_lo);
+    int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nimg = f.s_count * f.t_count;
+    if (gid >= nblk * nimg) return;
+    const int img = (int)(gid / nblk);
+    const int slot = slots ? slots[img] : img;
+    if (slot < 0) return;
+    const int rem = (int)(gid - (int64_t)img * nblk);
+    const int bx = rem % f.wb, by = by_lo + rem / f.wb;
+    const int s = img / f.t_count, t = img % f.t_count;
+    int32_t acc[3][B * B];
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int yy = 0; yy < B; ++yy)
+#pragma unroll
+            for (int xx = 0; xx < B; ++xx)
+                acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+        const uint8_t* rec = f.srv[c] + f.offsets[c][by * f.wb + bx];
+        int st = walk_chain<B * B>(f, rec, s, t, stop_level, acc[c], c_lut, c_nb<B>);
+        if (st) {
+            report(status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
+            return;
+        }
+    }
+    uint8_t* o = rgb + (int64_t)slot * img_stride;
+#pragma unroll
+    for (int yy = 0; yy < B; ++yy) {
+        int y = by * B + yy;
+        if (y >= f.height) break;
+        uint8_t* orow = o + (int64_t)(y - by_lo * B) * row_stride;
+#pragma unroll
+        for (int xx = 0; xx < B; ++xx) {
+            int x = bx * B + xx;
+            if (x >= f.width) break;
+            uint32_t r, g, b;
+            int j = yy * B + xx;
+            ycocg_to_rgb8(acc[0][j], acc[1][j], acc[2][j], r, g, b);
+            orow[3 * x] = (uint8_t)r;
+            orow[3 * x + 1] = (uint8_t)g;
+            orow[3 * x + 2] = (uint8_t)b;
+        }
+    }
+}
+
+// One thread per value of a batched BISE decode (kernels.py:128-159).
+__global__ void k_bise_decode(const uint8_t* __restrict__ data, const int64_t* __restrict__ offs,
+                              const uint8_t* __restrict__ descs, int n, int count,
+                              uint32_t* __restrict__ out, int32_t* __restrict__ status) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int d = descs[i];
+    const uint8_t* p = data + offs[i];
+    uint32_t* o = out + (int64_t)i * count;
+    if (d >= NUM_DESC) {
+        status[i] = 2;
+        return;
+    }
+    const int mode = desc_mode(d), b = desc_bits(d);
+    int st = 0;
+    for (int k = 0; k < count; ++k) {
+        uint32_t z;
+        if (mode == MODE_BITS) {
+            z = get_bits(p, (uint64_t)k * b, b);
+        } else {
+            const int G = mode == MODE_TRIT ? 5 : 3, PB = mode == MODE_TRIT ? 8 : 7;
+            int g = k / G, ii = k - G * g;
+            uint64_t gp = (uint64_t)g * (PB + G * b);
+            uint32_t pack = get_bits(p, gp, PB);
+            if (pack > (mode == MODE_TRIT ? 242u : 124u)) {
+                st = 1;
+                break;
+            }
+            uint32_t digit = mode == MODE_TRIT ? (c_lut.trit[pack] >> (2 * ii)) & 3u
+                                               : (c_lut.quint[pack] >> (3 * ii)) & 7u;
+            uint32_t low = b ? get_bits(p, gp + PB + ii * b, b) : 0u;
+            z = (digit << b) | low;
+        }
+        o[k] = z;
+    }
+    status[i] = st;
+}
+
+static bool valid_field(const rlfc_field* f) {
+    if (!f) return false;
+    if (f->block != 2 && f->block != 4 && f->block != 8 && f->block != 16) return false;
+    if (f->tree_height < 1 || f->tree_height > RLFC_MAX_LEVELS) return false;
+    if (f->s_count < 1 || f->t_count < 1 || f->width < 1 || f->height < 1) return false;
+    return true;
+}
+
+static int launch_status() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "rlfc_b200: CUDA launch error: %s\n", cudaGetErrorString(e));
+        return RLFC_ERR_CUDA;
+    }
+    return RLFC_OK;
+}
+
+}  // namespace rlfc
+
+using namespace rlfc;
+
+#define RLFC_DISPATCH_B(B_, ...)                       \
+    switch (B_) {                                      \
+        case 2: { constexpr int BB = 2; __VA_ARGS__; } break;  \
+        case 4: { constexpr int BB = 4; __VA_ARGS__; } break;  \
+        case 8: { constexpr int BB = 8; __VA_ARGS__; } break;  \
+        case 16: { constexpr int BB = 16; __VA_ARGS__; } break; \
+        default: return RLFC_ERR_ARGUMENT;             \
+    }
+
+extern "C" int rlfc_decode_blocks(const rlfc_field* f, const int32_t* req, int32_t n, int32_t* out,
+                                  int32_t* status, void* stream) {
+    if (!valid_field(f) || n < 0) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int threads = 128;
+    const int grid = (n + threads - 1) / threads;
+    RLFC_DISPATCH_B(f->block, k_decode_blocks<BB><<<grid, threads, 0, st>>>(*f, req, n, out, status));
+    return launch_status();
+}
+
+extern "C" int rlfc_decode_planes(const rlfc_field* f, int32_t stop_level, const int32_t* planes,
+                                  int32_t n, int32_t* out, uint64_t* status, void* stream) {
+    if (!valid_field(f) || n < 0 || stop_level < 0 || stop_level > f->tree_height) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int threads = 128;
+    const int64_t total = (int64_t)f->wb * f->hb * n;
+    const int64_t grid = (total + threads - 1) / threads;
+    RLFC_DISPATCH_B(f->block, k_decode_planes<BB><<<(unsigned)grid, threads, 0, st>>>(*f, stop_level, planes,
+                                                                                      n, out, status));
+    return launch_status();
+}
+
+extern "C" int rlfc_decode_field_simple(const rlfc_field* f, int32_t stop_level, const int32_t* slots,
+                                        int32_t by_lo, int32_t by_hi, uint8_t* rgb, int64_t img_stride,
+                                        int64_t row_stride, uint64_t* status, void* stream) {
+    if (!valid_field(f) || stop_level < 0 || stop_level > f->tree_height) return RLFC_ERR_ARGUMENT;
+    if (by_lo < 0 || by_hi > f->hb || by_lo > by_hi) return RLFC_ERR_ARGUMENT;
+    if (by_lo == by_hi) return RLFC_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int threads = 128;
+    const int64_t total = (int64_t)f->wb * (by_hi - by_lo) * f->s_count * f->t_count;
+    const int64_t grid = (total + threads - 1) / threads;
+    RLFC_DISPATCH_B(f->block, k_decode_field_simple<BB><<<(unsigned)grid, threads, 0, st>>>(
+                                  *f, stop_level, slots, by_lo, by_hi, rgb, img_stride, row_stride, status));
+    return launch_status();
+}
+
+extern "C" int rlfc_decode_field(const rlfc_field* f, int32_t stop_level, const int32_t* slots, int32_t by_lo,
+                                 int32_t by_hi, uint8_t* rgb, int64_t img_stride, int64_t row_stride,
+                                 uint64_t* status, void* stream) {
+    if (!valid_field(f) || stop_level < 0 || stop_level > f->tree_height) return RLFC_ERR_ARGUMENT;
+    if (by_lo < 0 || by_hi > f->hb || by_lo > by_hi) return RLFC_ERR_ARGUMENT;
+    if (by_lo == by_hi) return RLFC_OK;
+    int rc = launch_decode_field_tiled(*f, stop_level, slots, by_lo, by_hi, rgb, img_stride, row_stride, status,
+                                       (cudaStream_t)stream);
+    if (rc == RLFC_ERR_ARGUMENT)  // geometry outside the tiled kernel's envelope
+        return rlfc_decode_field_simple(f, stop_level, slots, by_lo, by_hi, rgb, img_stride, row_stride, status,
+                                        stream);
+    return rc;
+}
+
+extern "C" int rlfc_bise_decode(const uint8_t* data, const int64_t* offs, const uint8_t* descs, int32_t n,
+                                int32_t count, uint32_t* out, int32_t* status, void* stream) {
+    if (n < 0 || count < 0) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    const int threads = 128;
+    k_bise_decode<<<(n + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(data, offs, descs, n, count,
+                                                                                     out, status);
+    return launch_status();
+}
+
+extern "C" int rlfc_version(char* buf, int32_t len) {
+    const char* v = "rlfc_b200 0.1 sm_100a";
+    if (buf && len > 0) {
+        strncpy(buf, v, (size_t)len - 1);
+        buf[len - 1] = 0;
+    }
+    return 7;
+}

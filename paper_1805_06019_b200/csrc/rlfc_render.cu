@@ -1,0 +1,278 @@
+// rlfc_render.cu -- novel-view rendering over decoded camera images.
+//
+// Bit-exact restatement of the reference renderer's float64 arithmetic
+// (/root/reference/pkg/src/rlfc/renderer.py).  Every multiply / add / divide
+// is an explicit round-to-nearest intrinsic (__dmul_rn, __dadd_rn,
+// __ddiv_rn), so nvcc can never contract a*b+c into an FMA -- numpy does not
+// either -- and the operation order is numpy's.
+#include <cuda_runtime.h>
+#include <cstdio>
+
+#include "../../include/rlfc_b200.h"
+
+namespace rlfc {
+
+constexpr double SNAP_EPS = 1e-9;  // renderer.py:23
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dadd_rn(a, -b); }
+__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
+
+// renderer.py:82-84 _snap (Python round() is half-to-even = rint)
+__device__ __forceinline__ double snap(double f) {
+    double r = rint(f);
+    return fabs(sub(f, r)) < SNAP_EPS ? r : f;
+}
+
+// renderer.py:119-131 _axis_taps: clamp, split, drop zero-weight taps.
+__device__ __forceinline__ int axis_taps(double coord, int count, int* idx, double* w) {
+    double c = fmin(fmax(coord, 0.0), (double)(count - 1));
+    if (count == 1) {
+        idx[0] = 0;
+        w[0] = 1.0;
+        return 1;
+    }
+    int i0 = min((int)floor(c), count - 2);
+    double f = snap(sub(c, (double)i0));
+    int n = 0;
+    if (f < 1.0) { idx[n] = i0; w[n] = sub(1.0, f); ++n; }
+    if (f > 0.0) { idx[n] = i0 + 1; w[n] = f; ++n; }
+    return n;
+}
+
+// renderer.py:221-230 _vec_taps (keeps zero-weight taps).
+__device__ __forceinline__ void vec_tap(double coord, int count, int& i0, double& f) {
+    double c = fmin(fmax(coord, 0.0), (double)(count - 1));
+    if (count == 1) { i0 = 0; f = 0.0; return; }
+    double fl = fmin(floor(c), (double)(count - 2));
+    i0 = (int)fl;
+    double fr = sub(c, (double)i0);
+    double r = rint(fr);
+    f = fabs(sub(fr, r)) < SNAP_EPS ? r : fr;
+}
+
+// np.interp(x, arange(n), arange(n)) on the identity camera grid
+// (renderer.py:75-79, 177-178): x clamped to [0, n-1], exact inside.
+__device__ __forceinline__ double interp_identity(double x, int n) {
+    return x < 0.0 ? 0.0 : (x > (double)(n - 1) ? (double)(n - 1) : x);
+}
+
+__device__ __forceinline__ uint8_t round_clip(double a) {
+    double fl = floor(add(a, 0.5));  // renderer.py:274 floor(acc + 0.5).clip(0, 255)
+    return fl < 0.0 ? 0 : (fl > 255.0 ? 255 : (uint8_t)fl);
+}
+
+// One thread per output pixel of one slab pose (renderer.py:233-276).
+__global__ void k_render_slab(const uint8_t* __restrict__ field, const int32_t* __restrict__ slots, int S, int T,
+                              int W, int H,
+                              const double* __restrict__ poses, const rlfc_render_geom* __restrict__ geoms,
+                              const uint8_t* __restrict__ bgs, int ow, int oh, uint8_t* __restrict__ out) {
+    const int v = blockIdx.y;
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= (int64_t)ow * oh) return;
+    const int i = (int)(pix % ow), j = (int)(pix / ow);
+    const rlfc_render_geom g = geoms[v];
+    const double ps = poses[4 * v], pt = poses[4 * v + 1];
+    const double focal = poses[4 * v + 2] != 0.0 ? poses[4 * v + 3] : g.img_z;
+    uint8_t* o = out + ((int64_t)v * oh * ow + pix) * 3;
+    const uint8_t* bg = bgs + 3 * v;
+    // renderer.py:177-187 _slab_rays
+    const double ex = interp_identity(ps, S), ey = interp_identity(pt, T), ez = g.cam_z;
+    const double xw = sub(g.x1, g.x0), yw = sub(g.y1, g.y0);
+    const double tx = add(g.x0, dvd(mul(add((double)i, 0.5), xw), (double)ow));
+    const double ty = add(g.y0, dvd(mul(add((double)j, 0.5), yw), (double)oh));
+    const double dx = sub(tx, ex), dy = sub(ty, ey), dz = sub(focal, ez);
+    // renderer.py:251-257
+    const double tp = dvd(sub(g.img_z, ez), dz);
+    const double ix = add(ex, mul(tp, dx)), iy = add(ey, mul(tp, dy));
+    if (!(g.x0 <= ix && ix <= g.x1 && g.y0 <= iy && iy <= g.y1)) {
+        o[0] = bg[0]; o[1] = bg[1]; o[2] = bg[2];
+        return;
+    }
+    double u = sub(mul(dvd(sub(ix, g.x0), xw), (double)W), 0.5);
+    double vv = sub(mul(dvd(sub(iy, g.y0), yw), (double)H), 0.5);
+    {   // renderer.py:258-260
+        double ru = rint(u), rv = rint(vv);
+        if (fabs(sub(u, ru)) < SNAP_EPS) u = ru;
+        if (fabs(sub(vv, rv)) < SNAP_EPS) vv = rv;
+    }
+    int u0, v0;
+    double fu, fv;
+    vec_tap(u, W, u0, fu);
+    vec_tap(vv, H, v0, fv);
+    // renderer.py:265-266 camera taps (frame constants; recomputed per thread)
+    int si[2], ti[2];
+    double ws[2], wt[2];
+    const int ns = axis_taps(snap(ex), S, si, ws);
+    const int nt = axis_taps(snap(ey), T, ti, wt);
+    const int64_t img = (int64_t)W * H * 3;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int a = 0; a < ns; ++a)
+        for (int b = 0; b < nt; ++b) {
+            const int cam = si[a] * T + ti[b];
+            const uint8_t* im = field + (int64_t)(slots ? slots[cam] : cam) * img;
+            const double wst = mul(ws[a], wt[b]);
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const double wu = p ? fu : sub(1.0, fu);
+                const int gx = min(u0 + p, W - 1);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double wv = q ? fv : sub(1.0, fv);
+                    const int gy = min(v0 + q, H - 1);
+                    const double w = mul(mul(wst, wu), wv);
+                    const uint8_t* px = im + ((int64_t)gy * W + gx) * 3;
+                    acc0 = add(acc0, mul(w, (double)px[0]));
+                    acc1 = add(acc1, mul(w, (double)px[1]));
+                    acc2 = add(acc2, mul(w, (double)px[2]));
+                }
+            }
+        }
+    o[0] = round_clip(acc0);
+    o[1] = round_clip(acc1);
+    o[2] = round_clip(acc2);
+}
+
+struct PinholeCoord {
+    bool hit;
+    double s, t, u, v;
+};
+
+// renderer.py:190-209 per-pixel direction + renderer.py:87-116
+// ray_to_lf_coords.  parallel is set when |dir.z| < 1e-15.
+__device__ __forceinline__ PinholeCoord pinhole_coord(const double* fr, const rlfc_render_geom& g, int S, int T,
+                                                      int W, int H, int i, int j, int ow, int oh, bool& parallel) {
+    PinholeCoord c{false, 0, 0, 0, 0};
+    const double half = fr[12], aspect = fr[13];
+    const double px = sub(mul(dvd(add((double)i, 0.5), (double)ow), 2.0), 1.0);
+    const double py = sub(mul(dvd(add((double)j, 0.5), (double)oh), 2.0), 1.0);
+    const double a = mul(mul(px, half), aspect), b = mul(py, half);
+    double d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = add(add(fr[3 + k], mul(a, fr[6 + k])), mul(b, fr[9 + k]));
+    if (fabs(d[2]) < 1e-15) {
+        parallel = true;
+        return c;
+    }
+    const double tc = dvd(sub(g.cam_z, fr[2]), d[2]);
+    const double cx = add(fr[0], mul(tc, d[0])), cy = add(fr[1], mul(tc, d[1]));
+    if (!(0.0 <= cx && cx <= (double)(S - 1) && 0.0 <= cy && cy <= (double)(T - 1))) return c;
+    const double tt = dvd(sub(g.img_z, fr[2]), d[2]);
+    const double ix = add(fr[0], mul(tt, d[0])), iy = add(fr[1], mul(tt, d[1]));
+    if (!(g.x0 <= ix && ix <= g.x1 && g.y0 <= iy && iy <= g.y1)) return c;
+    c.hit = true;
+    c.s = snap(interp_identity(cx, S));
+    c.t = snap(interp_identity(cy, T));
+    c.u = snap(sub(mul(dvd(sub(ix, g.x0), sub(g.x1, g.x0)), (double)W), 0.5));
+    c.v = snap(sub(mul(dvd(sub(iy, g.y0), sub(g.y1, g.y0)), (double)H), 0.5));
+    return c;
+}
+
+// One thread per output pixel of one pinhole pose (renderer.py:295-305 +
+// sample_quadrilinear renderer.py:147-169).
+__global__ void k_render_pinhole(const uint8_t* __restrict__ field, const int32_t* __restrict__ slots, int S, int T,
+                                 int W, int H,
+                                 const double* __restrict__ frames, const rlfc_render_geom* __restrict__ geoms,
+                                 const uint8_t* __restrict__ bgs, int ow, int oh, uint8_t* __restrict__ out,
+                                 int32_t* status) {
+    const int v = blockIdx.y;
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= (int64_t)ow * oh) return;
+    const int i = (int)(pix % ow), j = (int)(pix / ow);
+    uint8_t* o = out + ((int64_t)v * oh * ow + pix) * 3;
+    const uint8_t* bg = bgs + 3 * v;
+    bool parallel = false;
+    PinholeCoord c = pinhole_coord(frames + 14 * v, geoms[v], S, T, W, H, i, j, ow, oh, parallel);
+    if (parallel) atomicExch(status + v, -2);
+    if (!c.hit) {
+        o[0] = bg[0]; o[1] = bg[1]; o[2] = bg[2];
+        return;
+    }
+    int si[2], ti[2], ui[2], vi[2];
+    double ws[2], wt[2], wu[2], wv[2];
+    const int ns = axis_taps(c.s, S, si, ws), nt = axis_taps(c.t, T, ti, wt);
+    const int nu = axis_taps(c.u, W, ui, wu), nv = axis_taps(c.v, H, vi, wv);
+    const int64_t img = (int64_t)W * H * 3;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int a = 0; a < ns; ++a)
+        for (int b = 0; b < nt; ++b)
+            for (int p = 0; p < nu; ++p)
+                for (int q = 0; q < nv; ++q) {
+                    const double w = mul(mul(mul(ws[a], wt[b]), wu[p]), wv[q]);
+                    const int cam = si[a] * T + ti[b];
+                    const uint8_t* px = field + (int64_t)(slots ? slots[cam] : cam) * img +
+                                        ((int64_t)vi[q] * W + ui[p]) * 3;
+                    acc0 = add(acc0, mul(w, (double)px[0]));
+                    acc1 = add(acc1, mul(w, (double)px[1]));
+                    acc2 = add(acc2, mul(w, (double)px[2]));
+                }
+    o[0] = round_clip(acc0);
+    o[1] = round_clip(acc1);
+    o[2] = round_clip(acc2);
+}
+
+__global__ void k_pinhole_needs(int S, int T, int W, int H, const double* __restrict__ frames,
+                                const rlfc_render_geom* __restrict__ geoms, int ow, int oh,
+                                uint8_t* __restrict__ need) {
+    const int v = blockIdx.y;
+    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= (int64_t)ow * oh) return;
+    bool parallel = false;
+    PinholeCoord c = pinhole_coord(frames + 14 * v, geoms[v], S, T, W, H, (int)(pix % ow), (int)(pix / ow), ow,
+                                   oh, parallel);
+    if (!c.hit) return;
+    int si[2], ti[2];
+    double ws[2], wt[2];
+    const int ns = axis_taps(c.s, S, si, ws), nt = axis_taps(c.t, T, ti, wt);
+    for (int a = 0; a < ns; ++a)
+        for (int b = 0; b < nt; ++b) need[si[a] * T + ti[b]] = 1;
+}
+
+static int launch_status() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "rlfc_b200: CUDA launch error: %s\n", cudaGetErrorString(e));
+        return RLFC_ERR_CUDA;
+    }
+    return RLFC_OK;
+}
+
+}  // namespace rlfc
+
+using namespace rlfc;
+
+extern "C" int rlfc_render_slab(const uint8_t* field, const int32_t* slots, int32_t S, int32_t T, int32_t W, int32_t H,
+                                const double* poses, const rlfc_render_geom* geoms, const uint8_t* bg, int32_t n,
+                                int32_t ow, int32_t oh, uint8_t* out, void* stream) {
+    if (S < 1 || T < 1 || W < 1 || H < 1 || n < 0 || ow < 1 || oh < 1 || n > 65535) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    const int threads = 256;
+    dim3 grid((unsigned)(((int64_t)ow * oh + threads - 1) / threads), (unsigned)n);
+    k_render_slab<<<grid, threads, 0, (cudaStream_t)stream>>>(field, slots, S, T, W, H, poses, geoms, bg, ow, oh, out);
+    return launch_status();
+}
+
+extern "C" int rlfc_render_pinhole(const uint8_t* field, const int32_t* slots, int32_t S, int32_t T, int32_t W, int32_t H,
+                                   const double* frames, const rlfc_render_geom* geoms, const uint8_t* bg,
+                                   int32_t n, int32_t ow, int32_t oh, uint8_t* out, int32_t* status,
+                                   void* stream) {
+    if (S < 1 || T < 1 || W < 1 || H < 1 || n < 0 || ow < 1 || oh < 1 || n > 65535) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    const int threads = 256;
+    dim3 grid((unsigned)(((int64_t)ow * oh + threads - 1) / threads), (unsigned)n);
+    k_render_pinhole<<<grid, threads, 0, (cudaStream_t)stream>>>(field, slots, S, T, W, H, frames, geoms, bg, ow, oh, out,
+                                                                 status);
+    return launch_status();
+}
+
+extern "C" int rlfc_render_pinhole_needs(int32_t S, int32_t T, int32_t W, int32_t H, const double* frames,
+                                         const rlfc_render_geom* geoms, int32_t n, int32_t ow, int32_t oh,
+                                         uint8_t* need, void* stream) {
+    if (S < 1 || T < 1 || W < 1 || H < 1 || n < 0 || ow < 1 || oh < 1 || n > 65535) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    const int threads = 256;
+    dim3 grid((unsigned)(((int64_t)ow * oh + threads - 1) / threads), (unsigned)n);
+    k_pinhole_needs<<<grid, threads, 0, (cudaStream_t)stream>>>(S, T, W, H, frames, geoms, ow, oh, need);
+    return launch_status();
+}

@@ -1,0 +1,403 @@
+"""Stream decoding on the B200: drop-in for the reference rlfc.decoder.
+
+Public functions keep the reference signatures, return types and exceptions
+(reference decoder.py:31-210): `init`, `decode_block_progressive`,
+`decode_block`, `decode_block_traced`, `decode_plane`, `decode_image`,
+`decode_all`.  `init` parses the header and root views on the host exactly
+once and uploads the SRV sections, offset arrays and root planes to HBM; every
+decode afterwards is a CUDA kernel from librlfc_b200.so (include/rlfc_b200.h).
+
+The batched, device-resident API used for throughput work is
+`decode_field` (whole light field or any image subset / block-row band,
+returned as a CUDA tensor), `decode_blocks` (random-access batches),
+`decode_planes` and `bise_decode_batch`.
+
+There is no CPU fallback: without the extension or a CUDA device these
+functions raise `_native.NativeUnavailable`.
+"""
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native, colorspace, container
+from .bise import RANGE_TABLE, payload_bytes_table
+from .errors import FormatError
+from .lightfield import LightFieldGrid, default_geometry, grid_positions
+
+SRV_TAIL_PAD = 16
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DeviceField:
+    """One stream resident in one GPU's HBM plus its `rlfc_field` descriptor.
+
+    Layout: per channel the SRV section as
+    raw bytes (+16 zero bytes so 8-byte bit-window loads never leave the
+    allocation) and the u64 offset array; the root planes as one
+    (rsx, rsy, 3, Hp, Wp) int16 tensor (int32 if any sample needs it).
+    """
+
+    def __init__(self, header, srv, offsets, root_planes, device):
+        torch = _torch()
+        self.device = torch.device(device)
+        self.header = header
+        S, T, h = header.s_count, header.t_count, header.tree_height
+        if h > _native.MAX_LEVELS:
+            raise FormatError(f"tree height {h} above the supported "
+                              f"{_native.MAX_LEVELS} levels")
+        self.srv = []
+        self.offsets = []
+        for c in range(3):
+            buf = torch.zeros(len(srv[c]) + SRV_TAIL_PAD, dtype=torch.uint8)
+            buf[:len(srv[c])] = torch.from_numpy(np.asarray(srv[c]).copy())
+            self.srv.append(buf.to(self.device))
+            off = np.ascontiguousarray(offsets[c]).view(np.int64)
+            self.offsets.append(torch.from_numpy(off.copy()).to(self.device))
+        i16 = bool(root_planes.size == 0 or (root_planes.min() >= -32768 and
+                                             root_planes.max() <= 32767))
+        rp = root_planes.astype(np.int16 if i16 else np.int32)
+        self.roots = torch.from_numpy(np.ascontiguousarray(rp)).to(self.device)
+        f = _native.RlfcField()
+        wp, hp = header.padded_dims
+        wb, hb = header.block_grid
+        rsx, rsy = container.level_dims(S, T, h)
+        m = container.total_srv_nodes(S, T, h)
+        f.s_count, f.t_count, f.width, f.height = S, T, header.width, \
+            header.height
+        f.block, f.tree_height, f.quant_shift = header.block_size, h, \
+            header.quant_shift
+        f.m_nodes, f.wp, f.hp, f.wb, f.hb, f.rsx, f.rsy = m, wp, hp, wb, hb, \
+            rsx, rsy
+        f.roots_i16 = int(i16)
+        f.bitmap_bytes = (m + 7) >> 3
+        for l, base in enumerate(container.level_bases(S, T, h)):
+            f.level_base[l] = base
+            f.level_sx[l], f.level_sy[l] = container.level_dims(S, T, l)
+        for c in range(3):
+            f.srv[c] = self.srv[c].data_ptr()
+            f.offsets[c] = self.offsets[c].data_ptr()
+            f.srv_len[c] = len(srv[c])
+        f.roots = self.roots.data_ptr()
+        self.cfield = f
+        self.ref = ctypes.byref(f)
+
+    @property
+    def hbm_bytes(self):
+        return sum(t.numel() * t.element_size()
+                   for t in self.srv + self.offsets + [self.roots])
+
+
+@dataclass(frozen=True)
+class DecoderState:
+    """Immutable, request-ready state (reference decoder.py:20-28) plus the
+    per-GPU device copies."""
+    header: container.RlfcHeader
+    data: bytes
+    root_planes: np.ndarray      # (rsx, rsy, 3, Hp, Wp) int32, unbiased
+    offsets: tuple               # per channel u64 array, one per block
+    srv: tuple                   # per channel uint8 view of the SRV stream
+    chains: np.ndarray           # (S, T, h) ascending serial ancestor indices
+    m_nodes: int
+    _devices: dict = field(default_factory=dict, compare=False, repr=False)
+    _lock: object = field(default_factory=threading.Lock, compare=False,
+                          repr=False)
+
+    def device_field(self, device=None) -> DeviceField:
+        """The stream's HBM copy on `device` (default: current CUDA device),
+        uploaded on first use."""
+        torch = _torch()
+        _native.lib()
+        dev = torch.device("cuda", torch.cuda.current_device()) \
+            if device is None else torch.device(device)
+        key = dev.index
+        with self._lock:
+            df = self._devices.get(key)
+            if df is None:
+                df = DeviceField(self.header, self.srv, self.offsets,
+                                 self.root_planes, dev)
+                self._devices[key] = df
+        return df
+
+
+def init(stream: bytes, device=None) -> DecoderState:
+    """Parse a stream and upload it to the GPU (reference decoder.py:31-48)."""
+    header = container.parse_header(stream)
+    container.check_stream_length(header, stream)
+    data = bytes(stream)
+    roots = container.parse_roots(data, header)
+    offsets = tuple(container.parse_offsets(data, header, c) for c in range(3))
+    srv = tuple(container.srv_section(data, header, c) for c in range(3))
+    chains = container.all_chains(header.s_count, header.t_count,
+                                  header.tree_height)
+    m = container.total_srv_nodes(header.s_count, header.t_count,
+                                  header.tree_height)
+    state = DecoderState(header=header, data=data, root_planes=roots,
+                         offsets=offsets, srv=srv, chains=chains, m_nodes=m)
+    state.device_field(device)
+    return state
+
+
+# --- argument checks and error mapping (decoder.py:51-70) ---------------------
+
+def _check_indices(state, s, t, bx=0, by=0):
+    hdr = state.header
+    if not (0 <= s < hdr.s_count and 0 <= t < hdr.t_count):
+        raise IndexError(f"image index ({s}, {t}) outside grid")
+    wb, hb = hdr.block_grid
+    if not (0 <= bx < wb and 0 <= by < hb):
+        raise IndexError(f"block index ({bx}, {by}) outside block grid")
+
+
+def _check_level(state, stop_level):
+    if not 0 <= stop_level <= state.header.tree_height:
+        raise ValueError(f"stop level {stop_level} outside [0, "
+                         f"{state.header.tree_height}]")
+
+
+def _raise_status(code):
+    if code == 1:
+        raise FormatError("corrupt coded pack in SRV payload")
+    if code == 2:
+        raise FormatError("descriptor outside range table")
+
+
+def _raise_word(word):
+    got = _native.decode_status_word(word)
+    if got is not None:
+        _raise_status(got[1])
+
+
+def _stream():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+# --- batched device API ------------------------------------------------------
+
+def decode_blocks(state, requests, device=None, raise_errors=True):
+    """Decode a batch of blocks on the GPU.
+
+    requests: (n, 6) ints (s, t, bx, by, channel, stop_level).  Returns
+    (CUDA int32 tensor (n, B, B), CUDA int32 status tensor (n,)).  With
+    raise_errors the first failing request (lowest index) raises the
+    reference's FormatError.
+    """
+    torch = _torch()
+    df = state.device_field(device)
+    req = torch.as_tensor(np.ascontiguousarray(requests, dtype=np.int32)
+                          .reshape(-1, 6)).to(df.device, non_blocking=True)
+    n = req.shape[0]
+    b = state.header.block_size
+    out = torch.empty((n, b, b), dtype=torch.int32, device=df.device)
+    status = torch.zeros(n, dtype=torch.int32, device=df.device)
+    with torch.cuda.device(df.device):
+        _native.check(_native.lib().rlfc_decode_blocks(
+            df.ref, req.data_ptr(), n, out.data_ptr(), status.data_ptr(),
+            _stream()), "rlfc_decode_blocks")
+    if raise_errors and n:
+        st = status.cpu().numpy()
+        bad = np.flatnonzero(st)
+        if bad.size:
+            _raise_status(int(st[bad[0]]))
+    return out, status
+
+
+def decode_planes(state, planes, stop_level=0, device=None):
+    """(n, Hp, Wp) int32 CUDA tensor of padded planes for (s, t, c) triples."""
+    torch = _torch()
+    df = state.device_field(device)
+    req = torch.as_tensor(np.ascontiguousarray(planes, dtype=np.int32)
+                          .reshape(-1, 3)).to(df.device)
+    n = req.shape[0]
+    wp, hp = state.header.padded_dims
+    out = torch.empty((n, hp, wp), dtype=torch.int32, device=df.device)
+    status = torch.zeros(1, dtype=torch.int64, device=df.device)
+    with torch.cuda.device(df.device):
+        _native.check(_native.lib().rlfc_decode_planes(
+            df.ref, stop_level, req.data_ptr(), n, out.data_ptr(),
+            status.data_ptr(), _stream()), "rlfc_decode_planes")
+    _raise_word(status.cpu().item())
+    return out
+
+
+def decode_field(state, stop_level=0, images=None, rows=None, out=None,
+                 device=None, kernel="fused", check=True):
+    """Decode many camera images straight into an RGB8 CUDA tensor.
+
+    images: None for the whole (S, T) grid -- the result is (S, T, H, W, 3)
+    -- or a sequence of (s, t) pairs -- the result is (n, H, W, 3) in that
+    order.  rows: optional block-row band (by_lo, by_hi); the result then
+    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "fused" (the
+    tiled sm_100a kernel) or "simple" (per-block kernel).  With check, a
+    corrupt stream raises the FormatError the reference raises first.
+    Returns (tensor, status) where status is the device status word tensor.
+    """
+    torch = _torch()
+    hdr = state.header
+    _check_level(state, stop_level)
+    df = state.device_field(device)
+    S, T, W, H, B = hdr.s_count, hdr.t_count, hdr.width, hdr.height, \
+        hdr.block_size
+    _, hb = hdr.block_grid
+    by_lo, by_hi = (0, hb) if rows is None else (int(rows[0]), int(rows[1]))
+    if not 0 <= by_lo <= by_hi <= hb:
+        raise ValueError(f"block-row band {rows} outside [0, {hb}]")
+    nrows = max(0, min(by_hi * B, H) - by_lo * B)
+    slots_t = None
+    if images is None:
+        shape = (S, T, nrows, W, 3)
+        nimg = S * T
+    else:
+        pairs = [tuple(map(int, p)) for p in images]
+        slots = np.full(S * T, -1, dtype=np.int32)
+        for i, (s, t) in enumerate(pairs):
+            _check_indices(state, s, t)
+            if slots[s * T + t] >= 0:
+                raise ValueError(f"image ({s}, {t}) requested twice")
+            slots[s * T + t] = i
+        shape = (len(pairs), nrows, W, 3)
+        nimg = len(pairs)
+        slots_t = torch.from_numpy(slots).to(df.device)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.uint8, device=df.device)
+    elif tuple(out.shape) != shape or out.dtype != torch.uint8 or \
+            not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous uint8 tensor {shape}")
+    status = torch.zeros(1, dtype=torch.int64, device=df.device)
+    if nimg and nrows:
+        fn = _native.lib().rlfc_decode_field if kernel == "fused" else \
+            _native.lib().rlfc_decode_field_simple
+        with torch.cuda.device(df.device):
+            _native.check(fn(
+                df.ref, stop_level,
+                None if slots_t is None else slots_t.data_ptr(), by_lo, by_hi,
+                out.data_ptr(), nrows * W * 3, W * 3, status.data_ptr(),
+                _stream()), "rlfc_decode_field")
+    if check:
+        _raise_word(status.cpu().item())
+    return out, status
+
+
+def bise_decode_batch(payloads, descs, count, device=None):
+    """Decode many BISE payloads on the GPU (kernels.bise_decode_core).
+
+    Returns (values uint32 (n, count) numpy, status int32 (n,) numpy).
+    """
+    torch = _torch()
+    _native.lib()
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if device is None else torch.device(device)
+    blobs = [bytes(p) for p in payloads]
+    offs = np.zeros(len(blobs), dtype=np.int64)
+    pos = 0
+    for i, b in enumerate(blobs):
+        offs[i] = pos
+        pos += len(b)
+    data = np.zeros(pos + SRV_TAIL_PAD, dtype=np.uint8)
+    data[:pos] = np.frombuffer(b"".join(blobs), dtype=np.uint8)
+    d_data = torch.from_numpy(data).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    d_desc = torch.from_numpy(np.asarray(descs, dtype=np.uint8)).to(dev)
+    n = len(blobs)
+    out = torch.zeros((n, count), dtype=torch.int32, device=dev)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _native.check(_native.lib().rlfc_bise_decode(
+            d_data.data_ptr(), d_offs.data_ptr(), d_desc.data_ptr(), n, count,
+            out.data_ptr(), status.data_ptr(), _stream()), "rlfc_bise_decode")
+    return out.cpu().numpy().view(np.uint32), status.cpu().numpy()
+
+
+# --- reference-signature API ---------------------------------------------------
+
+def decode_block_progressive(state: DecoderState, image_index, block_index,
+                             channel, stop_level):
+    """One B x B block summing SRV levels >= stop_level (decoder.py:81-106)."""
+    s, t = image_index
+    bx, by = block_index
+    _check_indices(state, s, t, bx, by)
+    _check_level(state, stop_level)
+    out, _ = decode_blocks(state, [(s, t, bx, by, channel, stop_level)])
+    return out[0].cpu().numpy()
+
+
+def decode_block(state: DecoderState, image_index, block_index, channel):
+    """Fully decode one block of one channel plane (decoder.py:109-112)."""
+    return decode_block_progressive(state, image_index, block_index, channel,
+                                    stop_level=0)
+
+
+def decode_block_traced(state: DecoderState, image_index, block_index,
+                        channel, stop_level=0):
+    """decode_block plus the absolute SRV byte ranges a decode reads.
+
+    Host-side read-locality mirror (decoder.py:115-162): the ranges come from
+    a walk of the record on the host; the block itself is decoded on the GPU.
+    """
+    s, t = image_index
+    bx, by = block_index
+    _check_indices(state, s, t, bx, by)
+    _check_level(state, stop_level)
+    hdr = state.header
+    wb, _ = hdr.block_grid
+    starts, _ = container.section_offsets(hdr)
+    rec = starts[channel][2] + int(state.offsets[channel][by * wb + bx])
+    nbm = (state.m_nodes + 7) >> 3
+    ranges = [(rec, rec + nbm)]
+    bits = np.unpackbits(np.frombuffer(state.data[rec:rec + nbm], np.uint8),
+                         bitorder="little")
+    targets = set(int(v) for v in
+                  state.chains[s, t, :hdr.tree_height - stop_level])
+    top = max(targets) if targets else -1
+    pbytes = payload_bytes_table(hdr.block_size ** 2)
+    cursor = rec + nbm
+    for node in np.flatnonzero(bits[:top + 1]):
+        desc = state.data[cursor]
+        ranges.append((cursor, cursor + 1))
+        if desc >= len(RANGE_TABLE):
+            raise FormatError(f"descriptor {desc} outside range table")
+        if int(node) in targets:
+            ranges.append((cursor + 1, cursor + 1 + int(pbytes[desc])))
+        cursor += 1 + int(pbytes[desc])
+    block = decode_block_progressive(state, image_index, block_index, channel,
+                                     stop_level)
+    return block, ranges
+
+
+def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
+    """One image channel plane at padded dims, int32 (decoder.py:165-184)."""
+    _check_indices(state, s, t)
+    _check_level(state, stop_level)
+    if stop_level == state.header.tree_height:
+        h = state.header.tree_height
+        return state.root_planes[s >> h, t >> h, channel].copy()
+    return decode_planes(state, [(s, t, channel)], stop_level)[0].cpu().numpy()
+
+
+def decode_image(state: DecoderState, image_index, stop_level=0):
+    """One camera image as true-dims RGB8 (decoder.py:187-194)."""
+    s, t = image_index
+    _check_indices(state, s, t)
+    out, _ = decode_field(state, stop_level, images=[(s, t)])
+    return out[0].cpu().numpy()
+
+
+def decode_all(state: DecoderState, stop_level=0) -> LightFieldGrid:
+    """The whole grid as a LightFieldGrid (decoder.py:197-210)."""
+    hdr = state.header
+    out, _ = decode_field(state, stop_level)
+    return LightFieldGrid(hdr.s_count, hdr.t_count, hdr.width, hdr.height,
+                          out.cpu().numpy(),
+                          grid_positions(hdr.s_count, hdr.t_count),
+                          default_geometry(hdr.s_count, hdr.t_count))
+
+
+def planes_to_rgb(planes):
+    """Host helper: three int32 planes -> clamped RGB8 (colorspace.py:46-56)."""
+    return colorspace.planes_to_grid(planes)

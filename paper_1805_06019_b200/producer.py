@@ -1,0 +1,178 @@
+"""Native stream producer: synthetic light fields and the .rlfc encoder.
+
+Binds librlfc_producer.so (producer/rlfc_producer.cpp).  Output streams are
+byte-identical to the reference encoder's (tests/test_producer.py pins them
+against streams the reference produced).  Cluster filter weights and cluster
+positions are computed here with numpy exactly as the reference computes them
+(hierarchy.py:141-162, 195-212); root views are encoded with Pillow through
+container.encode_root, as the reference does (container.py:152-172).
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build, container
+from .errors import FormatError
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = _build.PRODUCER_LIB
+        if not os.path.exists(path):
+            _build.build_producer()
+        L = ctypes.CDLL(path)
+        vp, i32, i64, u64 = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                             ctypes.c_uint64)
+        L.prod_set_threads.argtypes = [i32]
+        L.prod_synthesize.argtypes = [i32, i32, i32, i32, u64, vp]
+        L.prod_bise_encode.argtypes = [vp, i64, i32, i32, vp]
+        L.prod_bise_encode.restype = i64
+        L.prod_encode.argtypes = [i32, i32, i32, i32, vp, i32, i32, i32, i64,
+                                  i32, vp]
+        L.prod_encode.restype = vp
+        L.prod_result_error.argtypes = [vp]
+        L.prod_result_srv_len.argtypes = [vp, i32]
+        L.prod_result_srv_len.restype = i64
+        L.prod_result_copy.argtypes = [vp, i32, vp, vp]
+        L.prod_result_roots.argtypes = [vp, vp]
+        L.prod_result_present.argtypes = [vp, vp]
+        L.prod_free.argtypes = [vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def synthesize(spec, threads=0):
+    """(S, T, H, W, 3) uint8 of the reference's procedural scene."""
+    L = lib()
+    L.prod_set_threads(int(threads))
+    out = np.empty((spec.s_count, spec.t_count, spec.height, spec.width, 3),
+                   dtype=np.uint8)
+    L.prod_synthesize(spec.s_count, spec.t_count, spec.width, spec.height,
+                      spec.seed & 0xFFFFFFFFFFFFFFFF, _ptr(out))
+    return out
+
+
+def bise_encode(values, rng) -> bytes:
+    values = np.ascontiguousarray(values, dtype=np.uint32)
+    if values.size and int(values.max()) >= rng.cardinality:
+        raise ValueError(
+            f"value {int(values.max())} out of range N={rng.cardinality}")
+    from .bise import payload_size
+    nbits = payload_size(rng, values.size)
+    out = np.zeros((nbits + 7) // 8, dtype=np.uint8)
+    wrote = lib().prod_bise_encode(_ptr(values), values.size, rng.mode,
+                                   rng.low_bits, _ptr(out))
+    assert wrote == nbits
+    return out.tobytes()
+
+
+def filter_weights(positions, spec):
+    """Integer /256 cluster weights, largest-remainder rounding
+    (hierarchy.py:141-162 semantics, numpy float64)."""
+    n = len(positions)
+    if n == 1:
+        return np.array([256], dtype=np.int64)
+    if spec.kind == "uniform":
+        raw = np.ones(n)
+    else:
+        pos = np.asarray(positions, dtype=np.float64)
+        d2 = ((pos - pos.mean(axis=0)) ** 2).sum(axis=1)
+        sig = spec.quantized_sigma()
+        raw = np.exp(-d2 / (2.0 * sig * sig))
+    scaled = raw * (256 / raw.sum())
+    base = np.floor(scaled).astype(np.int64)
+    frac = scaled - base
+    for i in sorted(range(n), key=lambda i: (-frac[i], i))[:256 - int(base.sum())]:
+        base[i] += 1
+    return base
+
+
+def pyramid_weights(camera_positions, tree_height, spec):
+    """Flat int64 weights for prod_encode: per level 1..h, per parent (cx
+    outer, cy inner), 4 member slots (members x outer, y inner)."""
+    pos = np.asarray(camera_positions, dtype=np.float64)
+    flat = []
+    for _ in range(tree_height):
+        sx, sy = pos.shape[:2]
+        px, py = -(-sx // 2), -(-sy // 2)
+        up = np.zeros((px, py, 2))
+        for cx in range(px):
+            for cy in range(py):
+                members = [(x, y) for x in (2 * cx, 2 * cx + 1) if x < sx
+                           for y in (2 * cy, 2 * cy + 1) if y < sy]
+                cpos = [pos[x, y] for x, y in members]
+                w = filter_weights(cpos, spec)
+                slot = np.zeros(4, dtype=np.int64)
+                slot[:len(w)] = w
+                flat.append(slot)
+                up[cx, cy] = (w[:, None] * np.asarray(cpos)).sum(0) / 256.0
+        pos = up
+    return np.concatenate(flat) if flat else np.zeros(0, np.int64)
+
+
+def encode(lf, params, threads=0):
+    """(stream bytes, present blocks per level) for a LightFieldGrid."""
+    L = lib()
+    L.prod_set_threads(int(threads))
+    S, T, W, H = lf.s_count, lf.t_count, lf.width, lf.height
+    h, B = params.tree_height, params.block_size
+    rgb = np.ascontiguousarray(lf.rgb, dtype=np.uint8)
+    w = np.ascontiguousarray(pyramid_weights(lf.camera_positions, h,
+                                             params.filter))
+    handle = L.prod_encode(S, T, W, H, _ptr(rgb), h, B,
+                           params.pixel_threshold, params.block_threshold,
+                           params.quant_shift, _ptr(w))
+    try:
+        if L.prod_result_error(handle):
+            raise FormatError("residual value outside the range table")
+        wp, hp = container.padded_dims(W, H, B)
+        wb, hb = wp // B, hp // B
+        rsx, rsy = container.level_dims(S, T, h)
+        roots = np.empty((rsx, rsy, 3, hp, wp), dtype=np.int32)
+        L.prod_result_roots(handle, _ptr(roots))
+        present = np.zeros(h, dtype=np.int64)
+        L.prod_result_present(handle, _ptr(present))
+        srvs, offs = [], []
+        for c in range(3):
+            srv = np.empty(L.prod_result_srv_len(handle, c), dtype=np.uint8)
+            off = np.empty(wb * hb, dtype="<u8")
+            L.prod_result_copy(handle, c, _ptr(srv), _ptr(off))
+            srvs.append(srv)
+            offs.append(off)
+    finally:
+        L.prod_free(handle)
+    codec = container.CODEC_IDS[params.root_codec]
+    sections, lengths = [], []
+    for c in range(3):
+        chunks = []
+        for y in range(rsy):
+            for x in range(rsx):
+                blob = container.encode_root(
+                    roots[x, y, c].astype(np.int64) + container.CHANNEL_BIAS[c],
+                    codec)
+                chunks.append(len(blob).to_bytes(4, "little"))
+                chunks.append(blob)
+        root_sec = b"".join(chunks)
+        off_sec = offs[c].tobytes()
+        srv_sec = srvs[c].tobytes()
+        sections += [root_sec, off_sec, srv_sec]
+        lengths.append((len(root_sec), len(off_sec), len(srv_sec)))
+    header = container.RlfcHeader(
+        s_count=S, t_count=T, width=W, height=H, tree_height=h,
+        block_size=B, quant_shift=params.quant_shift,
+        pixel_threshold=params.pixel_threshold,
+        block_threshold=params.block_threshold,
+        filter_kind=params.filter.kind,
+        sigma_fp=params.filter.sigma_fp if params.filter.kind == "gaussian"
+        else 0,
+        root_codec_id=codec, section_lengths=tuple(lengths))
+    return container.pack_header(header) + b"".join(sections), tuple(present)

@@ -1,0 +1,302 @@
+"""Novel-view synthesis on the B200: drop-in for the reference rlfc.renderer.
+
+`render_view` keeps the reference signature (renderer.py:279-305).  A view is
+rendered in two device steps: the fused decode kernel writes the pose's tap
+cameras (<= 4 for a slab pose) as RGB8 into HBM, then one render kernel
+evaluates every output pixel with the reference's float64 arithmetic in the
+reference's operation order (bit-exact; rlfc_render.cu).  `render_views`
+batches many poses: the union of their tap cameras is decoded once and every
+view is rendered from it in one launch.
+
+Per-frame constants that the reference computes with numpy (pinhole basis,
+renderer.py:190-209) are computed here with the same numpy expressions, so
+they are identical to the reference's bit for bit.
+"""
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, colorspace, decoder
+from .lightfield import PlaneGeometry, default_geometry
+
+SNAP_EPS = 1e-9
+
+
+@dataclass(frozen=True)
+class LfCoord:
+    s: float
+    t: float
+    u: float
+    v: float
+
+
+@dataclass(frozen=True)
+class SlabPose:
+    """Eye on the camera plane at grid position (s, t); focal_z refocuses."""
+    s: float
+    t: float
+    width: int
+    height: int
+    focal_z: float = None
+
+
+@dataclass(frozen=True)
+class CameraPose:
+    """Free pinhole camera: eye point, look direction, vertical fov."""
+    eye: tuple
+    look: tuple
+    fov_deg: float
+    width: int
+    height: int
+
+    def __post_init__(self):
+        if self.fov_deg <= 0 or self.fov_deg >= 180:
+            raise ValueError("fov must be in (0, 180)")
+        if all(abs(v) < 1e-12 for v in self.look):
+            raise ValueError("look direction is zero")
+
+
+@dataclass(frozen=True)
+class GridInfo:
+    xs: np.ndarray
+    ys: np.ndarray
+    width: int
+    height: int
+
+
+def grid_info_for(state) -> GridInfo:
+    hdr = state.header
+    return GridInfo(xs=np.arange(hdr.s_count, dtype=np.float64),
+                    ys=np.arange(hdr.t_count, dtype=np.float64),
+                    width=hdr.width, height=hdr.height)
+
+
+def _snap(f):
+    r = round(f)
+    return float(r) if abs(f - r) < SNAP_EPS else float(f)
+
+
+def _axis_taps(coord, count):
+    """[(index, weight)] with zero weights dropped (renderer.py:119-131)."""
+    c = min(max(coord, 0.0), float(count - 1))
+    if count == 1:
+        return [(0, 1.0)]
+    i0 = min(int(math.floor(c)), count - 2)
+    f = _snap(c - i0)
+    taps = []
+    if f < 1.0:
+        taps.append((i0, 1.0 - f))
+    if f > 0.0:
+        taps.append((i0 + 1, f))
+    return taps
+
+
+def ray_to_lf_coords(ray, geometry: PlaneGeometry, grid):
+    """Fractional (s, t, u, v) of one ray, or None outside the slab."""
+    origin, direction = (np.asarray(v, dtype=np.float64) for v in ray)
+    if abs(direction[2]) < 1e-15:
+        raise ValueError("ray parallel to the light-slab planes")
+    if not isinstance(grid, GridInfo):
+        grid = GridInfo(xs=grid.camera_positions[:, 0, 0].astype(np.float64),
+                        ys=grid.camera_positions[0, :, 1].astype(np.float64),
+                        width=grid.width, height=grid.height)
+    tc = (geometry.camera_plane_z - origin[2]) / direction[2]
+    cx = origin[0] + tc * direction[0]
+    cy = origin[1] + tc * direction[1]
+    if not (grid.xs[0] <= cx <= grid.xs[-1] and
+            grid.ys[0] <= cy <= grid.ys[-1]):
+        return None
+    s = float(np.interp(cx, grid.xs, np.arange(len(grid.xs))))
+    t = float(np.interp(cy, grid.ys, np.arange(len(grid.ys))))
+    ti = (geometry.image_plane_z - origin[2]) / direction[2]
+    ix = origin[0] + ti * direction[0]
+    iy = origin[1] + ti * direction[1]
+    x0, y0, x1, y1 = geometry.image_plane_extent
+    if not (x0 <= ix <= x1 and y0 <= iy <= y1):
+        return None
+    u = (ix - x0) / (x1 - x0) * grid.width - 0.5
+    v = (iy - y0) / (y1 - y0) * grid.height - 0.5
+    return LfCoord(_snap(s), _snap(t), _snap(u), _snap(v))
+
+
+def _block_rgb(state, s, t, bx, by, stop_level, memo):
+    key = (s, t, bx, by, stop_level)
+    if memo is not None and key in memo:
+        return memo[key]
+    blocks, _ = decoder.decode_blocks(
+        state, [(s, t, bx, by, c, stop_level) for c in range(3)])
+    planes = blocks.cpu().numpy()
+    rgb = np.stack(colorspace.ycocgr_to_rgb(*planes)).clip(0, 255) \
+        .astype(np.float64)
+    if memo is not None:
+        memo[key] = rgb
+    return rgb
+
+
+def sample_quadrilinear(state, coord: LfCoord, stop_level=0, memo=None):
+    """16-tap blend around coord (renderer.py:147-169); GPU block decodes."""
+    hdr = state.header
+    b = hdr.block_size
+    acc = np.zeros(3)
+    for s, ws in _axis_taps(coord.s, hdr.s_count):
+        for t, wt in _axis_taps(coord.t, hdr.t_count):
+            for u, wu in _axis_taps(coord.u, hdr.width):
+                for v, wv in _axis_taps(coord.v, hdr.height):
+                    rgb = _block_rgb(state, s, t, u // b, v // b, stop_level,
+                                     memo)
+                    acc += (ws * wt * wu * wv) * rgb[:, v % b, u % b]
+    return np.floor(acc + 0.5).clip(0, 255).astype(np.uint8)
+
+
+def _slab_rays(pose: SlabPose, geometry, grid: GridInfo):
+    """Eye and per-pixel directions (renderer.py:172-187; host reference)."""
+    focal = pose.focal_z if pose.focal_z is not None else \
+        geometry.image_plane_z
+    if focal == geometry.camera_plane_z:
+        raise ValueError("focal plane coincides with the camera plane")
+    ex = float(np.interp(pose.s, np.arange(len(grid.xs)), grid.xs))
+    ey = float(np.interp(pose.t, np.arange(len(grid.ys)), grid.ys))
+    eye = np.array([ex, ey, geometry.camera_plane_z])
+    x0, y0, x1, y1 = geometry.image_plane_extent
+    tx = x0 + (np.arange(pose.width) + 0.5) * (x1 - x0) / pose.width
+    ty = y0 + (np.arange(pose.height) + 0.5) * (y1 - y0) / pose.height
+    targets = np.zeros((pose.height, pose.width, 3))
+    targets[:, :, 0] = tx[None, :]
+    targets[:, :, 1] = ty[:, None]
+    targets[:, :, 2] = focal
+    return eye, targets - eye
+
+
+def _pinhole_basis(pose: CameraPose, geometry):
+    """Per-frame eye / look / right / down / tan(fov/2) / aspect, computed
+    with the reference's numpy expressions (renderer.py:190-209)."""
+    eye = np.asarray(pose.eye, dtype=np.float64)
+    if abs(eye[2] - geometry.image_plane_z) < 1e-12:
+        raise ValueError("eye lies on the image plane")
+    look = np.asarray(pose.look, dtype=np.float64)
+    look = look / np.linalg.norm(look)
+    up = np.array([0.0, 1.0, 0.0])
+    if abs(np.dot(up, look)) > 1.0 - 1e-9:
+        up = np.array([1.0, 0.0, 0.0])
+    right = np.cross(look, up)
+    right /= np.linalg.norm(right)
+    down = np.cross(look, right)
+    half = math.tan(math.radians(pose.fov_deg) / 2.0)
+    aspect = pose.width / pose.height
+    return np.concatenate([eye, look, right, down, [half, aspect]])
+
+
+def _geom_struct(geometry):
+    x0, y0, x1, y1 = geometry.image_plane_extent
+    return (geometry.camera_plane_z, geometry.image_plane_z, x0, y0, x1, y1)
+
+
+def _slab_cameras(pose, S, T, geometry):
+    focal = pose.focal_z if pose.focal_z is not None else \
+        geometry.image_plane_z
+    if focal == geometry.camera_plane_z:
+        raise ValueError("focal plane coincides with the camera plane")
+    ex = min(max(float(pose.s), 0.0), float(S - 1))
+    ey = min(max(float(pose.t), 0.0), float(T - 1))
+    return [(si, ti) for si, _ in _axis_taps(_snap(ex), S)
+            for ti, _ in _axis_taps(_snap(ey), T)]
+
+
+def render_views(state, poses, stop_level=0, geometry=None,
+                 background=(0, 0, 0), device=None, out=None):
+    """Render a batch of same-size poses; returns a CUDA uint8 tensor
+    (n, height, width, 3).  geometry / background: one for all poses or one
+    per pose."""
+    import torch
+    hdr = state.header
+    decoder._check_level(state, stop_level)
+    poses = list(poses)
+    n = len(poses)
+    if n == 0:
+        raise ValueError("no poses")
+    kinds = {type(p) for p in poses}
+    for k in kinds:
+        if k not in (SlabPose, CameraPose):
+            raise TypeError(f"unknown pose type {k.__name__}")
+    if len(kinds) != 1:
+        raise TypeError("a batch must hold one pose type")
+    ow, oh = poses[0].width, poses[0].height
+    if any((p.width, p.height) != (ow, oh) for p in poses):
+        raise ValueError("a batch must share one output size")
+    S, T, W, H = hdr.s_count, hdr.t_count, hdr.width, hdr.height
+    geos = geometry if isinstance(geometry, (list, tuple)) and geometry and \
+        isinstance(geometry[0], (PlaneGeometry, type(None))) else [geometry] * n
+    geos = [default_geometry(S, T) if g is None else g for g in geos]
+    bgs = np.asarray(background, dtype=np.uint8).reshape(-1, 3)
+    bgs = np.broadcast_to(bgs, (n, 3)).copy() if bgs.shape[0] == 1 else bgs
+    df = state.device_field(device)
+    dev = df.device
+    L = _native.lib()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    d_geom = torch.from_numpy(np.array([_geom_struct(g) for g in geos],
+                                       dtype=np.float64)).to(dev)
+    d_bg = torch.from_numpy(bgs).to(dev)
+    if out is None:
+        out = torch.empty((n, oh, ow, 3), dtype=torch.uint8, device=dev)
+    if kinds == {SlabPose}:
+        cams = sorted({c for p, g in zip(poses, geos)
+                       for c in _slab_cameras(p, S, T, g)})
+        pose_arr = np.array([(p.s, p.t, float(p.focal_z is not None),
+                              float(p.focal_z or 0.0)) for p in poses],
+                            dtype=np.float64)
+        field, slots = _decode_cameras(state, cams, stop_level, device)
+        d_pose = torch.from_numpy(pose_arr).to(dev)
+        with torch.cuda.device(dev):
+            _native.check(L.rlfc_render_slab(
+                field.data_ptr(), slots.data_ptr(), S, T, W, H,
+                d_pose.data_ptr(), d_geom.data_ptr(), d_bg.data_ptr(), n, ow,
+                oh, out.data_ptr(), stream), "rlfc_render_slab")
+        return out
+    frames = np.stack([_pinhole_basis(p, g) for p, g in zip(poses, geos)])
+    d_frames = torch.from_numpy(np.ascontiguousarray(frames)).to(dev)
+    need = torch.zeros(S * T, dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _native.check(L.rlfc_render_pinhole_needs(
+            S, T, W, H, d_frames.data_ptr(), d_geom.data_ptr(), n, ow, oh,
+            need.data_ptr(), stream), "rlfc_render_pinhole_needs")
+    idx = np.flatnonzero(need.cpu().numpy())
+    cams = [(int(i) // T, int(i) % T) for i in idx]
+    field, slots = _decode_cameras(state, cams, stop_level, device)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _native.check(L.rlfc_render_pinhole(
+            field.data_ptr(), slots.data_ptr(), S, T, W, H,
+            d_frames.data_ptr(), d_geom.data_ptr(), d_bg.data_ptr(), n, ow,
+            oh, out.data_ptr(), status.data_ptr(), stream),
+            "rlfc_render_pinhole")
+    if (status.cpu().numpy() == -2).any():
+        raise ValueError("ray parallel to the light-slab planes")
+    return out
+
+
+def _decode_cameras(state, cams, stop_level, device):
+    import torch
+    hdr = state.header
+    S, T = hdr.s_count, hdr.t_count
+    df = state.device_field(device)
+    slots = np.full(S * T, -1, dtype=np.int32)
+    for i, (s, t) in enumerate(cams):
+        slots[s * T + t] = i
+    if cams:
+        field, _ = decoder.decode_field(state, stop_level, images=cams,
+                                        device=device)
+    else:
+        field = torch.zeros((1, hdr.height, hdr.width, 3), dtype=torch.uint8,
+                            device=df.device)
+    return field, torch.from_numpy(slots).to(df.device)
+
+
+def render_view(state, pose, stop_level=0, geometry: PlaneGeometry = None,
+                background=(0, 0, 0)):
+    """Render one view as uint8 RGB (reference renderer.py:279-305)."""
+    if not isinstance(pose, (SlabPose, CameraPose)):
+        raise TypeError(f"unknown pose type {type(pose).__name__}")
+    return render_views(state, [pose], stop_level, geometry,
+                        background)[0].cpu().numpy()

@@ -1,0 +1,64 @@
+"""The native producer reproduces the reference's synthesis and encoder
+byte for byte (streams in tests/golden/streams were written by the
+reference encoder, tools/make_goldens.py)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLD, load_stream, sha
+
+from paper_1805_06019_b200 import encoder, lightfield
+
+
+def _manifest():
+    with open(os.path.join(GOLD, "encoded_manifest.json")) as f:
+        return json.load(f)
+
+
+def _params(d):
+    d = dict(d)
+    if "filter" in d:
+        d["filter"] = encoder.FilterSpec(kind=d["filter"])
+    return encoder.EncodingParams(**d)
+
+
+def test_synthesis_matches_reference():
+    with open(os.path.join(GOLD, "synth_sha256.json")) as f:
+        want = json.load(f)
+    for key, digest in want.items():
+        dims, seed = key.split("s")
+        S, T, W, H = map(int, dims.split("x"))
+        lf = lightfield.synthesize_lightfield(
+            lightfield.SyntheticSpec(S, T, W, H, int(seed)))
+        assert sha(lf.rgb) == digest, key
+
+
+@pytest.mark.parametrize("name", sorted(_manifest()))
+def test_encoder_matches_reference_bytes(name):
+    m = _manifest()[name]
+    lf = lightfield.synthesize_lightfield(lightfield.SyntheticSpec(**m["spec"]))
+    data, rep = encoder.compress(lf, _params(m["params"]))
+    ref = load_stream(name)
+    assert len(data) == len(ref)
+    assert data == ref
+    if name == "kat8_default":      # reference test_encoder.py:26-34
+        assert len(data) == 194323
+        assert rep.present_blocks == (13036, 6721, 2322)
+
+
+@pytest.mark.skipif(os.environ.get("RLFC_FULL_PRODUCER") != "1",
+                    reason="full-size cfg2 encode (~14 GB RAM); set "
+                           "RLFC_FULL_PRODUCER=1")
+def test_cfg2_r4_full_size_matches_reference():
+    import hashlib
+    with open(os.path.join(GOLD, "cfg2_r4_reference.json")) as f:
+        ref = json.load(f)
+    lf = lightfield.synthesize_lightfield(
+        lightfield.SyntheticSpec(**ref["spec"]))
+    assert sha(lf.rgb) == ref["rgb_sha256"]
+    data, rep = encoder.compress(lf, encoder.EncodingParams(**ref["params"]))
+    assert len(data) == ref["stream_bytes"]
+    assert hashlib.sha256(data).hexdigest() == ref["stream_sha256"]
+    assert list(rep.present_blocks) == ref["present_blocks"]
