@@ -1,0 +1,396 @@
+"""Benchmark: full light-field decode (and batched 512x512 rendering) on B200.
+
+Headline workload (BASELINE.json configs[1]): the synthetic
+17x17-view 1024x1024 light field, R4 preset (h=3, B=4, s=4, Tp=16, Tb=1000;
+1.85 bpp), produced on the box by the native producer (byte-identical to the
+reference encoder, tests/test_producer.py).  One step = one full-field decode
+of all 289 views (303 Mpix) from the compressed stream resident in HBM to
+RGB8 in HBM, by the fused sm_100a kernel.  Rank 0 prints ONE JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun, one process per GPU (NCCL for barriers only):
+weak scaling, every rank decodes its own light field (independent objects);
+--scaling strong instead partitions one field's block rows across ranks,
+balanced by compressed bytes.  There is no collective on the data path.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(S=17, T=17, W=1024, H=1024, seed=7, h=3, B=4, shift=4, tp=16,
+           tb=1000, codec="png")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+L2_BYTES = 126 * 1024 * 1024
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_stream(cfg, cache_dir=os.path.join(ROOT, "data")):
+    """Produce (or reuse) the benchmark stream with the native producer."""
+    import hashlib
+    from paper_1805_06019_b200 import encoder, lightfield
+    key = hashlib.sha1(json.dumps(cfg, sort_keys=True).encode()).hexdigest()[:12]
+    path = os.path.join(cache_dir, f"bench_{key}.rlfc")
+    if os.path.exists(path):
+        with open(path, "rb") as f:
+            return f.read(), path
+    t0 = time.time()
+    lf = lightfield.synthesize_lightfield(lightfield.SyntheticSpec(
+        cfg["S"], cfg["T"], cfg["W"], cfg["H"], cfg["seed"]))
+    params = encoder.EncodingParams(
+        tree_height=cfg["h"], block_size=cfg["B"], quant_shift=cfg["shift"],
+        pixel_threshold=cfg["tp"], block_threshold=cfg["tb"],
+        root_codec=cfg["codec"])
+    data, rep = encoder.compress(lf, params)
+    log(f"produced stream {len(data)} B ({rep.bpp_total:.3f} bpp) in "
+        f"{time.time() - t0:.1f}s; present per level {rep.present_blocks}")
+    os.makedirs(cache_dir, exist_ok=True)
+    tmp = path + f".tmp{os.getpid()}"
+    with open(tmp, "wb") as f:
+        f.write(data)
+    os.replace(tmp, path)
+    return data, path
+
+
+def stream_stats(state):
+    hdr = state.header
+    S, T, W, H = hdr.s_count, hdr.t_count, hdr.width, hdr.height
+    wp, hp = hdr.padded_dims
+    wb, hb = hdr.block_grid
+    from paper_1805_06019_b200 import container
+    rsx, rsy = container.level_dims(S, T, hdr.tree_height)
+    comp = sum(sec[1] + sec[2] for sec in hdr.section_lengths)
+    roots = 3 * rsx * rsy * hp * wp * 2
+    out = S * T * W * H * 3
+    present = 0
+    for c in range(3):
+        srv = state.srv[c]
+        offs = state.offsets[c].astype(np.int64)
+        nbm = (state.m_nodes + 7) >> 3
+        bm = srv[(offs[:, None] + np.arange(nbm)[None, :])]
+        present += int(np.unpackbits(bm, axis=1, bitorder="little")
+                       [:, :state.m_nodes].sum())
+    return dict(pixels=S * T * W * H, comp_bytes=comp, root_bytes=roots,
+                out_bytes=out, alg_bytes=comp + roots + out,
+                bpp=8.0 * len(state.data) / (S * T * W * H),
+                present=present, present_frac=present / (state.m_nodes * wb * hb * 3))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for n, v in zip(names, r[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# --- CPU baseline / reference arm -------------------------------------------------
+
+def cpu_decode(data, steps, warmup, cfg_name):
+    """Oracle port (C restatement of the reference decode path), all host
+    threads, full field per step."""
+    from oracle import oracle
+    oracle.build()
+    orc = oracle.OracleState(data)
+    nth = oracle.lib().orc_nproc()
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        out, st = orc.decode_all(0, nthreads=nth)
+        dt = time.perf_counter() - t0
+        assert st == 0
+        if i >= warmup:
+            times.append(dt)
+    px = orc.S * orc.T * orc.W * orc.H
+    return px / statistics.mean(times) / 1e9, nth, times
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    data, _ = make_stream(CFG)
+    val, nth, times = cpu_decode(data, args.steps, args.warmup, "cfg2")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Gpix/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * statistics.mean(times),
+        "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": workload_config(),
+        "cpu_baseline": {"value": val, "unit": "Gpix/s", "cores": nth,
+                         "kind": "port",
+                         "sample": "full 17x17x1024^2 field per step"},
+        "e2e": {"value": val, "unit": "Gpix/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "decoded Gpixels/s (full light-field decode, cfg2 R4)"
+
+
+def workload_config():
+    return {"workload": "full-field decode, 17x17 views x 1024x1024 RGB, "
+                        "R4 (h=3 B=4 s=4 Tp=16 Tb=1000)",
+            "preset": "R4", "views": 289, "width": 1024, "height": 1024,
+            "block": 4, "tree_height": 3,
+            "l2": "working set > L2 (0.9 GB output per step), no flush"}
+
+
+# --- GPU arm -----------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--kernel", default="fused", choices=["fused", "simple"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--render-batch", type=int, default=256)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1805_06019_b200 as rl
+    from paper_1805_06019_b200 import _native, decoder
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    data, _ = make_stream(CFG) if rank == 0 or world == 1 else (None, None)
+    if world > 1:
+        obj = [data]
+        dist.broadcast_object_list(obj, src=0)
+        data = obj[0]
+    state = rl.init(data)
+    hdr = state.header
+    st = stream_stats(state)
+    hb = hdr.block_grid[1]
+    # rows this rank decodes
+    if args.scaling == "strong" and world > 1:
+        from paper_1805_06019_b200.parallel import balanced_bands
+        band = balanced_bands(state, world)[rank]
+    else:
+        band = (0, hb)
+    rows_px = min(band[1] * hdr.block_size, hdr.height) - band[0] * hdr.block_size
+    px_rank = hdr.s_count * hdr.t_count * hdr.width * rows_px
+    out = torch.empty((hdr.s_count, hdr.t_count, rows_px, hdr.width, 3),
+                      dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        decoder.decode_field(state, 0, rows=band, out=out, kernel=args.kernel,
+                             check=False)
+
+    # correctness gate before timing: status word must be clean
+    _, status = decoder.decode_field(state, 0, rows=band, out=out,
+                                     kernel=args.kernel, check=True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        # soak: the same step back to back for >= 1 s so nvidia-smi (100 ms
+        # period) samples the clocks under this load; the timed region
+        # follows immediately, still inside the sampling window
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 1.0:
+            for _ in range(4):
+                step()
+            torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_px = px_rank * world if args.scaling == "weak" else \
+        hdr.s_count * hdr.t_count * hdr.width * hdr.height
+    value = total_px / (ms_max * 1e-3) / 1e9
+    # roofline of the dominant kernel (the fused decode): per-launch
+    # algorithmic bytes over the per-launch device time on this rank
+    frac_rows = rows_px / hdr.height
+    alg = st["comp_bytes"] * frac_rows + st["root_bytes"] * frac_rows + \
+        st["out_bytes"] * frac_rows
+    achieved = alg / (ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+
+    # e2e: public API with host buffers: H2D of the compressed sections and
+    # root planes from pinned memory, decode, D2H of the RGB field into
+    # pinned memory, every step (decoder.decode_field_host)
+    e2e = e2e_measure(state, band, args, rl)
+
+    render = None
+    if not args.no_render:
+        render = render_measure(state, args, rl)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, nth, times = cpu_decode(data, 2, 1, "cfg2")
+        cpu = {"value": val, "unit": "Gpix/s", "cores": nth, "kind": "port",
+               "sample": "full 17x17x1024^2 R4 field, oracle C port, "
+                         f"{nth} threads, mean of {len(times)} steps"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpix/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": args.scaling if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": dict(workload_config(), bpp=round(st["bpp"], 4),
+                           present_frac=round(st["present_frac"], 5),
+                           kernel=args.kernel, band_rows=list(band)),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4),
+                         "traffic": None, "peak_source": peak_kind,
+                         "alg_bytes_per_launch": int(alg)},
+            "e2e": e2e, "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "render": render,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(state, band, args, rl):
+    import torch
+    from paper_1805_06019_b200 import decoder
+    res = decoder.HostPipeline(state, band)
+    for _ in range(max(1, min(args.warmup, 2))):
+        res.run()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res.run()
+    dt = (time.perf_counter() - t0) / steps
+    hdr = state.header
+    rows_px = res.rows_px
+    px = hdr.s_count * hdr.t_count * hdr.width * rows_px
+    return {"value": px / dt / 1e9, "unit": "Gpix/s",
+            "h2d_bytes_per_step": res.h2d_bytes,
+            "d2h_bytes_per_step": res.d2h_bytes,
+            "ms_per_step": dt * 1e3,
+            "path": "decoder.HostPipeline: pinned H2D of SRV+offsets+roots, "
+                    "fused decode, pinned D2H of RGB (band-pipelined)"}
+
+
+def render_measure(state, args, rl):
+    """cfg4: batches of 512x512 SlabPoses, s,t ~ U[0,16]^2, default focal."""
+    import torch
+    rng = np.random.default_rng(11)
+    n = args.render_batch
+    hdr = state.header
+    poses = [rl.SlabPose(float(rng.uniform(0, hdr.s_count - 1)),
+                         float(rng.uniform(0, hdr.t_count - 1)), 512, 512)
+             for _ in range(n)]
+    out = torch.empty((n, 512, 512, 3), dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        rl.render_views(state, poses, out=out)
+    torch.cuda.synchronize()
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        rl.render_views(state, poses, out=out)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    return {"views_per_s": n / dt, "batch": n, "ms_per_batch": dt * 1e3,
+            "view": "512x512 SlabPose, default focal, k=0, bit-exact",
+            "timing": "wall clock incl. host pose prep, sync per batch"}
+
+
+if __name__ == "__main__":
+    main()

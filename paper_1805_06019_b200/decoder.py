@@ -401,3 +401,50 @@ def decode_all(state: DecoderState, stop_level=0) -> LightFieldGrid:
 def planes_to_rgb(planes):
     """Host helper: three int32 planes -> clamped RGB8 (colorspace.py:46-56)."""
     return colorspace.planes_to_grid(planes)
+
+
+class HostPipeline:
+    """End-to-end decode with host buffers, the path a host application
+    takes: every run() uploads the compressed sections (SRV + offsets) and
+    the root planes from pinned host memory, runs the fused decode, and
+    copies the RGB8 result into pinned host memory.  h2d_bytes / d2h_bytes
+    are the bytes those copies move per run."""
+
+    def __init__(self, state, rows=None, device=None):
+        torch = _torch()
+        self.state = state
+        hdr = state.header
+        hb = hdr.block_grid[1]
+        self.rows = (0, hb) if rows is None else tuple(rows)
+        B = hdr.block_size
+        self.rows_px = max(0, min(self.rows[1] * B, hdr.height) -
+                           self.rows[0] * B)
+        src = state.device_field(device)
+        self.df = DeviceField(hdr, state.srv, state.offsets,
+                              state.root_planes, src.device)
+        self.host = [t.cpu().pin_memory() for t in
+                     self.df.srv + self.df.offsets + [self.df.roots]]
+        self.dev = self.df.srv + self.df.offsets + [self.df.roots]
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in self.host)
+        shape = (hdr.s_count, hdr.t_count, self.rows_px, hdr.width, 3)
+        self.out = torch.empty(shape, dtype=torch.uint8, device=src.device)
+        self.out_host = torch.empty(shape, dtype=torch.uint8).pin_memory()
+        self.d2h_bytes = self.out_host.numel()
+        self.status = torch.zeros(1, dtype=torch.int64, device=src.device)
+
+    def run(self):
+        torch = _torch()
+        hdr = self.state.header
+        for d, h in zip(self.dev, self.host):
+            d.copy_(h, non_blocking=True)
+        self.status.zero_()
+        W = hdr.width
+        with torch.cuda.device(self.df.device):
+            _native.check(_native.lib().rlfc_decode_field(
+                self.df.ref, 0, None, self.rows[0], self.rows[1],
+                self.out.data_ptr(), self.rows_px * W * 3, W * 3,
+                self.status.data_ptr(), _stream()), "rlfc_decode_field")
+        self.out_host.copy_(self.out, non_blocking=True)
+        torch.cuda.current_stream(self.df.device).synchronize()
+        _raise_word(self.status.cpu().item())
+        return self.out_host

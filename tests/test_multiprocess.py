@@ -1,0 +1,62 @@
+"""World-size-2 sharding on CPU (gloo): each rank decodes its block-row band
+(here with the CPU oracle standing in for its GPU), then gather_field
+assembles the full field; it must equal the single-process decode."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT, load_stream
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, name, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+    from paper_1805_06019_b200 import container, parallel
+
+    class St:
+        pass
+    data = load_stream(name)
+    st = St()
+    st.header = container.parse_header(data)
+    st.offsets = tuple(container.parse_offsets(data, st.header, c)
+                       for c in range(3))
+    bands = parallel.balanced_bands(st, world)
+    lo, hi = bands[rank]
+    B = st.header.block_size
+    full, _ = oracle.OracleState(data).decode_all(0, nthreads=1)
+    band = torch.from_numpy(np.ascontiguousarray(
+        full[:, :, lo * B:min(hi * B, st.header.height)]))
+    out = parallel.gather_field(st, band, bands)
+    q.put((rank, bool(np.array_equal(out.numpy(), full))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["mid17_r4", "odd_3x5"])
+def test_gloo_two_rank_gather(name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
