@@ -59,6 +59,13 @@ typedef struct rlfc_field {
     int32_t wp, hp, wb, hb, rsx, rsy;
     int32_t roots_i16; /* 1: roots are int16, 0: int32 */
     int32_t bitmap_bytes;
+    /* Largest compressed size (bytes, all three channels, +32 alignment
+     * slack per channel) of any run of TW/block consecutive records inside
+     * one block row, TW = 32 pixels (16 for block 16) -- the shared-memory
+     * staging need of the fused decode's tiles (host-computed from the
+     * offset arrays at init; 0 = unknown). */
+    int32_t tile_bytes_max;
+    int32_t _reserved;
     /* BFS geometry (container.py:102-145): level l (0..h-1) holds
      * level_sx[l] x level_sy[l] nodes starting at serial index level_base[l]. */
     int32_t level_base[RLFC_MAX_LEVELS];

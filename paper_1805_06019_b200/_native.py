@@ -28,7 +28,7 @@ class RlfcField(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "s_count", "t_count", "width", "height", "block", "tree_height",
         "quant_shift", "m_nodes", "wp", "hp", "wb", "hb", "rsx", "rsy",
-        "roots_i16", "bitmap_bytes")] + [
+        "roots_i16", "bitmap_bytes", "tile_bytes_max", "_reserved")] + [
         ("level_base", ctypes.c_int32 * MAX_LEVELS),
         ("level_sx", ctypes.c_int32 * MAX_LEVELS),
         ("level_sy", ctypes.c_int32 * MAX_LEVELS),

@@ -18,17 +18,32 @@ constexpr int MODE_QUINT = 2;
 constexpr int NUM_DESC = 30;   // bise.py:22-25
 
 // bise.py:22-60 RANGE_TABLE factored into (mode, low bits) per descriptor
-// (TABLE_MODE / TABLE_BITS, bise.py:59-60).
-__host__ __device__ constexpr int desc_mode(int d) {
-    constexpr int8_t M[30] = {0, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0,
-                              2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0};
-    return M[d];
-}
+// (TABLE_MODE / TABLE_BITS, bise.py:59-60), packed into 64-bit immediates so
+// a lookup is a shift + mask in registers (no memory table).
+constexpr uint64_t MODE_PACK = []() constexpr {
+    uint64_t v = 0;
+    const int m[30] = {0, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0,
+                       2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0, 2, 1, 0};
+    for (int d = 0; d < 30; ++d) v |= (uint64_t)m[d] << (2 * d);
+    return v;
+}();
+constexpr uint64_t BITS_LO = []() constexpr {   // descriptors 0..15
+    const int b[16] = {1, 0, 2, 0, 1, 3, 1, 2, 4, 2, 3, 5, 3, 4, 6, 4};
+    uint64_t v = 0;
+    for (int d = 0; d < 16; ++d) v |= (uint64_t)b[d] << (4 * d);
+    return v;
+}();
+constexpr uint64_t BITS_HI = []() constexpr {   // descriptors 16..29
+    const int b[14] = {5, 7, 5, 6, 8, 6, 7, 9, 7, 8, 10, 8, 9, 11};
+    uint64_t v = 0;
+    for (int d = 0; d < 14; ++d) v |= (uint64_t)b[d] << (4 * d);
+    return v;
+}();
+__host__ __device__ constexpr int desc_mode(int d) { return (int)((MODE_PACK >> (2 * d)) & 3u); }
 __host__ __device__ constexpr int desc_bits(int d) {
-    constexpr int8_t Bt[30] = {1, 0, 2, 0, 1, 3, 1, 2, 4, 2, 3, 5, 3, 4, 6,
-                               4, 5, 7, 5, 6, 8, 6, 7, 9, 7, 8, 10, 8, 9, 11};
-    return Bt[d];
+    return d < 16 ? (int)((BITS_LO >> (4 * d)) & 15u) : (int)((BITS_HI >> (4 * (d - 16))) & 15u);
 }
+static_assert(desc_mode(3) == 2 && desc_bits(29) == 11 && desc_bits(17) == 7 && desc_bits(15) == 4, "table");
 
 // kernels.py:63-70 payload_bits
 __host__ __device__ constexpr int payload_bits(int mode, int bits, int count) {

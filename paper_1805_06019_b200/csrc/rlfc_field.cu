@@ -1,37 +1,48 @@
-// rlfc_field.cu -- fused, tiled full-field decode for sm_100a.
+// rlfc_field.cu -- fused, tiled, software-pipelined full-field decode (sm_100a).
 //
 // One CTA owns one TILE: a block row `by` x NB consecutive block columns
 // (TW = NB*B pixels wide), for ALL S*T views and all three channels.  The
 // reference decodes view by view and re-walks every record once per view
-// (kernels.py:219-242: S*T walks of each record); here every record of the
-// tile is walked exactly once per launch and every present payload is
-// decoded exactly once, and the per-view work is a few integer adds.
+// (kernels.py:219-242 calls decode_chain_core per block per view); here each
+// record of the tile is walked once per launch, each present payload is
+// BISE-decoded once, and the per-view work is register adds + the colour
+// transform.
 //
-// Per CTA:
-//   1. stage the tile's records (three contiguous byte ranges, one per
-//      channel -- container.py:306-323) into shared memory with 16-byte
-//      vector loads;
-//   2. one thread per record pre-walks the descriptors of levels h-1..k+1 to
-//      find where each tree level starts inside the record;
-//   3. for every camera row t (and chunk of CH views along s):
-//        walk   - one thread per record walks the level rows / level-0 chunk
-//                 that row t needs (cursor per level, monotone), emitting a
-//                 work item per present node (kernels.py:181-215);
-//        decode - all threads BISE-decode the emitted payloads, four values
-//                 per item, closed-form bit offsets, digit LUTs in smem, and
-//                 store the dequantised residuals into per-node smem slots
-//                 (kernels.py:128-159, 202-211);
-//        blend  - a thread owns one 4-pixel quad of the tile and a pair of
-//                 neighbouring views; it keeps root + levels >= 1 as a
-//                 register partial sum (shared by the pair), adds the
-//                 level-0 residual, applies the YCoCg-R inverse + clamp
-//                 (colorspace.py:27-56) and writes RGB8 into a staging
-//                 buffer; the staged rows go out as 16-byte stores.
-//   Tiles whose records do not fit the staging budget, or any tile that saw
-//   a stream anomaly, fall back to the reference-order per-block walk
-//   (walk_chain) so values and error precedence stay exact.
+// Setup: the tile's records (three contiguous byte ranges, one per channel;
+// container.py:306-323) and its root-plane rows are staged into shared memory
+// with 16-byte loads, and one thread per record pre-walks the descriptors of
+// levels h-1..k+1 to find where each tree level starts inside its record.
+//
+// Pipeline, iteration i = 0..T (two CTA barriers per camera row):
+//   phase A   walk(i+1)   one thread per record walks the level-0 row i+1 and
+//                         any level row that starts at i+1 (one monotone
+//                         cursor per level), emitting a work item per present
+//                         node into ring E[(i+1)&1]: plain-bit payloads from
+//                         the front, trit/quint payloads from the back
+//                         (kernels.py:181-215);
+//             decode(i)   all threads BISE-decode ring E[i&1], four values per
+//                         item with straight-line code per mode, closed-form
+//                         bit offsets, digit LUTs in smem, dequantised into the
+//                         residual slots of row i (kernels.py:128-159,
+//                         202-211); level-0 slots are int32 so the per-view
+//                         loop never unpacks;
+//   --- barrier ---
+//   phase B   blend(i)    (pixel quad, view pair) items: root + levels >= 1 is
+//                         a register partial sum shared by the pair, the
+//                         level-0 residual is added per view, YCoCg-R inverse
+//                         + clamp + pack (colorspace.py:27-56) go to
+//                         staging[i&1];
+//             store(i-1)  one thread issues ONE 4-D TMA tensor store of the
+//                         whole staged row i-1 (all S views x B pixel rows x
+//                         TW*3 bytes) straight to HBM, overlapping the blend.
+//   --- barrier ---
+// Tiles whose records exceed the staging budget, and tiles that saw any stream
+// anomaly, run the reference-order per-block walk (walk_chain) so values and
+// error precedence are exactly the reference's.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstring>
 
 #include "rlfc_common.cuh"
 #include "rlfc_field.cuh"
@@ -40,10 +51,8 @@ namespace rlfc {
 
 namespace tiled {
 
-constexpr int THREADS = 256;
-constexpr int CH = 8;          // level-0 views decoded per chunk
 constexpr int MAXH = 8;        // tree levels handled by the tiled kernel
-constexpr int MAXROW = 32;     // max nodes in one level row (S <= 64)
+constexpr int MAXS = 64;       // camera columns handled by the tiled kernel
 
 struct Params {
     rlfc_field f;
@@ -54,46 +63,96 @@ struct Params {
     int64_t img_stride, row_stride;
     uint64_t* status;
     int tiles_x;
-    // smem carve (byte offsets)
-    int off_nbt, off_rec, off_cur, off_err, off_mask, off_ent, off_root, off_res, off_stage, off_bytes;
-    int bytes_cap, ent_cap, n_slots;
-    int slot_base[MAXH];
-    int vec_store;             // 1: 16-byte aligned output rows
+    int off_nbt, off_cur, off_err, off_cnt, off_mask, off_ent, off_root, off_rgb, off_list, off_res0, off_resl,
+        off_stage, off_bytes;
+    int bytes_cap, ent_cap;
+    int slot_base[MAXH];       // level l >= 1: first slot of its row in resl
+    int store_mode;            // 2: one 4-D TMA tensor store per row, 1: per-row
+                               // cp.async.bulk, 0: byte stores (unaligned rows)
+    int roots_all;             // 1: every root of the tile is staged at setup
+    int roots_vec;             // 1: root rows are 16-byte aligned in HBM
 };
 
-// One emitted decode job: payload byte offset in the staged tile, descriptor,
-// channel, destination slot and block.
 struct Entry {
-    uint32_t off;
-    uint32_t meta;   // desc | c << 5 | blk << 7 | slot << 16
+    uint32_t off;              // payload byte offset inside the staged tile
+    uint32_t meta;             // desc | c << 5 | blk << 7 | slot << 16
 };
 
-__device__ __forceinline__ uint32_t smem_bits32(const uint8_t* base, uint32_t bitpos) {
-    const uint32_t a = bitpos >> 3;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(base + (a & ~3u));
-    const uint32_t sh = ((a & 3u) << 3) + (bitpos & 7u);
-    return __funnelshift_r(w[0], w[1], sh);
+// 32 bits at bit position `bitpos` of the 16-byte aligned staging buffer.
+__device__ __forceinline__ uint32_t sbits(const uint32_t* w, uint32_t bitpos) {
+    const uint32_t i = bitpos >> 5;
+    return __funnelshift_r(w[i], w[i + 1], bitpos & 31u);
 }
 
-template <int B, int TW, typename VT>
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Clamp four int32 to [0, 255] and pack them little-endian into one word
+// (cvt.pack.sat: saturating convert + pack, two instructions).
+__device__ __forceinline__ uint32_t pack4_sat(int32_t b0, int32_t b1, int32_t b2, int32_t b3) {
+    uint32_t hi, d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(hi) : "r"(b3), "r"(b2), "r"(0));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(b1), "r"(b0), "r"(hi));
+    return d;
+}
+
+// kernels.py:202-211 dequantisation in 32-bit wrap arithmetic: identical to
+// the reference's int64 result truncated into its int32 accumulator.
+__device__ __forceinline__ int32_t deq(uint32_t z, int shift) {
+    if (shift >= 32) return dequant(z, shift);
+    const uint32_t mag = (((z + 1u) >> 1) << shift) + ((1u << shift) >> 1);
+    const uint32_t v = (z & 1u) ? 0u - mag : mag;
+    return z ? (int32_t)v : 0;
+}
+
+template <int B, int TW>
 struct Cfg {
     static constexpr int NB = TW / B;           // blocks per tile
     static constexpr int NREC = 3 * NB;         // records per tile
     static constexpr int BSQ = B * B;
-    static constexpr int QPB = BSQ / 4;         // quads per block
-    static constexpr int QPR = TW / 4;          // quads per tile row
-    static constexpr int QUADS = QPR * B;       // quads per tile
-    static constexpr int GROUPS = THREADS / QUADS;
-    static constexpr int SLOT_VALS = 3 * NB * BSQ;
-    static_assert(QUADS <= THREADS && THREADS % QUADS == 0, "tile shape");
+    static constexpr int QPB = BSQ / 4;         // value quads per block
+    static constexpr int QPR = TW / 4;          // pixel quads per tile row
+    static constexpr int QUADS = QPR * B;       // pixel quads per tile
+    static constexpr int MAX_THREADS = 256;
+    static_assert(NREC <= 32, "walkers live in one warp");
 };
 
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, int32_t* v);
+template <>
+__device__ __forceinline__ void load4<int16_t>(const int16_t* p, int32_t* v) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+    v[0] = (int32_t)(int16_t)(w.x & 0xFFFFu);
+    v[1] = (int32_t)w.x >> 16;
+    v[2] = (int32_t)(int16_t)(w.y & 0xFFFFu);
+    v[3] = (int32_t)w.y >> 16;
+}
+template <>
+__device__ __forceinline__ void load4<int32_t>(const int32_t* p, int32_t* v) {
+    const int4 w = *reinterpret_cast<const int4*>(p);
+    v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+}
+template <typename T>
+__device__ __forceinline__ void store4(T* p, const int32_t* v);
+template <>
+__device__ __forceinline__ void store4<int16_t>(int16_t* p, const int32_t* v) {
+    uint2 w;
+    w.x = ((uint32_t)v[0] & 0xFFFFu) | ((uint32_t)v[1] << 16);
+    w.y = ((uint32_t)v[2] & 0xFFFFu) | ((uint32_t)v[3] << 16);
+    *reinterpret_cast<uint2*>(p) = w;
+}
+template <>
+__device__ __forceinline__ void store4<int32_t>(int32_t* p, const int32_t* v) {
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
+}
+
 // Reference-order fallback for one tile: one thread per (view, block), three
-// chains walked from global memory exactly as kernels.py:162-216.  Also
-// reports the exact failure key when any anomaly was seen.
+// chains walked from global memory exactly as kernels.py:162-216; writes the
+// values and reports the exact failure key.
 template <int B>
 __device__ __noinline__ void tile_fallback(const Params& P, int by, int bx0, int nb, const DigitLut& lut,
-                              const NodeBytes& nb_tab) {
+                                           const NodeBytes& nb_tab) {
     const rlfc_field& f = P.f;
     const int nimg = f.s_count * f.t_count;
     for (int job = threadIdx.x; job < nimg * nb; job += blockDim.x) {
@@ -133,70 +192,41 @@ __device__ __noinline__ void tile_fallback(const Params& P, int by, int bx0, int
     }
 }
 
-// Decode values 4j..4j+3 of one payload staged in smem into the slot.
-template <int BSQ, typename VT>
-__device__ __forceinline__ bool decode_quad(const uint8_t* bytes, uint32_t off, int desc, int j, int shift,
-                                            const DigitLut& lut, VT* dst) {
-    const int mode = desc_mode(desc), b = desc_bits(desc);
-    const uint32_t base = off << 3;
-    bool ok = true;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int k = 4 * j + i;
-        uint32_t z;
-        if (mode == MODE_BITS) {
-            z = smem_bits32(bytes, base + (uint32_t)(k * b)) & ((1u << b) - 1u);
-        } else if (mode == MODE_TRIT) {
-            const int g = k / 5, ii = k - 5 * g;
-            const uint32_t gp = base + (uint32_t)(g * (8 + 5 * b));
-            const uint32_t pack = smem_bits32(bytes, gp) & 0xFFu;
-            ok &= pack <= 242u;
-            const uint32_t digit = (lut.trit[pack < 243u ? pack : 0] >> (2 * ii)) & 3u;
-            const uint32_t low = smem_bits32(bytes, gp + 8 + ii * b) & ((1u << b) - 1u);
-            z = (digit << b) | low;
-        } else {
-            const int g = k / 3, ii = k - 3 * g;
-            const uint32_t gp = base + (uint32_t)(g * (7 + 3 * b));
-            const uint32_t pack = smem_bits32(bytes, gp) & 0x7Fu;
-            ok &= pack <= 124u;
-            const uint32_t digit = (lut.quint[pack < 125u ? pack : 0] >> (3 * ii)) & 7u;
-            const uint32_t low = smem_bits32(bytes, gp + 7 + ii * b) & ((1u << b) - 1u);
-            z = (digit << b) | low;
-        }
-        dst[i] = (VT)dequant(z, shift);
-    }
-    return ok;
-}
-
 template <int B, int TW, typename VT, typename RT>
-__global__ void __launch_bounds__(THREADS, 2) k_decode_field_tiled(const Params P) {
-    using C = Cfg<B, TW, VT>;
-    extern __shared__ __align__(16) uint8_t smem[];
+__global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
+    k_decode_field_tiled(const Params P, const __grid_constant__ CUtensorMap out_map) {
+    using C = Cfg<B, TW>;
+    extern __shared__ __align__(128) uint8_t smem[];
     const rlfc_field& f = P.f;
     const int tid = threadIdx.x;
+    const int THREADS = blockDim.x;
     const int by = P.by_lo + blockIdx.x / P.tiles_x;
-    const int tx = blockIdx.x % P.tiles_x;
-    const int bx0 = tx * C::NB;
+    const int bx0 = (blockIdx.x % P.tiles_x) * C::NB;
     const int nb = min(C::NB, f.wb - bx0);
     const int k = P.stop_level, h = f.tree_height;
     const int S = f.s_count, T = f.t_count;
-    const int lmin = k > 0 ? k : 1;              // lowest level held as a full row
+    const int lmin = k > 0 ? k : 1;              // levels >= lmin are held as full rows
+    const int plane = 3 * B * TW;                // values per slot / root ([3][B][TW])
 
     DigitLut& lut = *reinterpret_cast<DigitLut*>(smem);
     NodeBytes& nbt = *reinterpret_cast<NodeBytes*>(smem + P.off_nbt);
-    uint32_t* rec_beg = reinterpret_cast<uint32_t*>(smem + P.off_rec);
     uint32_t* cur = reinterpret_cast<uint32_t*>(smem + P.off_cur);   // [NREC][MAXH]
-    int32_t* err = reinterpret_cast<int32_t*>(smem + P.off_err);     // [NREC + 2]
-    uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask); // [MAXH][NREC]
-    Entry* ent = reinterpret_cast<Entry*>(smem + P.off_ent);
-    RT* roots = reinterpret_cast<RT*>(smem + P.off_root);            // [rsx][3][B][TW]
-    VT* res = reinterpret_cast<VT*>(smem + P.off_res);               // [slot][3][B][TW]
-    uint8_t* stage = smem + P.off_stage;                             // [CH][B][TW*3]
+    int32_t* err = reinterpret_cast<int32_t*>(smem + P.off_err);     // [NREC]
+    // cnt[0..1]: plain-bit entries of ring 0/1 (front), cnt[2..3]: trit/quint
+    // entries (back), cnt[4]: anomaly flag, cnt[5]/[6]: dirty / clean items
+    int32_t* cnt = reinterpret_cast<int32_t*>(smem + P.off_cnt);
+    uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask); // [2 ring][MAXH][NREC][2]
+    Entry* ent = reinterpret_cast<Entry*>(smem + P.off_ent);         // [2 ring][ent_cap]
+    RT* roots = reinterpret_cast<RT*>(smem + P.off_root);            // [root][3][B][TW]
+    uint32_t* root_rgb = reinterpret_cast<uint32_t*>(smem + P.off_rgb); // [rx][B][TW*3/4] packed RGB8
+    uint2* lists = reinterpret_cast<uint2*>(smem + P.off_list);      // [S*NB]: dirty from 0, clean from the end
+    int32_t* res0 = reinterpret_cast<int32_t*>(smem + P.off_res0);   // [s][3][B][TW]
+    VT* resl = reinterpret_cast<VT*>(smem + P.off_resl);             // [slot][3][B][TW]
+    uint8_t* stage = smem + P.off_stage;                             // [S][B][TW*3]
     uint8_t* bytes = smem + P.off_bytes;
-    int32_t& n_ent = err[C::NREC];
-    int32_t& any_err = err[C::NREC + 1];
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(bytes);
 
-    // ---- digit LUTs --------------------------------------------------------
+    // ---- tables -------------------------------------------------------------
     {
         uint16_t* l16 = reinterpret_cast<uint16_t*>(smem);
         for (int i = tid; i < 243 + 125; i += THREADS) {
@@ -212,26 +242,25 @@ __global__ void __launch_bounds__(THREADS, 2) k_decode_field_tiled(const Params 
         }
         constexpr NodeBytes NBT = make_node_bytes<B * B>();
         if (tid < 32) nbt.v[tid] = NBT.v[tid];
+        if (tid < 8) cnt[tid] = 0;
     }
-    // ---- stage the tile's records (three contiguous ranges) ----------------
-    uint64_t beg[3], end[3], abeg[3];
+    // ---- the tile's record bytes --------------------------------------------
+    uint64_t abeg[3], aend[3];
     uint32_t sbase[3];
     uint32_t total = 0;
     const bool need_srv = k < h;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int64_t blk0 = (int64_t)by * f.wb + bx0;
-        beg[c] = f.offsets[c][blk0];
-        end[c] = (bx0 + nb < f.wb) ? f.offsets[c][blk0 + nb]
-                                   : ((by + 1 < f.hb) ? f.offsets[c][blk0 + nb] : f.srv_len[c]);
-        abeg[c] = beg[c] & ~uint64_t(15);
-        const uint64_t aend = (end[c] + 15) & ~uint64_t(15);
+        const uint64_t beg = f.offsets[c][blk0];
+        const uint64_t end = (blk0 + nb < (int64_t)f.wb * f.hb) ? f.offsets[c][blk0 + nb] : f.srv_len[c];
+        abeg[c] = beg & ~uint64_t(15);
+        aend[c] = (end + 15) & ~uint64_t(15);
         sbase[c] = total;
-        total += need_srv ? (uint32_t)(aend - abeg[c]) : 0u;
+        total += need_srv ? (uint32_t)(aend[c] - abeg[c]) : 0u;
     }
-    const bool fits = total + 16 <= (uint32_t)P.bytes_cap;
     __syncthreads();
-    if (!fits) {
+    if (total + 16 > (uint32_t)P.bytes_cap) {      // does not fit: reference-order walk
         tile_fallback<B>(P, by, bx0, nb, lut, nbt);
         return;
     }
@@ -240,246 +269,426 @@ __global__ void __launch_bounds__(THREADS, 2) k_decode_field_tiled(const Params 
         for (int c = 0; c < 3; ++c) {
             const uint4* src = reinterpret_cast<const uint4*>(f.srv[c] + abeg[c]);
             uint4* dst = reinterpret_cast<uint4*>(bytes + sbase[c]);
-            const uint32_t n16 = (uint32_t)((((end[c] + 15) & ~uint64_t(15)) - abeg[c]) >> 4);
+            const uint32_t n16 = (uint32_t)((aend[c] - abeg[c]) >> 4);
             for (uint32_t i = tid; i < n16; i += THREADS) dst[i] = __ldg(src + i);
         }
     }
-    if (tid < C::NREC) {
-        const int c = tid / C::NB, b = tid % C::NB;
-        uint32_t rb = 0;
-        if (b < nb) rb = sbase[c] + (uint32_t)(f.offsets[c][(int64_t)by * f.wb + bx0 + b] - abeg[c]);
-        rec_beg[tid] = rb;
-        err[tid] = 0;
+    // root rows of the tile: [root (rx*rsy + ry)][c][row][TW]; all of them at
+    // setup when they fit, else one root row (ry) at a time in decode()
+    const bool full_tile = (bx0 + C::NB) * B <= f.wp;
+    auto load_roots = [&](int ry0, int nry, RT* dst) {
+        const int64_t pl = (int64_t)f.hp * f.wp;
+        const int segs = nry * f.rsx * 3 * B;            // (ry, rx, c, row) segments of TW values
+        if (P.roots_vec && full_tile) {
+            constexpr int V = TW * (int)sizeof(RT) / 16;   // uint4 per segment
+            for (int i = tid; i < segs * V; i += THREADS) {
+                const int v = i % V, sg = i / V;
+                const int rr = sg % B, c = (sg / B) % 3, rx = (sg / (3 * B)) % f.rsx, ry = ry0 + sg / (3 * B * f.rsx);
+                const RT* src = reinterpret_cast<const RT*>(f.roots) +
+                                (((int64_t)rx * f.rsy + ry) * 3 + c) * pl + (int64_t)(by * B + rr) * f.wp + bx0 * B;
+                const int droot = P.roots_all ? rx * f.rsy + ry : rx;
+                reinterpret_cast<uint4*>(dst + ((droot * 3 + c) * B + rr) * TW)[v] =
+                    __ldg(reinterpret_cast<const uint4*>(src) + v);
+            }
+        } else {
+            for (int i = tid; i < segs * TW; i += THREADS) {
+                const int x = i % TW, sg = i / TW;
+                const int rr = sg % B, c = (sg / B) % 3, rx = (sg / (3 * B)) % f.rsx, ry = ry0 + sg / (3 * B * f.rsx);
+                const int gx = bx0 * B + x;
+                RT v = 0;
+                if (gx < f.wp)
+                    v = reinterpret_cast<const RT*>(f.roots)[(((int64_t)rx * f.rsy + ry) * 3 + c) * pl +
+                                                             (int64_t)(by * B + rr) * f.wp + gx];
+                const int droot = P.roots_all ? rx * f.rsy + ry : rx;
+                dst[((droot * 3 + c) * B + rr) * TW + x] = v;
+            }
+        }
+    };
+    if (P.roots_all) load_roots(0, f.rsy, roots);
+    // walkers: one thread per (channel, block) record, in the LAST warp
+    const int wid = tid - (THREADS - 32);
+    const bool walker = wid >= 0 && wid < C::NREC && (wid % C::NB) < nb && need_srv;
+    const int wc = walker ? wid / C::NB : 0, wblk = walker ? wid % C::NB : 0;
+    uint32_t my_beg = 0, my_len = 0;
+    if (walker) {
+        const int64_t blk = (int64_t)by * f.wb + bx0 + wblk;
+        const uint64_t rb = f.offsets[wc][blk];
+        const uint64_t re = (blk + 1 < (int64_t)f.wb * f.hb) ? f.offsets[wc][blk + 1] : f.srv_len[wc];
+        my_beg = sbase[wc] + (uint32_t)(rb - abeg[wc]);
+        my_len = (uint32_t)(re - rb);
     }
-    if (tid == 0) { n_ent = 0; any_err = 0; }
+    if (tid < C::NREC) err[tid] = 0;
     __syncthreads();
 
-    // ---- pre-walk: where does each level start inside each record ----------
-    if (tid < C::NREC && (tid % C::NB) < nb && need_srv) {
-        const uint8_t* rec = bytes + rec_beg[tid];
-        const uint32_t rbit = rec_beg[tid] << 3;
+    // ---- pre-walk: start of each level inside each record -------------------
+    uint32_t* mycur = cur + (walker ? wid : 0) * MAXH;
+    if (walker) {
+        const uint8_t* rec = bytes + my_beg;
+        const uint32_t rbit = my_beg << 3;
         uint32_t cu = (uint32_t)f.bitmap_bytes;
-        uint32_t* mycur = cur + tid * MAXH;
+        bool bad = cu > my_len;
         mycur[h - 1] = cu;
-        bool bad = false;
         for (int l = h - 1; l > k && !bad; --l) {
             const int n0 = f.level_base[l], n1 = n0 + f.level_sx[l] * f.level_sy[l];
             for (int w = n0; w < n1 && !bad; w += 32) {
-                uint32_t bits = smem_bits32(bytes, rbit + (uint32_t)w);
+                uint32_t bits = sbits(words, rbit + (uint32_t)w);
                 if (n1 - w < 32) bits &= (1u << (n1 - w)) - 1u;
                 while (bits) {
                     bits &= bits - 1u;
-                    const int d = rec[cu];
-                    if (d >= NUM_DESC) { bad = true; break; }
+                    const int d = cu < my_len ? rec[cu] : NUM_DESC;
+                    if (d >= NUM_DESC || cu + nbt.v[d] > my_len) { bad = true; break; }
                     cu += nbt.v[d];
                 }
             }
             mycur[l - 1] = cu;
         }
-        if (bad) { err[tid] = 1; any_err = 1; }
+        if (bad) { err[wid] = 1; cnt[4] = 1; }
     }
-    __syncthreads();
 
-    // thread roles for the blend: quad q (row yy, quad column xq) and group g
-    const int q = tid % C::QUADS, g = tid / C::QUADS;
-    const int yy = q / C::QPR, xq = q % C::QPR;
-    const int blk = (xq * 4) / B;
-    const bool qactive = blk < nb;
-    const int rsx = f.rsx;
-
-    for (int t = 0; t < T; ++t) {
-        // root row for this camera row
-        if ((t & ((1 << h) - 1)) == 0) {
-            const int ry = t >> h;
-            const int nval = rsx * 3 * B * TW;
-            const int64_t plane = (int64_t)f.hp * f.wp;
-            for (int i = tid; i < nval; i += THREADS) {
-                const int x = i % TW, rr = (i / TW) % B, c = (i / (TW * B)) % 3, rx = i / (TW * B * 3);
-                const int gx = bx0 * B + x;
-                RT v = 0;
-                if (gx < f.wp) {
-                    const int64_t idx = (((int64_t)rx * f.rsy + ry) * 3 + c) * plane +
-                                        (int64_t)(by * B + rr) * f.wp + gx;
-                    v = reinterpret_cast<const RT*>(f.roots)[idx];
+    // walk(t): level rows that start at t and the level-0 row t -> ring t&1.
+    // Level-l masks live in ring ((t >> l) & 1): a row's mask stays valid for
+    // all 2^l camera rows that use it.  Plain-bit payloads fill the ring from
+    // the front, trit/quint payloads from the back.
+    auto walk = [&](int t) {
+        if (!walker || err[wid]) return;
+        const uint8_t* rec = bytes + my_beg;
+        const uint32_t rbit = my_beg << 3;
+        Entry* E = ent + (t & 1) * P.ent_cap;
+        bool bad = false;
+        for (int l = h - 1; l >= k && !bad; --l) {
+            const bool row_level = l >= lmin;
+            if (row_level && (t & ((1 << l) - 1)) != 0) continue;
+            const int sx = f.level_sx[l];
+            const int n0 = f.level_base[l] + (t >> l) * sx;
+            const int sb = row_level ? P.slot_base[l] : 0;
+            const uint32_t lvl0 = row_level ? 0u : 1u;
+            uint32_t cu = mycur[l];
+            uint32_t mw[2] = {0u, 0u};
+            for (int w = 0; w < sx && !bad; w += 32) {
+                uint32_t bits = sbits(words, rbit + (uint32_t)(n0 + w));
+                if (sx - w < 32) bits &= (1u << (sx - w)) - 1u;
+                mw[w >> 5] = bits;
+                while (bits) {
+                    const int x = w + __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    const int d = cu < my_len ? rec[cu] : NUM_DESC;
+                    if (d >= NUM_DESC || cu + nbt.v[d] > my_len) { bad = true; break; }
+                    Entry en;
+                    en.off = my_beg + cu + 1;
+                    en.meta = (uint32_t)d | (uint32_t)wc << 5 | (uint32_t)wblk << 7 | lvl0 << 15 |
+                              (uint32_t)(sb + x) << 16;
+                    if (desc_mode(d) == MODE_BITS) E[atomicAdd(&cnt[t & 1], 1)] = en;
+                    else E[P.ent_cap - 1 - atomicAdd(&cnt[2 + (t & 1)], 1)] = en;
+                    cu += nbt.v[d];
                 }
-                roots[i] = v;
             }
+            mycur[l] = cu;
+            uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2 + wid * 2;
+            M[0] = mw[0];
+            M[1] = mw[1];
         }
-        for (int s0 = 0; s0 < S; s0 += CH) {
-            // skip chunks with no requested view
-            bool want = false;
-            for (int s = s0; s < min(S, s0 + CH); ++s) {
-                const int img = s * T + t;
-                if (!P.slots || P.slots[img] >= 0) want = true;
-            }
-            const bool rows_due = (s0 == 0);
-            // ---- walk ----------------------------------------------------------
-            if (tid < C::NREC && (tid % C::NB) < nb && need_srv && !err[tid]) {
-                const uint8_t* rec = bytes + rec_beg[tid];
-                const uint32_t rbit = rec_beg[tid] << 3;
-                uint32_t* mycur = cur + tid * MAXH;
-                const int c = tid / C::NB, b = tid % C::NB;
-                bool bad = false;
-                const int lfirst = rows_due ? h - 1 : 0;
-                for (int l = lfirst; l >= 0 && !bad; --l) {
-                    if (l < k) break;
-                    int x0, cnt, slot0;
-                    if (l >= lmin) {
-                        if (!rows_due || (t & ((1 << l) - 1)) != 0) continue;
-                        x0 = 0;
-                        cnt = f.level_sx[l];
-                        slot0 = P.slot_base[l];
-                    } else {  // level 0 chunk
-                        x0 = s0;
-                        cnt = min(CH, S - s0);
-                        slot0 = 0;
-                    }
-                    const int n0 = f.level_base[l] + (t >> l) * f.level_sx[l] + x0;
-                    uint32_t bits = smem_bits32(bytes, rbit + (uint32_t)n0);
-                    if (cnt < 32) bits &= (1u << cnt) - 1u;
-                    const bool emit = (l >= lmin) || want;
-                    uint32_t cu = mycur[l];
-                    uint32_t mbits = bits;
-                    while (bits) {
-                        const int x = __ffs(bits) - 1;
-                        bits &= bits - 1u;
-                        const int d = rec[cu];
-                        if (d >= NUM_DESC) { bad = true; break; }
-                        if (emit) {
-                            const int e = atomicAdd(&n_ent, 1);
-                            if (e < P.ent_cap) {
-                                Entry en;
-                                en.off = rec_beg[tid] + cu + 1;
-                                en.meta = (uint32_t)d | (uint32_t)c << 5 | (uint32_t)b << 7 |
-                                          (uint32_t)(slot0 + x) << 16;
-                                ent[e] = en;
-                            } else {
-                                bad = true;  // cannot happen with a host-sized ent_cap
-                            }
-                        }
-                        cu += nbt.v[d];
-                    }
-                    mycur[l] = cu;
-                    mask[l * C::NREC + tid] = mbits;
-                }
-                if (bad) { err[tid] = 1; any_err = 1; }
-            }
-            __syncthreads();
-            // ---- decode --------------------------------------------------------
-            const int ne = min(n_ent, P.ent_cap);
-            for (int it = tid; it < ne * C::QPB; it += THREADS) {
+        if (bad) { err[wid] = 1; cnt[4] = 1; }
+    };
+
+    // decode(t): ring t&1 -> residual slots (+ the root row when it starts).
+    // One item = 4 consecutive values of one payload (one pixel-row quad of
+    // its block).
+    const int shift = f.quant_shift;
+    auto put = [&](uint32_t meta, int j, const int32_t* v) {
+        const int c = (meta >> 5) & 3, b = (meta >> 7) & 255, slot = meta >> 16;
+        const int row = (4 * j) / B, col = (4 * j) % B;
+        const int o = (c * B + row) * TW + b * B + col;
+        if (meta & (1u << 15)) store4<int32_t>(res0 + slot * plane + o, v);
+        else store4<VT>(resl + slot * plane + o, v);
+    };
+    auto decode = [&](int t) {
+        const int nf = cnt[t & 1], nbk = cnt[2 + (t & 1)];
+        const Entry* E = ent + (t & 1) * P.ent_cap;
+        const int items_f = nf * C::QPB, items = items_f + nbk * C::QPB;
+        for (int it = tid; it < items; it += THREADS) {
+            int32_t v[4];
+            if (it < items_f) {
+                // plain b-bit fields: the quad's 4b <= 44 bits in one 64-bit window
                 const int e = it / C::QPB, j = it - e * C::QPB;
-                const Entry en = ent[e];
-                const int d = en.meta & 31, c = (en.meta >> 5) & 3, b = (en.meta >> 7) & 511;
-                const int slot = en.meta >> 16;
-                const int row = (4 * j) / B, col = (4 * j) % B;
-                VT* dst = res + (((size_t)slot * 3 + c) * B + row) * TW + b * B + col;
-                if (!decode_quad<C::BSQ, VT>(bytes, en.off, d, j, f.quant_shift, lut, dst)) {
-                    err[c * C::NB + b] = 1;
-                    any_err = 1;
+                const Entry en = E[e];
+                const int b = desc_bits(en.meta & 31);
+                const uint32_t p0 = (en.off << 3) + (uint32_t)(4 * j * b);
+                const uint64_t win = (uint64_t)sbits(words, p0) | ((uint64_t)sbits(words, p0 + 32) << 32);
+                const uint32_t lm = (1u << b) - 1u;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = deq((uint32_t)(win >> (i * b)) & lm, shift);
+                put(en.meta, j, v);
+            } else {
+                const int it2 = it - items_f;
+                const int e = it2 / C::QPB, j = it2 - e * C::QPB;
+                const Entry en = E[P.ent_cap - 1 - e];
+                const int d = en.meta & 31;
+                const bool trit = desc_mode(d) == MODE_TRIT;
+                const int b = desc_bits(d);
+                const uint32_t G = trit ? 5u : 3u, PBITS = trit ? 8u : 7u, DB = trit ? 2u : 3u;
+                const uint32_t PMAX = trit ? 242u : 124u, DMASK = trit ? 3u : 7u;
+                const uint32_t MAGIC = trit ? 13108u : 21846u;            // kk/G, kk < 256
+                const uint16_t* L = trit ? lut.trit : lut.quint;
+                const uint32_t gbits = PBITS + G * (uint32_t)b;
+                const uint32_t base = en.off << 3, lm = (1u << b) - 1u;
+                const uint32_t k0 = 4u * (uint32_t)j;
+                const uint32_t g0 = (k0 * MAGIC) >> 16, g1 = ((k0 + 3u) * MAGIC) >> 16;
+                const uint32_t pk0 = sbits(words, base + g0 * gbits) & ((1u << PBITS) - 1u);
+                const uint32_t pk1 = sbits(words, base + g1 * gbits) & ((1u << PBITS) - 1u);
+                if (pk0 > PMAX || pk1 > PMAX) {           // kernels.py:147-150
+                    err[((en.meta >> 5) & 3) * C::NB + ((en.meta >> 7) & 255)] = 1;
+                    cnt[4] = 1;
                 }
+                const uint32_t dg0 = L[pk0 <= PMAX ? pk0 : 0u], dg1 = L[pk1 <= PMAX ? pk1 : 0u];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t kk = k0 + (uint32_t)i;
+                    const uint32_t g = (kk * MAGIC) >> 16, ii = kk - g * G;
+                    const uint32_t digit = ((g == g0 ? dg0 : dg1) >> (DB * ii)) & DMASK;
+                    const uint32_t low = sbits(words, base + g * gbits + PBITS + ii * (uint32_t)b) & lm;
+                    v[i] = deq((digit << b) | low, shift);
+                }
+                put(en.meta, j, v);
             }
-            __syncthreads();
-            if (tid == 0) n_ent = 0;
-            // ---- blend + store ---------------------------------------------------
-            if (want && !any_err) {
-                for (int p = g; p < CH / 2; p += C::GROUPS) {
-                    const int sa = s0 + 2 * p;
-                    if (sa >= S || !qactive) continue;
-                    int32_t acc[3][4];
-                    const int rx = sa >> h;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const RT* rp = roots + ((rx * 3 + c) * B + yy) * TW + xq * 4;
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) acc[c][i] = (int32_t)rp[i];
-                    }
-                    for (int l = h - 1; l >= lmin; --l) {
-                        const int x = sa >> l;
-                        const int slot = P.slot_base[l] + x;
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            if ((mask[l * C::NREC + c * C::NB + blk] >> x) & 1u) {
-                                const VT* rp = res + (((size_t)slot * 3 + c) * B + yy) * TW + xq * 4;
-#pragma unroll
-                                for (int i = 0; i < 4; ++i) acc[c][i] += (int32_t)rp[i];
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int s = sa + e;
-                        if (s >= S) break;
-                        int32_t v[3][4];
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) v[c][i] = acc[c][i];
-                            if (k == 0) {
-                                const int x = s - s0;
-                                if ((mask[c * C::NB + blk] >> x) & 1u) {
-                                    const VT* rp = res + (((size_t)x * 3 + c) * B + yy) * TW + xq * 4;
-#pragma unroll
-                                    for (int i = 0; i < 4; ++i) v[c][i] += (int32_t)rp[i];
-                                }
-                            }
-                        }
-                        uint32_t w[3] = {0, 0, 0};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            uint32_t r, gg, bb;
-                            ycocg_to_rgb8(v[0][i], v[1][i], v[2][i], r, gg, bb);
-                            const int byte = 3 * i;
-                            w[byte >> 2] |= r << (8 * (byte & 3));
-                            w[(byte + 1) >> 2] |= gg << (8 * ((byte + 1) & 3));
-                            w[(byte + 2) >> 2] |= bb << (8 * ((byte + 2) & 3));
-                        }
-                        uint32_t* sp = reinterpret_cast<uint32_t*>(stage + ((s - s0) * B + yy) * (TW * 3) + xq * 12);
-                        sp[0] = w[0];
-                        sp[1] = w[1];
-                        sp[2] = w[2];
-                    }
-                }
-                __syncthreads();
-                // store the staged rows of every requested view in the chunk
-                const int row_bytes = min(TW, f.width - bx0 * B) * 3;
-                if (row_bytes > 0) {
-                    const int nvec = (TW * 3) / 16;
-                    const int items = CH * B * nvec;
-                    for (int it = tid; it < items; it += THREADS) {
-                        const int v16 = it % nvec, rr = (it / nvec) % B, sl = it / (nvec * B);
-                        const int s = s0 + sl;
-                        const int y = by * B + rr;
-                        if (s >= S || y >= f.height) continue;
-                        const int img = s * T + t;
-                        const int slot = P.slots ? P.slots[img] : img;
-                        if (slot < 0) continue;
-                        uint8_t* orow = P.rgb + (int64_t)slot * P.img_stride +
-                                        (int64_t)(y - P.by_lo * B) * P.row_stride + (int64_t)bx0 * B * 3;
-                        const uint8_t* src = stage + (sl * B + rr) * (TW * 3);
-                        const int b0 = v16 * 16;
-                        if (P.vec_store && b0 + 16 <= row_bytes) {
-                            *reinterpret_cast<uint4*>(orow + b0) = *reinterpret_cast<const uint4*>(src + b0);
-                        } else {
-                            for (int bb = b0; bb < min(b0 + 16, row_bytes); ++bb) orow[bb] = src[bb];
-                        }
-                    }
-                }
-            }
-            __syncthreads();
         }
-    }
-    // ---- anomaly: exact reference-order status (and values) ----------------
-    if (any_err) {
+        if (!P.roots_all && (t & ((1 << h) - 1)) == 0) load_roots(t >> h, 1, roots);
+    };
+
+    // classify(t), phase A: one item per (view s, block b) of row t.  The
+    // item is CLEAN when no residual of its chain is present in any channel
+    // -- its pixels are exactly RGB(root) -- else DIRTY.  Items are appended
+    // to two lists with warp-aggregated atomics (order is irrelevant), so the
+    // blend below runs each kind in homogeneous warps.  A dirty item carries
+    // its presence bits (bit 3l+c: level l, channel c).
+    const int nitem = S * C::NB;
+    const bool use_rgb = P.roots_all && f.rsx <= 8;
+    auto classify = [&](int t) {
+        for (int base = 0; base < nitem; base += THREADS) {
+            const int it = base + tid;
+            bool valid = false, dirty = false;
+            uint32_t pres = 0;
+            int sv = 0, bv = 0;
+            if (it < nitem) {
+                sv = it / C::NB;
+                bv = it % C::NB;
+                valid = bv < nb && (!P.slots || P.slots[sv * T + t] >= 0);
+                if (valid) {
+                    for (int l = h - 1; l >= k; --l) {
+                        const int x = sv >> l;
+                        const uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            pres |= ((M[(c * C::NB + bv) * 2 + (x >> 5)] >> (x & 31)) & 1u) << (3 * l + c);
+                    }
+                    dirty = pres != 0 || !use_rgb;
+                }
+            }
+            // warp-aggregated append
+            const unsigned full = 0xffffffffu;
+            const unsigned bd = __ballot_sync(full, valid && dirty), bc = __ballot_sync(full, valid && !dirty);
+            const int lane = tid & 31;
+            int od = 0, oc = 0;
+            if (lane == 0) {
+                if (bd) od = atomicAdd(&cnt[5], __popc(bd));
+                if (bc) oc = atomicAdd(&cnt[6], __popc(bc));
+            }
+            od = __shfl_sync(full, od, 0);
+            oc = __shfl_sync(full, oc, 0);
+            const unsigned below = (1u << lane) - 1u;
+            const uint2 item = make_uint2((uint32_t)sv | (uint32_t)bv << 8, pres);
+            if (valid && dirty) lists[od + __popc(bd & below)] = item;
+            if (valid && !dirty) lists[nitem - 1 - (oc + __popc(bc & below))] = item;
+        }
+        // RGB of the current root row, once per root row
+        if (use_rgb && (t & ((1 << h) - 1)) == 0) {
+            const RT* rrow = roots + (t >> h) * plane;         // roots_all: [rx*rsy + ry]
+            for (int it = tid; it < f.rsx * B * C::QPR; it += THREADS) {
+                const int xq = it % C::QPR, rr = (it / C::QPR) % B, rx = it / (C::QPR * B);
+                const RT* rp = rrow + (size_t)rx * f.rsy * plane + rr * TW + xq * 4;
+                int32_t v[3][4];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) load4<RT>(rp + c * B * TW, v[c]);
+                int32_t o[12];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int32_t tt = v[0][i] - (v[2][i] >> 1);
+                    const int32_t bb = tt - (v[1][i] >> 1);
+                    o[3 * i] = bb + v[1][i];
+                    o[3 * i + 1] = v[2][i] + tt;
+                    o[3 * i + 2] = bb;
+                }
+                uint32_t* d = root_rgb + (rx * B + rr) * (TW * 3 / 4) + xq * 3;
+                d[0] = pack4_sat(o[0], o[1], o[2], o[3]);
+                d[1] = pack4_sat(o[4], o[5], o[6], o[7]);
+                d[2] = pack4_sat(o[8], o[9], o[10], o[11]);
+            }
+        }
+    };
+
+    // blend(t), phase B: tasks = (item, pixel quad of its block).  Dirty
+    // tasks sum root + present residuals (colorspace.py:27-36 inverse lift,
+    // clamp, pack); clean tasks copy the precomputed RGB(root) bytes.
+    constexpr int QB = B / 4;                           // quads per block row
+    auto blend = [&](int t) {
+        const int nd = cnt[5], nc = cnt[6];
+        const int td = nd * C::QPB, tasks = td + nc * C::QPB;
+        const RT* rrow = roots + (P.roots_all ? (t >> h) : 0) * plane;
+        for (int it = tid; it < tasks; it += THREADS) {
+            const bool dirty = it < td;
+            const int i2 = dirty ? it : it - td;
+            const int li = i2 / C::QPB, j = i2 - li * C::QPB;
+            const uint2 item = dirty ? lists[li] : lists[nitem - 1 - li];
+            const int sv = item.x & 255, bv = (item.x >> 8) & 255;
+            const int row = j / QB, colq = (j % QB) * 4;
+            const int px = bv * B + colq;                   // pixel column in the tile
+            uint32_t* sp = reinterpret_cast<uint32_t*>(stage + (sv * B + row) * (TW * 3) + px * 3);
+            const int rx = sv >> h;
+            if (!dirty) {
+                const uint32_t* src = root_rgb + (rx * B + row) * (TW * 3 / 4) + (px * 3) / 4;
+                sp[0] = src[0];
+                sp[1] = src[1];
+                sp[2] = src[2];
+                continue;
+            }
+            const uint32_t pres = item.y;
+            const int poff = row * TW + px;
+            const int root_idx = P.roots_all ? rx * f.rsy : rx;
+            int32_t v[3][4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) load4<RT>(rrow + (root_idx * 3 + c) * B * TW + poff, v[c]);
+            for (int l = h - 1; l >= lmin; --l) {
+                const uint32_t pl = (pres >> (3 * l)) & 7u;
+                if (!pl) continue;
+                const VT* rp = resl + (P.slot_base[l] + (sv >> l)) * plane + poff;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    int32_t r[4] = {0, 0, 0, 0};
+                    if ((pl >> c) & 1u) load4<VT>(rp + c * B * TW, r);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[c][i] += r[i];
+                }
+            }
+            if (k == 0 && (pres & 7u)) {
+                const int32_t* rp = res0 + sv * plane + poff;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    int32_t r[4] = {0, 0, 0, 0};
+                    if ((pres >> c) & 1u) load4<int32_t>(rp + c * B * TW, r);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) v[c][i] += r[i];
+                }
+            }
+            int32_t o[12];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int32_t tt = v[0][i] - (v[2][i] >> 1);
+                const int32_t bb = tt - (v[1][i] >> 1);
+                o[3 * i] = bb + v[1][i];
+                o[3 * i + 1] = v[2][i] + tt;
+                o[3 * i + 2] = bb;
+            }
+            sp[0] = pack4_sat(o[0], o[1], o[2], o[3]);
+            sp[1] = pack4_sat(o[4], o[5], o[6], o[7]);
+            sp[2] = pack4_sat(o[8], o[9], o[10], o[11]);
+        }
+    };
+
+    // store(t): staging[t&1] -> HBM (true-dims crop)
+    const int row_bytes = min(TW, f.width - bx0 * B) * 3;
+    const int mode = P.store_mode == 1 && row_bytes != TW * 3 ? 0 : P.store_mode;
+    bool issued = false;
+    auto store = [&](int t) {
+        const uint8_t* stg = stage;
+        if (mode == 2) {
+            // one TMA tensor store: box (TW*3 bytes, B rows, 1 camera row, S
+            // columns) at (x0, y0, t, 0); TMA clips the right / bottom edges
+            if (tid == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                        &out_map),
+                    "r"(bx0 * B * 3), "r"((by - P.by_lo) * B), "r"(t), "r"(0), "r"(smem_addr(stg))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                issued = true;
+            }
+        } else if (mode == 1) {
+            for (int it = tid; it < S * B; it += THREADS) {
+                const int s = it / B, rr = it % B;
+                const int y = by * B + rr;
+                const int img = s * T + t;
+                const int slot = P.slots ? P.slots[img] : img;
+                if (slot < 0 || y >= f.height) continue;
+                uint8_t* orow = P.rgb + (int64_t)slot * P.img_stride + (int64_t)(y - P.by_lo * B) * P.row_stride +
+                                (int64_t)bx0 * B * 3;
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(orow),
+                             "r"(smem_addr(stg + (s * B + rr) * (TW * 3))), "n"(TW * 3)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                issued = true;
+            }
+        } else {
+            for (int it = tid; it < S * B * (TW * 3); it += THREADS) {
+                const int bcol = it % (TW * 3), rr = (it / (TW * 3)) % B, s = it / (TW * 3 * B);
+                const int y = by * B + rr;
+                if (bcol >= row_bytes || y >= f.height) continue;
+                const int img = s * T + t;
+                const int slot = P.slots ? P.slots[img] : img;
+                if (slot < 0) continue;
+                P.rgb[(int64_t)slot * P.img_stride + (int64_t)(y - P.by_lo * B) * P.row_stride +
+                      (int64_t)bx0 * B * 3 + bcol] = stg[(s * B + rr) * (TW * 3) + bcol];
+            }
+        }
+    };
+
+    // ---- the pipeline -----------------------------------------------------------
+    __syncthreads();
+    walk(0);
+    __syncthreads();
+    for (int i = 0; i <= T; ++i) {
+        if (i >= 1) store(i - 1);                     // staging holds row i-1
+        if (i + 1 < T) walk(i + 1);
+        if (i < T) {
+            decode(i);
+            classify(i);
+        }
+        if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
-        tile_fallback<B>(P, by, bx0, nb, lut, nbt);
+        if (i < T) blend(i);
+        if (tid == 0) {
+            cnt[i & 1] = 0;                           // ring i&1 free for walk(i+2)
+            cnt[2 + (i & 1)] = 0;
+            cnt[5] = 0;
+            cnt[6] = 0;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
     }
+    if (issued) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // ---- anomaly: exact reference-order values and status ----------------------
+    if (cnt[4]) tile_fallback<B>(P, by, bx0, nb, lut, nbt);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
 }
 
 template <int B, int TW, typename VT, typename RT>
 int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
            int64_t img_stride, int64_t row_stride, uint64_t* status, cudaStream_t stream) {
-    using C = Cfg<B, TW, VT>;
+    using C = Cfg<B, TW>;
     Params P{};
     P.f = f;
     P.stop_level = stop_level;
@@ -490,41 +699,66 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     P.row_stride = row_stride;
     P.status = status;
     P.tiles_x = (f.wb + C::NB - 1) / C::NB;
-    const int h = f.tree_height;
-    // slots: level-0 chunk [0, CH), then full rows of levels 1..h-1
-    int ns = CH;
+    const int h = f.tree_height, S = f.s_count;
+    // level rows 1..h-1 in resl; the level-0 row (S slots) in res0
+    int ns = 0;
     for (int l = 1; l < h; ++l) {
         P.slot_base[l] = ns;
         ns += f.level_sx[l];
     }
-    P.slot_base[0] = 0;
-    P.n_slots = ns;
-    int row_nodes = CH;
-    for (int l = 1; l < h; ++l) row_nodes += f.level_sx[l];
-    P.ent_cap = C::NREC * row_nodes;
-    auto al = [](int x) { return (x + 15) & ~15; };
+    P.ent_cap = C::NREC * (S + ns);               // every node of a row present
+    const int plane = 3 * B * TW;
+    const int root_row_bytes = f.rsx * plane * (int)sizeof(RT);
+    P.roots_all = f.rsy * root_row_bytes <= 16 * 1024;
+    P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
+    auto al = [](int x) { return (x + 127) & ~127; };
     int off = al((int)sizeof(DigitLut));
     P.off_nbt = off;   off = al(off + (int)sizeof(NodeBytes));
-    P.off_rec = off;   off = al(off + C::NREC * 4);
     P.off_cur = off;   off = al(off + C::NREC * MAXH * 4);
-    P.off_err = off;   off = al(off + (C::NREC + 2) * 4);
-    P.off_mask = off;  off = al(off + MAXH * C::NREC * 4);
-    P.off_ent = off;   off = al(off + P.ent_cap * (int)sizeof(Entry));
-    P.off_root = off;  off = al(off + f.rsx * 3 * B * TW * (int)sizeof(RT));
-    P.off_res = off;   off = al(off + ns * C::SLOT_VALS * (int)sizeof(VT));
-    P.off_stage = off; off = al(off + CH * B * TW * 3);
+    P.off_err = off;   off = al(off + C::NREC * 4);
+    P.off_cnt = off;   off = al(off + 8 * 4);
+    P.off_mask = off;  off = al(off + 2 * MAXH * C::NREC * 2 * 4);
+    P.off_ent = off;   off = al(off + 2 * P.ent_cap * (int)sizeof(Entry));
+    P.off_root = off;  off = al(off + (P.roots_all ? f.rsy : 1) * root_row_bytes);
+    P.off_rgb = off;   off = al(off + f.rsx * B * TW * 3);
+    P.off_list = off;  off = al(off + S * C::NB * 8);
+    P.off_res0 = off;  off = al(off + S * plane * 4);
+    P.off_resl = off;  off = al(off + ns * plane * (int)sizeof(VT));
+    P.off_stage = off; off = al(off + S * B * TW * 3);
     P.off_bytes = off;
-    const int budget = 113 * 1024;                  // two CTAs per SM
-    int cap = budget - off;
-    if (cap < 16 * 1024) cap = 16 * 1024;           // keep a useful window; 1 CTA/SM then
+    // staging window for the records: the host-measured worst tile when it
+    // fits next to the other buffers, else what is left (bigger tiles take the
+    // reference-order path)
+    const int want = f.tile_bytes_max > 0 ? f.tile_bytes_max + 64 : 32 * 1024;
+    const int cap = min(want, 227 * 1024 - off);
+    if (cap < 4096) return RLFC_ERR_ARGUMENT;
     P.bytes_cap = cap;
     const int smem = off + cap;
-    if (smem > 227 * 1024) return RLFC_ERR_ARGUMENT;
-    P.vec_store = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride) & 15) == 0;
+    // output path
+    const bool aligned = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride |
+                           (uintptr_t)(TW * 3)) & 15) == 0;
+    CUtensorMap map;
+    memset(&map, 0, sizeof(map));
+    P.store_mode = aligned ? 1 : 0;
+    const int nrows = min(by_hi * B, f.height) - by_lo * B;
+    EncodeTiledFn enc = encode_fn();
+    if (aligned && !slots && enc && S <= 256 && TW * 3 <= 256) {
+        const cuuint64_t dims[4] = {(cuuint64_t)f.width * 3, (cuuint64_t)nrows, (cuuint64_t)f.t_count,
+                                    (cuuint64_t)S};
+        const cuuint64_t strides[3] = {(cuuint64_t)row_stride, (cuuint64_t)img_stride,
+                                       (cuuint64_t)img_stride * f.t_count};
+        const cuuint32_t box[4] = {(cuuint32_t)(TW * 3), (cuuint32_t)B, 1u, (cuuint32_t)S};
+        const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+        if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, rgb, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            P.store_mode = 2;
+    }
     auto kern = k_decode_field_tiled<B, TW, VT, RT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int threads = C::MAX_THREADS;
     const int grid = P.tiles_x * (by_hi - by_lo);
-    kern<<<grid, THREADS, smem, stream>>>(P);
+    kern<<<grid, threads, smem, stream>>>(P, map);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "rlfc_b200: tiled decode launch error: %s\n", cudaGetErrorString(e));
@@ -539,10 +773,9 @@ int launch_decode_field_tiled(const rlfc_field& f, int stop_level, const int32_t
                               uint8_t* rgb, int64_t img_stride, int64_t row_stride, uint64_t* status,
                               cudaStream_t stream) {
     using namespace tiled;
-    // envelope of the tiled kernel
-    if (f.tree_height > MAXH || f.s_count > 64) return RLFC_ERR_ARGUMENT;
+    if (f.tree_height > MAXH || f.s_count > MAXS) return RLFC_ERR_ARGUMENT;
     for (int l = 1; l < f.tree_height; ++l)
-        if (f.level_sx[l] > MAXROW) return RLFC_ERR_ARGUMENT;
+        if (f.level_sx[l] > 32) return RLFC_ERR_ARGUMENT;
     const bool small_res = f.quant_shift <= 4;      // |dequant| <= 16392 fits int16
     const bool r16 = f.roots_i16 != 0;
 #define RLFC_TILED(B_, TW_)                                                                                       \
@@ -558,9 +791,9 @@ int launch_decode_field_tiled(const rlfc_field& f, int stop_level, const int32_t
     return launch<B_, TW_, int32_t, int32_t>(f, stop_level, slots, by_lo, by_hi, rgb, img_stride, row_stride,     \
                                              status, stream);
     switch (f.block) {
-        case 4: { RLFC_TILED(4, 64) }
-        case 8: { RLFC_TILED(8, 64) }
-        case 16: { RLFC_TILED(16, 32) }
+        case 4: { RLFC_TILED(4, 32) }
+        case 8: { RLFC_TILED(8, 32) }
+        case 16: { RLFC_TILED(16, 16) }
         default: return RLFC_ERR_ARGUMENT;
     }
 #undef RLFC_TILED

@@ -85,6 +85,7 @@ class DeviceField:
             f.offsets[c] = self.offsets[c].data_ptr()
             f.srv_len[c] = len(srv[c])
         f.roots = self.roots.data_ptr()
+        f.tile_bytes_max = tile_bytes_max(header, offsets)
         self.cfield = f
         self.ref = ctypes.byref(f)
 
@@ -92,6 +93,23 @@ class DeviceField:
     def hbm_bytes(self):
         return sum(t.numel() * t.element_size()
                    for t in self.srv + self.offsets + [self.roots])
+
+
+def tile_bytes_max(header, offsets):
+    """Staging need of the fused decode's tiles: the largest compressed size
+    of max(1, 32/B) consecutive records of one block row, summed over the
+    channels, plus alignment slack per channel (rlfc_b200.h)."""
+    wb, hb = header.block_grid
+    nb = 1 if header.block_size >= 16 else 32 // header.block_size
+    total = np.zeros((hb, -(-wb // nb)), dtype=np.int64)
+    for c in range(3):
+        offs = np.asarray(offsets[c], dtype=np.int64)
+        ends = np.append(offs[1:], header.section_lengths[c][2])
+        sizes = (ends - offs).reshape(hb, wb)
+        pad = (-wb) % nb
+        sizes = np.pad(sizes, ((0, 0), (0, pad)))
+        total += sizes.reshape(hb, -1, nb).sum(axis=2) + 32
+    return int(min(total.max(), 2**31 - 1)) if total.size else 0
 
 
 @dataclass(frozen=True)

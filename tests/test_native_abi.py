@@ -37,5 +37,5 @@ def test_cubin_targets_sm100a():
 
 def test_field_struct_layout():
     from paper_1805_06019_b200 import _native
-    # 16 int32 + 3*32 int32 + 3 ptr + 3 ptr + 3 u64 + 1 ptr
-    assert ctypes.sizeof(_native.RlfcField) == 16 * 4 + 96 * 4 + 10 * 8
+    # 18 int32 + 3*32 int32 + 3 ptr + 3 ptr + 3 u64 + 1 ptr
+    assert ctypes.sizeof(_native.RlfcField) == 18 * 4 + 96 * 4 + 10 * 8
