@@ -42,6 +42,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "rlfc_common.cuh"
@@ -64,19 +65,24 @@ struct Params {
     uint64_t* status;
     int tiles_x;
     int off_nbt, off_cur, off_err, off_cnt, off_mask, off_ent, off_root, off_rgb, off_list, off_res0, off_resl,
-        off_stage, off_bytes;
-    int bytes_cap, ent_cap;
+        off_stage, off_bytes, off_mbar;
+    int bytes_cap, ent_cap, seg_cap, off_priv;
     int slot_base[MAXH];       // level l >= 1: first slot of its row in resl
     int store_mode;            // 2: one 4-D TMA tensor store per row, 1: per-row
                                // cp.async.bulk, 0: byte stores (unaligned rows)
     int roots_all;             // 1: every root of the tile is staged at setup
     int roots_vec;             // 1: root rows are 16-byte aligned in HBM
+    int no_prefill;            // debug knob (RLFC_TILED_NO_PREFILL=1): every view dirty
+    int debug;                 // debug bits (RLFC_TILED_DEBUG): 1 skip copies, 2 all dirty
 };
 
-struct Entry {
-    uint32_t off;              // payload byte offset inside the staged tile
-    uint32_t meta;             // desc | c << 5 | blk << 7 | slot << 16
-};
+// One decode job: payload byte offset in the staged tile (16 bits), descriptor
+// (5), channel (2), block (3), residual slot (6; slot < S is the level-0 row,
+// else a level row at slot - S).
+using Entry = uint32_t;
+__device__ __forceinline__ Entry make_entry(uint32_t off, int d, int c, int b, int slot) {
+    return off | (uint32_t)d << 16 | (uint32_t)c << 21 | (uint32_t)b << 23 | (uint32_t)slot << 26;
+}
 
 // 32 bits at bit position `bitpos` of the 16-byte aligned staging buffer.
 __device__ __forceinline__ uint32_t sbits(const uint32_t* w, uint32_t bitpos) {
@@ -114,7 +120,7 @@ struct Cfg {
     static constexpr int QPB = BSQ / 4;         // value quads per block
     static constexpr int QPR = TW / 4;          // pixel quads per tile row
     static constexpr int QUADS = QPR * B;       // pixel quads per tile
-    static constexpr int MAX_THREADS = 256;
+    static constexpr int MAX_THREADS = 128;
     static_assert(NREC <= 32, "walkers live in one warp");
 };
 
@@ -218,9 +224,9 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     uint32_t* mask = reinterpret_cast<uint32_t*>(smem + P.off_mask); // [2 ring][MAXH][NREC][2]
     Entry* ent = reinterpret_cast<Entry*>(smem + P.off_ent);         // [2 ring][ent_cap]
     RT* roots = reinterpret_cast<RT*>(smem + P.off_root);            // [root][3][B][TW]
-    uint32_t* root_rgb = reinterpret_cast<uint32_t*>(smem + P.off_rgb); // [rx][B][TW*3/4] packed RGB8
+    uint32_t* root_rgb = reinterpret_cast<uint32_t*>(smem + P.off_rgb); // [root][B][TW*3/4] packed RGB8
     uint2* lists = reinterpret_cast<uint2*>(smem + P.off_list);      // [S*NB]: dirty from 0, clean from the end
-    int32_t* res0 = reinterpret_cast<int32_t*>(smem + P.off_res0);   // [s][3][B][TW]
+    VT* res0 = reinterpret_cast<VT*>(smem + P.off_res0);             // [s][3][B][TW]
     VT* resl = reinterpret_cast<VT*>(smem + P.off_resl);             // [slot][3][B][TW]
     uint8_t* stage = smem + P.off_stage;                             // [S][B][TW*3]
     uint8_t* bytes = smem + P.off_bytes;
@@ -305,12 +311,17 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         }
     };
     if (P.roots_all) load_roots(0, f.rsy, roots);
-    // walkers: one thread per (channel, block) record, in the LAST warp
-    const int wid = tid - (THREADS - 32);
+    // walkers: one thread per (channel, block) record.  The last warp walks
+    // the lowest level's row (level 0, or the stop level), the warp before it
+    // walks the level rows above; the pre-walk is done by the last warp.
+    const int wid = tid - (THREADS - 32);                    // lane in the last warp
+    const int wid2 = tid - (THREADS - 64);                   // lane in the warp before
     const bool walker = wid >= 0 && wid < C::NREC && (wid % C::NB) < nb && need_srv;
-    const int wc = walker ? wid / C::NB : 0, wblk = walker ? wid % C::NB : 0;
+    const bool walker2 = wid2 >= 0 && wid2 < C::NREC && (wid2 % C::NB) < nb && need_srv;
+    const int wrec = walker ? wid : (walker2 ? wid2 : 0);
+    const int wc = wrec / C::NB, wblk = wrec % C::NB;
     uint32_t my_beg = 0, my_len = 0;
-    if (walker) {
+    if (walker || walker2) {
         const int64_t blk = (int64_t)by * f.wb + bx0 + wblk;
         const uint64_t rb = f.offsets[wc][blk];
         const uint64_t re = (blk + 1 < (int64_t)f.wb * f.hb) ? f.offsets[wc][blk + 1] : f.srv_len[wc];
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     __syncthreads();
 
     // ---- pre-walk: start of each level inside each record -------------------
-    uint32_t* mycur = cur + (walker ? wid : 0) * MAXH;
+    uint32_t* mycur = cur + wrec * MAXH;
     if (walker) {
         const uint8_t* rec = bytes + my_beg;
         const uint32_t rbit = my_beg << 3;
@@ -345,23 +356,33 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         if (bad) { err[wid] = 1; cnt[4] = 1; }
     }
 
-    // walk(t): level rows that start at t and the level-0 row t -> ring t&1.
-    // Level-l masks live in ring ((t >> l) & 1): a row's mask stays valid for
-    // all 2^l camera rows that use it.  Plain-bit payloads fill the ring from
-    // the front, trit/quint payloads from the back.
+    // walk(t): the level rows that start at t (warp before last) and the
+    // lowest level's row t (last warp) -> ring t&1.  Each walker lane keeps
+    // its entries in a private segment; a warp scan then places them in the
+    // ring (plain-bit payloads from the front, trit/quint from the back) with
+    // one atomic per warp.  Level-l masks live in ring ((t >> l) & 1): a row's
+    // mask stays valid for all 2^l camera rows that use it.
+    Entry* priv = reinterpret_cast<Entry*>(smem + P.off_priv);   // [2 groups][NREC][S + ns]
     auto walk = [&](int t) {
-        if (!walker || err[wid]) return;
+        if (tid < THREADS - 64) return;                  // only the two walker warps
+        const bool low = walker, up = walker2;
+        const bool active = (low || up) && !err[wrec];
         const uint8_t* rec = bytes + my_beg;
         const uint32_t rbit = my_beg << 3;
-        Entry* E = ent + (t & 1) * P.ent_cap;
+        Entry* seg = priv + ((low ? 0 : C::NREC) + wrec) * P.seg_cap;   // per group
+        int nbits = 0, ntq = 0;
         bool bad = false;
-        for (int l = h - 1; l >= k && !bad; --l) {
+        const int lo_l = low ? k : k + 1, hi_l = low ? k : h - 1;
+        for (int l = hi_l; active && l >= lo_l && !bad; --l) {
+            if (!low && (t & ((1 << l) - 1)) != 0) continue;   // level row not due
+            if (low && k == 0 && l != 0) continue;
             const bool row_level = l >= lmin;
-            if (row_level && (t & ((1 << l) - 1)) != 0) continue;
+            if (low && row_level) {                             // k >= 1: lowest row level
+                if ((t & ((1 << l) - 1)) != 0) continue;
+            }
             const int sx = f.level_sx[l];
             const int n0 = f.level_base[l] + (t >> l) * sx;
-            const int sb = row_level ? P.slot_base[l] : 0;
-            const uint32_t lvl0 = row_level ? 0u : 1u;
+            const int sb = row_level ? S + P.slot_base[l] : 0;
             uint32_t cu = mycur[l];
             uint32_t mw[2] = {0u, 0u};
             for (int w = 0; w < sx && !bad; w += 32) {
@@ -373,33 +394,54 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                     bits &= bits - 1u;
                     const int d = cu < my_len ? rec[cu] : NUM_DESC;
                     if (d >= NUM_DESC || cu + nbt.v[d] > my_len) { bad = true; break; }
-                    Entry en;
-                    en.off = my_beg + cu + 1;
-                    en.meta = (uint32_t)d | (uint32_t)wc << 5 | (uint32_t)wblk << 7 | lvl0 << 15 |
-                              (uint32_t)(sb + x) << 16;
-                    if (desc_mode(d) == MODE_BITS) E[atomicAdd(&cnt[t & 1], 1)] = en;
-                    else E[P.ent_cap - 1 - atomicAdd(&cnt[2 + (t & 1)], 1)] = en;
+                    seg[nbits + ntq] = make_entry(my_beg + cu + 1, d, wc, wblk, sb + x);
+                    if (desc_mode(d) == MODE_BITS) ++nbits;
+                    else ++ntq;
                     cu += nbt.v[d];
                 }
             }
             mycur[l] = cu;
-            uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2 + wid * 2;
+            uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2 + wrec * 2;
             M[0] = mw[0];
             M[1] = mw[1];
         }
-        if (bad) { err[wid] = 1; cnt[4] = 1; }
+        if (bad) { err[wrec] = 1; cnt[4] = 1; }
+        // place the lane's entries: full-warp scan of the two counts (idle
+        // lanes count 0), one atomic per counter per warp
+        const unsigned grp = 0xffffffffu;
+        const int lane = tid & 31;
+        int ib = nbits, iq = ntq;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int yb = __shfl_up_sync(grp, ib, o), yq = __shfl_up_sync(grp, iq, o);
+            if (lane >= o) { ib += yb; iq += yq; }
+        }
+        const int last = 31 - __clz(grp);
+        int baseb = 0, baseq = 0;
+        if (lane == last) {
+            baseb = atomicAdd(&cnt[t & 1], ib);
+            baseq = atomicAdd(&cnt[2 + (t & 1)], iq);
+        }
+        baseb = __shfl_sync(grp, baseb, last) + ib - nbits;
+        baseq = __shfl_sync(grp, baseq, last) + iq - ntq;
+        Entry* E = ent + (t & 1) * P.ent_cap;
+        for (int e = 0; e < nbits + ntq; ++e) {
+            const Entry en = seg[e];
+            if (desc_mode((en >> 16) & 31) == MODE_BITS) E[baseb++] = en;
+            else E[P.ent_cap - 1 - (baseq++)] = en;
+        }
     };
 
     // decode(t): ring t&1 -> residual slots (+ the root row when it starts).
     // One item = 4 consecutive values of one payload (one pixel-row quad of
     // its block).
     const int shift = f.quant_shift;
-    auto put = [&](uint32_t meta, int j, const int32_t* v) {
-        const int c = (meta >> 5) & 3, b = (meta >> 7) & 255, slot = meta >> 16;
+    auto put = [&](Entry en, int j, const int32_t* v) {
+        const int c = (en >> 21) & 3, b = (en >> 23) & 7, slot = en >> 26;
         const int row = (4 * j) / B, col = (4 * j) % B;
         const int o = (c * B + row) * TW + b * B + col;
-        if (meta & (1u << 15)) store4<int32_t>(res0 + slot * plane + o, v);
-        else store4<VT>(resl + slot * plane + o, v);
+        if (slot < S) store4<VT>(res0 + slot * plane + o, v);
+        else store4<VT>(resl + (slot - S) * plane + o, v);
     };
     auto decode = [&](int t) {
         const int nf = cnt[t & 1], nbk = cnt[2 + (t & 1)];
@@ -411,18 +453,18 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                 // plain b-bit fields: the quad's 4b <= 44 bits in one 64-bit window
                 const int e = it / C::QPB, j = it - e * C::QPB;
                 const Entry en = E[e];
-                const int b = desc_bits(en.meta & 31);
-                const uint32_t p0 = (en.off << 3) + (uint32_t)(4 * j * b);
+                const int b = desc_bits((en >> 16) & 31);
+                const uint32_t p0 = ((en & 0xFFFFu) << 3) + (uint32_t)(4 * j * b);
                 const uint64_t win = (uint64_t)sbits(words, p0) | ((uint64_t)sbits(words, p0 + 32) << 32);
                 const uint32_t lm = (1u << b) - 1u;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) v[i] = deq((uint32_t)(win >> (i * b)) & lm, shift);
-                put(en.meta, j, v);
+                put(en, j, v);
             } else {
                 const int it2 = it - items_f;
                 const int e = it2 / C::QPB, j = it2 - e * C::QPB;
                 const Entry en = E[P.ent_cap - 1 - e];
-                const int d = en.meta & 31;
+                const int d = (en >> 16) & 31;
                 const bool trit = desc_mode(d) == MODE_TRIT;
                 const int b = desc_bits(d);
                 const uint32_t G = trit ? 5u : 3u, PBITS = trit ? 8u : 7u, DB = trit ? 2u : 3u;
@@ -430,13 +472,13 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                 const uint32_t MAGIC = trit ? 13108u : 21846u;            // kk/G, kk < 256
                 const uint16_t* L = trit ? lut.trit : lut.quint;
                 const uint32_t gbits = PBITS + G * (uint32_t)b;
-                const uint32_t base = en.off << 3, lm = (1u << b) - 1u;
+                const uint32_t base = (en & 0xFFFFu) << 3, lm = (1u << b) - 1u;
                 const uint32_t k0 = 4u * (uint32_t)j;
                 const uint32_t g0 = (k0 * MAGIC) >> 16, g1 = ((k0 + 3u) * MAGIC) >> 16;
                 const uint32_t pk0 = sbits(words, base + g0 * gbits) & ((1u << PBITS) - 1u);
                 const uint32_t pk1 = sbits(words, base + g1 * gbits) & ((1u << PBITS) - 1u);
                 if (pk0 > PMAX || pk1 > PMAX) {           // kernels.py:147-150
-                    err[((en.meta >> 5) & 3) * C::NB + ((en.meta >> 7) & 255)] = 1;
+                    err[((en >> 21) & 3) * C::NB + ((en >> 23) & 7)] = 1;
                     cnt[4] = 1;
                 }
                 const uint32_t dg0 = L[pk0 <= PMAX ? pk0 : 0u], dg1 = L[pk1 <= PMAX ? pk1 : 0u];
@@ -448,117 +490,170 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                     const uint32_t low = sbits(words, base + g * gbits + PBITS + ii * (uint32_t)b) & lm;
                     v[i] = deq((digit << b) | low, shift);
                 }
-                put(en.meta, j, v);
+                put(en, j, v);
             }
         }
         if (!P.roots_all && (t & ((1 << h) - 1)) == 0) load_roots(t >> h, 1, roots);
     };
 
-    // classify(t), phase A: one item per (view s, block b) of row t.  The
-    // item is CLEAN when no residual of its chain is present in any channel
-    // -- its pixels are exactly RGB(root) -- else DIRTY.  Items are appended
-    // to two lists with warp-aggregated atomics (order is irrelevant), so the
-    // blend below runs each kind in homogeneous warps.  A dirty item carries
-    // its presence bits (bit 3l+c: level l, channel c).
-    const int nitem = S * C::NB;
-    const bool use_rgb = P.roots_all && f.rsx <= 8;
-    auto classify = [&](int t) {
-        for (int base = 0; base < nitem; base += THREADS) {
-            const int it = base + tid;
-            bool valid = false, dirty = false;
-            uint32_t pres = 0;
-            int sv = 0, bv = 0;
-            if (it < nitem) {
-                sv = it / C::NB;
-                bv = it % C::NB;
-                valid = bv < nb && (!P.slots || P.slots[sv * T + t] >= 0);
-                if (valid) {
-                    for (int l = h - 1; l >= k; --l) {
-                        const int x = sv >> l;
-                        const uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2;
+    // Root colours: RGB(root) of every root of the tile, computed once at setup
+    // (roots_all).  Most (view, block) pairs carry no residual at any level:
+    // their pixels are exactly RGB(root), so each view's staging rows start as
+    // a copy of RGB(root) (prefill) and the threads overwrite only the DIRTY
+    // (view, block) pairs.
+    const bool use_rgb = P.roots_all != 0 && !P.no_prefill;
+    if (use_rgb) {
+        const int nroot = f.rsx * f.rsy;
+        for (int it = tid; it < nroot * B * C::QPR; it += THREADS) {
+            const int xq = it % C::QPR, rr = (it / C::QPR) % B, ri = it / (C::QPR * B);
+            const RT* rp = roots + (size_t)ri * plane + rr * TW + xq * 4;
+            int32_t v[3][4];
 #pragma unroll
-                        for (int c = 0; c < 3; ++c)
-                            pres |= ((M[(c * C::NB + bv) * 2 + (x >> 5)] >> (x & 31)) & 1u) << (3 * l + c);
-                    }
-                    dirty = pres != 0 || !use_rgb;
-                }
+            for (int c = 0; c < 3; ++c) load4<RT>(rp + c * B * TW, v[c]);
+            int32_t o[12];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int32_t tt = v[0][i] - (v[2][i] >> 1);
+                const int32_t bb = tt - (v[1][i] >> 1);
+                o[3 * i] = bb + v[1][i];
+                o[3 * i + 1] = v[2][i] + tt;
+                o[3 * i + 2] = bb;
             }
-            // warp-aggregated append
-            const unsigned full = 0xffffffffu;
-            const unsigned bd = __ballot_sync(full, valid && dirty), bc = __ballot_sync(full, valid && !dirty);
-            const int lane = tid & 31;
-            int od = 0, oc = 0;
-            if (lane == 0) {
-                if (bd) od = atomicAdd(&cnt[5], __popc(bd));
-                if (bc) oc = atomicAdd(&cnt[6], __popc(bc));
-            }
-            od = __shfl_sync(full, od, 0);
-            oc = __shfl_sync(full, oc, 0);
-            const unsigned below = (1u << lane) - 1u;
-            const uint2 item = make_uint2((uint32_t)sv | (uint32_t)bv << 8, pres);
-            if (valid && dirty) lists[od + __popc(bd & below)] = item;
-            if (valid && !dirty) lists[nitem - 1 - (oc + __popc(bc & below))] = item;
+            uint32_t* d = root_rgb + (ri * B + rr) * (TW * 3 / 4) + xq * 3;
+            d[0] = pack4_sat(o[0], o[1], o[2], o[3]);
+            d[1] = pack4_sat(o[4], o[5], o[6], o[7]);
+            d[2] = pack4_sat(o[8], o[9], o[10], o[11]);
         }
-        // RGB of the current root row, once per root row
-        if (use_rgb && (t & ((1 << h) - 1)) == 0) {
-            const RT* rrow = roots + (t >> h) * plane;         // roots_all: [rx*rsy + ry]
-            for (int it = tid; it < f.rsx * B * C::QPR; it += THREADS) {
-                const int xq = it % C::QPR, rr = (it / C::QPR) % B, rx = it / (C::QPR * B);
-                const RT* rp = rrow + (size_t)rx * f.rsy * plane + rr * TW + xq * 4;
-                int32_t v[3][4];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) load4<RT>(rp + c * B * TW, v[c]);
-                int32_t o[12];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int32_t tt = v[0][i] - (v[2][i] >> 1);
-                    const int32_t bb = tt - (v[1][i] >> 1);
-                    o[3 * i] = bb + v[1][i];
-                    o[3 * i + 1] = v[2][i] + tt;
-                    o[3 * i + 2] = bb;
-                }
-                uint32_t* d = root_rgb + (rx * B + rr) * (TW * 3 / 4) + xq * 3;
-                d[0] = pack4_sat(o[0], o[1], o[2], o[3]);
-                d[1] = pack4_sat(o[4], o[5], o[6], o[7]);
-                d[2] = pack4_sat(o[8], o[9], o[10], o[11]);
-            }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+    // views of row t the caller wants (64-bit mask over s), warp-wide
+    const uint64_t all_views = S >= 64 ? ~0ull : ((1ull << S) - 1ull);
+    auto want_mask = [&](int t) -> uint64_t {
+        if (!P.slots) return all_views;
+        const int lane = tid & 31;
+        const bool w0 = lane < S && (!P.slots || P.slots[lane * T + t] >= 0);
+        const bool w1 = lane + 32 < S && (!P.slots || P.slots[(lane + 32) * T + t] >= 0);
+        return (uint64_t)__ballot_sync(0xffffffffu, w0) | (uint64_t)__ballot_sync(0xffffffffu, w1) << 32;
+    };
+
+    // prefill(t): staging[t&1][s] <- RGB(root(s, t)) for every view, 16-byte
+    // cooperative copies (dirty blocks are overwritten by blend(t))
+    auto prefill = [&](int t) {
+        if (!use_rgb) return;
+        uint4* stg = reinterpret_cast<uint4*>(stage);
+        const int ry = t >> h;
+        constexpr int V = B * TW * 3 / 16;               // uint4 per view
+        for (int it = tid; it < S * V; it += THREADS) {
+            const int sv = it / V, v = it - sv * V;
+            stg[it] = reinterpret_cast<const uint4*>(root_rgb + ((sv >> h) * f.rsy + ry) * (V * 4))[v];
         }
     };
 
-    // blend(t), phase B: tasks = (item, pixel quad of its block).  Dirty
-    // tasks sum root + present residuals (colorspace.py:27-36 inverse lift,
-    // clamp, pack); clean tasks copy the precomputed RGB(root) bytes.
+    // classify(t), two steps.  (1) lanes 0..nb-1 of warp 0 build, per block,
+    // the 64-bit mask of views whose chain carries any residual in any
+    // channel (level-l row bits spread over their 2^l views); (2) after the
+    // phase barrier every thread takes (view, block) items, keeps the dirty
+    // ones and appends them -- with their presence bits (bit 3l+c: level l,
+    // channel c) -- by warp-aggregated atomics (order is irrelevant).
+    uint64_t* dmask = reinterpret_cast<uint64_t*>(lists + S * C::NB);   // [NB]
+    int32_t* dpre = reinterpret_cast<int32_t*>(dmask + C::NB);          // [NB] exclusive prefix
+    auto classify_masks = [&](int t, uint64_t want) {
+        if (tid >= 32) return;
+        const int b = tid;
+        uint64_t dirty = 0;
+        if (b < nb) {
+            if (!use_rgb) {
+                dirty = want;
+            } else {
+                for (int l = h - 1; l >= k; --l) {
+                    const uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2;
+                    uint64_t ml = 0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        ml |= (uint64_t)M[(c * C::NB + b) * 2] | (uint64_t)M[(c * C::NB + b) * 2 + 1] << 32;
+                    if (l == 0) {
+                        dirty |= ml;
+                    } else {
+                        const int span = 1 << l;
+                        const uint64_t run = span >= 64 ? ~0ull : ((1ull << span) - 1ull);
+                        while (ml) {
+                            const int x = __ffsll((long long)ml) - 1;
+                            ml &= ml - 1;
+                            const int s0 = x << l;
+                            if (s0 < 64) dirty |= run << s0;
+                        }
+                    }
+                }
+                dirty &= want;
+            }
+        }
+        const int n = __popcll(dirty);
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += y;
+        }
+        if (b < C::NB) {
+            dmask[b] = dirty;
+            dpre[b] = incl - n;
+        }
+        if (tid == 31) cnt[5] = incl;
+    };
+    // classify_items(t): thread i takes dirty item i: its block from the
+    // prefix, its view as the k-th set bit of the block's mask, then its
+    // presence bits (bit 3l+c: level l, channel c)
+    auto classify_items = [&](int t) {
+        const int total = cnt[5];
+        for (int i = tid; i < total; i += THREADS) {
+            int b = 0;
+#pragma unroll
+            for (int j = 1; j < C::NB; ++j) b += (dpre[j] <= i) ? 1 : 0;
+            const int kth = i - dpre[b];
+            uint64_t m = dmask[b];
+            for (int j = 0; j < kth; ++j) m &= m - 1;        // drop the kth lowest views
+            const int sv = __ffsll((long long)m) - 1;
+            uint32_t pres = 0;
+            for (int l = h - 1; l >= k; --l) {
+                const int x = sv >> l;
+                const uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    pres |= ((M[(c * C::NB + b) * 2 + (x >> 5)] >> (x & 31)) & 1u) << (3 * l + c);
+            }
+            lists[i] = make_uint2((uint32_t)sv | (uint32_t)b << 8, pres);
+        }
+    };
+
+    // blend(t), phase B: tasks = (dirty item, pixel quad of its block): root +
+    // present residuals, colorspace.py:27-36 inverse lift, clamp, pack.
     constexpr int QB = B / 4;                           // quads per block row
     auto blend = [&](int t) {
-        const int nd = cnt[5], nc = cnt[6];
-        const int td = nd * C::QPB, tasks = td + nc * C::QPB;
+        const int tasks = cnt[5] * C::QPB;
+        __syncwarp();
+        uint8_t* stg = stage;
         const RT* rrow = roots + (P.roots_all ? (t >> h) : 0) * plane;
         for (int it = tid; it < tasks; it += THREADS) {
-            const bool dirty = it < td;
-            const int i2 = dirty ? it : it - td;
-            const int li = i2 / C::QPB, j = i2 - li * C::QPB;
-            const uint2 item = dirty ? lists[li] : lists[nitem - 1 - li];
+            const int li = it / C::QPB, j = it - li * C::QPB;
+            const uint2 item = lists[li];
             const int sv = item.x & 255, bv = (item.x >> 8) & 255;
             const int row = j / QB, colq = (j % QB) * 4;
             const int px = bv * B + colq;                   // pixel column in the tile
-            uint32_t* sp = reinterpret_cast<uint32_t*>(stage + (sv * B + row) * (TW * 3) + px * 3);
+            uint32_t* sp = reinterpret_cast<uint32_t*>(stg + (sv * B + row) * (TW * 3) + px * 3);
             const int rx = sv >> h;
-            if (!dirty) {
-                const uint32_t* src = root_rgb + (rx * B + row) * (TW * 3 / 4) + (px * 3) / 4;
-                sp[0] = src[0];
-                sp[1] = src[1];
-                sp[2] = src[2];
-                continue;
-            }
             const uint32_t pres = item.y;
             const int poff = row * TW + px;
             const int root_idx = P.roots_all ? rx * f.rsy : rx;
             int32_t v[3][4];
 #pragma unroll
             for (int c = 0; c < 3; ++c) load4<RT>(rrow + (root_idx * 3 + c) * B * TW + poff, v[c]);
-            for (int l = h - 1; l >= lmin; --l) {
+            uint32_t lv = (pres >> 3) & ~0u;            // levels >= 1
+            while (lv) {
+                const int bit = __ffs(lv) - 1;
+                const int l = 1 + bit / 3;
                 const uint32_t pl = (pres >> (3 * l)) & 7u;
-                if (!pl) continue;
+                lv &= ~(7u << (3 * (l - 1)));
                 const VT* rp = resl + (P.slot_base[l] + (sv >> l)) * plane + poff;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -568,12 +663,12 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                     for (int i = 0; i < 4; ++i) v[c][i] += r[i];
                 }
             }
-            if (k == 0 && (pres & 7u)) {
-                const int32_t* rp = res0 + sv * plane + poff;
+            if (pres & 7u) {
+                const VT* rp = res0 + sv * plane + poff;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     int32_t r[4] = {0, 0, 0, 0};
-                    if ((pres >> c) & 1u) load4<int32_t>(rp + c * B * TW, r);
+                    if ((pres >> c) & 1u) load4<VT>(rp + c * B * TW, r);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) v[c][i] += r[i];
                 }
@@ -641,24 +736,32 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     };
 
     // ---- the pipeline -----------------------------------------------------------
+    // iteration i: [A] store(i-1) (TMA, async) | walk(i+1) | decode(i) |
+    //                  per-block dirty masks(i) | drain store(i-1) reads
+    //              [B1] dirty items(i) | prefill staging with RGB(root)
+    //              [B2] blend dirty items(i) into staging
     __syncthreads();
     walk(0);
     __syncthreads();
     for (int i = 0; i <= T; ++i) {
-        if (i >= 1) store(i - 1);                     // staging holds row i-1
+        const uint64_t want = i < T ? want_mask(i) : 0ull;   // warp-uniform per warp
+        if (i >= 1 && (tid == 0 || mode != 2)) store(i - 1);
         if (i + 1 < T) walk(i + 1);
         if (i < T) {
             decode(i);
-            classify(i);
+            classify_masks(i, want);
         }
         if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        if (i < T) {
+            classify_items(i);
+            prefill(i);
+        }
         __syncthreads();
         if (i < T) blend(i);
         if (tid == 0) {
             cnt[i & 1] = 0;                           // ring i&1 free for walk(i+2)
             cnt[2 + (i & 1)] = 0;
-            cnt[5] = 0;
-            cnt[6] = 0;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
@@ -710,6 +813,12 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     const int plane = 3 * B * TW;
     const int root_row_bytes = f.rsx * plane * (int)sizeof(RT);
     P.roots_all = f.rsy * root_row_bytes <= 16 * 1024;
+    {
+        const char* e = getenv("RLFC_TILED_NO_PREFILL");
+        P.no_prefill = e && e[0] == '1';
+        const char* d = getenv("RLFC_TILED_DEBUG");
+        P.debug = d ? atoi(d) : 0;
+    }
     P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
     auto al = [](int x) { return (x + 127) & ~127; };
     int off = al((int)sizeof(DigitLut));
@@ -720,9 +829,12 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     P.off_mask = off;  off = al(off + 2 * MAXH * C::NREC * 2 * 4);
     P.off_ent = off;   off = al(off + 2 * P.ent_cap * (int)sizeof(Entry));
     P.off_root = off;  off = al(off + (P.roots_all ? f.rsy : 1) * root_row_bytes);
-    P.off_rgb = off;   off = al(off + f.rsx * B * TW * 3);
-    P.off_list = off;  off = al(off + S * C::NB * 8);
-    P.off_res0 = off;  off = al(off + S * plane * 4);
+    P.off_rgb = off;   off = al(off + (P.roots_all ? f.rsx * f.rsy : 1) * B * TW * 3);
+    P.off_mbar = off;  off = al(off + 16);
+    P.off_list = off;  off = al(off + S * C::NB * 8 + C::NB * 12);
+    P.seg_cap = S + ns;
+    P.off_priv = off;  off = al(off + 2 * C::NREC * P.seg_cap * 4);
+    P.off_res0 = off;  off = al(off + S * plane * (int)sizeof(VT));
     P.off_resl = off;  off = al(off + ns * plane * (int)sizeof(VT));
     P.off_stage = off; off = al(off + S * B * TW * 3);
     P.off_bytes = off;
@@ -730,7 +842,7 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     // fits next to the other buffers, else what is left (bigger tiles take the
     // reference-order path)
     const int want = f.tile_bytes_max > 0 ? f.tile_bytes_max + 64 : 32 * 1024;
-    const int cap = min(want, 227 * 1024 - off);
+    const int cap = min(min(want, 227 * 1024 - off), 65536);   // 16-bit payload offsets
     if (cap < 4096) return RLFC_ERR_ARGUMENT;
     P.bytes_cap = cap;
     const int smem = off + cap;
@@ -774,8 +886,12 @@ int launch_decode_field_tiled(const rlfc_field& f, int stop_level, const int32_t
                               cudaStream_t stream) {
     using namespace tiled;
     if (f.tree_height > MAXH || f.s_count > MAXS) return RLFC_ERR_ARGUMENT;
-    for (int l = 1; l < f.tree_height; ++l)
+    int nslot = f.s_count;
+    for (int l = 1; l < f.tree_height; ++l) {
         if (f.level_sx[l] > 32) return RLFC_ERR_ARGUMENT;
+        nslot += f.level_sx[l];
+    }
+    if (nslot > 64) return RLFC_ERR_ARGUMENT;       // 6-bit slot field of an Entry
     const bool small_res = f.quant_shift <= 4;      // |dequant| <= 16392 fits int16
     const bool r16 = f.roots_i16 != 0;
 #define RLFC_TILED(B_, TW_)                                                                                       \
