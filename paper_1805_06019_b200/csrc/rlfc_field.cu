@@ -200,7 +200,7 @@ __device__ __noinline__ void tile_fallback(const Params& P, int by, int bx0, int
 
 template <int B, int TW, typename VT, typename RT>
 __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
-    k_decode_field_tiled(const Params P, const __grid_constant__ CUtensorMap out_map) {
+    k_decode_field_tiled(const __grid_constant__ Params P, const __grid_constant__ CUtensorMap out_map) {
     using C = Cfg<B, TW>;
     extern __shared__ __align__(128) uint8_t smem[];
     const rlfc_field& f = P.f;
@@ -246,8 +246,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
             }
             l16[i] = (uint16_t)v;
         }
-        constexpr NodeBytes NBT = make_node_bytes<B * B>();
-        if (tid < 32) nbt.v[tid] = NBT.v[tid];
+        if (tid < 32) nbt.v[tid] = tid < NUM_DESC ? (uint16_t)(1 + payload_bytes(tid, B * B)) : (uint16_t)0;
         if (tid < 8) cnt[tid] = 0;
     }
     // ---- the tile's record bytes --------------------------------------------
@@ -384,11 +383,12 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
             const int n0 = f.level_base[l] + (t >> l) * sx;
             const int sb = row_level ? S + P.slot_base[l] : 0;
             uint32_t cu = mycur[l];
-            uint32_t mw[2] = {0u, 0u};
+            uint32_t mw0 = 0u, mw1 = 0u;
             for (int w = 0; w < sx && !bad; w += 32) {
                 uint32_t bits = sbits(words, rbit + (uint32_t)(n0 + w));
                 if (sx - w < 32) bits &= (1u << (sx - w)) - 1u;
-                mw[w >> 5] = bits;
+                if (w == 0) mw0 = bits;
+                else mw1 = bits;
                 while (bits) {
                     const int x = w + __ffs(bits) - 1;
                     bits &= bits - 1u;
@@ -402,8 +402,8 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
             }
             mycur[l] = cu;
             uint32_t* M = mask + (((t >> l) & 1) * MAXH + l) * C::NREC * 2 + wrec * 2;
-            M[0] = mw[0];
-            M[1] = mw[1];
+            M[0] = mw0;
+            M[1] = mw1;
         }
         if (bad) { err[wrec] = 1; cnt[4] = 1; }
         // place the lane's entries: full-warp scan of the two counts (idle
