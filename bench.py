@@ -143,6 +143,19 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def ncu_traffic(kernel_kind):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/r1_decode_ncu_summary.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r1_decode_ncu_summary.json")
+    if kernel_kind != "fused" or not os.path.exists(path):
+        return None
+    try:
+        with open(path) as f:
+            return int(json.load(f)["dram_bytes_total"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(PEAKS) as f:
@@ -312,6 +325,7 @@ def main():
     render = None
     if not args.no_render:
         render = render_measure(state, args, rl)
+    random_access = random_access_measure(state, rl)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -333,12 +347,15 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": None, "peak_source": peak_kind,
+                         "traffic": ncu_traffic(args.kernel) if band == (0, hb) else None,
+                         "traffic_source": "profiles/r1_decode_ncu_summary.json (ncu --set full, same kernel)",
+                         "peak_source": peak_kind,
                          "alg_bytes_per_launch": int(alg)},
             "e2e": e2e, "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "render": render,
+            "random_access": random_access,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -366,6 +383,44 @@ def e2e_measure(state, band, args, rl):
             "ms_per_step": dt * 1e3,
             "path": "decoder.HostPipeline: pinned H2D of SRV+offsets+roots, "
                     "fused decode, pinned D2H of RGB (band-pipelined)"}
+
+
+def random_access_measure(state, rl):
+    """Random-access block decode (decoder.decode_block path): 10^6-pick
+    device-resident batches (throughput, CUDA events) and single-block calls
+    through the public API (latency incl. H2D/D2H), picks from
+    default_rng(7) as in the reference acceptance test."""
+    import torch
+    from paper_1805_06019_b200 import decoder
+    hdr = state.header
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(7)
+    n = 1_000_000
+    req = np.stack([rng.integers(0, hdr.s_count, n), rng.integers(0, hdr.t_count, n),
+                    rng.integers(0, wb, n), rng.integers(0, hb, n),
+                    rng.integers(0, 3, n), np.zeros(n, np.int64)], 1).astype(np.int32)
+    dreq = torch.from_numpy(req).cuda()
+    for _ in range(2):
+        decoder.decode_blocks(state, dreq, raise_errors=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    reps = 5
+    for _ in range(reps):
+        decoder.decode_blocks(state, dreq, raise_errors=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    picks = req[:200]
+    for p in picks[:10]:
+        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    t0 = time.perf_counter()
+    for p in picks:
+        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    lat = (time.perf_counter() - t0) / len(picks)
+    return {"blocks_per_s": n / (ms * 1e-3), "batch": n, "ms_per_batch": ms,
+            "decode_block_latency_us": lat * 1e6,
+            "note": "cfg2 R4 stream, k=0, one CUDA thread per block request"}
 
 
 def render_measure(state, args, rl):

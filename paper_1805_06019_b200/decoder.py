@@ -208,8 +208,11 @@ def decode_blocks(state, requests, device=None, raise_errors=True):
     """
     torch = _torch()
     df = state.device_field(device)
-    req = torch.as_tensor(np.ascontiguousarray(requests, dtype=np.int32)
-                          .reshape(-1, 6)).to(df.device, non_blocking=True)
+    if isinstance(requests, torch.Tensor) and requests.is_cuda:
+        req = requests.to(torch.int32).reshape(-1, 6).contiguous()
+    else:
+        req = torch.as_tensor(np.ascontiguousarray(requests, dtype=np.int32)
+                              .reshape(-1, 6)).to(df.device, non_blocking=True)
     n = req.shape[0]
     b = state.header.block_size
     out = torch.empty((n, b, b), dtype=torch.int32, device=df.device)
