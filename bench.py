@@ -231,9 +231,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--render-batch", type=int, default=256)
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.config == "cfg5":
+        return run_cfg5(args)
 
     import torch
     import torch.distributed as dist
@@ -445,6 +448,111 @@ def render_measure(state, args, rl):
     return {"views_per_s": n / dt, "batch": n, "ms_per_batch": dt * 1e3,
             "view": "512x512 SlabPose, default focal, k=0, bit-exact",
             "timing": "wall clock incl. host pose prep, sync per batch"}
+
+
+CFG5 = dict(S=32, T=32, W=2048, H=2048, seed=7, h=3, B=4, shift=4, tp=16,
+            tb=1000, codec="raw")
+
+
+def make_stream_cfg5(cache_dir="/tmp/rlfc_cache"):
+    """cfg5 (BASELINE configs[4]): 32x32x2048^2, 3-level tree, R4 params,
+    produced band by band (producer.encode_synthetic_striped)."""
+    from paper_1805_06019_b200 import encoder, lightfield, producer
+    path = os.path.join(cache_dir, "cfg5_r4.rlfc")
+    if os.path.exists(path):
+        with open(path, "rb") as f:
+            return f.read()
+    t0 = time.time()
+    params = encoder.EncodingParams(
+        tree_height=CFG5["h"], block_size=CFG5["B"], quant_shift=CFG5["shift"],
+        pixel_threshold=CFG5["tp"], block_threshold=CFG5["tb"],
+        root_codec=CFG5["codec"])
+    data, present = producer.encode_synthetic_striped(
+        lightfield.SyntheticSpec(CFG5["S"], CFG5["T"], CFG5["W"], CFG5["H"],
+                                 CFG5["seed"]), params, strip_rows=32)
+    log(f"cfg5 stream {len(data)} B in {time.time() - t0:.0f}s, present {present}")
+    os.makedirs(cache_dir, exist_ok=True)
+    with open(path + ".tmp", "wb") as f:
+        f.write(data)
+    os.replace(path + ".tmp", path)
+    return data
+
+
+def run_cfg5(args):
+    """Random-access block decode on the 32x32x2048^2 field: latency of
+    single decode_block calls (10,000 picks, default_rng(7), as
+    test_acceptance.py:165-177) and throughput of 10^6-pick device batches;
+    plus one full-field decode (4.29 Gpix) for scale."""
+    import torch
+    import paper_1805_06019_b200 as rl
+    from paper_1805_06019_b200 import decoder
+    data = make_stream_cfg5()
+    t0 = time.time()
+    state = rl.init(data)
+    init_s = time.time() - t0
+    hdr = state.header
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(7)
+    picks = np.stack([rng.integers(0, hdr.s_count, 10000), rng.integers(0, hdr.t_count, 10000),
+                      rng.integers(0, wb, 10000), rng.integers(0, hb, 10000),
+                      rng.integers(0, 3, 10000)], 1)
+    for p in picks[:50]:
+        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for p in picks:
+        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    lat_us = (time.perf_counter() - t0) / len(picks) * 1e6
+    n = 1_000_000
+    req = np.stack([rng.integers(0, hdr.s_count, n), rng.integers(0, hdr.t_count, n),
+                    rng.integers(0, wb, n), rng.integers(0, hb, n),
+                    rng.integers(0, 3, n), np.zeros(n, np.int64)], 1).astype(np.int32)
+    dreq = torch.from_numpy(req).cuda()
+    for _ in range(args.warmup):
+        decoder.decode_blocks(state, dreq, raise_errors=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        decoder.decode_blocks(state, dreq, raise_errors=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    out = torch.empty((hdr.s_count, hdr.t_count, hdr.height, hdr.width, 3),
+                      dtype=torch.uint8, device="cuda")
+    decoder.decode_field(state, 0, out=out)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(3):
+        decoder.decode_field(state, 0, out=out, check=False)
+    f1.record()
+    torch.cuda.synchronize()
+    field_ms = f0.elapsed_time(f1) / 3
+    # CPU port: single-thread decode_block latency on 2,000 of the picks
+    from oracle import oracle
+    orc = oracle.OracleState(data)
+    t0 = time.perf_counter()
+    for p in picks[:2000]:
+        orc.decode_block(int(p[0]), int(p[1]), int(p[2]), int(p[3]), int(p[4]), 0)
+    cpu_us = (time.perf_counter() - t0) / 2000 * 1e6
+    px = hdr.s_count * hdr.t_count * hdr.width * hdr.height
+    line = {
+        "metric": "random-access blocks/s (cfg5 32x32x2048^2, 10^6-pick batches)",
+        "value": n / (ms * 1e-3), "unit": "blocks/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "cfg5 random-access block decode, 32x32 views x 2048^2, h=3 B=4 R4 params, RAW roots",
+                   "stream_bytes": len(data), "m_nodes": state.m_nodes,
+                   "bpp": 8.0 * len(data) / px, "init_s": init_s},
+        "decode_block_latency_us": lat_us,
+        "full_field": {"gpix_per_s": px / (field_ms * 1e-3) / 1e9, "ms": field_ms},
+        "cpu_baseline": {"value": 1e6 / cpu_us, "unit": "blocks/s", "cores": 1,
+                         "kind": "port", "sample": "2,000 single decode_block picks, oracle C port",
+                         "latency_us": cpu_us},
+    }
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -120,7 +120,7 @@ struct Cfg {
     static constexpr int QPB = BSQ / 4;         // value quads per block
     static constexpr int QPR = TW / 4;          // pixel quads per tile row
     static constexpr int QUADS = QPR * B;       // pixel quads per tile
-    static constexpr int MAX_THREADS = 128;
+    static constexpr int MAX_THREADS = 256;
     static_assert(NREC <= 32, "walkers live in one warp");
 };
 
@@ -868,7 +868,8 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     }
     auto kern = k_decode_field_tiled<B, TW, VT, RT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int threads = C::MAX_THREADS;
+    int threads = 128;                               // measured best (profiles/)
+    if (const char* e = getenv("RLFC_TILED_THREADS")) threads = atoi(e) == 256 ? 256 : 128;
     const int grid = P.tiles_x * (by_hi - by_lo);
     kern<<<grid, threads, smem, stream>>>(P, map);
     cudaError_t e = cudaGetLastError();

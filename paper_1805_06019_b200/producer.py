@@ -35,6 +35,11 @@ def lib():
         L.prod_encode.argtypes = [i32, i32, i32, i32, vp, i32, i32, i32, i64,
                                   i32, vp]
         L.prod_encode.restype = vp
+        L.prod_encode_strip.argtypes = [i32, i32, i32, i32, i32, vp, i32, i32,
+                                        i32, i64, i32, vp]
+        L.prod_encode_strip.restype = vp
+        L.prod_synthesize_rows.argtypes = [i32, i32, i32, i32, u64, i32, i32,
+                                           vp]
         L.prod_result_error.argtypes = [vp]
         L.prod_result_srv_len.argtypes = [vp, i32]
         L.prod_result_srv_len.restype = i64
@@ -119,37 +124,41 @@ def pyramid_weights(camera_positions, tree_height, spec):
     return np.concatenate(flat) if flat else np.zeros(0, np.int64)
 
 
-def encode(lf, params, threads=0):
-    """(stream bytes, present blocks per level) for a LightFieldGrid."""
+def _encode_rows(rgb, S, T, W, h_valid, hp_rows, params, weights):
+    """Encode one block-aligned row band: (roots band, [srv_c], [offsets_c],
+    present per level)."""
     L = lib()
-    L.prod_set_threads(int(threads))
-    S, T, W, H = lf.s_count, lf.t_count, lf.width, lf.height
-    h, B = params.tree_height, params.block_size
-    rgb = np.ascontiguousarray(lf.rgb, dtype=np.uint8)
-    w = np.ascontiguousarray(pyramid_weights(lf.camera_positions, h,
-                                             params.filter))
-    handle = L.prod_encode(S, T, W, H, _ptr(rgb), h, B,
-                           params.pixel_threshold, params.block_threshold,
-                           params.quant_shift, _ptr(w))
+    B, h = params.block_size, params.tree_height
+    rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+    handle = L.prod_encode_strip(S, T, W, h_valid, hp_rows, _ptr(rgb), h, B,
+                                 params.pixel_threshold,
+                                 params.block_threshold, params.quant_shift,
+                                 _ptr(weights))
     try:
         if L.prod_result_error(handle):
             raise FormatError("residual value outside the range table")
-        wp, hp = container.padded_dims(W, H, B)
-        wb, hb = wp // B, hp // B
+        wp = -(-W // B) * B
+        nblk = (wp // B) * (hp_rows // B)
         rsx, rsy = container.level_dims(S, T, h)
-        roots = np.empty((rsx, rsy, 3, hp, wp), dtype=np.int32)
+        roots = np.empty((rsx, rsy, 3, hp_rows, wp), dtype=np.int32)
         L.prod_result_roots(handle, _ptr(roots))
         present = np.zeros(h, dtype=np.int64)
         L.prod_result_present(handle, _ptr(present))
         srvs, offs = [], []
         for c in range(3):
             srv = np.empty(L.prod_result_srv_len(handle, c), dtype=np.uint8)
-            off = np.empty(wb * hb, dtype="<u8")
+            off = np.empty(nblk, dtype="<u8")
             L.prod_result_copy(handle, c, _ptr(srv), _ptr(off))
             srvs.append(srv)
             offs.append(off)
     finally:
         L.prod_free(handle)
+    return roots, srvs, offs, present
+
+
+def _assemble(S, T, W, H, params, roots, srvs, offs, present):
+    """Root streams + header + sections (container.py:269-339 layout)."""
+    rsx, rsy = container.level_dims(S, T, params.tree_height)
     codec = container.CODEC_IDS[params.root_codec]
     sections, lengths = [], []
     for c in range(3):
@@ -162,17 +171,77 @@ def encode(lf, params, threads=0):
                 chunks.append(len(blob).to_bytes(4, "little"))
                 chunks.append(blob)
         root_sec = b"".join(chunks)
-        off_sec = offs[c].tobytes()
+        off_sec = np.ascontiguousarray(offs[c], dtype="<u8").tobytes()
         srv_sec = srvs[c].tobytes()
         sections += [root_sec, off_sec, srv_sec]
         lengths.append((len(root_sec), len(off_sec), len(srv_sec)))
     header = container.RlfcHeader(
-        s_count=S, t_count=T, width=W, height=H, tree_height=h,
-        block_size=B, quant_shift=params.quant_shift,
+        s_count=S, t_count=T, width=W, height=H,
+        tree_height=params.tree_height, block_size=params.block_size,
+        quant_shift=params.quant_shift,
         pixel_threshold=params.pixel_threshold,
         block_threshold=params.block_threshold,
         filter_kind=params.filter.kind,
         sigma_fp=params.filter.sigma_fp if params.filter.kind == "gaussian"
         else 0,
         root_codec_id=codec, section_lengths=tuple(lengths))
-    return container.pack_header(header) + b"".join(sections), tuple(present)
+    return container.pack_header(header) + b"".join(sections), \
+        tuple(int(v) for v in present)
+
+
+def encode(lf, params, threads=0):
+    """(stream bytes, present blocks per level) for a LightFieldGrid."""
+    lib().prod_set_threads(int(threads))
+    S, T, W, H = lf.s_count, lf.t_count, lf.width, lf.height
+    w = np.ascontiguousarray(pyramid_weights(lf.camera_positions,
+                                             params.tree_height, params.filter))
+    hp = -(-H // params.block_size) * params.block_size
+    roots, srvs, offs, present = _encode_rows(lf.rgb, S, T, W, H, hp, params,
+                                              w)
+    return _assemble(S, T, W, H, params, roots, srvs, offs, present)
+
+
+def encode_synthetic_striped(spec, params, strip_rows=64, threads=0):
+    """Synthesise and encode a large synthetic field band by band.
+
+    Every RKV/SRV operation is per pixel or per block (hierarchy.py:182-271)
+    and records are per block (container.py:306-323), so encoding
+    block-aligned row bands independently and stitching the records, offsets
+    and root rows reproduces the monolithic stream byte for byte
+    (tests/test_producer.py).  Peak memory is one band, which makes the
+    32x32x2048^2 configuration (12.9 GB of RGB) feasible.
+    """
+    from .lightfield import grid_positions
+    L = lib()
+    L.prod_set_threads(int(threads))
+    S, T, W, H = spec.s_count, spec.t_count, spec.width, spec.height
+    B, h = params.block_size, params.tree_height
+    strip_rows = max(B, strip_rows // B * B)
+    hp = -(-H // B) * B
+    wp = -(-W // B) * B
+    w = np.ascontiguousarray(pyramid_weights(grid_positions(S, T), h,
+                                             params.filter))
+    rsx, rsy = container.level_dims(S, T, h)
+    roots = np.empty((rsx, rsy, 3, hp, wp), dtype=np.int32)
+    srv_parts = [[], [], []]
+    off_parts = [[], [], []]
+    base = [0, 0, 0]
+    present = np.zeros(h, dtype=np.int64)
+    for y0 in range(0, hp, strip_rows):
+        y1 = min(y0 + strip_rows, hp)
+        valid = max(0, min(y1, H) - y0)
+        rgb = np.empty((S, T, valid, W, 3), dtype=np.uint8)
+        if valid:
+            L.prod_synthesize_rows(S, T, W, H, spec.seed & 0xFFFFFFFFFFFFFFFF,
+                                   y0, y0 + valid, _ptr(rgb))
+        r, srvs, offs, pres = _encode_rows(rgb, S, T, W, valid, y1 - y0,
+                                           params, w)
+        roots[:, :, :, y0:y1] = r
+        present += pres
+        for c in range(3):
+            off_parts[c].append(offs[c] + np.uint64(base[c]))
+            srv_parts[c].append(srvs[c])
+            base[c] += len(srvs[c])
+    srvs = [np.concatenate(p) for p in srv_parts]
+    offs = [np.concatenate(p) for p in off_parts]
+    return _assemble(S, T, W, H, params, roots, srvs, offs, present)

@@ -95,8 +95,17 @@ extern "C" {
 
 void prod_set_threads(int n) { g_threads = n; }
 
+// Rows [r0, r1) of every view of the scene; rgb: (S, T, r1-r0, W, 3) uint8.
+// The scene is per pixel, so any row band reproduces the full synthesis.
+int prod_synthesize_rows(int S, int T, int W, int H, uint64_t seed, int r0, int r1, uint8_t* rgb);
+
 // rgb: (S, T, H, W, 3) uint8
 int prod_synthesize(int S, int T, int W, int H, uint64_t seed, uint8_t* rgb) {
+    return prod_synthesize_rows(S, T, W, H, seed, 0, H, rgb);
+}
+
+int prod_synthesize_rows(int S, int T, int W, int H, uint64_t seed, int r0, int r1, uint8_t* rgb) {
+    const int NR = r1 - r0;
     const double x0 = -1.5, y0 = -1.5, x1 = S - 1 + 1.5, y1 = T - 1 + 1.5;
     const double zi = 1.0 - 0.0;
     const double z_bg = zi * 1.12, z_oc = zi * 1.05;
@@ -118,6 +127,7 @@ int prod_synthesize(int S, int T, int W, int H, uint64_t seed, uint8_t* rgb) {
         const double ox_off = (1.0 - oc_scale) * cam_x, oy_off = (1.0 - oc_scale) * cam_y;
         std::vector<double> wxo(W), wyo(H);
         std::vector<Axis> bxc(W), bxf(W), oxc(W), oxf(W), byc(H), byf(H), oyc(H), oyf(H);
+        (void)NR;
         for (int i = 0; i < W; ++i) {
             double wxb = bg_scale * ux[i] + bx_off;
             wxo[i] = oc_scale * ux[i] + ox_off;
@@ -126,7 +136,7 @@ int prod_synthesize(int S, int T, int W, int H, uint64_t seed, uint8_t* rgb) {
             oxc[i] = axis_of(wxo[i], oc_freq);
             oxf[i] = axis_of(wxo[i], oc_freq3);
         }
-        for (int j = 0; j < H; ++j) {
+        for (int j = r0; j < r1; ++j) {
             double wyb = bg_scale * uy[j] + by_off;
             wyo[j] = oc_scale * uy[j] + oy_off;
             byc[j] = axis_of(wyb, bg_freq);
@@ -134,8 +144,8 @@ int prod_synthesize(int S, int T, int W, int H, uint64_t seed, uint8_t* rgb) {
             oyc[j] = axis_of(wyo[j], oc_freq);
             oyf[j] = axis_of(wyo[j], oc_freq3);
         }
-        uint8_t* img = rgb + st * (int64_t)W * H * 3;
-        for (int j = 0; j < H; ++j) {
+        uint8_t* img = rgb + st * (int64_t)W * NR * 3 - (int64_t)r0 * W * 3;
+        for (int j = r0; j < r1; ++j) {
             const bool my = std::fabs(wyo[j] - oc_cy) < oc_hh;
             for (int i = 0; i < W; ++i) {
                 const bool inside = my && std::fabs(wxo[i] - oc_cx) < oc_hw;
@@ -217,10 +227,23 @@ struct EncodeResult {
 // Encode a light field.  rgb: (S,T,H,W,3) uint8.  weights: for level
 // l = 1..h, parent (cx, cy) (cx outer), 4 slots of member weights in the
 // reference member order (x outer, y inner); unused slots are 0.
+// Strip form: rgb holds H valid rows; the planes have hp_rows rows (a multiple
+// of B, zero beyond H), so a block-aligned row band of a large field can be
+// encoded on its own -- every RKV/SRV operation is per pixel or per block
+// (hierarchy.py:182-271), and records are per block (container.py:306-323).
+void* prod_encode_strip(int S, int T, int W, int H, int hp_rows, const uint8_t* rgb, int h, int B,
+                        int pixel_threshold, int64_t block_threshold, int shift, const int64_t* weights);
+
 void* prod_encode(int S, int T, int W, int H, const uint8_t* rgb, int h, int B, int pixel_threshold,
                   int64_t block_threshold, int shift, const int64_t* weights) {
+    return prod_encode_strip(S, T, W, H, (H + B - 1) / B * B, rgb, h, B, pixel_threshold, block_threshold, shift,
+                             weights);
+}
+
+void* prod_encode_strip(int S, int T, int W, int H, int hp_rows, const uint8_t* rgb, int h, int B,
+                        int pixel_threshold, int64_t block_threshold, int shift, const int64_t* weights) {
     auto* R = new EncodeResult();
-    const int wp = (W + B - 1) / B * B, hp = (H + B - 1) / B * B;
+    const int wp = (W + B - 1) / B * B, hp = hp_rows;
     const int wb = wp / B, hb = hp / B, bsq = B * B;
     const int64_t plane = (int64_t)wp * hp;
     auto ldim = [](int n, int l) { return (n + (1 << l) - 1) >> l; };
