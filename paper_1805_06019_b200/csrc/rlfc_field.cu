@@ -52,6 +52,10 @@ namespace rlfc {
 
 namespace tiled {
 
+#ifdef RLFC_PHASE_TIMING
+__device__ long long g_phase[4096 * 8 * 8];
+#endif
+
 constexpr int MAXH = 8;        // tree levels handled by the tiled kernel
 constexpr int MAXS = 64;       // camera columns handled by the tiled kernel
 
@@ -743,29 +747,52 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     __syncthreads();
     walk(0);
     __syncthreads();
+#ifdef RLFC_PHASE_TIMING
+    // per-warp cycle counters: [0] store+walk, [1] decode, [2] classify masks,
+    // [3] barrier A wait, [4] items+prefill, [5] barrier B1 wait, [6] blend,
+    // [7] barrier B2 wait
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+#define RLFC_TICK(k) do { const long long tn = clock64(); ph[k] += tn - tc; tc = tn; } while (0)
+#else
+#define RLFC_TICK(k) do { } while (0)
+#endif
     for (int i = 0; i <= T; ++i) {
         const uint64_t want = i < T ? want_mask(i) : 0ull;   // warp-uniform per warp
         if (i >= 1 && (tid == 0 || mode != 2)) store(i - 1);
         if (i + 1 < T) walk(i + 1);
+        RLFC_TICK(0);
         if (i < T) {
             decode(i);
+            RLFC_TICK(1);
             classify_masks(i, want);
+            RLFC_TICK(2);
         }
         if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
+        RLFC_TICK(3);
         if (i < T) {
             classify_items(i);
             prefill(i);
         }
+        RLFC_TICK(4);
         __syncthreads();
+        RLFC_TICK(5);
         if (i < T) blend(i);
+        RLFC_TICK(6);
         if (tid == 0) {
             cnt[i & 1] = 0;                           // ring i&1 free for walk(i+2)
             cnt[2 + (i & 1)] = 0;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
+        RLFC_TICK(7);
     }
+#ifdef RLFC_PHASE_TIMING
+    if ((tid & 31) == 0 && blockIdx.x < 4096) {
+        for (int q = 0; q < 8; ++q) g_phase[(blockIdx.x * 8 + (tid >> 5)) * 8 + q] = ph[q];
+    }
+#endif
     if (issued) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncthreads();
     // ---- anomaly: exact reference-order values and status ----------------------
@@ -881,6 +908,12 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
 }
 
 }  // namespace tiled
+
+#ifdef RLFC_PHASE_TIMING
+extern "C" int rlfc_debug_phase(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, tiled::g_phase, sizeof(tiled::g_phase)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 int launch_decode_field_tiled(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo, int by_hi,
                               uint8_t* rgb, int64_t img_stride, int64_t row_stride, uint64_t* status,
