@@ -77,6 +77,7 @@ struct Params {
     int roots_all;             // 1: every root of the tile is staged at setup
     int roots_vec;             // 1: root rows are 16-byte aligned in HBM
     int no_prefill;            // debug knob (RLFC_TILED_NO_PREFILL=1): every view dirty
+    int specialized;           // 1: dedicated walker warps (named-barrier handoff)
     int debug;                 // debug bits (RLFC_TILED_DEBUG): 1 skip copies, 2 all dirty
 };
 
@@ -210,6 +211,9 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     const rlfc_field& f = P.f;
     const int tid = threadIdx.x;
     const int THREADS = blockDim.x;
+    // specialized launch: warps 0..NCONS/32-1 consume (decode, classify,
+    // blend, store); the last two warps only walk, running ahead of them
+    const int NCONS = P.specialized ? THREADS - 64 : THREADS;
     const int by = P.by_lo + blockIdx.x / P.tiles_x;
     const int bx0 = (blockIdx.x % P.tiles_x) * C::NB;
     const int nb = min(C::NB, f.wb - bx0);
@@ -365,24 +369,32 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     // ring (plain-bit payloads from the front, trit/quint from the back) with
     // one atomic per warp.  Level-l masks live in ring ((t >> l) & 1): a row's
     // mask stays valid for all 2^l camera rows that use it.
-    Entry* priv = reinterpret_cast<Entry*>(smem + P.off_priv);   // [2 groups][NREC][S + ns]
+    // Ring of work items for parity p = t & 1: one segment per (walker group,
+    // record) -- plain-bit entries grow from the front of a segment,
+    // trit/quint entries from its back -- and, per group and kind, the
+    // exclusive prefix of the records' entry counts ([NREC] = group total).
+    const int seg_cap = P.seg_cap;
+    auto seg_of = [&](int p, int g, int r) -> Entry* {
+        return ent + ((size_t)(p * 2 + g) * C::NREC + r) * seg_cap;
+    };
+    auto pre_of = [&](int p, int g, int kind) -> int32_t* {
+        return reinterpret_cast<int32_t*>(smem + P.off_priv) + ((p * 2 + g) * 2 + kind) * 32;
+    };
     auto walk = [&](int t) {
         if (tid < THREADS - 64) return;                  // only the two walker warps
         const bool low = walker, up = walker2;
+        const int g = (tid >= THREADS - 32) ? 0 : 1;     // 0: lowest level row, 1: level rows
         const bool active = (low || up) && !err[wrec];
         const uint8_t* rec = bytes + my_beg;
         const uint32_t rbit = my_beg << 3;
-        Entry* seg = priv + ((low ? 0 : C::NREC) + wrec) * P.seg_cap;   // per group
+        Entry* seg = seg_of(t & 1, g, wrec);
         int nbits = 0, ntq = 0;
         bool bad = false;
         const int lo_l = low ? k : k + 1, hi_l = low ? k : h - 1;
         for (int l = hi_l; active && l >= lo_l && !bad; --l) {
             if (!low && (t & ((1 << l) - 1)) != 0) continue;   // level row not due
-            if (low && k == 0 && l != 0) continue;
             const bool row_level = l >= lmin;
-            if (low && row_level) {                             // k >= 1: lowest row level
-                if ((t & ((1 << l) - 1)) != 0) continue;
-            }
+            if (low && row_level && (t & ((1 << l) - 1)) != 0) continue;   // k >= 1: lowest row level
             const int sx = f.level_sx[l];
             const int n0 = f.level_base[l] + (t >> l) * sx;
             const int sb = row_level ? S + P.slot_base[l] : 0;
@@ -398,9 +410,9 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                     bits &= bits - 1u;
                     const int d = cu < my_len ? rec[cu] : NUM_DESC;
                     if (d >= NUM_DESC || cu + nbt.v[d] > my_len) { bad = true; break; }
-                    seg[nbits + ntq] = make_entry(my_beg + cu + 1, d, wc, wblk, sb + x);
-                    if (desc_mode(d) == MODE_BITS) ++nbits;
-                    else ++ntq;
+                    const Entry en = make_entry(my_beg + cu + 1, d, wc, wblk, sb + x);
+                    if (desc_mode(d) == MODE_BITS) seg[nbits++] = en;
+                    else seg[seg_cap - 1 - (ntq++)] = en;
                     cu += nbt.v[d];
                 }
             }
@@ -410,29 +422,24 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
             M[1] = mw1;
         }
         if (bad) { err[wrec] = 1; cnt[4] = 1; }
-        // place the lane's entries: full-warp scan of the two counts (idle
-        // lanes count 0), one atomic per counter per warp
-        const unsigned grp = 0xffffffffu;
+        // exclusive prefix of the per-record counts (idle lanes count 0)
         const int lane = tid & 31;
-        int ib = nbits, iq = ntq;
+        int ib = (low || up) ? nbits : 0, iq = (low || up) ? ntq : 0;
+        const int cb = ib, cq = iq;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int yb = __shfl_up_sync(grp, ib, o), yq = __shfl_up_sync(grp, iq, o);
+            const int yb = __shfl_up_sync(0xffffffffu, ib, o), yq = __shfl_up_sync(0xffffffffu, iq, o);
             if (lane >= o) { ib += yb; iq += yq; }
         }
-        const int last = 31 - __clz(grp);
-        int baseb = 0, baseq = 0;
-        if (lane == last) {
-            baseb = atomicAdd(&cnt[t & 1], ib);
-            baseq = atomicAdd(&cnt[2 + (t & 1)], iq);
+        int32_t* pb = pre_of(t & 1, g, 0);
+        int32_t* pq = pre_of(t & 1, g, 1);
+        if (lane < C::NREC) {
+            pb[lane] = ib - cb;
+            pq[lane] = iq - cq;
         }
-        baseb = __shfl_sync(grp, baseb, last) + ib - nbits;
-        baseq = __shfl_sync(grp, baseq, last) + iq - ntq;
-        Entry* E = ent + (t & 1) * P.ent_cap;
-        for (int e = 0; e < nbits + ntq; ++e) {
-            const Entry en = seg[e];
-            if (desc_mode((en >> 16) & 31) == MODE_BITS) E[baseb++] = en;
-            else E[P.ent_cap - 1 - (baseq++)] = en;
+        if (lane == 31) {
+            pb[C::NREC] = ib;
+            pq[C::NREC] = iq;
         }
     };
 
@@ -447,16 +454,31 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         if (slot < S) store4<VT>(res0 + slot * plane + o, v);
         else store4<VT>(resl + (slot - S) * plane + o, v);
     };
+    // find the record owning entry e of (group g, kind) at parity p: the
+    // last r with prefix[r] <= e
+    auto owner = [&](const int32_t* pre, int e) -> int {
+        int r = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+            if (r + step < C::NREC && pre[r + step] <= e) r += step;
+        return r;
+    };
     auto decode = [&](int t) {
-        const int nf = cnt[t & 1], nbk = cnt[2 + (t & 1)];
-        const Entry* E = ent + (t & 1) * P.ent_cap;
+        const int p = t & 1;
+        const int32_t *pb0 = pre_of(p, 0, 0), *pb1 = pre_of(p, 1, 0);
+        const int32_t *pq0 = pre_of(p, 0, 1), *pq1 = pre_of(p, 1, 1);
+        const int nb0 = pb0[C::NREC], nf = nb0 + pb1[C::NREC];
+        const int nq0 = pq0[C::NREC], nbk = nq0 + pq1[C::NREC];
         const int items_f = nf * C::QPB, items = items_f + nbk * C::QPB;
-        for (int it = tid; it < items; it += THREADS) {
+        for (int it = tid; it < items; it += NCONS) {
             int32_t v[4];
             if (it < items_f) {
                 // plain b-bit fields: the quad's 4b <= 44 bits in one 64-bit window
                 const int e = it / C::QPB, j = it - e * C::QPB;
-                const Entry en = E[e];
+                const int g = e < nb0 ? 0 : 1, eg = e - (g ? nb0 : 0);
+                const int32_t* pre = g ? pb1 : pb0;
+                const int r = owner(pre, eg);
+                const Entry en = seg_of(p, g, r)[eg - pre[r]];
                 const int b = desc_bits((en >> 16) & 31);
                 const uint32_t p0 = ((en & 0xFFFFu) << 3) + (uint32_t)(4 * j * b);
                 const uint64_t win = (uint64_t)sbits(words, p0) | ((uint64_t)sbits(words, p0 + 32) << 32);
@@ -467,7 +489,10 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
             } else {
                 const int it2 = it - items_f;
                 const int e = it2 / C::QPB, j = it2 - e * C::QPB;
-                const Entry en = E[P.ent_cap - 1 - e];
+                const int g = e < nq0 ? 0 : 1, eg = e - (g ? nq0 : 0);
+                const int32_t* pre = g ? pq1 : pq0;
+                const int r = owner(pre, eg);
+                const Entry en = seg_of(p, g, r)[seg_cap - 1 - (eg - pre[r])];
                 const int d = (en >> 16) & 31;
                 const bool trit = desc_mode(d) == MODE_TRIT;
                 const int b = desc_bits(d);
@@ -489,9 +514,9 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const uint32_t kk = k0 + (uint32_t)i;
-                    const uint32_t g = (kk * MAGIC) >> 16, ii = kk - g * G;
-                    const uint32_t digit = ((g == g0 ? dg0 : dg1) >> (DB * ii)) & DMASK;
-                    const uint32_t low = sbits(words, base + g * gbits + PBITS + ii * (uint32_t)b) & lm;
+                    const uint32_t gg = (kk * MAGIC) >> 16, ii = kk - gg * G;
+                    const uint32_t digit = ((gg == g0 ? dg0 : dg1) >> (DB * ii)) & DMASK;
+                    const uint32_t low = sbits(words, base + gg * gbits + PBITS + ii * (uint32_t)b) & lm;
                     v[i] = deq((digit << b) | low, shift);
                 }
                 put(en, j, v);
@@ -548,7 +573,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         uint4* stg = reinterpret_cast<uint4*>(stage);
         const int ry = t >> h;
         constexpr int V = B * TW * 3 / 16;               // uint4 per view
-        for (int it = tid; it < S * V; it += THREADS) {
+        for (int it = tid; it < S * V; it += NCONS) {
             const int sv = it / V, v = it - sv * V;
             stg[it] = reinterpret_cast<const uint4*>(root_rgb + ((sv >> h) * f.rsy + ry) * (V * 4))[v];
         }
@@ -610,7 +635,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
     // presence bits (bit 3l+c: level l, channel c)
     auto classify_items = [&](int t) {
         const int total = cnt[5];
-        for (int i = tid; i < total; i += THREADS) {
+        for (int i = tid; i < total; i += NCONS) {
             int b = 0;
 #pragma unroll
             for (int j = 1; j < C::NB; ++j) b += (dpre[j] <= i) ? 1 : 0;
@@ -638,7 +663,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         __syncwarp();
         uint8_t* stg = stage;
         const RT* rrow = roots + (P.roots_all ? (t >> h) : 0) * plane;
-        for (int it = tid; it < tasks; it += THREADS) {
+        for (int it = tid; it < tasks; it += NCONS) {
             const int li = it / C::QPB, j = it - li * C::QPB;
             const uint2 item = lists[li];
             const int sv = item.x & 255, bv = (item.x >> 8) & 255;
@@ -711,7 +736,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                 issued = true;
             }
         } else if (mode == 1) {
-            for (int it = tid; it < S * B; it += THREADS) {
+            for (int it = tid; it < S * B; it += NCONS) {
                 const int s = it / B, rr = it % B;
                 const int y = by * B + rr;
                 const int img = s * T + t;
@@ -726,7 +751,7 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
                 issued = true;
             }
         } else {
-            for (int it = tid; it < S * B * (TW * 3); it += THREADS) {
+            for (int it = tid; it < S * B * (TW * 3); it += NCONS) {
                 const int bcol = it % (TW * 3), rr = (it / (TW * 3)) % B, s = it / (TW * 3 * B);
                 const int y = by * B + rr;
                 if (bcol >= row_bytes || y >= f.height) continue;
@@ -757,36 +782,65 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
 #else
 #define RLFC_TICK(k) do { } while (0)
 #endif
+    if (P.specialized) {
+        // named barriers: 1/2 row walked (parity), 3/4 row consumed (parity),
+        // 5 consumer-internal.  Walkers run up to two camera rows ahead.
+        if (tid >= NCONS) {
+            for (int t = 1; t < T; ++t) {
+                if (t >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + (t & 1)), "r"(THREADS) : "memory");
+                walk(t);
+                asm volatile("bar.arrive %0, %1;" ::"r"(1 + (t & 1)), "r"(THREADS) : "memory");
+            }
+        } else {
+            for (int i = 0; i <= T; ++i) {
+                const uint64_t want = i < T ? want_mask(i) : 0ull;
+                if (i >= 1 && (tid == 0 || mode != 2)) store(i - 1);
+                if (i < T) {
+                    if (i >= 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + (i & 1)), "r"(THREADS) : "memory");
+                    decode(i);
+                    classify_masks(i, want);
+                }
+                if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                asm volatile("bar.sync 5, %0;" ::"r"(NCONS) : "memory");
+                if (i < T) {
+                    classify_items(i);
+                    prefill(i);
+                }
+                asm volatile("bar.sync 5, %0;" ::"r"(NCONS) : "memory");
+                if (i < T) blend(i);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 5, %0;" ::"r"(NCONS) : "memory");
+                if (i < T) asm volatile("bar.arrive %0, %1;" ::"r"(3 + (i & 1)), "r"(THREADS) : "memory");
+            }
+        }
+    } else {
     for (int i = 0; i <= T; ++i) {
-        const uint64_t want = i < T ? want_mask(i) : 0ull;   // warp-uniform per warp
-        if (i >= 1 && (tid == 0 || mode != 2)) store(i - 1);
-        if (i + 1 < T) walk(i + 1);
-        RLFC_TICK(0);
-        if (i < T) {
-            decode(i);
-            RLFC_TICK(1);
-            classify_masks(i, want);
-            RLFC_TICK(2);
+            const uint64_t want = i < T ? want_mask(i) : 0ull;   // warp-uniform per warp
+            if (i >= 1 && (tid == 0 || mode != 2)) store(i - 1);
+            if (i + 1 < T) walk(i + 1);
+            RLFC_TICK(0);
+            if (i < T) {
+                decode(i);
+                RLFC_TICK(1);
+                classify_masks(i, want);
+                RLFC_TICK(2);
+            }
+            if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncthreads();
+            RLFC_TICK(3);
+            if (i < T) {
+                classify_items(i);
+                prefill(i);
+            }
+            RLFC_TICK(4);
+            __syncthreads();
+            RLFC_TICK(5);
+            if (i < T) blend(i);
+            RLFC_TICK(6);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            RLFC_TICK(7);
         }
-        if (issued) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncthreads();
-        RLFC_TICK(3);
-        if (i < T) {
-            classify_items(i);
-            prefill(i);
-        }
-        RLFC_TICK(4);
-        __syncthreads();
-        RLFC_TICK(5);
-        if (i < T) blend(i);
-        RLFC_TICK(6);
-        if (tid == 0) {
-            cnt[i & 1] = 0;                           // ring i&1 free for walk(i+2)
-            cnt[2 + (i & 1)] = 0;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        RLFC_TICK(7);
     }
 #ifdef RLFC_PHASE_TIMING
     if ((tid & 31) == 0 && blockIdx.x < 4096) {
@@ -854,13 +908,13 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     P.off_err = off;   off = al(off + C::NREC * 4);
     P.off_cnt = off;   off = al(off + 8 * 4);
     P.off_mask = off;  off = al(off + 2 * MAXH * C::NREC * 2 * 4);
-    P.off_ent = off;   off = al(off + 2 * P.ent_cap * (int)sizeof(Entry));
+    P.seg_cap = S + ns;
+    P.off_ent = off;   off = al(off + 2 * 2 * C::NREC * P.seg_cap * (int)sizeof(Entry));
     P.off_root = off;  off = al(off + (P.roots_all ? f.rsy : 1) * root_row_bytes);
     P.off_rgb = off;   off = al(off + (P.roots_all ? f.rsx * f.rsy : 1) * B * TW * 3);
     P.off_mbar = off;  off = al(off + 16);
     P.off_list = off;  off = al(off + S * C::NB * 8 + C::NB * 12);
-    P.seg_cap = S + ns;
-    P.off_priv = off;  off = al(off + 2 * C::NREC * P.seg_cap * 4);
+    P.off_priv = off;  off = al(off + 2 * 2 * 2 * 32 * 4);     // prefix arrays
     P.off_res0 = off;  off = al(off + S * plane * (int)sizeof(VT));
     P.off_resl = off;  off = al(off + ns * plane * (int)sizeof(VT));
     P.off_stage = off; off = al(off + S * B * TW * 3);
@@ -897,8 +951,15 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int threads = 128;                               // measured best (profiles/)
     if (const char* e = getenv("RLFC_TILED_THREADS")) threads = atoi(e) == 256 ? 256 : 128;
+    {
+        // dedicated walker warps measured slower (152 vs 199 Gpix/s, cfg2 R4):
+        // opt-in only
+        const char* e = getenv("RLFC_TILED_SPEC");
+        P.specialized = e && e[0] == '1';
+        if (P.specialized) threads += 64;            // + two dedicated walker warps
+    }
     const int grid = P.tiles_x * (by_hi - by_lo);
-    kern<<<grid, threads, smem, stream>>>(P, map);
+    kern<<<grid, threads, smem, stream>>>(P, map);  // P.specialized set above
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "rlfc_b200: tiled decode launch error: %s\n", cudaGetErrorString(e));

@@ -337,6 +337,35 @@ def bise_decode_batch(payloads, descs, count, device=None):
 
 # --- reference-signature API ---------------------------------------------------
 
+class _BlockScratch:
+    """Per-thread pinned host + device buffers for single-block requests:
+    one H2D copy, one kernel, one D2H copy, one stream sync."""
+
+    def __init__(self, df, b):
+        torch = _torch()
+        self.req_h = torch.empty(6, dtype=torch.int32).pin_memory()
+        self.req_d = torch.empty(6, dtype=torch.int32, device=df.device)
+        self.out_d = torch.empty(b * b + 1, dtype=torch.int32,
+                                 device=df.device)
+        self.out_h = torch.empty(b * b + 1, dtype=torch.int32).pin_memory()
+        self.req_np = self.req_h.numpy()
+        self.out_np = self.out_h.numpy()
+
+
+_tls = threading.local()
+
+
+def _block_scratch(state, df):
+    cache = getattr(_tls, "blocks", None)
+    if cache is None:
+        cache = _tls.blocks = {}
+    key = (id(state), df.device.index)
+    sc = cache.get(key)
+    if sc is None:
+        sc = cache[key] = _BlockScratch(df, state.header.block_size)
+    return sc
+
+
 def decode_block_progressive(state: DecoderState, image_index, block_index,
                              channel, stop_level):
     """One B x B block summing SRV levels >= stop_level (decoder.py:81-106)."""
@@ -344,8 +373,21 @@ def decode_block_progressive(state: DecoderState, image_index, block_index,
     bx, by = block_index
     _check_indices(state, s, t, bx, by)
     _check_level(state, stop_level)
-    out, _ = decode_blocks(state, [(s, t, bx, by, channel, stop_level)])
-    return out[0].cpu().numpy()
+    torch = _torch()
+    df = state.device_field()
+    sc = _block_scratch(state, df)
+    b = state.header.block_size
+    sc.req_np[:] = (s, t, bx, by, channel, stop_level)
+    stream = torch.cuda.current_stream(df.device)
+    sc.req_d.copy_(sc.req_h, non_blocking=True)
+    _native.check(_native.lib().rlfc_decode_blocks(
+        df.ref, sc.req_d.data_ptr(), 1, sc.out_d.data_ptr(),
+        sc.out_d.data_ptr() + 4 * b * b, stream.cuda_stream),
+        "rlfc_decode_blocks")
+    sc.out_h.copy_(sc.out_d, non_blocking=True)
+    stream.synchronize()
+    _raise_status(int(sc.out_np[b * b]))
+    return sc.out_np[:b * b].reshape(b, b).copy()
 
 
 def decode_block(state: DecoderState, image_index, block_index, channel):
