@@ -227,7 +227,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--kernel", default="fused", choices=["fused", "simple"])
+    ap.add_argument("--kernel", default="staged", choices=["staged", "fused", "simple"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--render-batch", type=int, default=256)

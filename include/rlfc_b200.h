@@ -117,6 +117,30 @@ int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
                              int64_t row_stride, uint64_t *status,
                              void *stream);
 
+/* Staged full-field decode: the same contract and output as
+ * rlfc_decode_field, computed as three launches -- a record index (one lane
+ * per record: bitmap popcount + descriptor walk, kernels.py:162-200), a
+ * payload decode (one lane per present payload, kernels.py:128-159 +
+ * 202-211) into a residual array, and a blend (residual gather by bitmap
+ * rank + YCoCg-R inverse + clamp, colorspace.py:27-56) -- with the
+ * intermediates in a caller-owned device workspace of
+ * rlfc_decode_workspace_bytes(f, present_total) bytes (256-byte aligned).
+ * present_total: the number of present nodes over all records
+ * (rlfc_count_present).  Returns RLFC_ERR_ARGUMENT when the geometry is
+ * outside this path's envelope (block 4/8/16, S <= 64, h <= 8); the caller
+ * then uses rlfc_decode_field.  Records with any stream anomaly are decoded
+ * by the reference-order walk, so values and the failure word are identical
+ * to rlfc_decode_field's. */
+int rlfc_count_present(const rlfc_field *f, uint64_t *count, void *stream);
+int rlfc_decode_workspace_bytes(const rlfc_field *f, uint64_t present_total,
+                                uint64_t *bytes);
+int rlfc_decode_field_staged(const rlfc_field *f, int32_t stop_level,
+                             const int32_t *image_slots, int32_t by_lo,
+                             int32_t by_hi, uint8_t *rgb, int64_t img_stride,
+                             int64_t row_stride, void *workspace,
+                             uint64_t workspace_bytes, uint64_t present_total,
+                             uint64_t *status, void *stream);
+
 /* BISE payload decode, batched.  Replaces kernels.bise_decode_core
  * (kernels.py:128-159) / bise.bise_decode (bise.py:108-118).  payload i
  * starts at data + offs[i], has descriptor descs[i] and `count` values;

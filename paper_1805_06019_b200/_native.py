@@ -51,6 +51,10 @@ _SIGS = {
     "rlfc_decode_field": ["p", "i", "p", "i", "i", "p", "q", "q", "p", "p"],
     "rlfc_decode_field_simple": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "p"],
+    "rlfc_count_present": ["p", "p", "p"],
+    "rlfc_decode_workspace_bytes": ["p", "u", "p"],
+    "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
+                                 "u", "u", "p", "p"],
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
     "rlfc_render_slab": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
                          "i", "i", "p", "p"],
@@ -60,7 +64,8 @@ _SIGS = {
                                   "p", "p"],
     "rlfc_version": ["p", "i"],
 }
-_CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64}
+_CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64,
+       "u": ctypes.c_uint64}
 EXPORTS = tuple(_SIGS)
 
 

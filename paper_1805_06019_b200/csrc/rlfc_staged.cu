@@ -1,0 +1,1001 @@
+// rlfc_staged.cu -- staged full-field decode (sm_100a): index -> payloads -> blend.
+//
+// The reference decodes image by image and re-walks every record once per
+// image (decoder.py:187-210 -> kernels.py:219-242 -> decode_chain_core
+// kernels.py:162-216).  Here the work is split into three launches, each
+// with full-warp parallelism and no per-camera-row barriers:
+//
+//   k_index     one lane per record (channel, block): popcount of the
+//               presence bitmap (kernels.py:181-183) reserves a dense run of
+//               payload slots (one atomic per warp), then the lane walks the
+//               descriptors (kernels.py:185-200) and writes one entry per
+//               present node: payload byte offset, descriptor, channel,
+//               block.  Records with any anomaly are flagged.
+//   k_payloads  one lane per payload: BISE decode (kernels.py:128-159) with
+//               one state machine for all three modes -- a plain-bit payload
+//               is a "group" of one value with no pack -- over a sequential
+//               64-bit bit reader, dequantised (kernels.py:202-211) into the
+//               residual array.  A corrupt pack flags its record.
+//   k_blend     one CTA per (block row, camera row, TW-pixel column chunk),
+//               all S views: residual slots are found by popcount rank in the
+//               record bitmaps, clean (view, block) pairs are RGB(root)
+//               copies, dirty ones add their residuals, YCoCg-R inverse +
+//               clamp (colorspace.py:27-56), and TMA tensor stores write the
+//               staged rows straight to HBM.  (view, block) pairs touching a
+//               flagged record run the reference-order walk (walk_chain),
+//               which reproduces the reference's values and failure order.
+//
+// Workspace (caller-owned device memory, rlfc_decode_workspace_bytes):
+//   u64 slot counter | u32 rec_base[3*nblk] | u32 rec_flag[3*nblk] |
+//   uint2 entries[cap] | VT residuals[cap][B*B]   (VT int16 when the
+//   quantisation shift keeps |residual| <= 16392, else int32).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "rlfc_common.cuh"
+
+namespace rlfc {
+namespace staged {
+
+constexpr int MAXH = 8;
+constexpr int MAXS = 64;
+constexpr int THREADS = 256;
+constexpr uint32_t SKIP = 31;       // entry descriptor: slot not decoded
+constexpr int STRIP = 64;           // pixels per TMA box column (192 bytes)
+
+__device__ const DigitLut g_lut = make_digit_lut();
+__device__ const NodeBytes g_nb4 = make_node_bytes<16>();
+__device__ const NodeBytes g_nb8 = make_node_bytes<64>();
+__device__ const NodeBytes g_nb16 = make_node_bytes<256>();
+
+template <int BSQ>
+__device__ __forceinline__ const NodeBytes& node_bytes() {
+    return BSQ == 16 ? g_nb4 : BSQ == 64 ? g_nb8 : g_nb16;
+}
+
+struct Ws {
+    unsigned long long* counter;
+    uint32_t* rec_base;
+    uint32_t* rec_flag;
+    uint2* entries;
+    void* res;
+    uint8_t* root_rgb;     // RGB8 of every root sample, rows of rgb_stride bytes
+    int rgb_stride;
+    uint32_t* bm;          // [3*nblk][nwp] record bitmaps as aligned 32-bit words
+    uint32_t* rk;          // [3*nblk][nwp] slot of the first present node of each word
+    int nwp;
+    uint64_t cap;
+};
+
+static uint64_t al256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+static int value_bytes(const rlfc_field& f) { return f.quant_shift <= 4 ? 2 : 4; }
+
+// Carve the workspace; returns the bytes needed for `cap` payload slots.
+static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
+    const uint64_t nrec = 3ull * (uint64_t)f.wb * (uint64_t)f.hb;
+    const uint64_t bsq = (uint64_t)f.block * (uint64_t)f.block;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t o = off;
+        off = al256(off + bytes);
+        return o;
+    };
+    const int rgb_stride = (f.wp * 3 + 15) & ~15;
+    const int nwp = (f.m_nodes + 31) / 32 + 2;
+    const uint64_t o_cnt = take(8), o_base = take(4 * nrec), o_flag = take(4 * nrec), o_ent = take(8 * cap),
+                   o_res = take(cap * bsq * (uint64_t)value_bytes(f)),
+                   o_rgb = take((uint64_t)f.rsx * f.rsy * f.hp * (uint64_t)rgb_stride),
+                   o_bm = take(4 * nrec * (uint64_t)nwp), o_rk = take(4 * nrec * (uint64_t)nwp);
+    if (w) {
+        uint8_t* b = static_cast<uint8_t*>(base);
+        w->counter = reinterpret_cast<unsigned long long*>(b + o_cnt);
+        w->rec_base = reinterpret_cast<uint32_t*>(b + o_base);
+        w->rec_flag = reinterpret_cast<uint32_t*>(b + o_flag);
+        w->entries = reinterpret_cast<uint2*>(b + o_ent);
+        w->res = b + o_res;
+        w->root_rgb = b + o_rgb;
+        w->rgb_stride = rgb_stride;
+        w->bm = reinterpret_cast<uint32_t*>(b + o_bm);
+        w->rk = reinterpret_cast<uint32_t*>(b + o_rk);
+        w->nwp = nwp;
+        w->cap = cap;
+    }
+    return off;
+}
+
+// Record (c, blk) bounds: [off, end) inside channel c's SRV section, or false
+// when the offsets are inconsistent or the bitmap does not fit.
+__device__ __forceinline__ bool record_span(const rlfc_field& f, int c, int64_t blk, uint64_t& off,
+                                            uint64_t& len) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    off = f.offsets[c][blk];
+    const uint64_t end = blk + 1 < nblk ? f.offsets[c][blk + 1] : f.srv_len[c];
+    if (off > end || end > f.srv_len[c] || end - off < (uint64_t)f.bitmap_bytes) return false;
+    len = end - off;
+    return true;
+}
+
+// Present nodes among [0, n) of a record bitmap.
+__device__ __forceinline__ uint32_t popc_prefix(const uint8_t* rec, int n) {
+    uint32_t cnt = 0;
+    int n0 = 0;
+    for (; n0 + 32 <= n; n0 += 32) cnt += __popc(bitmap_word(rec, n0));
+    if (n0 < n) cnt += __popc(bitmap_word(rec, n0) & ((1u << (n - n0)) - 1u));
+    return cnt;
+}
+
+// ---- presence count (workspace sizing) -----------------------------------------
+__global__ void k_count_present(const __grid_constant__ rlfc_field f, unsigned long long* out) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t n = 0;
+    if (i < 3 * nblk) {
+        const int c = (int)(i / nblk);
+        const int64_t blk = i % nblk;
+        uint64_t off, len;
+        if (record_span(f, c, blk, off, len)) n = popc_prefix(f.srv[c] + off, f.m_nodes);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if ((threadIdx.x & 31) == 0 && n) atomicAdd(out, (unsigned long long)n);
+}
+
+// ---- pass 1: index -----------------------------------------------------------------
+// Levels >= k occupy serial nodes [0, node_end) (level h-1 first,
+// container.py:102-145); only those are indexed and decoded.
+template <int BSQ>
+__global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_field f, int k, int by_lo,
+                                                   int by_hi, Ws w) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t band = (int64_t)(by_hi - by_lo) * f.wb;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < 3 * band;
+    const int c = valid ? (int)(i / band) : 0;
+    const int64_t blk = valid ? (int64_t)by_lo * f.wb + i % band : 0;
+    const int node_end = f.level_base[k] + f.level_sx[k] * f.level_sy[k];
+    uint64_t off = 0, len = 0;
+    uint32_t flag = 0, count = 0;
+    if (valid) {
+        if (record_span(f, c, blk, off, len)) count = popc_prefix(f.srv[c] + off, node_end);
+        else flag = 1;
+    }
+    // dense slot run per record: warp scan + one atomic per warp
+    const int lane = threadIdx.x & 31;
+    uint32_t incl = count;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    unsigned long long wbase = 0;
+    if (lane == 31 && incl) wbase = atomicAdd(w.counter, (unsigned long long)incl);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    const uint64_t slot0 = wbase + incl - count;
+    if (!valid) return;
+    if (slot0 + count > w.cap) flag = 1;
+    uint32_t rank = 0;
+    if (!flag && count) {
+        const uint8_t* rec = f.srv[c] + off;
+        const NodeBytes& nb = node_bytes<BSQ>();
+        uint32_t cursor = (uint32_t)f.bitmap_bytes;
+        for (int n0 = 0; n0 < node_end && !flag; n0 += 32) {
+            uint32_t bits = bitmap_word(rec, n0);
+            if (node_end - n0 < 32) bits &= (1u << (node_end - n0)) - 1u;
+            while (bits) {
+                bits &= bits - 1u;
+                const int d = cursor < len ? rec[cursor] : NUM_DESC;
+                if (d >= NUM_DESC || cursor + nb.v[d] > len) {
+                    flag = 1;
+                    break;
+                }
+                w.entries[slot0 + rank] =
+                    make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
+                cursor += nb.v[d];
+                ++rank;
+            }
+        }
+    }
+    // every reserved slot below the capacity is written (SKIP when not decoded)
+    for (uint64_t r = rank; r < count && slot0 + r < w.cap; ++r) w.entries[slot0 + r] = make_uint2(0u, SKIP);
+    const int64_t ri = (int64_t)c * nblk + blk;
+    if (!flag) {
+        // bitmap words of levels >= k and the slot at each word start, for
+        // the blend's row masks and ranks (k_blend)
+        const uint8_t* rec = f.srv[c] + off;
+        uint32_t* bm = w.bm + ri * w.nwp;
+        uint32_t* rk = w.rk + ri * w.nwp;
+        uint32_t run = (uint32_t)slot0;
+        for (int wi = 0; wi < w.nwp; ++wi) {
+            const int n0 = wi * 32;
+            uint32_t word = 0;
+            if (n0 < node_end) {
+                word = bitmap_word(rec, n0);
+                if (node_end - n0 < 32) word &= (1u << (node_end - n0)) - 1u;
+            }
+            bm[wi] = word;
+            rk[wi] = run;
+            run += __popc(word);
+        }
+    }
+    w.rec_flag[ri] = flag;
+    w.rec_base[ri] = (uint32_t)slot0;
+}
+
+// ---- pass 2: payloads ----------------------------------------------------------------
+// Sequential LSB-first bit reader over a byte address (kernels.py:1-11 bit
+// order); reads at most 8 bytes past the last consumed bit (device SRV copies
+// carry 16 bytes of zero padding).
+struct BitReader {
+    const uint32_t* w;
+    uint64_t buf;
+    uint32_t n;
+    __device__ __forceinline__ explicit BitReader(const uint8_t* p) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+        const uint32_t sh = (uint32_t)(a & 3) * 8u;
+        buf = ((uint64_t)__ldg(w) | (uint64_t)__ldg(w + 1) << 32) >> sh;
+        n = 64u - sh;
+        w += 2;
+    }
+    __device__ __forceinline__ uint32_t get(uint32_t k) {     // k <= 11
+        if (n < 32u) {
+            buf |= (uint64_t)__ldg(w) << n;
+            ++w;
+            n += 32u;
+        }
+        const uint32_t v = (uint32_t)buf & ((1u << k) - 1u);
+        buf >>= k;
+        n -= k;
+        return v;
+    }
+};
+
+// kernels.py:202-211 dequantisation in 32-bit wrap arithmetic: identical to
+// the reference's int64 result truncated into its int32 accumulator.
+__device__ __forceinline__ int32_t deq(uint32_t z, int shift) {
+    if (shift >= 32) return dequant(z, shift);
+    const uint32_t mag = (((z + 1u) >> 1) << shift) + ((1u << shift) >> 1);
+    const uint32_t v = (z & 1u) ? 0u - mag : mag;
+    return z ? (int32_t)v : 0;
+}
+
+template <typename VT>
+__device__ __forceinline__ void store4(VT* p, const int32_t* v);
+template <>
+__device__ __forceinline__ void store4<int16_t>(int16_t* p, const int32_t* v) {
+    uint2 w;
+    w.x = ((uint32_t)v[0] & 0xFFFFu) | ((uint32_t)v[1] << 16);
+    w.y = ((uint32_t)v[2] & 0xFFFFu) | ((uint32_t)v[3] << 16);
+    *reinterpret_cast<uint2*>(p) = w;
+}
+template <>
+__device__ __forceinline__ void store4<int32_t>(int32_t* p, const int32_t* v) {
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
+}
+template <typename VT>
+__device__ __forceinline__ void add4(const VT* p, int32_t* v);
+template <>
+__device__ __forceinline__ void add4<int16_t>(const int16_t* p, int32_t* v) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
+    v[0] += (int32_t)(int16_t)(w.x & 0xFFFFu);
+    v[1] += (int32_t)w.x >> 16;
+    v[2] += (int32_t)(int16_t)(w.y & 0xFFFFu);
+    v[3] += (int32_t)w.y >> 16;
+}
+template <>
+__device__ __forceinline__ void add4<int32_t>(const int32_t* p, int32_t* v) {
+    const int4 w = __ldg(reinterpret_cast<const int4*>(p));
+    v[0] += w.x; v[1] += w.y; v[2] += w.z; v[3] += w.w;
+}
+
+template <int BSQ, typename VT>
+__global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w) {
+    const uint64_t n = min((uint64_t)*w.counter, w.cap);
+    const int shift = f.quant_shift;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    VT* res = static_cast<VT*>(w.res);
+    for (uint64_t slot = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < n;
+         slot += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 e = w.entries[slot];
+        const uint32_t d = e.y & 31u;
+        if (d >= (uint32_t)NUM_DESC) continue;
+        const int c = (int)(e.y >> 5) & 3;
+        const int mode = desc_mode((int)d);
+        const uint32_t b = (uint32_t)desc_bits((int)d);
+        // one group = G values behind a PB-bit pack (plain bits: G = 1, no pack)
+        const uint32_t G = mode == MODE_TRIT ? 5u : mode == MODE_QUINT ? 3u : 1u;
+        const uint32_t PB = mode == MODE_TRIT ? 8u : mode == MODE_QUINT ? 7u : 0u;
+        const uint32_t DB = mode == MODE_TRIT ? 2u : 3u;
+        const uint32_t DMASK = mode == MODE_TRIT ? 3u : mode == MODE_QUINT ? 7u : 0u;
+        const uint32_t PMAX = mode == MODE_TRIT ? 242u : 124u;
+        const uint16_t* L = mode == MODE_TRIT ? g_lut.trit : g_lut.quint;
+        BitReader br(f.srv[c] + e.x);
+        uint32_t gi = 0, digits = 0;
+        bool bad = false;
+        VT* out = res + slot * BSQ;
+        for (int q = 0; q < BSQ / 4; ++q) {
+            int32_t v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (gi == 0 && PB) {
+                    const uint32_t pk = br.get(PB);
+                    bad |= pk > PMAX;
+                    digits = L[pk <= PMAX ? pk : 0u];
+                }
+                const uint32_t low = br.get(b);
+                const uint32_t z = (((digits >> (DB * gi)) & DMASK) << b) | low;
+                gi = gi + 1 == G ? 0u : gi + 1;
+                v[j] = deq(z, shift);
+            }
+            store4<VT>(out + 4 * q, v);
+        }
+        if (bad) w.rec_flag[(int64_t)c * nblk + (e.y >> 7)] = 1u;   // kernels.py:147-150
+    }
+}
+
+// ---- pass 3: blend -------------------------------------------------------------------
+struct BlendParams {
+    rlfc_field f;
+    int k;
+    const int32_t* slots;
+    int by_lo;
+    uint8_t* rgb;
+    int64_t img_stride, row_stride;
+    uint64_t* status;
+    const uint32_t* rec_base;
+    const uint32_t* rec_flag;
+    const void* res;
+    const uint8_t* root_rgb_g;   // RGB8 of every root sample [root][hp][rgb_stride]
+    int rgb_stride;
+    const uint32_t* bm;          // record bitmap words / word ranks (k_index)
+    const uint32_t* rk;
+    int nwp;
+    int TW, NB, nchunks, nstrip;
+    int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
+    int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
+    int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
+    int off_flag, off_mask, off_sbase, off_roots, off_rgb, off_dmask, off_dpre, off_cnt, off_list, off_stage,
+        off_mbar;
+};
+
+__device__ __forceinline__ uint32_t pack4_sat(int32_t b0, int32_t b1, int32_t b2, int32_t b3) {
+    uint32_t hi, d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(hi) : "r"(b3), "r"(b2), "r"(0));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(b1), "r"(b0), "r"(hi));
+    return d;
+}
+
+// colorspace.py:27-36 on four pixels, packed to 12 RGB bytes.
+__device__ __forceinline__ void ycocg4_pack(const int32_t (*v)[4], uint32_t* o3) {
+    int32_t o[12];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int32_t tt = v[0][i] - (v[2][i] >> 1);
+        const int32_t bb = tt - (v[1][i] >> 1);
+        o[3 * i] = bb + v[1][i];
+        o[3 * i + 1] = v[2][i] + tt;
+        o[3 * i + 2] = bb;
+    }
+    o3[0] = pack4_sat(o[0], o[1], o[2], o[3]);
+    o3[1] = pack4_sat(o[4], o[5], o[6], o[7]);
+    o3[2] = pack4_sat(o[8], o[9], o[10], o[11]);
+}
+
+template <typename RT>
+__device__ __forceinline__ void load4s(const RT* p, int32_t* v) {
+    if (sizeof(RT) == 2) {
+        const uint2 w = *reinterpret_cast<const uint2*>(p);
+        v[0] = (int32_t)(int16_t)(w.x & 0xFFFFu);
+        v[1] = (int32_t)w.x >> 16;
+        v[2] = (int32_t)(int16_t)(w.y & 0xFFFFu);
+        v[3] = (int32_t)w.y >> 16;
+    } else {
+        const int4 w = *reinterpret_cast<const int4*>(p);
+        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+    }
+}
+
+// ---- root colours: RGB8 of every root sample (colorspace.py:27-56) -------------------
+template <typename RT>
+__global__ void __launch_bounds__(THREADS) k_root_rgb(const __grid_constant__ rlfc_field f, uint8_t* out,
+                                                      int rgb_stride, int y0, int y1) {
+    const int quads = f.wp / 4;
+    const int rows = y1 - y0;
+    const int64_t n = (int64_t)f.rsx * f.rsy * rows * quads;
+    const int64_t pl = (int64_t)f.hp * f.wp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int xq = (int)(i % quads);
+        const int64_t rr = i / quads;                  // root * rows + (y - y0)
+        const int y = y0 + (int)(rr % rows);
+        const int64_t r = rr / rows;
+        const int64_t ry = r * f.hp + y;
+        int32_t v[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const RT* src = reinterpret_cast<const RT*>(f.roots) + (r * 3 + c) * pl + (int64_t)y * f.wp + xq * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[c][j] = (int32_t)src[j];
+        }
+        ycocg4_pack(v, reinterpret_cast<uint32_t*>(out + ry * rgb_stride + xq * 12));
+    }
+}
+
+// Spread a level-l row mask over the 2^l views each node covers.
+__device__ __forceinline__ uint64_t spread(uint64_t m, int l) {
+    if (l == 0) return m;
+    const int span = 1 << l;
+    const uint64_t run = span >= 64 ? ~0ull : ((1ull << span) - 1ull);
+    uint64_t out = 0;
+    while (m) {
+        const int x = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        if ((x << l) < 64) out |= run << (x << l);
+    }
+    return out;
+}
+
+// position of the k-th (0-based) set bit of m (k < popcount(m))
+__device__ __forceinline__ int kth_bit(uint64_t m, int k) {
+    int pos = 0;
+    int c = __popc((uint32_t)m);
+    if (k >= c) { k -= c; m >>= 32; pos = 32; }
+    uint32_t w = (uint32_t)m;
+#pragma unroll
+    for (int half = 16; half >= 1; half >>= 1) {
+        c = __popc(w & ((1u << half) - 1u));
+        if (k >= c) { k -= c; w >>= half; pos += half; }
+    }
+    return pos;
+}
+
+// byte offset of pixel (view s, row, tile column px) in the strip-major
+// staging buffer [strip][S][B][STRIP*3]
+template <int B>
+__device__ __forceinline__ int stage_off(int S, int s, int row, int px) {
+    return (((px / STRIP) * S + s) * B + row) * (STRIP * 3) + (px % STRIP) * 3;
+}
+
+// Reference-order decode of one (view, block) whose records carry an anomaly:
+// walk_chain per channel (kernels.py:162-216) into the staging buffer, or the
+// failure word with the reference's key.
+template <int B>
+__device__ __noinline__ void unit_fallback(const BlendParams& P, uint8_t* stage, int s, int t, int by, int bx,
+                                           int px0) {
+    const rlfc_field& f = P.f;
+    constexpr int BSQ = B * B;
+    int32_t acc[3][BSQ];
+    const int img = s * f.t_count + t;
+    for (int c = 0; c < 3; ++c) {
+        for (int yy = 0; yy < B; ++yy)
+            for (int xx = 0; xx < B; ++xx) acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+        const uint8_t* rec = f.srv[c] + f.offsets[c][(int64_t)by * f.wb + bx];
+        const int st = walk_chain<BSQ>(f, rec, s, t, P.k, acc[c], g_lut, node_bytes<BSQ>());
+        if (st) {
+            report(P.status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
+            return;
+        }
+    }
+    for (int yy = 0; yy < B; ++yy)
+        for (int xx = 0; xx < B; ++xx) {
+            uint32_t r, g, b;
+            const int j = yy * B + xx;
+            ycocg_to_rgb8(acc[0][j], acc[1][j], acc[2][j], r, g, b);
+            uint8_t* o = stage + stage_off<B>(f.s_count, s, yy, px0 + xx);
+            o[0] = (uint8_t)r;
+            o[1] = (uint8_t)g;
+            o[2] = (uint8_t)b;
+        }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int B, typename VT, typename RT>
+__global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ BlendParams P,
+                                                   const __grid_constant__ CUtensorMap out_map,
+                                                   const __grid_constant__ CUtensorMap rgb_map,
+                                                   const __grid_constant__ CUtensorMap root_map) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr int BSQ = B * B;
+    constexpr int QB = B / 4;                      // pixel quads per block row
+    constexpr int TPU = B * QB;                    // tasks per (view, block) unit
+    const rlfc_field& f = P.f;
+    const int tid = threadIdx.x;
+    const int chunk = blockIdx.x % P.nchunks, t = blockIdx.x / P.nchunks;
+    const int by = P.by_lo + blockIdx.y;
+    const int NB = P.NB, TW = P.TW, NR = 3 * NB;
+    const int bx0 = chunk * NB;
+    const int nb = min(NB, f.wb - bx0);
+    const int h = f.tree_height, k = P.k, S = f.s_count, T = f.t_count;
+    const int nlev = h - k;
+    const int ry = t >> h;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+
+    uint32_t* rflag = reinterpret_cast<uint32_t*>(smem + P.off_flag);       // [NR]
+    uint64_t* mask = reinterpret_cast<uint64_t*>(smem + P.off_mask);        // [nlev][NR]
+    uint32_t* sbase = reinterpret_cast<uint32_t*>(smem + P.off_sbase);      // [nlev][NR]
+    RT* roots = reinterpret_cast<RT*>(smem + P.off_roots);                 // [rsx][3][B][TW]
+    uint8_t* root_rgb = smem + P.off_rgb;                                   // [strip][rsx][B][STRIP*3] (manual)
+    uint64_t* dmask = reinterpret_cast<uint64_t*>(smem + P.off_dmask);      // [NB]
+    int32_t* dpre = reinterpret_cast<int32_t*>(smem + P.off_dpre);          // [NB]
+    int32_t* cnt = reinterpret_cast<int32_t*>(smem + P.off_cnt);            // [0] units, [1] warp-0 total
+    uint2* list = reinterpret_cast<uint2*>(smem + P.off_list);              // [S*NB]
+    uint8_t* stage = smem + P.off_stage;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_mbar);
+
+    // ---- TMA: RGB(root) rows into every view's staging rows, raw roots ----------------
+    if (P.tma_in && tid == 0) {
+        const uint32_t bar = smem_u32(mbar);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t bytes =
+            (uint32_t)(P.nstrip * S * B * STRIP * 3) + (uint32_t)(f.rsx * 3 * B * TW * (int)sizeof(RT));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        for (int st = 0; st < P.nstrip; ++st)
+            for (int s = 0; s < S; ++s)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                    "%4}], [%5];" ::"r"(smem_u32(stage + ((st * S + s) * B) * (STRIP * 3))),
+                    "l"(&rgb_map), "r"((bx0 * B + st * STRIP) * 3), "r"(by * B), "r"((s >> h) * f.rsy + ry), "r"(bar)
+                    : "memory");
+        for (int rx = 0; rx < f.rsx; ++rx)
+            for (int c = 0; c < 3; ++c)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                    "%4}], [%5];" ::"r"(smem_u32(roots + (rx * 3 + c) * B * TW)),
+                    "l"(&root_map), "r"(bx0 * B), "r"(by * B), "r"((rx * f.rsy + ry) * 3 + c), "r"(bar)
+                    : "memory");
+    }
+
+    // ---- records: residual row masks and slot bases of this camera row --------
+    for (int r = tid; r < NR; r += THREADS) {
+        const int c = r / NB, b = r - c * NB;
+        uint32_t fl = 0;
+        if (b < nb && nlev > 0) {
+            const int64_t blk = (int64_t)by * f.wb + bx0 + b;
+            const int64_t ri = (int64_t)c * nblk + blk;
+            fl = P.rec_flag[ri];
+            if (!fl) {
+                const uint32_t* bmr = P.bm + ri * P.nwp;
+                const uint32_t* rkr = P.rk + ri * P.nwp;
+                for (int l = h - 1; l >= k; --l) {
+                    const int sx = f.level_sx[l];
+                    const int n0 = f.level_base[l] + (t >> l) * sx;
+                    const int wi = n0 >> 5, o = n0 & 31;
+                    const uint32_t lo = __ldg(bmr + wi), hi = __ldg(bmr + wi + 1);
+                    uint64_t m = __funnelshift_r(lo, hi, o);
+                    if (sx > 32) m |= (uint64_t)__funnelshift_r(hi, __ldg(bmr + wi + 2), o) << 32;
+                    if (sx < 64) m &= (1ull << sx) - 1ull;
+                    mask[(l - k) * NR + r] = m;
+                    sbase[(l - k) * NR + r] = __ldg(rkr + wi) + __popc(lo & ((1u << o) - 1u));
+                }
+            }
+        } else if (nlev > 0) {
+            for (int l = k; l < h; ++l) mask[(l - k) * NR + r] = 0;
+        }
+        rflag[r] = fl;
+    }
+    // ---- manual path: roots of this camera row and their RGB8 -------------------------
+    if (!P.tma_in) {
+        const int quads = TW / 4;
+        const int64_t pl = (int64_t)f.hp * f.wp;
+        for (int it = tid; it < f.rsx * B * quads; it += THREADS) {
+            const int xq = it % quads, rr = (it / quads) % B, rx = it / (quads * B);
+            const int gx = bx0 * B + xq * 4;
+            int32_t v[3][4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const RT* src = reinterpret_cast<const RT*>(f.roots) + (((int64_t)rx * f.rsy + ry) * 3 + c) * pl +
+                                (int64_t)(by * B + rr) * f.wp + gx;
+                if (P.roots_vec && gx + 4 <= f.wp) {
+                    load4s<RT>(src, v[c]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[c][j] = gx + j < f.wp ? (int32_t)src[j] : 0;
+                }
+                RT* dst = roots + ((rx * 3 + c) * B + rr) * TW + xq * 4;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dst[j] = (RT)v[c][j];
+            }
+            const int px = xq * 4;
+            uint32_t* o = reinterpret_cast<uint32_t*>(root_rgb + (((px / STRIP) * f.rsx + rx) * B + rr) * (STRIP * 3) +
+                                                      (px % STRIP) * 3);
+            ycocg4_pack(v, o);
+        }
+    }
+    __syncthreads();
+
+    // ---- dirty views per block (warps 0-1, one block per lane) | manual prefill ------
+    const int lane = tid & 31;
+    if (tid < 64) {
+        const int b = tid;
+        uint64_t want = S >= 64 ? ~0ull : ((1ull << S) - 1ull);
+        if (P.slots) {
+            const bool w0 = lane < S && P.slots[lane * T + t] >= 0;
+            const bool w1 = lane + 32 < S && P.slots[(lane + 32) * T + t] >= 0;
+            want = (uint64_t)__ballot_sync(0xffffffffu, w0) | (uint64_t)__ballot_sync(0xffffffffu, w1) << 32;
+        }
+        uint64_t dirty = 0;
+        bool fb = false;
+        if (b < nb) {
+            for (int c = 0; c < 3; ++c) fb |= rflag[c * NB + b] != 0;
+            if (fb) {
+                dirty = ~0ull;
+            } else {
+                for (int l = k; l < h; ++l) {
+                    uint64_t ml = 0;
+                    for (int c = 0; c < 3; ++c) ml |= mask[(l - k) * NR + c * NB + b];
+                    dirty |= spread(ml, l);
+                }
+            }
+            dirty &= want;
+        }
+        const int n = __popcll(dirty);
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (tid == 31) cnt[1] = incl;
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        const int base = tid >= 32 ? cnt[1] : 0;
+        if (b < NB) {
+            dmask[b] = dirty;
+            dpre[b] = base + incl - n;
+        }
+        if (fb && b < NB) rflag[b] = 2u;                 // block needs the reference-order walk
+        if (tid == 63) cnt[0] = base + incl;
+    } else if (!P.tma_in) {
+        // staging[strip][s][row] <- root_rgb[strip][s >> h][row]: one warp per
+        // staged (strip, view), B*12 16-byte copies
+        constexpr int V = B * STRIP * 3 / 16;
+        for (int sv = (tid >> 5) - 2; sv < P.nstrip * S; sv += THREADS / 32 - 2) {
+            const int st = sv / S, s = sv - st * S;
+            const uint4* src = reinterpret_cast<const uint4*>(root_rgb + (st * f.rsx + (s >> h)) * B * (STRIP * 3));
+            uint4* dst = reinterpret_cast<uint4*>(stage + sv * B * (STRIP * 3));
+            for (int v = lane; v < V; v += 32) dst[v] = src[v];
+        }
+    }
+    __syncthreads();
+
+    // ---- dirty (view, block) units with their presence bits (bit 3(l-k)+c) ---------
+    const int units = cnt[0];
+    for (int u = tid; u < units; u += THREADS) {
+        int b = 0;
+#pragma unroll
+        for (int step = 32; step > 0; step >>= 1)
+            if (b + step < NB && dpre[b + step] <= u) b += step;
+        const int s = kth_bit(dmask[b], u - dpre[b]);
+        const bool fb = rflag[b] == 2u;
+        uint32_t pres = 0;
+        if (!fb) {
+            for (int l = k; l < h; ++l) {
+                const int x = s >> l;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    pres |= (uint32_t)((mask[(l - k) * NR + c * NB + b] >> x) & 1ull) << (3 * (l - k) + c);
+            }
+        }
+        list[u] = make_uint2((uint32_t)s | (uint32_t)b << 8 | (fb ? 1u << 16 : 0u), pres);
+    }
+    if (P.tma_in) {
+        const uint32_t bar = smem_u32(mbar);
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(bar)
+                : "memory");
+    }
+    __syncthreads();
+
+    // ---- dirty units: root + present residuals, YCoCg-R inverse, clamp, pack ----------
+    {
+        const VT* res = static_cast<const VT*>(P.res);
+        for (int it = tid; it < units * TPU; it += THREADS) {
+            const int u = it / TPU, q = it - u * TPU;
+            const int row = q / QB, quad = q - row * QB;
+            const uint2 e = list[u];
+            const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
+            if (e.x >> 16) {
+                if (q == 0) unit_fallback<B>(P, stage, s, t, by, bx0 + b, b * B);
+                continue;
+            }
+            const int px = b * B + quad * 4;
+            const int rx = s >> h;
+            int32_t v[3][4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) load4s<RT>(roots + ((rx * 3 + c) * B + row) * TW + px, v[c]);
+            const int voff = row * B + quad * 4;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                uint32_t pc = e.y & (0x249249u << c);        // bits 3i + c: levels k + i
+                while (pc) {
+                    const int bit = __ffs(pc) - 1;
+                    pc &= pc - 1u;
+                    const int li = bit / 3;
+                    const int r = li * NR + c * NB + b;
+                    const uint64_t m = mask[r];
+                    const int x = s >> (k + li);
+                    const uint32_t slot = sbase[r] + (uint32_t)__popcll(m & ((1ull << x) - 1ull));
+                    add4<VT>(res + (uint64_t)slot * BSQ + voff, v[c]);
+                }
+            }
+            ycocg4_pack(v, reinterpret_cast<uint32_t*>(stage + stage_off<B>(S, s, row, px)));
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+
+    // ---- store ------------------------------------------------------------------------
+    const int nrows_band = min(by * B + B, f.height) - by * B;   // rows of this block row
+    if (P.store_mode == 2) {
+        if (tid == 0) {
+            for (int st = 0; st < P.nstrip; ++st) {
+                const int x0 = (bx0 * B + st * STRIP) * 3;
+                if (x0 >= f.width * 3) break;
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                        &out_map),
+                    "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0),
+                    "r"(smem_u32(stage + st * S * B * STRIP * 3))
+                    : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+    } else {
+        // per (view, row, strip): bulk copy when the strip is whole, else bytes
+        bool issued = false;
+        for (int it = tid; it < S * B * P.nstrip; it += THREADS) {
+            const int st = it % P.nstrip, rr = (it / P.nstrip) % B, s = it / (P.nstrip * B);
+            if (rr >= nrows_band) continue;
+            const int img = s * T + t;
+            const int slot = P.slots ? P.slots[img] : img;
+            if (slot < 0) continue;
+            const int x0 = bx0 * B + st * STRIP;
+            if (x0 >= f.width) continue;
+            const int npx = min(STRIP, f.width - x0);
+            uint8_t* orow = P.rgb + (int64_t)slot * P.img_stride + (int64_t)((by - P.by_lo) * B + rr) * P.row_stride +
+                            (int64_t)x0 * 3;
+            const uint8_t* src = stage + stage_off<B>(S, s, rr, st * STRIP);
+            if (P.store_mode == 1 && npx == STRIP) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(orow),
+                             "r"(smem_u32(src)), "n"(STRIP * 3)
+                             : "memory");
+                issued = true;
+            } else {
+                for (int j = 0; j < npx * 3; ++j) orow[j] = src[j];
+            }
+        }
+        if (issued) {
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+static bool encode_map(CUtensorMap* map, CUtensorMapDataType dt, cuuint32_t rank, void* base, const cuuint64_t* dims,
+                       const cuuint64_t* strides, const cuuint32_t* box) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    return enc(map, dt, rank, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Plan {
+    BlendParams P;
+    int smem;
+};
+
+// Blend geometry and shared-memory layout; false when outside the envelope.
+template <typename RT>
+static bool plan_blend(const rlfc_field& f, int k, Plan& pl) {
+    const int B = f.block, S = f.s_count, h = f.tree_height;
+    BlendParams& P = pl.P;
+    auto al = [](int x) { return (x + 127) & ~127; };
+    for (int TW : {128, 64}) {
+        if (TW % B) continue;
+        const int NB = TW / B;
+        if (NB > 64) continue;
+        const int NR = 3 * NB, nlev = h - k;
+        int off = 0;
+        P.off_mbar = off;  off = al(off + 16);
+        P.off_flag = off;  off = al(off + NR * 4);
+        P.off_mask = off;  off = al(off + nlev * NR * 8);
+        P.off_sbase = off; off = al(off + nlev * NR * 4);
+        P.off_roots = off; off = al(off + f.rsx * 3 * B * TW * (int)sizeof(RT));
+        P.off_rgb = off;   off = al(off + f.rsx * B * TW * 3);
+        P.off_dmask = off; off = al(off + NB * 8);
+        P.off_dpre = off;  off = al(off + NB * 4);
+        P.off_cnt = off;   off = al(off + 16);
+        P.off_list = off;  off = al(off + S * NB * 8);
+        P.off_stage = off; off = al(off + S * B * TW * 3);
+        if (off <= 100 * 1024) {
+            P.TW = TW;
+            P.NB = NB;
+            P.nstrip = TW / STRIP;
+            P.nchunks = (f.wb + NB - 1) / NB;
+            pl.smem = off;
+            return true;
+        }
+    }
+    return false;
+}
+
+template <int B, typename VT, typename RT>
+static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
+                  int64_t img_stride, int64_t row_stride, const Ws& w, uint64_t* status, cudaStream_t stream) {
+    constexpr int BSQ = B * B;
+    Plan pl{};
+    if (!plan_blend<RT>(f, k, pl)) return RLFC_ERR_ARGUMENT;
+    BlendParams& P = pl.P;
+    P.f = f;
+    P.k = k;
+    P.slots = slots;
+    P.by_lo = by_lo;
+    P.rgb = rgb;
+    P.img_stride = img_stride;
+    P.row_stride = row_stride;
+    P.status = status;
+    P.rec_base = w.rec_base;
+    P.rec_flag = w.rec_flag;
+    P.res = w.res;
+    P.root_rgb_g = w.root_rgb;
+    P.rgb_stride = w.rgb_stride;
+    P.bm = w.bm;
+    P.rk = w.rk;
+    P.nwp = w.nwp;
+    P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
+    const int h = f.tree_height, S = f.s_count;
+    // output path
+    const bool aligned = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride) & 15) == 0;
+    CUtensorMap out_map, rgb_map, root_map;
+    memset(&out_map, 0, sizeof(out_map));
+    memset(&rgb_map, 0, sizeof(rgb_map));
+    memset(&root_map, 0, sizeof(root_map));
+    P.store_mode = aligned ? 1 : 0;
+    const int nrows = min(by_hi * B, f.height) - by_lo * B;
+    if (aligned && !slots && S <= 256) {
+        const cuuint64_t dims[4] = {(cuuint64_t)f.width * 3, (cuuint64_t)nrows, (cuuint64_t)f.t_count,
+                                    (cuuint64_t)S};
+        const cuuint64_t strides[3] = {(cuuint64_t)row_stride, (cuuint64_t)img_stride,
+                                       (cuuint64_t)img_stride * f.t_count};
+        const cuuint32_t box[4] = {(cuuint32_t)(STRIP * 3), (cuuint32_t)B, 1u, (cuuint32_t)S};
+        if (encode_map(&out_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, rgb, dims, strides, box)) P.store_mode = 2;
+    }
+    // input path: RGB(root) rows + raw roots by TMA when the layouts allow it
+    P.tma_in = 0;
+    const int nroot = f.rsx * f.rsy;
+    if (w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 && ((f.wp * (int)sizeof(RT)) % 16) == 0) {
+        const cuuint64_t d1[3] = {(cuuint64_t)f.wp * 3, (cuuint64_t)f.hp, (cuuint64_t)nroot};
+        const cuuint64_t s1[2] = {(cuuint64_t)w.rgb_stride, (cuuint64_t)w.rgb_stride * f.hp};
+        const cuuint32_t b1[3] = {(cuuint32_t)(STRIP * 3), (cuuint32_t)B, 1u};
+        const cuuint64_t d2[3] = {(cuuint64_t)f.wp, (cuuint64_t)f.hp, (cuuint64_t)nroot * 3};
+        const cuuint64_t s2[2] = {(cuuint64_t)f.wp * sizeof(RT), (cuuint64_t)f.wp * f.hp * sizeof(RT)};
+        const cuuint32_t b2[3] = {(cuuint32_t)P.TW, (cuuint32_t)B, 1u};
+        if (encode_map(&rgb_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, w.root_rgb, d1, s1, b1) &&
+            encode_map(&root_map, sizeof(RT) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_INT32,
+                       3, const_cast<void*>(f.roots), d2, s2, b2))
+            P.tma_in = 1;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (P.tma_in) {
+        const int64_t n = (int64_t)nroot * (by_hi - by_lo) * B * (f.wp / 4);
+        const int64_t want = (n + THREADS - 1) / THREADS;
+        k_root_rgb<RT><<<(unsigned)(want < sms * 16 ? want : sms * 16), THREADS, 0, stream>>>(
+            f, w.root_rgb, w.rgb_stride, by_lo * B, by_hi * B);
+    }
+    if (k < h) {
+        cudaMemsetAsync(w.counter, 0, 8, stream);
+        const int64_t nrec = 3ll * (by_hi - by_lo) * f.wb;
+        k_index<BSQ><<<(unsigned)((nrec + THREADS - 1) / THREADS), THREADS, 0, stream>>>(f, k, by_lo, by_hi, w);
+        const uint64_t want = (w.cap + THREADS - 1) / THREADS;
+        const uint64_t cap_grid = (uint64_t)sms * 16;
+        const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
+        k_payloads<BSQ, VT><<<grid, THREADS, 0, stream>>>(f, w);
+    }
+    auto kern = k_blend<B, VT, RT>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
+    const dim3 grid((unsigned)(P.nchunks * f.t_count), (unsigned)(by_hi - by_lo));
+    kern<<<grid, THREADS, pl.smem, stream>>>(P, out_map, rgb_map, root_map);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "rlfc_b200: staged decode launch error: %s\n", cudaGetErrorString(e));
+        return RLFC_ERR_CUDA;
+    }
+    return RLFC_OK;
+}
+
+static bool in_envelope(const rlfc_field& f) {
+    if (f.tree_height < 1 || f.tree_height > MAXH || f.s_count > MAXS || f.t_count > 65535) return false;
+    if (f.block != 4 && f.block != 8 && f.block != 16) return false;
+    for (int l = 0; l < f.tree_height; ++l)
+        if (f.level_sx[l] > 64) return false;
+    if ((int64_t)f.wb * f.hb >= (1ll << 25)) return false;        // entry block field
+    for (int c = 0; c < 3; ++c)
+        if (f.srv_len[c] >= (1ull << 32) - 64) return false;      // 32-bit payload offsets
+    return true;
+}
+
+}  // namespace staged
+}  // namespace rlfc
+
+using namespace rlfc;
+
+extern "C" int rlfc_count_present(const rlfc_field* f, uint64_t* count, void* stream) {
+    if (!f || !count) return RLFC_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(count, 0, 8, s);
+    const int64_t nrec = 3ll * f->wb * f->hb;
+    if (nrec > 0)
+        staged::k_count_present<<<(unsigned)((nrec + 255) / 256), 256, 0, s>>>(
+            *f, reinterpret_cast<unsigned long long*>(count));
+    return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
+extern "C" int rlfc_decode_workspace_bytes(const rlfc_field* f, uint64_t present_total, uint64_t* bytes) {
+    if (!f || !bytes) return RLFC_ERR_ARGUMENT;
+    *bytes = staged::carve(*f, nullptr, present_total, nullptr);
+    return staged::in_envelope(*f) ? RLFC_OK : RLFC_ERR_ARGUMENT;
+}
+
+extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level, const int32_t* image_slots,
+                                        int32_t by_lo, int32_t by_hi, uint8_t* rgb, int64_t img_stride,
+                                        int64_t row_stride, void* workspace, uint64_t workspace_bytes,
+                                        uint64_t present_total, uint64_t* status, void* stream) {
+    if (!f || !rgb || !status || !workspace) return RLFC_ERR_ARGUMENT;
+    if (stop_level < 0 || stop_level > f->tree_height || by_lo < 0 || by_hi > f->hb || by_lo > by_hi)
+        return RLFC_ERR_ARGUMENT;
+    if (!staged::in_envelope(*f)) return RLFC_ERR_ARGUMENT;
+    if (by_lo == by_hi) return RLFC_OK;
+    staged::Ws w;
+    if (staged::carve(*f, workspace, present_total, &w) > workspace_bytes) return RLFC_ERR_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0) return RLFC_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool small = f->quant_shift <= 4, r16 = f->roots_i16 != 0;
+#define RLFC_STAGED(B_)                                                                                            \
+    if (small && r16)                                                                                              \
+        return staged::launch<B_, int16_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
+                                                    row_stride, w, status, s);                                     \
+    if (small)                                                                                                     \
+        return staged::launch<B_, int16_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
+                                                    row_stride, w, status, s);                                     \
+    if (r16)                                                                                                       \
+        return staged::launch<B_, int32_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
+                                                    row_stride, w, status, s);                                     \
+    return staged::launch<B_, int32_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,       \
+                                                row_stride, w, status, s);
+    switch (f->block) {
+        case 4: { RLFC_STAGED(4) }
+        case 8: { RLFC_STAGED(8) }
+        case 16: { RLFC_STAGED(16) }
+        default: return RLFC_ERR_ARGUMENT;
+    }
+#undef RLFC_STAGED
+}

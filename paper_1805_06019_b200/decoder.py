@@ -88,6 +88,40 @@ class DeviceField:
         f.tile_bytes_max = tile_bytes_max(header, offsets)
         self.cfield = f
         self.ref = ctypes.byref(f)
+        self._ws_lock = threading.Lock()
+        self._ws = {}
+        self._ws_bytes = 0
+        self._present = None
+
+    def staged_workspace(self, stream_handle):
+        """(tensor, bytes, present_total) for the staged decode on one CUDA
+        stream, allocated on first use.  present_total (the number of
+        present nodes over all records) is counted on the device once per
+        field; the workspace holds the record index, the payload entries and
+        the decoded residuals (rlfc_staged.cu)."""
+        torch = _torch()
+        L = _native.lib()
+        with self._ws_lock:
+            if self._present is None:
+                cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+                with torch.cuda.device(self.device):
+                    _native.check(L.rlfc_count_present(self.ref, cnt.data_ptr(),
+                                                       _stream()),
+                                  "rlfc_count_present")
+                self._present = int(cnt.item())
+                need = ctypes.c_uint64(0)
+                rc = L.rlfc_decode_workspace_bytes(self.ref, self._present,
+                                                   ctypes.byref(need))
+                self._ws_bytes = int(need.value) if rc == _native.RLFC_OK \
+                    else 0
+            if not self._ws_bytes:
+                return None
+            ws = self._ws.get(stream_handle)
+            if ws is None:
+                ws = torch.empty(self._ws_bytes, dtype=torch.uint8,
+                                 device=self.device)
+                self._ws[stream_handle] = ws
+            return ws, self._ws_bytes, self._present
 
     @property
     def hbm_bytes(self):
@@ -248,14 +282,16 @@ def decode_planes(state, planes, stop_level=0, device=None):
 
 
 def decode_field(state, stop_level=0, images=None, rows=None, out=None,
-                 device=None, kernel="fused", check=True):
+                 device=None, kernel="staged", check=True):
     """Decode many camera images straight into an RGB8 CUDA tensor.
 
     images: None for the whole (S, T) grid -- the result is (S, T, H, W, 3)
     -- or a sequence of (s, t) pairs -- the result is (n, H, W, 3) in that
     order.  rows: optional block-row band (by_lo, by_hi); the result then
-    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "fused" (the
-    tiled sm_100a kernel) or "simple" (per-block kernel).  With check, a
+    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "staged"
+    (index -> payload decode -> blend, rlfc_staged.cu; falls back to
+    "fused" outside its envelope), "fused" (the single tiled kernel,
+    rlfc_field.cu) or "simple" (per-block kernel).  With check, a
     corrupt stream raises the FormatError the reference raises first.
     Returns (tensor, status) where status is the device status word tensor.
     """
@@ -291,15 +327,32 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
             not out.is_contiguous():
         raise ValueError(f"out must be a contiguous uint8 tensor {shape}")
     status = torch.zeros(1, dtype=torch.int64, device=df.device)
+    if kernel not in ("staged", "fused", "simple"):
+        raise ValueError(f"unknown decode kernel {kernel!r}")
     if nimg and nrows:
-        fn = _native.lib().rlfc_decode_field if kernel == "fused" else \
-            _native.lib().rlfc_decode_field_simple
+        L = _native.lib()
+        slots_p = None if slots_t is None else slots_t.data_ptr()
         with torch.cuda.device(df.device):
-            _native.check(fn(
-                df.ref, stop_level,
-                None if slots_t is None else slots_t.data_ptr(), by_lo, by_hi,
-                out.data_ptr(), nrows * W * 3, W * 3, status.data_ptr(),
-                _stream()), "rlfc_decode_field")
+            done = False
+            if kernel == "staged":
+                stream = _stream()
+                ws = df.staged_workspace(stream)
+                if ws is not None:
+                    rc = L.rlfc_decode_field_staged(
+                        df.ref, stop_level, slots_p, by_lo, by_hi,
+                        out.data_ptr(), nrows * W * 3, W * 3,
+                        ws[0].data_ptr(), ws[1], ws[2], status.data_ptr(),
+                        stream)
+                    if rc != _native.RLFC_ERR_ARGUMENT:
+                        _native.check(rc, "rlfc_decode_field_staged")
+                        done = True
+            if not done:
+                fn = L.rlfc_decode_field_simple if kernel == "simple" else \
+                    L.rlfc_decode_field
+                _native.check(fn(
+                    df.ref, stop_level, slots_p, by_lo, by_hi,
+                    out.data_ptr(), nrows * W * 3, W * 3, status.data_ptr(),
+                    _stream()), "rlfc_decode_field")
     if check:
         _raise_word(status.cpu().item())
     return out, status

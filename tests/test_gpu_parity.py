@@ -36,10 +36,12 @@ def test_decode_all_every_level(rl, name):
     g = load_golden(name)
     st = state_for(rl, name)
     for k in range(g["meta"]["h"] + 1):
-        fused, _ = rl.decode_field(st, k)
+        staged, _ = rl.decode_field(st, k)
+        fused, _ = rl.decode_field(st, k, kernel="fused")
         simple, _ = rl.decode_field(st, k, kernel="simple")
-        f = fused.cpu().numpy()
+        f = staged.cpu().numpy()
         assert sha(f) == str(g[f"all_k{k}_sha"]), (name, k)
+        assert np.array_equal(f, fused.cpu().numpy()), (name, k)
         assert np.array_equal(f, simple.cpu().numpy()), (name, k)
     grid = rl.decode_all(st)
     assert sha(grid.rgb) == str(g["all_k0_sha"])
@@ -106,20 +108,90 @@ def test_render_batch_equals_single(rl):
         assert np.array_equal(img, rl.render_view(st, p))
 
 
-def test_bands_and_subsets(rl):
-    st = state_for(rl, "mid17_r4")
-    full, _ = rl.decode_field(st)
+@pytest.mark.parametrize("kernel", ["staged", "fused"])
+@pytest.mark.parametrize("name", ["mid17_r4", "b8_h2", "b16_h4", "odd_3x5"])
+def test_bands_and_subsets(rl, kernel, name):
+    st = state_for(rl, name)
+    full, _ = rl.decode_field(st, kernel="simple")
     full = full.cpu().numpy()
+    S, T = st.header.s_count, st.header.t_count
     hb = st.header.block_grid[1]
     B = st.header.block_size
-    for lo, hi in [(0, 3), (3, 9), (9, hb), (5, 5)]:
-        band, _ = rl.decode_field(st, rows=(lo, hi))
+    for lo, hi in [(0, 3), (3, min(9, hb)), (min(9, hb), hb), (2, 2)]:
+        lo, hi = min(lo, hb), min(hi, hb)
+        for k in (0, 1):
+            band, _ = rl.decode_field(st, k, rows=(lo, hi), kernel=kernel)
+            ref, _ = rl.decode_field(st, k, rows=(lo, hi), kernel="simple")
+            assert np.array_equal(band.cpu().numpy(), ref.cpu().numpy())
+        band, _ = rl.decode_field(st, rows=(lo, hi), kernel=kernel)
         assert np.array_equal(band.cpu().numpy(),
                               full[:, :, lo * B:hi * B])
-    imgs = [(16, 0), (3, 7), (0, 16), (8, 8)]
-    sub, _ = rl.decode_field(st, images=imgs)
+    imgs = [(S - 1, 0), (min(3, S - 1), min(2, T - 1)), (0, T - 1),
+            (S // 2, T // 2)]
+    imgs = list(dict.fromkeys(imgs))
+    sub, _ = rl.decode_field(st, images=imgs, kernel=kernel)
     for i, (s, t) in enumerate(imgs):
         assert np.array_equal(sub[i].cpu().numpy(), full[s, t])
+    sub, _ = rl.decode_field(st, images=imgs, rows=(1, min(4, hb)),
+                             kernel=kernel)
+    for i, (s, t) in enumerate(imgs):
+        assert np.array_equal(sub[i].cpu().numpy(),
+                              full[s, t, B:min(4, hb) * B])
+
+
+@pytest.mark.parametrize("name", ["kat8_default", "mid17_r4", "b8_h2",
+                                  "b16_h4", "grid32", "cfg1_h3_r4"])
+def test_staged_path_taken(rl, name):
+    """Inside its envelope the staged kernels really run (no silent
+    fallback to the single-kernel path)."""
+    import ctypes
+    from paper_1805_06019_b200 import _native
+    st = state_for(rl, name)
+    df = st.device_field()
+    ws, nbytes, present = df.staged_workspace(0)
+    hdr = st.header
+    out = torch.empty((hdr.s_count, hdr.t_count, hdr.height, hdr.width, 3),
+                      dtype=torch.uint8, device="cuda")
+    status = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rc = _native.lib().rlfc_decode_field_staged(
+        df.ref, 0, None, 0, hdr.block_grid[1], out.data_ptr(),
+        hdr.height * hdr.width * 3, hdr.width * 3, ws.data_ptr(), nbytes,
+        present, status.data_ptr(), 0)
+    assert rc == _native.RLFC_OK
+    torch.cuda.synchronize()
+    assert status.item() == 0
+    assert sha(out.cpu().numpy()) == str(load_golden(name)["all_k0_sha"])
+
+
+@pytest.mark.parametrize("name", ["kat8_default", "mid17_r4", "b8_h2",
+                                  "b16_h4", "alldesc_b4"])
+def test_staged_fuzz_matches_simple(rl, name):
+    """Random SRV corruptions: the staged path reports the same failure word
+    (same key, same code) as the per-block kernel, and identical pixels when
+    the reference would not raise."""
+    from paper_1805_06019_b200 import container
+    data = load_stream(name)
+    hdr = container.parse_header(data)
+    starts, _ = container.section_offsets(hdr)
+    rng = np.random.default_rng(1234)
+    agree = 0
+    for trial in range(24):
+        bad = bytearray(data)
+        c = int(rng.integers(0, 3))
+        lo = starts[c][2]
+        n = hdr.section_lengths[c][2]
+        for _ in range(int(rng.integers(1, 4))):
+            pos = lo + int(rng.integers(0, n))
+            bad[pos] = int(rng.integers(0, 256))
+        st = rl.init(bytes(bad))
+        for k in (0, hdr.tree_height - 1):
+            a, sa = rl.decode_field(st, k, check=False)
+            b, sb = rl.decode_field(st, k, kernel="simple", check=False)
+            assert sa.item() == sb.item(), (trial, k)
+            if sa.item() == 0:
+                assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+            agree += 1
+    assert agree == 48
 
 
 def test_corrupt_streams_raise_like_reference(rl):
@@ -143,7 +215,7 @@ def test_corrupt_streams_raise_like_reference(rl):
                     s, t, k = args
                     from paper_1805_06019_b200 import decoder
                     return decoder.decode_image(st, (s, t), k)
-                for kern in ("fused", "simple"):
+                for kern in ("staged", "fused", "simple"):
                     rl.decode_field(st, args[0], kernel=kern)
                 return rl.decode_all(st, args[0])
             if call["exc"] is None:

@@ -1,6 +1,6 @@
 """Minimal driver for ncu captures of the decode kernels (one GPU).
 
-    python tools/profile_decode.py [--kernel fused|simple] [--iters N]
+    python tools/profile_decode.py [--kernel staged|fused|simple] [--iters N]
 """
 import argparse
 import os
@@ -16,7 +16,7 @@ import paper_1805_06019_b200 as rl  # noqa: E402
 from paper_1805_06019_b200 import decoder  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--kernel", default="fused")
+ap.add_argument("--kernel", default="staged")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--render", type=int, default=0)
 a = ap.parse_args()
