@@ -64,8 +64,9 @@ struct Ws {
     void* res;
     uint8_t* root_rgb;     // RGB8 of every root sample, rows of rgb_stride bytes
     int rgb_stride;
-    uint32_t* bm;          // [3*nblk][nwp] record bitmaps as aligned 32-bit words
-    uint32_t* rk;          // [3*nblk][nwp] slot of the first present node of each word
+    uint32_t* bm;          // [nwp][3*nblk] record bitmaps as aligned 32-bit words (word-major:
+                           // one level row's words of consecutive records are contiguous)
+    uint32_t* rk;          // [nwp][3*nblk] slot of the first present node of each word
     int nwp;
     uint64_t cap;
 };
@@ -206,8 +207,7 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
         // bitmap words of levels >= k and the slot at each word start, for
         // the blend's row masks and ranks (k_blend)
         const uint8_t* rec = f.srv[c] + off;
-        uint32_t* bm = w.bm + ri * w.nwp;
-        uint32_t* rk = w.rk + ri * w.nwp;
+        const int64_t nrec = 3 * nblk;
         uint32_t run = (uint32_t)slot0;
         for (int wi = 0; wi < w.nwp; ++wi) {
             const int n0 = wi * 32;
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
                 word = bitmap_word(rec, n0);
                 if (node_end - n0 < 32) word &= (1u << (node_end - n0)) - 1u;
             }
-            bm[wi] = word;
-            rk[wi] = run;
+            w.bm[wi * nrec + ri] = word;
+            w.rk[wi * nrec + ri] = run;
             run += __popc(word);
         }
     }
@@ -292,6 +292,25 @@ __device__ __forceinline__ void add4<int32_t>(const int32_t* p, int32_t* v) {
     v[0] += w.x; v[1] += w.y; v[2] += w.z; v[3] += w.w;
 }
 
+template <typename VT>
+__device__ __forceinline__ void add8(const VT* p, int32_t* v);
+template <>
+__device__ __forceinline__ void add8<int16_t>(const int16_t* p, int32_t* v) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] += (int32_t)(int16_t)(x[i] & 0xFFFFu);
+        v[2 * i + 1] += (int32_t)x[i] >> 16;
+    }
+}
+template <>
+__device__ __forceinline__ void add8<int32_t>(const int32_t* p, int32_t* v) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(p)), b = __ldg(reinterpret_cast<const int4*>(p) + 1);
+    v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+    v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+}
+
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w) {
     const uint64_t n = min((uint64_t)*w.counter, w.cap);
@@ -357,8 +376,10 @@ struct BlendParams {
     int TW, NB, nchunks, nstrip;
     int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
     int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
+    int debug;                   // timing experiments only (RLFC_BLEND_DEBUG): 1 no tasks,
+                                 // 2 no store, 4 no input TMA, 8 no records
     int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
-    int off_flag, off_mask, off_sbase, off_roots, off_rgb, off_dmask, off_dpre, off_cnt, off_list, off_stage,
+    int off_flag, off_mask, off_sbase, off_roots, off_rgb, off_cnt, off_list, off_stage,
         off_mbar;
 };
 
@@ -424,34 +445,6 @@ __global__ void __launch_bounds__(THREADS) k_root_rgb(const __grid_constant__ rl
     }
 }
 
-// Spread a level-l row mask over the 2^l views each node covers.
-__device__ __forceinline__ uint64_t spread(uint64_t m, int l) {
-    if (l == 0) return m;
-    const int span = 1 << l;
-    const uint64_t run = span >= 64 ? ~0ull : ((1ull << span) - 1ull);
-    uint64_t out = 0;
-    while (m) {
-        const int x = __ffsll((long long)m) - 1;
-        m &= m - 1;
-        if ((x << l) < 64) out |= run << (x << l);
-    }
-    return out;
-}
-
-// position of the k-th (0-based) set bit of m (k < popcount(m))
-__device__ __forceinline__ int kth_bit(uint64_t m, int k) {
-    int pos = 0;
-    int c = __popc((uint32_t)m);
-    if (k >= c) { k -= c; m >>= 32; pos = 32; }
-    uint32_t w = (uint32_t)m;
-#pragma unroll
-    for (int half = 16; half >= 1; half >>= 1) {
-        c = __popc(w & ((1u << half) - 1u));
-        if (k >= c) { k -= c; w >>= half; pos += half; }
-    }
-    return pos;
-}
-
 // byte offset of pixel (view s, row, tile column px) in the strip-major
 // staging buffer [strip][S][B][STRIP*3]
 template <int B>
@@ -493,15 +486,14 @@ __device__ __noinline__ void unit_fallback(const BlendParams& P, uint8_t* stage,
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int B, typename VT, typename RT>
-__global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ BlendParams P,
+template <int B, typename VT, typename RT, int BT>
+__global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__ BlendParams P,
                                                    const __grid_constant__ CUtensorMap out_map,
                                                    const __grid_constant__ CUtensorMap rgb_map,
                                                    const __grid_constant__ CUtensorMap root_map) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int BSQ = B * B;
     constexpr int QB = B / 4;                      // pixel quads per block row
-    constexpr int TPU = B * QB;                    // tasks per (view, block) unit
     const rlfc_field& f = P.f;
     const int tid = threadIdx.x;
     const int chunk = blockIdx.x % P.nchunks, t = blockIdx.x / P.nchunks;
@@ -519,58 +511,70 @@ __global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ Bl
     uint32_t* sbase = reinterpret_cast<uint32_t*>(smem + P.off_sbase);      // [nlev][NR]
     RT* roots = reinterpret_cast<RT*>(smem + P.off_roots);                 // [rsx][3][B][TW]
     uint8_t* root_rgb = smem + P.off_rgb;                                   // [strip][rsx][B][STRIP*3] (manual)
-    uint64_t* dmask = reinterpret_cast<uint64_t*>(smem + P.off_dmask);      // [NB]
-    int32_t* dpre = reinterpret_cast<int32_t*>(smem + P.off_dpre);          // [NB]
     int32_t* cnt = reinterpret_cast<int32_t*>(smem + P.off_cnt);            // [0] units, [1] warp-0 total
     uint2* list = reinterpret_cast<uint2*>(smem + P.off_list);              // [S*NB]
     uint8_t* stage = smem + P.off_stage;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_mbar);
 
     // ---- TMA: RGB(root) rows into every view's staging rows, raw roots ----------------
-    if (P.tma_in && tid == 0) {
+    if (P.tma_in && tid < 32 && !(P.debug & 4)) {
+        // warp 0: lane 0 arms the barrier, then every lane issues its share of
+        // the tensor loads
         const uint32_t bar = smem_u32(mbar);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t bytes =
-            (uint32_t)(P.nstrip * S * B * STRIP * 3) + (uint32_t)(f.rsx * 3 * B * TW * (int)sizeof(RT));
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        for (int st = 0; st < P.nstrip; ++st)
-            for (int s = 0; s < S; ++s)
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const uint32_t bytes =
+                (uint32_t)(P.nstrip * S * B * STRIP * 3) + (uint32_t)(f.rsx * 3 * B * TW * (int)sizeof(RT));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        }
+        __syncwarp();
+        const int nrgb = P.nstrip * S;
+        for (int i = tid; i < nrgb + f.rsx * 3; i += 32) {
+            if (i < nrgb) {
+                const int st = i / S, s = i - st * S;
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                     "%4}], [%5];" ::"r"(smem_u32(stage + ((st * S + s) * B) * (STRIP * 3))),
                     "l"(&rgb_map), "r"((bx0 * B + st * STRIP) * 3), "r"(by * B), "r"((s >> h) * f.rsy + ry), "r"(bar)
                     : "memory");
-        for (int rx = 0; rx < f.rsx; ++rx)
-            for (int c = 0; c < 3; ++c)
+            } else {
+                const int q = i - nrgb, rx = q / 3, c = q - rx * 3;
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                     "%4}], [%5];" ::"r"(smem_u32(roots + (rx * 3 + c) * B * TW)),
                     "l"(&root_map), "r"(bx0 * B), "r"(by * B), "r"((rx * f.rsy + ry) * 3 + c), "r"(bar)
                     : "memory");
+            }
+        }
     }
 
+    if (tid == 0) cnt[0] = 0;
     // ---- records: residual row masks and slot bases of this camera row --------
-    for (int r = tid; r < NR; r += THREADS) {
+    for (int r = tid; r < NR; r += BT) {
         const int c = r / NB, b = r - c * NB;
         uint32_t fl = 0;
-        if (b < nb && nlev > 0) {
+        if (b < nb && nlev > 0 && !(P.debug & 8)) {
             const int64_t blk = (int64_t)by * f.wb + bx0 + b;
             const int64_t ri = (int64_t)c * nblk + blk;
-            fl = P.rec_flag[ri];
-            if (!fl) {
-                const uint32_t* bmr = P.bm + ri * P.nwp;
-                const uint32_t* rkr = P.rk + ri * P.nwp;
+            fl = __ldg(P.rec_flag + ri);
+            {
+                // loaded regardless of the flag (stale for flagged records,
+                // which never read them) so every load of a lane is in flight
+                // at once
+                const int64_t nrec = 3 * nblk;
+                const uint32_t* bmr = P.bm + ri;
+                const uint32_t* rkr = P.rk + ri;
                 for (int l = h - 1; l >= k; --l) {
                     const int sx = f.level_sx[l];
                     const int n0 = f.level_base[l] + (t >> l) * sx;
                     const int wi = n0 >> 5, o = n0 & 31;
-                    const uint32_t lo = __ldg(bmr + wi), hi = __ldg(bmr + wi + 1);
+                    const uint32_t lo = __ldg(bmr + wi * nrec), hi = __ldg(bmr + (wi + 1) * nrec);
                     uint64_t m = __funnelshift_r(lo, hi, o);
-                    if (sx > 32) m |= (uint64_t)__funnelshift_r(hi, __ldg(bmr + wi + 2), o) << 32;
+                    if (sx > 32) m |= (uint64_t)__funnelshift_r(hi, __ldg(bmr + (wi + 2) * nrec), o) << 32;
                     if (sx < 64) m &= (1ull << sx) - 1ull;
                     mask[(l - k) * NR + r] = m;
-                    sbase[(l - k) * NR + r] = __ldg(rkr + wi) + __popc(lo & ((1u << o) - 1u));
+                    sbase[(l - k) * NR + r] = __ldg(rkr + wi * nrec) + __popc(lo & ((1u << o) - 1u));
                 }
             }
         } else if (nlev > 0) {
@@ -582,7 +586,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ Bl
     if (!P.tma_in) {
         const int quads = TW / 4;
         const int64_t pl = (int64_t)f.hp * f.wp;
-        for (int it = tid; it < f.rsx * B * quads; it += THREADS) {
+        for (int it = tid; it < f.rsx * B * quads; it += BT) {
             const int xq = it % quads, rr = (it / quads) % B, rx = it / (quads * B);
             const int gx = bx0 * B + xq * 4;
             int32_t v[3][4];
@@ -608,81 +612,50 @@ __global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ Bl
     }
     __syncthreads();
 
-    // ---- dirty views per block (warps 0-1, one block per lane) | manual prefill ------
+    // ---- dirty (view, block) units: one thread per pair tests the chain's
+    // presence bits (bit 3(l-k)+c: level l, channel c) and appends dirty pairs
+    // with a warp-aggregated shared-memory atomic (unit order is irrelevant);
+    // pairs touching a flagged record are tagged for the reference-order walk
     const int lane = tid & 31;
-    if (tid < 64) {
-        const int b = tid;
-        uint64_t want = S >= 64 ? ~0ull : ((1ull << S) - 1ull);
-        if (P.slots) {
-            const bool w0 = lane < S && P.slots[lane * T + t] >= 0;
-            const bool w1 = lane + 32 < S && P.slots[(lane + 32) * T + t] >= 0;
-            want = (uint64_t)__ballot_sync(0xffffffffu, w0) | (uint64_t)__ballot_sync(0xffffffffu, w1) << 32;
-        }
-        uint64_t dirty = 0;
-        bool fb = false;
-        if (b < nb) {
-            for (int c = 0; c < 3; ++c) fb |= rflag[c * NB + b] != 0;
-            if (fb) {
-                dirty = ~0ull;
-            } else {
+    for (int p0 = 0; p0 < S * NB; p0 += BT) {
+        const int pi = p0 + tid;
+        const int s = pi / NB, b = pi - s * NB;
+        bool emit = false, fb = false;
+        uint32_t pres = 0;
+        if (pi < S * NB && b < nb && (!P.slots || P.slots[s * T + t] >= 0)) {
+            fb = (rflag[b] | rflag[NB + b] | rflag[2 * NB + b]) != 0;
+            if (!fb) {
                 for (int l = k; l < h; ++l) {
-                    uint64_t ml = 0;
-                    for (int c = 0; c < 3; ++c) ml |= mask[(l - k) * NR + c * NB + b];
-                    dirty |= spread(ml, l);
+                    const int x = s >> l;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        pres |= (uint32_t)((mask[(l - k) * NR + c * NB + b] >> x) & 1ull) << (3 * (l - k) + c);
                 }
             }
-            dirty &= want;
+            emit = fb || pres != 0;
         }
-        const int n = __popcll(dirty);
-        int incl = n;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+        const uint32_t bal = __ballot_sync(0xffffffffu, emit);
+        if (bal) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&cnt[0], __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (emit)
+                list[base + __popc(bal & ((1u << lane) - 1u))] =
+                    make_uint2((uint32_t)s | (uint32_t)b << 8 | (fb ? 1u << 16 : 0u), pres);
         }
-        if (tid == 31) cnt[1] = incl;
-        asm volatile("bar.sync 1, 64;" ::: "memory");
-        const int base = tid >= 32 ? cnt[1] : 0;
-        if (b < NB) {
-            dmask[b] = dirty;
-            dpre[b] = base + incl - n;
-        }
-        if (fb && b < NB) rflag[b] = 2u;                 // block needs the reference-order walk
-        if (tid == 63) cnt[0] = base + incl;
-    } else if (!P.tma_in) {
+    }
+    if (!P.tma_in) {
         // staging[strip][s][row] <- root_rgb[strip][s >> h][row]: one warp per
         // staged (strip, view), B*12 16-byte copies
         constexpr int V = B * STRIP * 3 / 16;
-        for (int sv = (tid >> 5) - 2; sv < P.nstrip * S; sv += THREADS / 32 - 2) {
+        for (int sv = tid >> 5; sv < P.nstrip * S; sv += BT / 32) {
             const int st = sv / S, s = sv - st * S;
             const uint4* src = reinterpret_cast<const uint4*>(root_rgb + (st * f.rsx + (s >> h)) * B * (STRIP * 3));
             uint4* dst = reinterpret_cast<uint4*>(stage + sv * B * (STRIP * 3));
             for (int v = lane; v < V; v += 32) dst[v] = src[v];
         }
     }
-    __syncthreads();
-
-    // ---- dirty (view, block) units with their presence bits (bit 3(l-k)+c) ---------
-    const int units = cnt[0];
-    for (int u = tid; u < units; u += THREADS) {
-        int b = 0;
-#pragma unroll
-        for (int step = 32; step > 0; step >>= 1)
-            if (b + step < NB && dpre[b + step] <= u) b += step;
-        const int s = kth_bit(dmask[b], u - dpre[b]);
-        const bool fb = rflag[b] == 2u;
-        uint32_t pres = 0;
-        if (!fb) {
-            for (int l = k; l < h; ++l) {
-                const int x = s >> l;
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    pres |= (uint32_t)((mask[(l - k) * NR + c * NB + b] >> x) & 1ull) << (3 * (l - k) + c);
-            }
-        }
-        list[u] = make_uint2((uint32_t)s | (uint32_t)b << 8 | (fb ? 1u << 16 : 0u), pres);
-    }
-    if (P.tma_in) {
+    if (P.tma_in && !(P.debug & 4)) {
         const uint32_t bar = smem_u32(mbar);
         uint32_t done = 0;
         while (!done)
@@ -695,38 +668,70 @@ __global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ Bl
     __syncthreads();
 
     // ---- dirty units: root + present residuals, YCoCg-R inverse, clamp, pack ----------
+    // one task = two consecutive pixel quad-rows of a unit (8 consecutive
+    // values of each payload), so a present residual is one 16-byte gather
     {
+        constexpr int TP = B * QB / 2;                   // tasks per unit
+        const int units = (P.debug & 1) ? 0 : cnt[0];
         const VT* res = static_cast<const VT*>(P.res);
-        for (int it = tid; it < units * TPU; it += THREADS) {
-            const int u = it / TPU, q = it - u * TPU;
-            const int row = q / QB, quad = q - row * QB;
+        for (int it = tid; it < units * TP; it += BT) {
+            const int u = it / TP, j = it - u * TP;
             const uint2 e = list[u];
             const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
             if (e.x >> 16) {
-                if (q == 0) unit_fallback<B>(P, stage, s, t, by, bx0 + b, b * B);
+                if (j == 0) unit_fallback<B>(P, stage, s, t, by, bx0 + b, b * B);
                 continue;
             }
-            const int px = b * B + quad * 4;
             const int rx = s >> h;
-            int32_t v[3][4];
+            int row[2], px[2];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) load4s<RT>(roots + ((rx * 3 + c) * B + row) * TW + px, v[c]);
-            const int voff = row * B + quad * 4;
+            for (int hh = 0; hh < 2; ++hh) {
+                const int qi = 2 * j + hh;
+                row[hh] = qi / QB;
+                px[hh] = b * B + (qi - row[hh] * QB) * 4;
+            }
+            int32_t v[2][3][4];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) load4s<RT>(roots + ((rx * 3 + c) * B + row[hh]) * TW + px[hh], v[hh][c]);
+            const int voff = 8 * j;
+            // first present level of each channel: the three gathers are all
+            // issued before any is consumed; further levels (rare) follow
+            auto addr = [&](int c, uint32_t pc) -> const VT* {
+                const int li = (__ffs(pc) - 1) / 3;
+                const int r = li * NR + c * NB + b;
+                const int x = s >> (k + li);
+                const uint32_t slot = sbase[r] + (uint32_t)__popcll(mask[r] & ((1ull << x) - 1ull));
+                return res + (uint64_t)slot * BSQ + voff;
+            };
+            uint32_t pcs[3];
+            int32_t rv[3][8];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                uint32_t pc = e.y & (0x249249u << c);        // bits 3i + c: levels k + i
-                while (pc) {
-                    const int bit = __ffs(pc) - 1;
-                    pc &= pc - 1u;
-                    const int li = bit / 3;
-                    const int r = li * NR + c * NB + b;
-                    const uint64_t m = mask[r];
-                    const int x = s >> (k + li);
-                    const uint32_t slot = sbase[r] + (uint32_t)__popcll(m & ((1ull << x) - 1ull));
-                    add4<VT>(res + (uint64_t)slot * BSQ + voff, v[c]);
+                pcs[c] = e.y & (0x249249u << c);             // bits 3i + c: levels k + i
+#pragma unroll
+                for (int i = 0; i < 8; ++i) rv[c][i] = 0;
+                if (pcs[c]) {
+                    add8<VT>(addr(c, pcs[c]), rv[c]);
+                    pcs[c] &= pcs[c] - 1u;
                 }
             }
-            ycocg4_pack(v, reinterpret_cast<uint32_t*>(stage + stage_off<B>(S, s, row, px)));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                while (pcs[c]) {
+                    add8<VT>(addr(c, pcs[c]), rv[c]);
+                    pcs[c] &= pcs[c] - 1u;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v[0][c][i] += rv[c][i];
+                    v[1][c][i] += rv[c][4 + i];
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+                ycocg4_pack(v[hh], reinterpret_cast<uint32_t*>(stage + stage_off<B>(S, s, row[hh], px[hh])));
         }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -734,7 +739,8 @@ __global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ Bl
 
     // ---- store ------------------------------------------------------------------------
     const int nrows_band = min(by * B + B, f.height) - by * B;   // rows of this block row
-    if (P.store_mode == 2) {
+    if (P.debug & 2) {
+    } else if (P.store_mode == 2) {
         if (tid == 0) {
             for (int st = 0; st < P.nstrip; ++st) {
                 const int x0 = (bx0 * B + st * STRIP) * 3;
@@ -752,7 +758,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_blend(const __grid_constant__ Bl
     } else {
         // per (view, row, strip): bulk copy when the strip is whole, else bytes
         bool issued = false;
-        for (int it = tid; it < S * B * P.nstrip; it += THREADS) {
+        for (int it = tid; it < S * B * P.nstrip; it += BT) {
             const int st = it % P.nstrip, rr = (it / P.nstrip) % B, s = it / (P.nstrip * B);
             if (rr >= nrows_band) continue;
             const int img = s * T + t;
@@ -813,11 +819,12 @@ struct Plan {
 
 // Blend geometry and shared-memory layout; false when outside the envelope.
 template <typename RT>
-static bool plan_blend(const rlfc_field& f, int k, Plan& pl) {
+static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_first, Plan& pl) {
     const int B = f.block, S = f.s_count, h = f.tree_height;
     BlendParams& P = pl.P;
     auto al = [](int x) { return (x + 127) & ~127; };
-    for (int TW : {128, 64}) {
+    const int tws[2] = {tw_first, tw_first == 128 ? 64 : 128};
+    for (int TW : tws) {
         if (TW % B) continue;
         const int NB = TW / B;
         if (NB > 64) continue;
@@ -828,9 +835,7 @@ static bool plan_blend(const rlfc_field& f, int k, Plan& pl) {
         P.off_mask = off;  off = al(off + nlev * NR * 8);
         P.off_sbase = off; off = al(off + nlev * NR * 4);
         P.off_roots = off; off = al(off + f.rsx * 3 * B * TW * (int)sizeof(RT));
-        P.off_rgb = off;   off = al(off + f.rsx * B * TW * 3);
-        P.off_dmask = off; off = al(off + NB * 8);
-        P.off_dpre = off;  off = al(off + NB * 4);
+        P.off_rgb = off;   off = al(off + (manual_roots ? f.rsx * B * TW * 3 : 0));
         P.off_cnt = off;   off = al(off + 16);
         P.off_list = off;  off = al(off + S * NB * 8);
         P.off_stage = off; off = al(off + S * B * TW * 3);
@@ -850,8 +855,16 @@ template <int B, typename VT, typename RT>
 static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
                   int64_t img_stride, int64_t row_stride, const Ws& w, uint64_t* status, cudaStream_t stream) {
     constexpr int BSQ = B * B;
+    const bool tma_ok = w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 &&
+                        ((f.wp * (int)sizeof(RT)) % 16) == 0 && encode_fn() != nullptr;
+    // blend CTA shape: 128 threads on 64-pixel tiles by default (more
+    // independent CTAs per SM to overlap their latency phases)
+    int bt = 128, tw = 64;
+    if (const char* e = getenv("RLFC_BLEND_THREADS")) bt = atoi(e) == 256 ? 256 : 128;
+    if (const char* e = getenv("RLFC_BLEND_TW")) tw = atoi(e) == 128 ? 128 : 64;
+    const char* dbg = getenv("RLFC_BLEND_DEBUG");
     Plan pl{};
-    if (!plan_blend<RT>(f, k, pl)) return RLFC_ERR_ARGUMENT;
+    if (!plan_blend<RT>(f, k, !tma_ok, tw, pl)) return RLFC_ERR_ARGUMENT;
     BlendParams& P = pl.P;
     P.f = f;
     P.k = k;
@@ -870,6 +883,7 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     P.rk = w.rk;
     P.nwp = w.nwp;
     P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
+    P.debug = dbg ? atoi(dbg) : 0;
     const int h = f.tree_height, S = f.s_count;
     // output path
     const bool aligned = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride) & 15) == 0;
@@ -890,7 +904,7 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     // input path: RGB(root) rows + raw roots by TMA when the layouts allow it
     P.tma_in = 0;
     const int nroot = f.rsx * f.rsy;
-    if (w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 && ((f.wp * (int)sizeof(RT)) % 16) == 0) {
+    if (tma_ok) {
         const cuuint64_t d1[3] = {(cuuint64_t)f.wp * 3, (cuuint64_t)f.hp, (cuuint64_t)nroot};
         const cuuint64_t s1[2] = {(cuuint64_t)w.rgb_stride, (cuuint64_t)w.rgb_stride * f.hp};
         const cuuint32_t b1[3] = {(cuuint32_t)(STRIP * 3), (cuuint32_t)B, 1u};
@@ -901,6 +915,8 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
             encode_map(&root_map, sizeof(RT) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_INT32,
                        3, const_cast<void*>(f.roots), d2, s2, b2))
             P.tma_in = 1;
+        else
+            return RLFC_ERR_ARGUMENT;        // planned without the manual root buffers
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -920,10 +936,10 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
         k_payloads<BSQ, VT><<<grid, THREADS, 0, stream>>>(f, w);
     }
-    auto kern = k_blend<B, VT, RT>;
+    auto kern = bt == 256 ? k_blend<B, VT, RT, 256> : k_blend<B, VT, RT, 128>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     const dim3 grid((unsigned)(P.nchunks * f.t_count), (unsigned)(by_hi - by_lo));
-    kern<<<grid, THREADS, pl.smem, stream>>>(P, out_map, rgb_map, root_map);
+    kern<<<grid, bt, pl.smem, stream>>>(P, out_map, rgb_map, root_map);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "rlfc_b200: staged decode launch error: %s\n", cudaGetErrorString(e));
