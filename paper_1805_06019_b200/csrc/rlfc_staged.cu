@@ -311,48 +311,151 @@ __device__ __forceinline__ void add8<int32_t>(const int32_t* p, int32_t* v) {
     v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
 }
 
+// NV consecutive values of one payload starting at a group boundary, fully
+// unrolled for a compile-time mode: groups of G values behind a PB-bit pack
+// (plain bits: G = 1, PB = 0), kernels.py:128-159 bit layout.
+template <int G, int PB, int NV, typename VT>
+__device__ __forceinline__ void decode_run(BitReader& br, const uint16_t* lut, uint32_t b, int shift, VT* out,
+                                           bool& bad) {
+    constexpr uint32_t DB = G == 5 ? 2u : 3u, DMASK = G == 5 ? 3u : 7u, PMAX = G == 5 ? 242u : 124u;
+    uint32_t digits = 0;
+    int32_t v[4];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        if (PB && k % G == 0) {
+            const uint32_t pk = br.get(PB);
+            bad |= pk > PMAX;
+            digits = lut[pk <= PMAX ? pk : 0u];
+        }
+        const uint32_t low = br.get(b);
+        const uint32_t z = PB ? ((((digits >> (DB * (uint32_t)(k % G))) & DMASK) << b) | low) : low;
+        v[k & 3] = deq(z, shift);
+        if ((k & 3) == 3) store4<VT>(out + (k & ~3), v);
+    }
+}
+
+template <int G, int PB, int BSQ, typename VT>
+__device__ __forceinline__ bool decode_payload(const uint8_t* p, const uint16_t* lut, uint32_t b, int shift,
+                                               VT* out) {
+    constexpr int CH = 4 * G;                        // values per unrolled chunk (group- and quad-aligned)
+    BitReader br(p);
+    bool bad = false;
+#pragma unroll 1
+    for (int q = 0; q + CH <= BSQ; q += CH) decode_run<G, PB, CH, VT>(br, lut, b, shift, out + q, bad);
+    if constexpr (BSQ % CH != 0) decode_run<G, PB, BSQ % CH, VT>(br, lut, b, shift, out + BSQ - BSQ % CH, bad);
+    return bad;
+}
+
+// B = 4 (16 values, <= 176 payload bits): the payload's aligned words sit in
+// a per-thread shared-memory slot; each BISE group (or plain-bit quad) is one
+// 64-bit window at its closed-form bit offset (every group but the last is
+// full), so all reads of a payload are independent;
+// dequantisation is a table lookup (z < 2048 for every descriptor).
+constexpr int SLOT_WORDS = 9;     // odd stride: conflict-free slot fills
+__device__ __forceinline__ uint64_t win64(const uint32_t* sw, uint32_t pos) {
+    const uint32_t wi = pos >> 5, o = pos & 31u;
+    const uint32_t a = sw[wi], b = sw[wi + 1], c = sw[wi + 2];
+    return (uint64_t)__funnelshift_r(a, b, o) | (uint64_t)__funnelshift_r(b, c, o) << 32;
+}
+
+template <int MODE, typename VT>
+__device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint32_t b, const uint16_t* dlut,
+                                         const VT* dq, VT* out) {
+    const uint32_t lm = (1u << b) - 1u;
+    int32_t v[16];
+    bool bad = false;
+    if (MODE == MODE_BITS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint64_t w = win64(sw, bit0 + 4u * (uint32_t)q * b);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[4 * q + i] = dq[(uint32_t)(w >> ((uint32_t)i * b)) & lm];
+        }
+    } else {
+        constexpr int G = MODE == MODE_TRIT ? 5 : 3, PB = MODE == MODE_TRIT ? 8 : 7;
+        constexpr uint32_t DB = MODE == MODE_TRIT ? 2u : 3u, DMASK = MODE == MODE_TRIT ? 3u : 7u;
+        constexpr uint32_t PMAX = MODE == MODE_TRIT ? 242u : 124u;
+        const uint32_t gbits = PB + G * b;
+#pragma unroll
+        for (int g = 0; g * G < 16; ++g) {
+            const uint64_t w = win64(sw, bit0 + (uint32_t)g * gbits);
+            const uint32_t pk = (uint32_t)w & ((1u << PB) - 1u);
+            bad |= pk > PMAX;
+            const uint32_t dg = dlut[pk <= PMAX ? pk : 0u];
+#pragma unroll
+            for (int i = 0; i < G && g * G + i < 16; ++i) {
+                const uint32_t low = (uint32_t)(w >> (PB + (uint32_t)i * b)) & lm;
+                v[g * G + i] = dq[(((dg >> (DB * i)) & DMASK) << b) | low];
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) store4<VT>(out + 4 * q, v + 4 * q);
+    return bad;
+}
+
+// One CTA takes PAY_CHUNK consecutive slots, buckets their entries by BISE
+// mode in shared memory, then decodes each bucket with the mode's unrolled
+// code so every warp runs one code path.
+constexpr int PAY_CHUNK = 512;
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w) {
-    const uint64_t n = min((uint64_t)*w.counter, w.cap);
+    __shared__ uint2 bucket[3][PAY_CHUNK];
+    __shared__ uint32_t bslot[3][PAY_CHUNK];
+    __shared__ int bcount[3];
+    __shared__ uint16_t lut[243 + 125];
+    __shared__ VT dq[BSQ == 16 ? 2048 : 1];
+    __shared__ uint32_t scratch[BSQ == 16 ? THREADS * SLOT_WORDS : 1];
+    const int tid = threadIdx.x;
     const int shift = f.quant_shift;
+    for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
+    if (BSQ == 16)
+        for (int z = tid; z < 2048; z += THREADS) dq[z] = (VT)deq((uint32_t)z, shift);
+    const uint64_t n = min((uint64_t)*w.counter, w.cap);
     const int64_t nblk = (int64_t)f.wb * f.hb;
     VT* res = static_cast<VT*>(w.res);
-    for (uint64_t slot = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; slot < n;
-         slot += (uint64_t)gridDim.x * blockDim.x) {
-        const uint2 e = w.entries[slot];
-        const uint32_t d = e.y & 31u;
-        if (d >= (uint32_t)NUM_DESC) continue;
-        const int c = (int)(e.y >> 5) & 3;
-        const int mode = desc_mode((int)d);
-        const uint32_t b = (uint32_t)desc_bits((int)d);
-        // one group = G values behind a PB-bit pack (plain bits: G = 1, no pack)
-        const uint32_t G = mode == MODE_TRIT ? 5u : mode == MODE_QUINT ? 3u : 1u;
-        const uint32_t PB = mode == MODE_TRIT ? 8u : mode == MODE_QUINT ? 7u : 0u;
-        const uint32_t DB = mode == MODE_TRIT ? 2u : 3u;
-        const uint32_t DMASK = mode == MODE_TRIT ? 3u : mode == MODE_QUINT ? 7u : 0u;
-        const uint32_t PMAX = mode == MODE_TRIT ? 242u : 124u;
-        const uint16_t* L = mode == MODE_TRIT ? g_lut.trit : g_lut.quint;
-        BitReader br(f.srv[c] + e.x);
-        uint32_t gi = 0, digits = 0;
-        bool bad = false;
-        VT* out = res + slot * BSQ;
-        for (int q = 0; q < BSQ / 4; ++q) {
-            int32_t v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (gi == 0 && PB) {
-                    const uint32_t pk = br.get(PB);
-                    bad |= pk > PMAX;
-                    digits = L[pk <= PMAX ? pk : 0u];
-                }
-                const uint32_t low = br.get(b);
-                const uint32_t z = (((digits >> (DB * gi)) & DMASK) << b) | low;
-                gi = gi + 1 == G ? 0u : gi + 1;
-                v[j] = deq(z, shift);
-            }
-            store4<VT>(out + 4 * q, v);
+    uint32_t* sw = scratch + (BSQ == 16 ? tid * SLOT_WORDS : 0);
+    for (uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK; base < n; base += (uint64_t)gridDim.x * PAY_CHUNK) {
+        if (tid < 3) bcount[tid] = 0;
+        __syncthreads();
+        for (int i = tid; i < PAY_CHUNK && base + i < n; i += THREADS) {
+            const uint2 e = w.entries[base + i];
+            const uint32_t d = e.y & 31u;
+            if (d >= (uint32_t)NUM_DESC) continue;
+            const int m = desc_mode((int)d);
+            const int pos = atomicAdd(&bcount[m], 1);
+            bucket[m][pos] = e;
+            bslot[m][pos] = (uint32_t)(base + i);
         }
-        if (bad) w.rec_flag[(int64_t)c * nblk + (e.y >> 7)] = 1u;   // kernels.py:147-150
+        __syncthreads();
+        const int n0 = bcount[0], n1 = bcount[1], n2 = bcount[2];
+        for (int j = tid; j < n0 + n1 + n2; j += THREADS) {
+            const int m = j < n0 ? 0 : j < n0 + n1 ? 1 : 2;
+            const int jj = j - (m == 0 ? 0 : m == 1 ? n0 : n0 + n1);
+            const uint2 e = bucket[m][jj];
+            const uint64_t slot = bslot[m][jj];
+            const int c = (int)(e.y >> 5) & 3;
+            const uint32_t b = (uint32_t)desc_bits((int)(e.y & 31u));
+            const uint8_t* p = f.srv[c] + e.x;
+            VT* out = res + slot * BSQ;
+            bool bad;
+            if constexpr (BSQ == 16) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+#pragma unroll
+                for (int q = 0; q < SLOT_WORDS; ++q) sw[q] = __ldg(src + q);
+                const uint32_t bit0 = (uint32_t)(a & 3) * 8u;
+                if (m == MODE_BITS) bad = decode16<MODE_BITS, VT>(sw, bit0, b, lut, dq, out);
+                else if (m == MODE_TRIT) bad = decode16<MODE_TRIT, VT>(sw, bit0, b, lut, dq, out);
+                else bad = decode16<MODE_QUINT, VT>(sw, bit0, b, lut + 243, dq, out);
+            } else {
+                if (m == MODE_BITS) bad = decode_payload<1, 0, BSQ, VT>(p, lut, b, shift, out);
+                else if (m == MODE_TRIT) bad = decode_payload<5, 8, BSQ, VT>(p, lut, b, shift, out);
+                else bad = decode_payload<3, 7, BSQ, VT>(p, lut + 243, b, shift, out);
+            }
+            if (bad) w.rec_flag[(int64_t)c * nblk + (e.y >> 7)] = 1u;   // kernels.py:147-150
+        }
+        __syncthreads();
     }
 }
 
@@ -931,8 +1034,8 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         cudaMemsetAsync(w.counter, 0, 8, stream);
         const int64_t nrec = 3ll * (by_hi - by_lo) * f.wb;
         k_index<BSQ><<<(unsigned)((nrec + THREADS - 1) / THREADS), THREADS, 0, stream>>>(f, k, by_lo, by_hi, w);
-        const uint64_t want = (w.cap + THREADS - 1) / THREADS;
-        const uint64_t cap_grid = (uint64_t)sms * 16;
+        const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
+        const uint64_t cap_grid = (uint64_t)sms * 8;
         const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
         k_payloads<BSQ, VT><<<grid, THREADS, 0, stream>>>(f, w);
     }
@@ -950,6 +1053,7 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
 
 static bool in_envelope(const rlfc_field& f) {
     if (f.tree_height < 1 || f.tree_height > MAXH || f.s_count > MAXS || f.t_count > 65535) return false;
+    if (f.quant_shift < 0 || f.quant_shift > 20) return false;    // dequantised codes fit int32
     if (f.block != 4 && f.block != 8 && f.block != 16) return false;
     for (int l = 0; l < f.tree_height; ++l)
         if (f.level_sx[l] > 64) return false;
