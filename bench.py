@@ -5,7 +5,9 @@ Headline workload (BASELINE.json configs[1]): the synthetic
 1.85 bpp), produced on the box by the native producer (byte-identical to the
 reference encoder, tests/test_producer.py).  One step = one full-field decode
 of all 289 views (303 Mpix) from the compressed stream resident in HBM to
-RGB8 in HBM, by the fused sm_100a kernel.  Rank 0 prints ONE JSON line.
+RGB8 in HBM, by the staged sm_100a decode (record index, payload decode,
+TMA-fed blend: four kernel launches per step; --kernel fused runs the single
+tiled kernel instead).  Rank 0 prints ONE JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -143,17 +145,25 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+NCU_SUMMARY = {"fused": "profiles/r1_decode_ncu_summary.json",
+               "staged": "profiles/r1_staged_ncu_summary.json"}
+KERNELS = {"fused": ["k_decode_field_tiled"],
+           "staged": ["k_root_rgb", "k_index", "k_payloads", "k_blend"],
+           "simple": ["k_decode_field_simple"]}
+
+
 def ncu_traffic(kernel_kind):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture (profiles/r1_decode_ncu_summary.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r1_decode_ncu_summary.json")
-    if kernel_kind != "fused" or not os.path.exists(path):
-        return None
+    """DRAM bytes per decode step (all of the step's kernels) from the
+    committed ncu capture of the same path, or None."""
+    rel = NCU_SUMMARY.get(kernel_kind)
+    path = os.path.join(ROOT, rel) if rel else None
+    if not path or not os.path.exists(path):
+        return None, None
     try:
         with open(path) as f:
-            return int(json.load(f)["dram_bytes_total"])
+            return int(json.load(f)["dram_bytes_total"]), rel
     except (OSError, KeyError, ValueError):
-        return None
+        return None, None
 
 
 def peaks():
@@ -312,8 +322,9 @@ def main():
     total_px = px_rank * world if args.scaling == "weak" else \
         hdr.s_count * hdr.t_count * hdr.width * hdr.height
     value = total_px / (ms_max * 1e-3) / 1e9
-    # roofline of the dominant kernel (the fused decode): per-launch
-    # algorithmic bytes over the per-launch device time on this rank
+    # roofline of the decode step (the fused kernel, or the staged path's
+    # four launches together): algorithmic bytes over the device time per
+    # step on this rank
     frac_rows = rows_px / hdr.height
     alg = st["comp_bytes"] * frac_rows + st["root_bytes"] * frac_rows + \
         st["out_bytes"] * frac_rows
@@ -337,6 +348,7 @@ def main():
                "sample": "full 17x17x1024^2 R4 field, oracle C port, "
                          f"{nth} threads, mean of {len(times)} steps"}
 
+    traffic, traffic_src = ncu_traffic(args.kernel) if band == (0, hb) else (None, None)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gpix/s",
@@ -350,11 +362,14 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
-                         "traffic": ncu_traffic(args.kernel) if band == (0, hb) else None,
-                         "traffic_source": "profiles/r1_decode_ncu_summary.json (ncu --set full, same kernel)",
+                         "traffic": traffic,
+                         "traffic_source": traffic_src and (
+                             traffic_src + " (ncu, DRAM bytes summed over "
+                             "the step's kernels)"),
                          "peak_source": peak_kind,
+                         "kernels": KERNELS[args.kernel],
                          "alg_bytes_per_launch": int(alg)},
-            "e2e": e2e, "gpu_launches": args.steps,
+            "e2e": e2e, "gpu_launches": args.steps * len(KERNELS[args.kernel]),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "render": render,
@@ -385,7 +400,7 @@ def e2e_measure(state, band, args, rl):
             "d2h_bytes_per_step": res.d2h_bytes,
             "ms_per_step": dt * 1e3,
             "path": "decoder.HostPipeline: pinned H2D of SRV+offsets+roots, "
-                    "fused decode, pinned D2H of RGB (band-pipelined)"}
+                    "staged decode, pinned D2H of RGB"}
 
 
 def random_access_measure(state, rl):

@@ -522,7 +522,7 @@ def planes_to_rgb(planes):
 class HostPipeline:
     """End-to-end decode with host buffers, the path a host application
     takes: every run() uploads the compressed sections (SRV + offsets) and
-    the root planes from pinned host memory, runs the fused decode, and
+    the root planes from pinned host memory, runs the staged decode, and
     copies the RGB8 result into pinned host memory.  h2d_bytes / d2h_bytes
     are the bytes those copies move per run."""
 
@@ -555,11 +555,23 @@ class HostPipeline:
             d.copy_(h, non_blocking=True)
         self.status.zero_()
         W = hdr.width
+        L = _native.lib()
         with torch.cuda.device(self.df.device):
-            _native.check(_native.lib().rlfc_decode_field(
-                self.df.ref, 0, None, self.rows[0], self.rows[1],
-                self.out.data_ptr(), self.rows_px * W * 3, W * 3,
-                self.status.data_ptr(), _stream()), "rlfc_decode_field")
+            stream = _stream()
+            ws = self.df.staged_workspace(stream)
+            rc = _native.RLFC_ERR_ARGUMENT
+            if ws is not None:
+                rc = L.rlfc_decode_field_staged(
+                    self.df.ref, 0, None, self.rows[0], self.rows[1],
+                    self.out.data_ptr(), self.rows_px * W * 3, W * 3,
+                    ws[0].data_ptr(), ws[1], ws[2], self.status.data_ptr(),
+                    stream)
+            if rc == _native.RLFC_ERR_ARGUMENT:
+                rc = L.rlfc_decode_field(
+                    self.df.ref, 0, None, self.rows[0], self.rows[1],
+                    self.out.data_ptr(), self.rows_px * W * 3, W * 3,
+                    self.status.data_ptr(), stream)
+            _native.check(rc, "rlfc_decode_field")
         self.out_host.copy_(self.out, non_blocking=True)
         torch.cuda.current_stream(self.df.device).synchronize()
         _raise_word(self.status.cpu().item())
