@@ -346,12 +346,12 @@ __device__ __forceinline__ bool decode_payload(const uint8_t* p, const uint16_t*
     return bad;
 }
 
-// B = 4 (16 values, <= 176 payload bits): the payload's aligned words sit in
-// a per-thread shared-memory slot; each BISE group (or plain-bit quad) is one
+// B = 4 (16 values, <= 176 payload bits): the payload's aligned words are
+// read from the chunk's staged SRV bytes in shared memory; each BISE group
+// (or plain-bit quad) is one
 // 64-bit window at its closed-form bit offset (every group but the last is
 // full), so all reads of a payload are independent;
 // dequantisation is a table lookup (z < 2048 for every descriptor).
-constexpr int SLOT_WORDS = 9;     // odd stride: conflict-free slot fills
 __device__ __forceinline__ uint64_t win64(const uint32_t* sw, uint32_t pos) {
     const uint32_t wi = pos >> 5, o = pos & 31u;
     const uint32_t a = sw[wi], b = sw[wi + 1], c = sw[wi + 2];
@@ -398,14 +398,16 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
 // mode in shared memory, then decodes each bucket with the mode's unrolled
 // code so every warp runs one code path.
 constexpr int PAY_CHUNK = 512;
+constexpr int PAY_BUF = 12 * 1024;       // staged SRV bytes per chunk
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w) {
     __shared__ uint2 bucket[3][PAY_CHUNK];
     __shared__ uint32_t bslot[3][PAY_CHUNK];
     __shared__ int bcount[3];
+    __shared__ uint32_t range[3];            // min / max payload offset, channel mask
     __shared__ uint16_t lut[243 + 125];
     __shared__ VT dq[BSQ == 16 ? 2048 : 1];
-    __shared__ uint32_t scratch[BSQ == 16 ? THREADS * SLOT_WORDS : 1];
+    __shared__ __align__(16) uint32_t cbuf[BSQ == 16 ? PAY_BUF / 4 : 4];
     const int tid = threadIdx.x;
     const int shift = f.quant_shift;
     for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
@@ -414,10 +416,15 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     const uint64_t n = min((uint64_t)*w.counter, w.cap);
     const int64_t nblk = (int64_t)f.wb * f.hb;
     VT* res = static_cast<VT*>(w.res);
-    uint32_t* sw = scratch + (BSQ == 16 ? tid * SLOT_WORDS : 0);
     for (uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK; base < n; base += (uint64_t)gridDim.x * PAY_CHUNK) {
         if (tid < 3) bcount[tid] = 0;
+        if (tid == 0) {
+            range[0] = ~0u;
+            range[1] = 0u;
+            range[2] = 0u;
+        }
         __syncthreads();
+        uint32_t lo = ~0u, hi = 0u, cm = 0u;
         for (int i = tid; i < PAY_CHUNK && base + i < n; i += THREADS) {
             const uint2 e = w.entries[base + i];
             const uint32_t d = e.y & 31u;
@@ -426,9 +433,42 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
             const int pos = atomicAdd(&bcount[m], 1);
             bucket[m][pos] = e;
             bslot[m][pos] = (uint32_t)(base + i);
+            lo = min(lo, e.x);
+            hi = max(hi, e.x);
+            cm |= 1u << ((e.y >> 5) & 3);
+        }
+        if (BSQ == 16) {
+            // the chunk's payloads are consecutive nodes of consecutive records
+            // of one channel: one contiguous byte range of its SRV section
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+                cm |= __shfl_xor_sync(0xffffffffu, cm, o);
+            }
+            if ((tid & 31) == 0 && cm) {
+                atomicMin(&range[0], lo);
+                atomicMax(&range[1], hi);
+                atomicOr(&range[2], cm);
+            }
         }
         __syncthreads();
         const int n0 = bcount[0], n1 = bcount[1], n2 = bcount[2];
+        bool staged = false;
+        uint32_t lo16 = 0;
+        int sc = 0;
+        if (BSQ == 16 && range[2] && __popc(range[2]) == 1) {
+            sc = __ffs(range[2]) - 1;
+            lo16 = range[0] & ~15u;
+            const uint64_t end = min((uint64_t)range[1] + 48, f.srv_len[sc] + 16);
+            staged = (uint64_t)range[1] + 48 - lo16 <= (uint64_t)PAY_BUF;
+            if (staged) {
+                const uint4* src = reinterpret_cast<const uint4*>(f.srv[sc] + lo16);
+                const int n16 = (int)((end - lo16) >> 4);
+                for (int q = tid; q < n16; q += THREADS) reinterpret_cast<uint4*>(cbuf)[q] = __ldg(src + q);
+                __syncthreads();
+            }
+        }
         for (int j = tid; j < n0 + n1 + n2; j += THREADS) {
             const int m = j < n0 ? 0 : j < n0 + n1 ? 1 : 2;
             const int jj = j - (m == 0 ? 0 : m == 1 ? n0 : n0 + n1);
@@ -436,19 +476,18 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
             const uint64_t slot = bslot[m][jj];
             const int c = (int)(e.y >> 5) & 3;
             const uint32_t b = (uint32_t)desc_bits((int)(e.y & 31u));
-            const uint8_t* p = f.srv[c] + e.x;
             VT* out = res + slot * BSQ;
             bool bad;
             if constexpr (BSQ == 16) {
-                const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-                const uint32_t* src = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-#pragma unroll
-                for (int q = 0; q < SLOT_WORDS; ++q) sw[q] = __ldg(src + q);
-                const uint32_t bit0 = (uint32_t)(a & 3) * 8u;
+                // payload words from the staged chunk, else straight from HBM
+                const uint32_t* sw = staged ? cbuf + ((e.x - lo16) >> 2)
+                                            : reinterpret_cast<const uint32_t*>(f.srv[c] + (e.x & ~3u));
+                const uint32_t bit0 = (e.x & 3u) * 8u;
                 if (m == MODE_BITS) bad = decode16<MODE_BITS, VT>(sw, bit0, b, lut, dq, out);
                 else if (m == MODE_TRIT) bad = decode16<MODE_TRIT, VT>(sw, bit0, b, lut, dq, out);
                 else bad = decode16<MODE_QUINT, VT>(sw, bit0, b, lut + 243, dq, out);
             } else {
+                const uint8_t* p = f.srv[c] + e.x;
                 if (m == MODE_BITS) bad = decode_payload<1, 0, BSQ, VT>(p, lut, b, shift, out);
                 else if (m == MODE_TRIT) bad = decode_payload<5, 8, BSQ, VT>(p, lut, b, shift, out);
                 else bad = decode_payload<3, 7, BSQ, VT>(p, lut + 243, b, shift, out);
