@@ -86,6 +86,21 @@ typedef struct rlfc_field {
 int rlfc_decode_blocks(const rlfc_field *f, const int32_t *req, int32_t n,
                        int32_t *out, int32_t *status, void *stream);
 
+/* One block, synchronously: the random-access latency path of
+ * decoder.decode_block / decode_block_progressive (decoder.py:73-112).  The
+ * request travels in the kernel parameters; the B*B values followed by the
+ * status code (0 / 1 / 2, kernels.py:165-171) land in dev (device, B*B+1
+ * int32) and are copied into host (pinned host memory, B*B+1 int32); with
+ * dev NULL the kernel writes them straight into host, which must then be
+ * pinned and device-addressable (unified addressing).  The call returns after
+ * the result is in host (cudaStreamSynchronize on stream).
+ * Out-of-range requests return RLFC_ERR_ARGUMENT (the host checks them first,
+ * decoder.py:51-63). */
+int rlfc_decode_block_sync(const rlfc_field *f, int32_t s, int32_t t,
+                           int32_t bx, int32_t by, int32_t channel,
+                           int32_t stop_level, int32_t *dev, int32_t *host,
+                           void *stream);
+
 /* Whole padded planes.  Replaces kernels.decode_plane_core
  * (kernels.py:219-242) as called by decoder.decode_plane (decoder.py:165-184).
  * planes: n x 3 int32 (s, t, channel); out: n x hp x wp int32.  Failure key =

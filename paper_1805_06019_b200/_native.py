@@ -47,6 +47,8 @@ class RenderGeom(ctypes.Structure):
 _lib = None
 _SIGS = {
     "rlfc_decode_blocks": ["p", "p", "i", "p", "p", "p"],
+    "rlfc_decode_block_sync": ["p", "i", "i", "i", "i", "i", "i", "p", "p",
+                               "p"],
     "rlfc_decode_planes": ["p", "i", "p", "i", "p", "p", "p"],
     "rlfc_decode_field": ["p", "i", "p", "i", "i", "p", "q", "q", "p", "p"],
     "rlfc_decode_field_simple": ["p", "i", "p", "i", "i", "p", "q", "q", "p",

@@ -95,15 +95,26 @@ __host__ __device__ constexpr DigitLut make_digit_lut() {
 // Reads the two aligned 32-bit words covering the position; the buffer must
 // be readable 8 bytes past the last payload byte (device SRV copies carry
 // >= 16 bytes of zero padding).
+// GEN: generic loads (the bytes may sit in shared memory), else read-only
+// global loads.
+template <bool GEN = false>
 __device__ __forceinline__ uint32_t load_bits32(const uint8_t* base, uint64_t bitpos) {
     uintptr_t a = reinterpret_cast<uintptr_t>(base) + (bitpos >> 3);
     const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
     uint32_t sh = (uint32_t)((a & 3) << 3) + (uint32_t)(bitpos & 7);
-    uint32_t lo = __ldg(w), hi = __ldg(w + 1);
+    uint32_t lo, hi;
+    if (GEN) {
+        lo = w[0];
+        hi = w[1];
+    } else {
+        lo = __ldg(w);
+        hi = __ldg(w + 1);
+    }
     return __funnelshift_r(lo, hi, sh);
 }
+template <bool GEN = false>
 __device__ __forceinline__ uint32_t get_bits(const uint8_t* base, uint64_t bitpos, int nbits) {
-    return load_bits32(base, bitpos) & ((1u << nbits) - 1u);
+    return load_bits32<GEN>(base, bitpos) & ((1u << nbits) - 1u);
 }
 
 // Dequantise one zigzag code (bise.py:69-72 unzigzag + hierarchy.py:232-237
@@ -122,7 +133,7 @@ __device__ __forceinline__ int32_t dequant(uint32_t z, int shift) {
 // dequantised values into acc[0..BSQ).  Returns 0 or 1 (corrupt pack).  The
 // whole payload is validated before any value is added, as the reference
 // decodes into tmp first.
-template <int BSQ>
+template <int BSQ, bool GEN = false>
 __device__ int decode_payload_acc(const uint8_t* p, int desc, int shift, int32_t* acc,
                                   const DigitLut& lut) {
     const int mode = desc_mode(desc), b = desc_bits(desc);
@@ -132,25 +143,25 @@ __device__ int decode_payload_acc(const uint8_t* p, int desc, int shift, int32_t
         const uint32_t PMAX = mode == MODE_TRIT ? 242u : 124u;
         const int gbits = PB + G * b;
         for (int g = 0; g * G < BSQ; ++g)
-            if (get_bits(p, (uint64_t)g * gbits, PB) > PMAX) return 1;
+            if (get_bits<GEN>(p, (uint64_t)g * gbits, PB) > PMAX) return 1;
     }
     for (int k = 0; k < BSQ; ++k) {
         uint32_t z;
         if (mode == MODE_BITS) {
-            z = get_bits(p, (uint64_t)k * b, b);
+            z = get_bits<GEN>(p, (uint64_t)k * b, b);
         } else if (mode == MODE_TRIT) {
             int g = k / 5, i = k - 5 * g;
             uint64_t gp = (uint64_t)g * (8 + 5 * b);
-            uint32_t pack = get_bits(p, gp, 8);
+            uint32_t pack = get_bits<GEN>(p, gp, 8);
             uint32_t digit = (lut.trit[pack] >> (2 * i)) & 3u;
-            uint32_t low = b ? get_bits(p, gp + 8 + i * b, b) : 0u;
+            uint32_t low = b ? get_bits<GEN>(p, gp + 8 + i * b, b) : 0u;
             z = (digit << b) | low;
         } else {
             int g = k / 3, i = k - 3 * g;
             uint64_t gp = (uint64_t)g * (7 + 3 * b);
-            uint32_t pack = get_bits(p, gp, 7);
+            uint32_t pack = get_bits<GEN>(p, gp, 7);
             uint32_t digit = (lut.quint[pack] >> (3 * i)) & 7u;
-            uint32_t low = b ? get_bits(p, gp + 7 + i * b, b) : 0u;
+            uint32_t low = b ? get_bits<GEN>(p, gp + 7 + i * b, b) : 0u;
             z = (digit << b) | low;
         }
         acc[k] += dequant(z, shift);
@@ -160,8 +171,9 @@ __device__ int decode_payload_acc(const uint8_t* p, int desc, int shift, int32_t
 
 // 32 presence bits of nodes [n0, n0+32) of a record's bitmap (bit i of the
 // record = byte i>>3 bit i&7, kernels.py:181-183), n0 a multiple of 32.
+template <bool GEN = false>
 __device__ __forceinline__ uint32_t bitmap_word(const uint8_t* rec, int n0) {
-    return load_bits32(rec, (uint64_t)n0);
+    return load_bits32<GEN>(rec, (uint64_t)n0);
 }
 
 // Serial index of image (s, t)'s level-l ancestor (container.py:122-145).
@@ -175,7 +187,7 @@ __device__ __forceinline__ int chain_node(const rlfc_field& f, int l, int s, int
 // find-first-set over the bitmap, so the walk costs one step per PRESENT
 // node; the result and the status (0 / 1 / 2) are identical to the
 // reference's node-by-node loop.
-template <int BSQ>
+template <int BSQ, bool GEN = false>
 __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t, int stop_level,
                           int32_t* acc, const DigitLut& lut, const NodeBytes& nb) {
     const int h = f.tree_height;
@@ -186,7 +198,7 @@ __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t,
     const int last = chain_node(f, stop_level, s, t);
     uint64_t cursor = (uint64_t)f.bitmap_bytes;  // relative to rec
     for (int n0 = 0; n0 <= last; n0 += 32) {
-        uint32_t bits = bitmap_word(rec, n0);
+        uint32_t bits = bitmap_word<GEN>(rec, n0);
         int span = last - n0 + 1;                // nodes n0..last
         if (span < 32) bits &= (1u << span) - 1u;
         while (bits) {
@@ -199,7 +211,7 @@ __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t,
             int desc = rec[cursor];
             if (desc >= NUM_DESC) return 2;
             if (target == node) {
-                int st = decode_payload_acc<BSQ>(rec + cursor + 1, desc, f.quant_shift, acc, lut);
+                int st = decode_payload_acc<BSQ, GEN>(rec + cursor + 1, desc, f.quant_shift, acc, lut);
                 if (st) return st;
                 if (++ti == nt) return 0;
                 target = chain_node(f, h - 1 - ti, s, t);

@@ -39,6 +39,44 @@ __global__ void k_decode_blocks(const rlfc_field f, const int32_t* __restrict__ 
     for (int j = 0; j < B * B; ++j) o[j] = acc[j];
 }
 
+// One block, request in the kernel parameters (random-access latency path):
+// one warp fetches the record offsets and the root samples in one round
+// trip, then the whole record (coalesced 16-byte loads) in a second; lane 0
+// walks it in shared memory (a walk straight from HBM is a chain of
+// dependent cold loads, one per present node).  Values then the status code
+// go to out[0 .. B*B].
+constexpr int ONE_REC_CAP = 16 * 1024;
+template <int B>
+__global__ void __launch_bounds__(32) k_decode_block_one(const rlfc_field f, int s, int t, int bx, int by, int c,
+                                                         int k, int32_t* __restrict__ out) {
+    __shared__ __align__(16) uint8_t rec_s[ONE_REC_CAP];
+    __shared__ int32_t root_s[B * B];
+    const int lane = threadIdx.x;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t blk = (int64_t)by * f.wb + bx;
+    for (int j = lane; j < B * B; j += 32)
+        root_s[j] = root_sample(f, s, t, c, by * B + j / B, bx * B + j % B);
+    const uint64_t off = f.offsets[c][blk];
+    const uint64_t end = blk + 1 < nblk ? f.offsets[c][blk + 1] : f.srv_len[c];
+    const uint64_t lo16 = off & ~uint64_t(15);
+    const bool staged = off <= end && end <= f.srv_len[c] && end + 16 - lo16 <= (uint64_t)ONE_REC_CAP;
+    if (staged) {
+        const uint4* src = reinterpret_cast<const uint4*>(f.srv[c] + lo16);
+        const int n16 = (int)((end + 16 - lo16 + 15) >> 4);
+        for (int q = lane; q < n16; q += 32) reinterpret_cast<uint4*>(rec_s)[q] = __ldg(src + q);
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    int32_t acc[B * B];
+#pragma unroll
+    for (int j = 0; j < B * B; ++j) acc[j] = root_s[j];
+    const int st = staged ? walk_chain<B * B, true>(f, rec_s + (off - lo16), s, t, k, acc, c_lut, c_nb<B>)
+                          : walk_chain<B * B>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<B>);
+#pragma unroll
+    for (int j = 0; j < B * B; ++j) out[j] = acc[j];
+    out[B * B] = st;
+}
+
 // One thread per (plane request, block): kernels.py:219-242 decode_plane_core.
 template <int B>
 __global__ void k_decode_planes(const rlfc_field f, int stop_level, const int32_t* __restrict__ planes,
@@ -192,6 +230,27 @@ extern "C" int rlfc_decode_blocks(const rlfc_field* f, const int32_t* req, int32
     const int grid = (n + threads - 1) / threads;
     RLFC_DISPATCH_B(f->block, k_decode_blocks<BB><<<grid, threads, 0, st>>>(*f, req, n, out, status));
     return launch_status();
+}
+
+extern "C" int rlfc_decode_block_sync(const rlfc_field* f, int32_t s, int32_t t, int32_t bx, int32_t by,
+                                      int32_t c, int32_t stop_level, int32_t* dev, int32_t* host, void* stream) {
+    if (!valid_field(f) || !host) return RLFC_ERR_ARGUMENT;
+    if (s < 0 || s >= f->s_count || t < 0 || t >= f->t_count || bx < 0 || bx >= f->wb || by < 0 ||
+        by >= f->hb || c < 0 || c > 2 || stop_level < 0 || stop_level > f->tree_height)
+        return RLFC_ERR_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dev) {
+        RLFC_DISPATCH_B(f->block, k_decode_block_one<BB><<<1, 32, 0, st>>>(*f, s, t, bx, by, c, stop_level, dev));
+        const int bsq = f->block * f->block;
+        if (cudaMemcpyAsync(host, dev, (size_t)(bsq + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess)
+            return RLFC_ERR_CUDA;
+    } else {
+        // host is pinned, device-addressable memory (unified addressing):
+        // the kernel writes the result straight into it
+        RLFC_DISPATCH_B(f->block, k_decode_block_one<BB><<<1, 32, 0, st>>>(*f, s, t, bx, by, c, stop_level, host));
+    }
+    return cudaStreamSynchronize(st) == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }
 
 extern "C" int rlfc_decode_planes(const rlfc_field* f, int32_t stop_level, const int32_t* planes,

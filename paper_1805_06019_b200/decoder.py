@@ -391,31 +391,43 @@ def bise_decode_batch(payloads, descs, count, device=None):
 # --- reference-signature API ---------------------------------------------------
 
 class _BlockScratch:
-    """Per-thread pinned host + device buffers for single-block requests:
-    one H2D copy, one kernel, one D2H copy, one stream sync."""
+    """Per-thread state for single-block requests: the field's device copy,
+    a device + pinned host buffer of B*B+1 int32 and a private CUDA stream
+    (the decode reads only immutable state), so a request is one ctypes call
+    into rlfc_decode_block_sync (kernel, D2H copy, stream sync)."""
 
     def __init__(self, df, b):
         torch = _torch()
-        self.req_h = torch.empty(6, dtype=torch.int32).pin_memory()
-        self.req_d = torch.empty(6, dtype=torch.int32, device=df.device)
-        self.out_d = torch.empty(b * b + 1, dtype=torch.int32,
-                                 device=df.device)
+        self.df = df
+        self.b = b
+        # pinned host memory is device-addressable (unified addressing): the
+        # kernel writes the block and its status straight into it
         self.out_h = torch.empty(b * b + 1, dtype=torch.int32).pin_memory()
-        self.req_np = self.req_h.numpy()
         self.out_np = self.out_h.numpy()
+        self.stream = torch.cuda.Stream(device=df.device)
+        self.args = (df.ref, None, self.out_h.data_ptr(),
+                     self.stream.cuda_stream)
+        self.fn = _native.lib().rlfc_decode_block_sync
 
 
 _tls = threading.local()
 
 
-def _block_scratch(state, df):
+def _block_scratch(state):
+    last = getattr(_tls, "last", None)
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    if last is not None and last[0] is state and last[1] == dev:
+        return last[2]
     cache = getattr(_tls, "blocks", None)
     if cache is None:
         cache = _tls.blocks = {}
-    key = (id(state), df.device.index)
+    key = (id(state), dev)
     sc = cache.get(key)
-    if sc is None:
-        sc = cache[key] = _BlockScratch(df, state.header.block_size)
+    if sc is None or sc.df is not state.device_field():
+        sc = cache[key] = _BlockScratch(state.device_field(),
+                                        state.header.block_size)
+    _tls.last = (state, dev, sc)
     return sc
 
 
@@ -426,21 +438,21 @@ def decode_block_progressive(state: DecoderState, image_index, block_index,
     bx, by = block_index
     _check_indices(state, s, t, bx, by)
     _check_level(state, stop_level)
-    torch = _torch()
-    df = state.device_field()
-    sc = _block_scratch(state, df)
-    b = state.header.block_size
-    sc.req_np[:] = (s, t, bx, by, channel, stop_level)
-    stream = torch.cuda.current_stream(df.device)
-    sc.req_d.copy_(sc.req_h, non_blocking=True)
-    _native.check(_native.lib().rlfc_decode_blocks(
-        df.ref, sc.req_d.data_ptr(), 1, sc.out_d.data_ptr(),
-        sc.out_d.data_ptr() + 4 * b * b, stream.cuda_stream),
-        "rlfc_decode_blocks")
-    sc.out_h.copy_(sc.out_d, non_blocking=True)
-    stream.synchronize()
-    _raise_status(int(sc.out_np[b * b]))
-    return sc.out_np[:b * b].reshape(b, b).copy()
+    # the reference indexes root_planes[..., channel] and srv[channel]
+    # (decoder.py:73-78, 99-101): Python indexing, so -3..-1 alias 0..2
+    if not -3 <= channel < 3:
+        raise IndexError(f"index {channel} is out of bounds for axis 2 with "
+                         "size 3")
+    channel = int(channel) % 3
+    sc = _block_scratch(state)
+    ref, dev, host, stream = sc.args
+    rc = sc.fn(ref, s, t, bx, by, channel, stop_level, dev, host, stream)
+    if rc:
+        _native.check(rc, "rlfc_decode_block_sync")
+    b = sc.b
+    out = sc.out_np.copy()
+    _raise_status(int(out[b * b]))
+    return out[:b * b].reshape(b, b)
 
 
 def decode_block(state: DecoderState, image_index, block_index, channel):

@@ -70,6 +70,10 @@ def test_block_equals_plane_region(rl, st):
 
 
 def test_index_and_level_errors(rl, st):
+    # channel indexes the reference's per-channel tuples: -1 is channel 2
+    assert np.array_equal(rl.decode_block(st, (2, 3), (4, 5), -1), rl.decode_block(st, (2, 3), (4, 5), 2))
+    with pytest.raises(IndexError):
+        rl.decode_block(st, (0, 0), (0, 0), 3)
     with pytest.raises(IndexError):
         rl.decode_block(st, (8, 0), (0, 0), 0)
     with pytest.raises(IndexError):

@@ -1,0 +1,29 @@
+"""Single-block decode latency through the public API (decode_block), as a
+host application calls it: 2,000 random picks on the bench stream."""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1805_06019_b200 as rl  # noqa: E402
+
+data, _ = bench.make_stream(bench.CFG)
+st = rl.init(data)
+hdr = st.header
+wb, hb = hdr.block_grid
+rng = np.random.default_rng(7)
+picks = [(int(rng.integers(0, hdr.s_count)), int(rng.integers(0, hdr.t_count)),
+          int(rng.integers(0, wb)), int(rng.integers(0, hb)), int(rng.integers(0, 3)))
+         for _ in range(2000)]
+for s, t, bx, by, c in picks[:50]:
+    rl.decode_block(st, (s, t), (bx, by), c)
+t0 = time.perf_counter()
+for s, t, bx, by, c in picks:
+    rl.decode_block(st, (s, t), (bx, by), c)
+dt = (time.perf_counter() - t0) / len(picks)
+print(f"decode_block latency {dt * 1e6:.2f} us (mean of {len(picks)})")
