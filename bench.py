@@ -400,7 +400,8 @@ def e2e_measure(state, band, args, rl):
             "d2h_bytes_per_step": res.d2h_bytes,
             "ms_per_step": dt * 1e3,
             "path": "decoder.HostPipeline: pinned H2D of SRV+offsets+roots, "
-                    "staged decode, pinned D2H of RGB"}
+                    "staged decode, pinned D2H of RGB; 8 block-row bands "
+                    "pipelined over three CUDA streams (PCIe D2H-bound)"}
 
 
 def random_access_measure(state, rl):

@@ -206,6 +206,12 @@ int rlfc_render_pinhole_needs(int32_t S, int32_t T, int32_t W, int32_t H,
                               int32_t ow, int32_t oh, uint8_t *need,
                               void *stream);
 
+/* Host plumbing for band-pipelined host-buffer decodes (decoder.HostPipeline):
+ * an asynchronous strided copy (cudaMemcpy2DAsync), kind 0 host->device,
+ * 1 device->host, 2 device->device.  Not part of the reference interface. */
+int rlfc_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                int64_t width, int64_t height, int32_t kind, void *stream);
+
 /* Library identification: returns the number of kernels this build exposes
  * and writes a short version string. */
 int rlfc_version(char *buf, int32_t len);

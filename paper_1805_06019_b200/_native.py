@@ -64,6 +64,7 @@ _SIGS = {
                             "i", "i", "p", "p", "p"],
     "rlfc_render_pinhole_needs": ["i", "i", "i", "i", "p", "p", "i", "i", "i",
                                   "p", "p"],
+    "rlfc_copy2d": ["p", "q", "p", "q", "q", "q", "i", "p"],
     "rlfc_version": ["p", "i"],
 }
 _CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64,

@@ -305,6 +305,19 @@ extern "C" int rlfc_bise_decode(const uint8_t* data, const int64_t* offs, const 
     return launch_status();
 }
 
+extern "C" int rlfc_copy2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                           int64_t height, int32_t kind, void* stream) {
+    if (!dst || !src || width < 0 || height < 0 || kind < 0 || kind > 2) return RLFC_ERR_ARGUMENT;
+    if (width == 0 || height == 0) return RLFC_OK;
+    const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                           : kind == 1 ? cudaMemcpyDeviceToHost
+                                       : cudaMemcpyDeviceToDevice;
+    return cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height, k,
+                             (cudaStream_t)stream) == cudaSuccess
+               ? RLFC_OK
+               : RLFC_ERR_CUDA;
+}
+
 extern "C" int rlfc_version(char* buf, int32_t len) {
     const char* v = "rlfc_b200 0.1 sm_100a";
     if (buf && len > 0) {

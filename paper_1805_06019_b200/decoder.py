@@ -535,10 +535,13 @@ class HostPipeline:
     """End-to-end decode with host buffers, the path a host application
     takes: every run() uploads the compressed sections (SRV + offsets) and
     the root planes from pinned host memory, runs the staged decode, and
-    copies the RGB8 result into pinned host memory.  h2d_bytes / d2h_bytes
+    copies the RGB8 result into pinned host memory.  The rows are split into
+    `bands` block-row bands pipelined over three CUDA streams (upload of band
+    i+1 | decode of band i | download of band i-1), so the PCIe transfers in
+    both directions overlap each other and the decode.  h2d_bytes / d2h_bytes
     are the bytes those copies move per run."""
 
-    def __init__(self, state, rows=None, device=None):
+    def __init__(self, state, rows=None, device=None, bands=8):
         torch = _torch()
         self.state = state
         hdr = state.header
@@ -550,41 +553,100 @@ class HostPipeline:
         src = state.device_field(device)
         self.df = DeviceField(hdr, state.srv, state.offsets,
                               state.root_planes, src.device)
-        self.host = [t.cpu().pin_memory() for t in
-                     self.df.srv + self.df.offsets + [self.df.roots]]
-        self.dev = self.df.srv + self.df.offsets + [self.df.roots]
-        self.h2d_bytes = sum(t.numel() * t.element_size() for t in self.host)
+        self.host_srv = [t.cpu().pin_memory() for t in self.df.srv]
+        self.host_off = [t.cpu().pin_memory() for t in self.df.offsets]
+        self.host_roots = self.df.roots.cpu().pin_memory()
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in
+                             self.host_srv + self.host_off) + \
+            self.host_roots.numel() * self.host_roots.element_size()
         shape = (hdr.s_count, hdr.t_count, self.rows_px, hdr.width, 3)
         self.out = torch.empty(shape, dtype=torch.uint8, device=src.device)
         self.out_host = torch.empty(shape, dtype=torch.uint8).pin_memory()
         self.d2h_bytes = self.out_host.numel()
         self.status = torch.zeros(1, dtype=torch.int64, device=src.device)
+        lo, hi = self.rows
+        # banded uploads need the records in block order (a corrupt stream
+        # may not have them): else one band with everything uploaded
+        self.monotone = all(bool(np.all(np.diff(o.astype(np.int64)) >= 0))
+                            for o in state.offsets)
+        n = max(1, min(bands, hi - lo)) if self.monotone else 1
+        cuts = [lo + (hi - lo) * i // n for i in range(n + 1)]
+        self.bands = [(a, b) for a, b in zip(cuts, cuts[1:]) if b > a]
+        self.streams = [torch.cuda.Stream(device=src.device) for _ in range(3)]
+
+    def _srv_range(self, c, lo, hi):
+        hdr = self.state.header
+        wb, hb = hdr.block_grid
+        if not self.monotone:
+            return 0, self.host_srv[c].numel()
+        offs = self.state.offsets[c]
+        a = int(offs[lo * wb]) if lo < hb else len(self.state.srv[c])
+        b = int(offs[hi * wb]) if hi < hb else len(self.state.srv[c])
+        if hi >= hb:
+            b = self.host_srv[c].numel()              # + the zero tail padding
+        return a, b
 
     def run(self):
         torch = _torch()
         hdr = self.state.header
-        for d, h in zip(self.dev, self.host):
-            d.copy_(h, non_blocking=True)
-        self.status.zero_()
-        W = hdr.width
         L = _native.lib()
-        with torch.cuda.device(self.df.device):
-            stream = _stream()
-            ws = self.df.staged_workspace(stream)
-            rc = _native.RLFC_ERR_ARGUMENT
-            if ws is not None:
-                rc = L.rlfc_decode_field_staged(
-                    self.df.ref, 0, None, self.rows[0], self.rows[1],
-                    self.out.data_ptr(), self.rows_px * W * 3, W * 3,
-                    ws[0].data_ptr(), ws[1], ws[2], self.status.data_ptr(),
-                    stream)
-            if rc == _native.RLFC_ERR_ARGUMENT:
-                rc = L.rlfc_decode_field(
-                    self.df.ref, 0, None, self.rows[0], self.rows[1],
-                    self.out.data_ptr(), self.rows_px * W * 3, W * 3,
-                    self.status.data_ptr(), stream)
-            _native.check(rc, "rlfc_decode_field")
-        self.out_host.copy_(self.out, non_blocking=True)
-        torch.cuda.current_stream(self.df.device).synchronize()
+        W, B = hdr.width, hdr.block_size
+        s_in, s_dec, s_out = self.streams
+        df = self.df
+        rt = df.roots
+        esz = rt.element_size()
+        plane = hdr.padded_dims[0] * hdr.padded_dims[1] * esz
+        row_b = hdr.padded_dims[0] * B * esz             # one block row of a root plane
+        nplanes = rt.numel() * esz // plane if plane else 0
+        img = self.rows_px * W * 3
+        self.status.zero_()
+        cur = torch.cuda.current_stream(df.device)
+        for s in self.streams:
+            s.wait_stream(cur)
+        with torch.cuda.device(df.device):
+            ws = df.staged_workspace(s_dec.cuda_stream)
+            with torch.cuda.stream(s_in):
+                for d, h in zip(df.offsets, self.host_off):
+                    d.copy_(h, non_blocking=True)
+            for lo, hi in self.bands:
+                with torch.cuda.stream(s_in):
+                    for c in range(3):
+                        a, b = self._srv_range(c, lo, hi)
+                        if b > a:
+                            df.srv[c][a:b].copy_(self.host_srv[c][a:b],
+                                                 non_blocking=True)
+                    _native.check(L.rlfc_copy2d(
+                        rt.data_ptr() + lo * row_b, plane,
+                        self.host_roots.data_ptr() + lo * row_b, plane,
+                        (hi - lo) * row_b, nplanes, 0, s_in.cuda_stream),
+                        "rlfc_copy2d")
+                    ev = torch.cuda.Event()
+                    ev.record(s_in)
+                s_dec.wait_event(ev)
+                y0 = lo * B - self.rows[0] * B
+                y1 = min(hi * B, hdr.height) - self.rows[0] * B
+                dst = self.out.data_ptr() + y0 * W * 3
+                rc = _native.RLFC_ERR_ARGUMENT
+                if ws is not None:
+                    rc = L.rlfc_decode_field_staged(
+                        df.ref, 0, None, lo, hi, dst, img, W * 3,
+                        ws[0].data_ptr(), ws[1], ws[2],
+                        self.status.data_ptr(), s_dec.cuda_stream)
+                if rc == _native.RLFC_ERR_ARGUMENT:
+                    rc = L.rlfc_decode_field(
+                        df.ref, 0, None, lo, hi, dst, img, W * 3,
+                        self.status.data_ptr(), s_dec.cuda_stream)
+                _native.check(rc, "rlfc_decode_field")
+                ev2 = torch.cuda.Event()
+                ev2.record(s_dec)
+                s_out.wait_event(ev2)
+                if y1 > y0:
+                    _native.check(L.rlfc_copy2d(
+                        self.out_host.data_ptr() + y0 * W * 3, img,
+                        self.out.data_ptr() + y0 * W * 3, img,
+                        (y1 - y0) * W * 3, hdr.s_count * hdr.t_count, 1,
+                        s_out.cuda_stream), "rlfc_copy2d")
+        s_out.synchronize()
+        s_dec.synchronize()
         _raise_word(self.status.cpu().item())
         return self.out_host

@@ -271,3 +271,21 @@ def test_gpu_matches_oracle_random_access(rl):
         for r, got in zip(req, out):
             want, code = orc.decode_block(*map(int, r))
             assert code == 0 and np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", ["kat8_default", "mid17_r4", "b8_h2", "odd_3x5", "b16_h4"])
+def test_host_pipeline_matches_device_decode(rl, name):
+    """decoder.HostPipeline (banded H2D | decode | D2H over three streams,
+    the bench's e2e path) returns the same pixels as decode_field."""
+    from paper_1805_06019_b200 import decoder
+    st = state_for(rl, name)
+    full, _ = rl.decode_field(st, kernel="simple")
+    full = full.cpu().numpy()
+    hb = st.header.block_grid[1]
+    B = st.header.block_size
+    for bands in (1, 3, 8):
+        out = decoder.HostPipeline(st, bands=bands).run()
+        assert np.array_equal(out.numpy(), full), bands
+    lo, hi = (1, max(2, hb - 1)) if hb > 2 else (0, hb)
+    out = decoder.HostPipeline(st, rows=(lo, hi), bands=2).run()
+    assert np.array_equal(out.numpy(), full[:, :, lo * B:min(hi * B, st.header.height)])
