@@ -19,8 +19,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--kernel", default="staged")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--render", type=int, default=0)
+ap.add_argument("--preset", default="R4", help="cfg2 bitrate preset (tools/bitrate_sweep.py)")
 a = ap.parse_args()
-data, _ = bench.make_stream(bench.CFG)
+cfg = bench.CFG
+if a.preset != "R4":
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from bitrate_sweep import PRESETS
+    h, B, s, tp, tb = PRESETS[a.preset]
+    cfg = dict(bench.CFG, h=h, B=B, shift=s, tp=tp, tb=tb)
+data, _ = bench.make_stream(cfg)
 st = rl.init(data)
 hdr = st.header
 out = torch.empty((hdr.s_count, hdr.t_count, hdr.height, hdr.width, 3),
