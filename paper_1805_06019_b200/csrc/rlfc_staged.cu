@@ -499,6 +499,17 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
 }
 
 // ---- pass 3: blend -------------------------------------------------------------------
+#ifdef RLFC_BLEND_TIMING
+// per-CTA %globaltimer stamps of k_blend (debug build, tools/blend_timing.py):
+// start, records done, sync1, units done, TMA wait + sync2, tasks done, sync3,
+// store read
+__device__ long long g_btime[65536 * 8];
+#define RLFC_BSTAMP(q) do { if (threadIdx.x == 0 && bidx < 65536) { long long tt; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)); g_btime[bidx * 8 + (q)] = tt; } } while (0)
+#else
+#define RLFC_BSTAMP(q) do { } while (0)
+#endif
+
 struct BlendParams {
     rlfc_field f;
     int k;
@@ -519,7 +530,7 @@ struct BlendParams {
     int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
     int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
     int debug;                   // timing experiments only (RLFC_BLEND_DEBUG): 1 no tasks,
-                                 // 2 no store, 4 no input TMA, 8 no records
+                                 // 2 no store, 4 no input TMA, 8 no records, 16 no L2 hint
     int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
     int off_flag, off_mask, off_sbase, off_roots, off_rgb, off_cnt, off_list, off_stage,
         off_mbar;
@@ -657,13 +668,17 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     uint2* list = reinterpret_cast<uint2*>(smem + P.off_list);              // [S*NB]
     uint8_t* stage = smem + P.off_stage;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_mbar);
+#ifdef RLFC_BLEND_TIMING
+    const int64_t bidx = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+#endif
+    RLFC_BSTAMP(0);
 
     // ---- TMA: RGB(root) rows into every view's staging rows, raw roots ----------------
-    if (P.tma_in && tid < 32 && !(P.debug & 4)) {
-        // warp 0: lane 0 arms the barrier, then every lane issues its share of
-        // the tensor loads
+    if (P.tma_in && tid >= BT - 32 && !(P.debug & 4)) {
+        // last warp (no record work when NR <= BT - 32): lane 0 arms the
+        // barrier, then every lane issues its share of the tensor loads
         const uint32_t bar = smem_u32(mbar);
-        if (tid == 0) {
+        if (tid == BT - 32) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             const uint32_t bytes =
@@ -672,7 +687,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         }
         __syncwarp();
         const int nrgb = P.nstrip * S;
-        for (int i = tid; i < nrgb + f.rsx * 3; i += 32) {
+        for (int i = tid - (BT - 32); i < nrgb + f.rsx * 3; i += 32) {
             if (i < nrgb) {
                 const int st = i / S, s = i - st * S;
                 asm volatile(
@@ -701,22 +716,49 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
             const int64_t ri = (int64_t)c * nblk + blk;
             fl = __ldg(P.rec_flag + ri);
             {
+                // every table word of the first RL levels is loaded before
+                // any is used (one round trip, not one per level); they are
                 // loaded regardless of the flag (stale for flagged records,
-                // which never read them) so every load of a lane is in flight
-                // at once
+                // which never read them)
+                constexpr int RL = 3;
                 const int64_t nrec = 3 * nblk;
                 const uint32_t* bmr = P.bm + ri;
                 const uint32_t* rkr = P.rk + ri;
-                for (int l = h - 1; l >= k; --l) {
-                    const int sx = f.level_sx[l];
+                uint32_t lo[RL], hi[RL], hi2[RL], rkv[RL];
+#pragma unroll
+                for (int li = 0; li < RL; ++li) {
+                    lo[li] = hi[li] = hi2[li] = rkv[li] = 0u;
+                    if (li < nlev) {
+                        const int l = k + li, sx = f.level_sx[l];
+                        const int wi = (f.level_base[l] + (t >> l) * sx) >> 5;
+                        lo[li] = __ldg(bmr + wi * nrec);
+                        hi[li] = __ldg(bmr + (wi + 1) * nrec);
+                        if (sx > 32) hi2[li] = __ldg(bmr + (wi + 2) * nrec);
+                        rkv[li] = __ldg(rkr + wi * nrec);
+                    }
+                }
+#pragma unroll
+                for (int li = 0; li < RL; ++li) {
+                    if (li < nlev) {
+                        const int l = k + li, sx = f.level_sx[l];
+                        const int o = (f.level_base[l] + (t >> l) * sx) & 31;
+                        uint64_t m = __funnelshift_r(lo[li], hi[li], o);
+                        if (sx > 32) m |= (uint64_t)__funnelshift_r(hi[li], hi2[li], o) << 32;
+                        if (sx < 64) m &= (1ull << sx) - 1ull;
+                        mask[li * NR + r] = m;
+                        sbase[li * NR + r] = rkv[li] + __popc(lo[li] & ((1u << o) - 1u));
+                    }
+                }
+                for (int li = RL; li < nlev; ++li) {             // deeper trees
+                    const int l = k + li, sx = f.level_sx[l];
                     const int n0 = f.level_base[l] + (t >> l) * sx;
                     const int wi = n0 >> 5, o = n0 & 31;
-                    const uint32_t lo = __ldg(bmr + wi * nrec), hi = __ldg(bmr + (wi + 1) * nrec);
-                    uint64_t m = __funnelshift_r(lo, hi, o);
-                    if (sx > 32) m |= (uint64_t)__funnelshift_r(hi, __ldg(bmr + (wi + 2) * nrec), o) << 32;
+                    const uint32_t a = __ldg(bmr + wi * nrec), c2 = __ldg(bmr + (wi + 1) * nrec);
+                    uint64_t m = __funnelshift_r(a, c2, o);
+                    if (sx > 32) m |= (uint64_t)__funnelshift_r(c2, __ldg(bmr + (wi + 2) * nrec), o) << 32;
                     if (sx < 64) m &= (1ull << sx) - 1ull;
-                    mask[(l - k) * NR + r] = m;
-                    sbase[(l - k) * NR + r] = __ldg(rkr + wi * nrec) + __popc(lo & ((1u << o) - 1u));
+                    mask[li * NR + r] = m;
+                    sbase[li * NR + r] = __ldg(rkr + wi * nrec) + __popc(a & ((1u << o) - 1u));
                 }
             }
         } else if (nlev > 0) {
@@ -752,7 +794,9 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
             ycocg4_pack(v, o);
         }
     }
+    RLFC_BSTAMP(1);
     __syncthreads();
+    RLFC_BSTAMP(2);
 
     // ---- dirty (view, block) units: one thread per pair tests the chain's
     // presence bits (bit 3(l-k)+c: level l, channel c) and appends dirty pairs
@@ -797,6 +841,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
             for (int v = lane; v < V; v += 32) dst[v] = src[v];
         }
     }
+    RLFC_BSTAMP(3);
     if (P.tma_in && !(P.debug & 4)) {
         const uint32_t bar = smem_u32(mbar);
         uint32_t done = 0;
@@ -808,6 +853,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                 : "memory");
     }
     __syncthreads();
+    RLFC_BSTAMP(4);
 
     // ---- dirty units: root + present residuals, YCoCg-R inverse, clamp, pack ----------
     // one task = two consecutive pixel quad-rows of a unit (8 consecutive
@@ -876,26 +922,42 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                 ycocg4_pack(v[hh], reinterpret_cast<uint32_t*>(stage + stage_off<B>(S, s, row[hh], px[hh])));
         }
     }
+    RLFC_BSTAMP(5);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
+    RLFC_BSTAMP(6);
 
     // ---- store ------------------------------------------------------------------------
     const int nrows_band = min(by * B + B, f.height) - by * B;   // rows of this block row
     if (P.debug & 2) {
     } else if (P.store_mode == 2) {
         if (tid == 0) {
+            // the output streams through L2 once: evict it first so the
+            // record tables, residuals and root colours the other tiles
+            // gather stay resident
+            uint64_t pol = 0;
+            if (!(P.debug & 16)) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             for (int st = 0; st < P.nstrip; ++st) {
                 const int x0 = (bx0 * B + st * STRIP) * 3;
                 if (x0 >= f.width * 3) break;
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                        &out_map),
-                    "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0),
-                    "r"(smem_u32(stage + st * S * B * STRIP * 3))
-                    : "memory");
+                if (P.debug & 16)
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                            &out_map),
+                        "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0),
+                        "r"(smem_u32(stage + st * S * B * STRIP * 3))
+                        : "memory");
+                else
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], "
+                        "[%5], %6;" ::"l"(&out_map),
+                        "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0),
+                        "r"(smem_u32(stage + st * S * B * STRIP * 3)), "l"(pol)
+                        : "memory");
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            RLFC_BSTAMP(7);
         }
     } else {
         // per (view, row, strip): bulk copy when the strip is whole, else bytes
@@ -1106,6 +1168,12 @@ static bool in_envelope(const rlfc_field& f) {
 }  // namespace rlfc
 
 using namespace rlfc;
+
+#ifdef RLFC_BLEND_TIMING
+extern "C" int rlfc_debug_blend(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, staged::g_btime, sizeof(staged::g_btime)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 extern "C" int rlfc_count_present(const rlfc_field* f, uint64_t* count, void* stream) {
     if (!f || !count) return RLFC_ERR_ARGUMENT;
