@@ -187,12 +187,20 @@ __device__ __forceinline__ int chain_node(const rlfc_field& f, int l, int s, int
 // find-first-set over the bitmap, so the walk costs one step per PRESENT
 // node; the result and the status (0 / 1 / 2) are identical to the
 // reference's node-by-node loop.
+//
+// avail: bytes of the stream readable from rec (the SRV section from the
+// record on; bit windows may read 8 bytes further, into the 16-byte
+// padding).  A descriptor or payload past avail returns WALK_OOB: the
+// reference has no defined behaviour there (numba does not bounds-check),
+// and the device must not fault; callers report it as code 2.
+constexpr int WALK_OOB = 3;
 template <int BSQ, bool GEN = false>
 __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t, int stop_level,
-                          int32_t* acc, const DigitLut& lut, const NodeBytes& nb) {
+                          int32_t* acc, const DigitLut& lut, const NodeBytes& nb, uint64_t avail) {
     const int h = f.tree_height;
     const int nt = h - stop_level;
     if (nt <= 0) return 0;
+    if ((uint64_t)f.bitmap_bytes > avail) return WALK_OOB;
     int ti = 0;                                  // next target, level h-1-ti
     int target = chain_node(f, h - 1, s, t);
     const int last = chain_node(f, stop_level, s, t);
@@ -208,8 +216,10 @@ __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t,
                 if (++ti == nt) return 0;
                 target = chain_node(f, h - 1 - ti, s, t);
             }
+            if (cursor >= avail) return WALK_OOB;
             int desc = rec[cursor];
             if (desc >= NUM_DESC) return 2;
+            if (cursor + nb.v[desc] > avail) return WALK_OOB;
             if (target == node) {
                 int st = decode_payload_acc<BSQ, GEN>(rec + cursor + 1, desc, f.quant_shift, acc, lut);
                 if (st) return st;
@@ -220,6 +230,11 @@ __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t,
         }
     }
     return 0;
+}
+
+// Bytes of channel c's SRV section from byte offset off on (0 past the end).
+__device__ __forceinline__ uint64_t srv_avail(const rlfc_field& f, int c, uint64_t off) {
+    return off < f.srv_len[c] ? f.srv_len[c] - off : 0;
 }
 
 __device__ __forceinline__ int32_t root_sample(const rlfc_field& f, int s, int t, int c, int y, int x) {

@@ -31,8 +31,9 @@ __global__ void k_decode_blocks(const rlfc_field f, const int32_t* __restrict__ 
     for (int yy = 0; yy < B; ++yy)
 #pragma unroll
         for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
-    const uint8_t* rec = f.srv[c] + f.offsets[c][by * f.wb + bx];
-    int st = walk_chain<B * B>(f, rec, s, t, k, acc, c_lut, c_nb<B>);
+    const uint64_t off = f.offsets[c][by * f.wb + bx];
+    int st = walk_chain<B * B>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<B>, srv_avail(f, c, off));
+    if (st == WALK_OOB) st = 2;
     status[i] = st;
     int32_t* o = out + (int64_t)i * B * B;
 #pragma unroll
@@ -70,8 +71,23 @@ __global__ void __launch_bounds__(32) k_decode_block_one(const rlfc_field f, int
     int32_t acc[B * B];
 #pragma unroll
     for (int j = 0; j < B * B; ++j) acc[j] = root_s[j];
-    const int st = staged ? walk_chain<B * B, true>(f, rec_s + (off - lo16), s, t, k, acc, c_lut, c_nb<B>)
-                          : walk_chain<B * B>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<B>);
+    // the staged copy holds the record (+16 bytes); a corrupt record whose
+    // walk runs past it is walked again from the stream in HBM
+    int st = WALK_OOB;
+    if (staged) {
+        int32_t acc2[B * B];
+#pragma unroll
+        for (int j = 0; j < B * B; ++j) acc2[j] = acc[j];
+        st = walk_chain<B * B, true>(f, rec_s + (off - lo16), s, t, k, acc2, c_lut, c_nb<B>, end - off);
+        if (st != WALK_OOB) {
+#pragma unroll
+            for (int j = 0; j < B * B; ++j) acc[j] = acc2[j];
+        }
+    }
+    if (st == WALK_OOB) {
+        st = walk_chain<B * B>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<B>, srv_avail(f, c, off));
+        if (st == WALK_OOB) st = 2;
+    }
 #pragma unroll
     for (int j = 0; j < B * B; ++j) out[j] = acc[j];
     out[B * B] = st;
@@ -93,8 +109,9 @@ __global__ void k_decode_planes(const rlfc_field f, int stop_level, const int32_
     for (int yy = 0; yy < B; ++yy)
 #pragma unroll
         for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
-    const uint8_t* rec = f.srv[c] + f.offsets[c][blk];
-    int st = walk_chain<B * B>(f, rec, s, t, stop_level, acc, c_lut, c_nb<B>);
+    const uint64_t off = f.offsets[c][blk];
+    int st = walk_chain<B * B>(f, f.srv[c] + off, s, t, stop_level, acc, c_lut, c_nb<B>, srv_avail(f, c, off));
+    if (st == WALK_OOB) st = 2;
     if (st) report(status, (uint64_t)r * nblk + blk, st);
     int32_t* o = out + (int64_t)r * f.hp * f.wp;
 #pragma unroll
@@ -126,8 +143,10 @@ __global__ void k_decode_field_simple(const rlfc_field f, int stop_level, const 
 #pragma unroll
             for (int xx = 0; xx < B; ++xx)
                 acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
-        const uint8_t* rec = f.srv[c] + f.offsets[c][by * f.wb + bx];
-        int st = walk_chain<B * B>(f, rec, s, t, stop_level, acc[c], c_lut, c_nb<B>);
+        const uint64_t off = f.offsets[c][by * f.wb + bx];
+        int st = walk_chain<B * B>(f, f.srv[c] + off, s, t, stop_level, acc[c], c_lut, c_nb<B>,
+                                   srv_avail(f, c, off));
+        if (st == WALK_OOB) st = 2;
         if (st) {
             report(status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
             return;

@@ -176,8 +176,10 @@ __device__ __noinline__ void tile_fallback(const Params& P, int by, int bx0, int
         for (int c = 0; c < 3 && !bad; ++c) {
             for (int yy = 0; yy < B; ++yy)
                 for (int xx = 0; xx < B; ++xx) acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
-            const uint8_t* rec = f.srv[c] + f.offsets[c][by * f.wb + bx];
-            int st = walk_chain<B * B>(f, rec, s, t, P.stop_level, acc[c], lut, nb_tab);
+            const uint64_t off = f.offsets[c][by * f.wb + bx];
+            int st = walk_chain<B * B>(f, f.srv[c] + off, s, t, P.stop_level, acc[c], lut, nb_tab,
+                                       srv_avail(f, c, off));
+            if (st == WALK_OOB) st = 2;
             if (st) {
                 report(P.status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
                 bad = true;
@@ -258,22 +260,26 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         if (tid < 8) cnt[tid] = 0;
     }
     // ---- the tile's record bytes --------------------------------------------
-    uint64_t abeg[3], aend[3];
+    uint64_t abeg[3], aend[3], tend[3];
     uint32_t sbase[3];
-    uint32_t total = 0;
+    uint64_t total = 0;
+    bool range_ok = true;
     const bool need_srv = k < h;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int64_t blk0 = (int64_t)by * f.wb + bx0;
         const uint64_t beg = f.offsets[c][blk0];
         const uint64_t end = (blk0 + nb < (int64_t)f.wb * f.hb) ? f.offsets[c][blk0 + nb] : f.srv_len[c];
+        range_ok &= beg <= end && end <= f.srv_len[c];
+        tend[c] = end;
         abeg[c] = beg & ~uint64_t(15);
         aend[c] = (end + 15) & ~uint64_t(15);
-        sbase[c] = total;
-        total += need_srv ? (uint32_t)(aend[c] - abeg[c]) : 0u;
+        sbase[c] = (uint32_t)total;
+        total += need_srv && range_ok ? aend[c] - abeg[c] : 0u;
     }
     __syncthreads();
-    if (total + 16 > (uint32_t)P.bytes_cap) {      // does not fit: reference-order walk
+    // does not fit, or the offsets leave the section: reference-order walk
+    if ((need_srv && !range_ok) || total + 16 > (uint64_t)P.bytes_cap) {
         tile_fallback<B>(P, by, bx0, nb, lut, nbt);
         return;
     }
@@ -332,8 +338,12 @@ __global__ void __launch_bounds__(Cfg<B, TW>::MAX_THREADS)
         const int64_t blk = (int64_t)by * f.wb + bx0 + wblk;
         const uint64_t rb = f.offsets[wc][blk];
         const uint64_t re = (blk + 1 < (int64_t)f.wb * f.hb) ? f.offsets[wc][blk + 1] : f.srv_len[wc];
-        my_beg = sbase[wc] + (uint32_t)(rb - abeg[wc]);
-        my_len = (uint32_t)(re - rb);
+        // a record outside the tile's staged range (non-monotone offsets)
+        // gets length 0: the pre-walk flags it and the tile falls back
+        if (rb >= abeg[wc] && rb <= re && re <= tend[wc]) {
+            my_beg = sbase[wc] + (uint32_t)(rb - abeg[wc]);
+            my_len = (uint32_t)(re - rb);
+        }
     }
     if (tid < C::NREC) err[tid] = 0;
     __syncthreads();

@@ -618,8 +618,9 @@ __device__ __noinline__ void unit_fallback(const BlendParams& P, uint8_t* stage,
     for (int c = 0; c < 3; ++c) {
         for (int yy = 0; yy < B; ++yy)
             for (int xx = 0; xx < B; ++xx) acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
-        const uint8_t* rec = f.srv[c] + f.offsets[c][(int64_t)by * f.wb + bx];
-        const int st = walk_chain<BSQ>(f, rec, s, t, P.k, acc[c], g_lut, node_bytes<BSQ>());
+        const uint64_t off = f.offsets[c][(int64_t)by * f.wb + bx];
+        int st = walk_chain<BSQ>(f, f.srv[c] + off, s, t, P.k, acc[c], g_lut, node_bytes<BSQ>(), srv_avail(f, c, off));
+        if (st == WALK_OOB) st = 2;
         if (st) {
             report(P.status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
             return;

@@ -289,3 +289,36 @@ def test_host_pipeline_matches_device_decode(rl, name):
     lo, hi = (1, max(2, hb - 1)) if hb > 2 else (0, hb)
     out = decoder.HostPipeline(st, rows=(lo, hi), bands=2).run()
     assert np.array_equal(out.numpy(), full[:, :, lo * B:min(hi * B, st.header.height)])
+
+
+@pytest.mark.parametrize("name", ["kat8_default", "mid17_r4"])
+def test_corrupt_offsets_never_fault(rl, name):
+    """Record offsets that leave the SRV section or run backwards (undefined
+    in the reference, which does not bounds-check) must not fault the
+    device: every kernel reports the same failure word, and decode_block
+    raises FormatError or returns a block."""
+    from paper_1805_06019_b200 import container
+    data = load_stream(name)
+    hdr = container.parse_header(data)
+    starts, _ = container.section_offsets(hdr)
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(99)
+    for trial in range(6):
+        bad = bytearray(data)
+        c = int(rng.integers(0, 3))
+        blk = int(rng.integers(1, wb * hb - 1))
+        pos = starts[c][1] + 8 * blk
+        val = [hdr.section_lengths[c][2] + 4096, 2 ** 40, 0, int(rng.integers(0, hdr.section_lengths[c][2]))][trial % 4]
+        bad[pos:pos + 8] = int(val).to_bytes(8, "little")
+        st = rl.init(bytes(bad))
+        words = []
+        for kern in ("staged", "fused", "simple"):
+            _, sw = rl.decode_field(st, 0, kernel=kern, check=False)
+            words.append(sw.item())
+        assert words[0] == words[1] == words[2], (trial, words)
+        by, bx = divmod(blk, wb)
+        try:
+            rl.decode_block(st, (0, 0), (bx, by), c)
+        except rl.FormatError:
+            pass
+    torch.cuda.synchronize()
