@@ -63,75 +63,106 @@ __device__ __forceinline__ uint8_t round_clip(double a) {
     return fl < 0.0 ? 0 : (fl > 255.0 ? 255 : (uint8_t)fl);
 }
 
-// One thread per output pixel of one slab pose (renderer.py:233-276).
-__global__ void k_render_slab(const uint8_t* __restrict__ field, const int32_t* __restrict__ slots, int S, int T,
-                              int W, int H,
-                              const double* __restrict__ poses, const rlfc_render_geom* __restrict__ geoms,
-                              const uint8_t* __restrict__ bgs, int ow, int oh, uint8_t* __restrict__ out) {
+// Slab poses (renderer.py:233-276).  A ray's image-plane hit, hence its u
+// tap, depends only on the output column, and its v tap only on the row
+// (the eye and the focal plane are per pose), so one CTA per (pose, band of
+// RB output rows) evaluates the column and row terms once into shared memory
+// with exactly the reference's operations, and each pixel then only blends
+// its 16 taps in the reference's (s, t, p, q) order.
+constexpr int RB = 16;
+struct AxisTap {
+    double f;      // fraction of the upper tap
+    int i0;        // lower tap index
+    int inside;    // hit within the image-plane window along this axis
+};
+
+// renderer.py:177-187 + 251-261 along one axis: target, direction, hit,
+// window test, texel coordinate, snap, _vec_taps.
+__device__ __forceinline__ AxisTap slab_axis(int i, int n_out, double lo, double hi, double e, double tp, int n_px) {
+    const double wdt = sub(hi, lo);
+    const double tx = add(lo, dvd(mul(add((double)i, 0.5), wdt), (double)n_out));
+    const double dx = sub(tx, e);
+    const double ix = add(e, mul(tp, dx));
+    AxisTap a;
+    a.inside = lo <= ix && ix <= hi;
+    double u = sub(mul(dvd(sub(ix, lo), wdt), (double)n_px), 0.5);
+    const double ru = rint(u);
+    if (fabs(sub(u, ru)) < SNAP_EPS) u = ru;
+    vec_tap(u, n_px, a.i0, a.f);
+    return a;
+}
+
+__global__ void __launch_bounds__(256) k_render_slab(const uint8_t* __restrict__ field,
+                                                     const int32_t* __restrict__ slots, int S, int T, int W, int H,
+                                                     const double* __restrict__ poses,
+                                                     const rlfc_render_geom* __restrict__ geoms,
+                                                     const uint8_t* __restrict__ bgs, int ow, int oh,
+                                                     uint8_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t rsm[];
+    AxisTap* cols = reinterpret_cast<AxisTap*>(rsm);          // [ow]
+    AxisTap* rows = cols + ow;                                 // [RB]
     const int v = blockIdx.y;
-    const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (pix >= (int64_t)ow * oh) return;
-    const int i = (int)(pix % ow), j = (int)(pix / ow);
+    const int j0 = blockIdx.x * RB;
+    const int nrow = min(RB, oh - j0);
     const rlfc_render_geom g = geoms[v];
     const double ps = poses[4 * v], pt = poses[4 * v + 1];
     const double focal = poses[4 * v + 2] != 0.0 ? poses[4 * v + 3] : g.img_z;
-    uint8_t* o = out + ((int64_t)v * oh * ow + pix) * 3;
-    const uint8_t* bg = bgs + 3 * v;
-    // renderer.py:177-187 _slab_rays
     const double ex = interp_identity(ps, S), ey = interp_identity(pt, T), ez = g.cam_z;
-    const double xw = sub(g.x1, g.x0), yw = sub(g.y1, g.y0);
-    const double tx = add(g.x0, dvd(mul(add((double)i, 0.5), xw), (double)ow));
-    const double ty = add(g.y0, dvd(mul(add((double)j, 0.5), yw), (double)oh));
-    const double dx = sub(tx, ex), dy = sub(ty, ey), dz = sub(focal, ez);
-    // renderer.py:251-257
+    const double dz = sub(focal, ez);
     const double tp = dvd(sub(g.img_z, ez), dz);
-    const double ix = add(ex, mul(tp, dx)), iy = add(ey, mul(tp, dy));
-    if (!(g.x0 <= ix && ix <= g.x1 && g.y0 <= iy && iy <= g.y1)) {
-        o[0] = bg[0]; o[1] = bg[1]; o[2] = bg[2];
-        return;
+    for (int i = threadIdx.x; i < ow + nrow; i += blockDim.x) {
+        if (i < ow) cols[i] = slab_axis(i, ow, g.x0, g.x1, ex, tp, W);
+        else rows[i - ow] = slab_axis(j0 + i - ow, oh, g.y0, g.y1, ey, tp, H);
     }
-    double u = sub(mul(dvd(sub(ix, g.x0), xw), (double)W), 0.5);
-    double vv = sub(mul(dvd(sub(iy, g.y0), yw), (double)H), 0.5);
-    {   // renderer.py:258-260
-        double ru = rint(u), rv = rint(vv);
-        if (fabs(sub(u, ru)) < SNAP_EPS) u = ru;
-        if (fabs(sub(vv, rv)) < SNAP_EPS) vv = rv;
-    }
-    int u0, v0;
-    double fu, fv;
-    vec_tap(u, W, u0, fu);
-    vec_tap(vv, H, v0, fv);
-    // renderer.py:265-266 camera taps (frame constants; recomputed per thread)
+    // renderer.py:265-266 camera taps (per pose)
     int si[2], ti[2];
     double ws[2], wt[2];
     const int ns = axis_taps(snap(ex), S, si, ws);
     const int nt = axis_taps(snap(ey), T, ti, wt);
     const int64_t img = (int64_t)W * H * 3;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    const uint8_t* ims[4];
+    double wst[4];
+    int nab = 0;
     for (int a = 0; a < ns; ++a)
         for (int b = 0; b < nt; ++b) {
             const int cam = si[a] * T + ti[b];
-            const uint8_t* im = field + (int64_t)(slots ? slots[cam] : cam) * img;
-            const double wst = mul(ws[a], wt[b]);
+            ims[nab] = field + (int64_t)(slots ? slots[cam] : cam) * img;
+            wst[nab] = mul(ws[a], wt[b]);
+            ++nab;
+        }
+    __syncthreads();
+    const uint8_t* bg = bgs + 3 * v;
+    for (int q = threadIdx.x; q < nrow * ow; q += blockDim.x) {
+        const int jr = q / ow, i = q - jr * ow;
+        const AxisTap cu = cols[i], cv = rows[jr];
+        uint8_t* o = out + (((int64_t)v * oh + j0 + jr) * ow + i) * 3;
+        if (!(cu.inside && cv.inside)) {
+            o[0] = bg[0]; o[1] = bg[1]; o[2] = bg[2];
+            continue;
+        }
+        const int gx0 = min(cu.i0, W - 1), gx1 = min(cu.i0 + 1, W - 1);
+        const int gy0 = min(cv.i0, H - 1), gy1 = min(cv.i0 + 1, H - 1);
+        const double wu[2] = {sub(1.0, cu.f), cu.f}, wv[2] = {sub(1.0, cv.f), cv.f};
+        const int gx[2] = {gx0, gx1}, gy[2] = {gy0, gy1};
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+        for (int ab = 0; ab < nab; ++ab) {
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                const double wu = p ? fu : sub(1.0, fu);
-                const int gx = min(u0 + p, W - 1);
+                const double wsu = mul(wst[ab], wu[p]);
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const double wv = q ? fv : sub(1.0, fv);
-                    const int gy = min(v0 + q, H - 1);
-                    const double w = mul(mul(wst, wu), wv);
-                    const uint8_t* px = im + ((int64_t)gy * W + gx) * 3;
+                for (int qq = 0; qq < 2; ++qq) {
+                    const double w = mul(wsu, wv[qq]);
+                    const uint8_t* px = ims[ab] + ((int64_t)gy[qq] * W + gx[p]) * 3;
                     acc0 = add(acc0, mul(w, (double)px[0]));
                     acc1 = add(acc1, mul(w, (double)px[1]));
                     acc2 = add(acc2, mul(w, (double)px[2]));
                 }
             }
         }
-    o[0] = round_clip(acc0);
-    o[1] = round_clip(acc1);
-    o[2] = round_clip(acc2);
+        o[0] = round_clip(acc0);
+        o[1] = round_clip(acc1);
+        o[2] = round_clip(acc2);
+    }
 }
 
 struct PinholeCoord {
@@ -247,9 +278,11 @@ extern "C" int rlfc_render_slab(const uint8_t* field, const int32_t* slots, int3
                                 int32_t ow, int32_t oh, uint8_t* out, void* stream) {
     if (S < 1 || T < 1 || W < 1 || H < 1 || n < 0 || ow < 1 || oh < 1 || n > 65535) return RLFC_ERR_ARGUMENT;
     if (n == 0) return RLFC_OK;
-    const int threads = 256;
-    dim3 grid((unsigned)(((int64_t)ow * oh + threads - 1) / threads), (unsigned)n);
-    k_render_slab<<<grid, threads, 0, (cudaStream_t)stream>>>(field, slots, S, T, W, H, poses, geoms, bg, ow, oh, out);
+    const size_t smem = (size_t)(ow + RB) * sizeof(AxisTap);
+    if (smem > 200 * 1024) return RLFC_ERR_ARGUMENT;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_render_slab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((unsigned)((oh + RB - 1) / RB), (unsigned)n);
+    k_render_slab<<<grid, 256, smem, (cudaStream_t)stream>>>(field, slots, S, T, W, H, poses, geoms, bg, ow, oh, out);
     return launch_status();
 }
 
