@@ -358,6 +358,35 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
     return out, status
 
 
+def decode_field_slots(state, stop_level, slots, n, device=None):
+    """decode_field for a prebuilt device slot table (slots[s*T + t] = output
+    index or -1, n outputs): the renderer's tap-camera decode.  Returns
+    (field (n, H, W, 3), status word tensor) without synchronising."""
+    torch = _torch()
+    hdr = state.header
+    df = state.device_field(device)
+    W, H = hdr.width, hdr.height
+    out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=df.device)
+    status = torch.zeros(1, dtype=torch.int64, device=df.device)
+    L = _native.lib()
+    hb = hdr.block_grid[1]
+    with torch.cuda.device(df.device):
+        stream = _stream()
+        ws = df.staged_workspace(stream)
+        rc = _native.RLFC_ERR_ARGUMENT
+        if ws is not None:
+            rc = L.rlfc_decode_field_staged(
+                df.ref, stop_level, slots.data_ptr(), 0, hb, out.data_ptr(),
+                H * W * 3, W * 3, ws[0].data_ptr(), ws[1], ws[2],
+                status.data_ptr(), stream)
+        if rc == _native.RLFC_ERR_ARGUMENT:
+            rc = L.rlfc_decode_field(df.ref, stop_level, slots.data_ptr(), 0,
+                                     hb, out.data_ptr(), H * W * 3, W * 3,
+                                     status.data_ptr(), stream)
+        _native.check(rc, "rlfc_decode_field")
+    return out, status
+
+
 def bise_decode_batch(payloads, descs, count, device=None):
     """Decode many BISE payloads on the GPU (kernels.bise_decode_core).
 

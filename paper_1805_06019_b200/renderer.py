@@ -193,17 +193,6 @@ def _geom_struct(geometry):
     return (geometry.camera_plane_z, geometry.image_plane_z, x0, y0, x1, y1)
 
 
-def _slab_cameras(pose, S, T, geometry):
-    focal = pose.focal_z if pose.focal_z is not None else \
-        geometry.image_plane_z
-    if focal == geometry.camera_plane_z:
-        raise ValueError("focal plane coincides with the camera plane")
-    ex = min(max(float(pose.s), 0.0), float(S - 1))
-    ey = min(max(float(pose.t), 0.0), float(T - 1))
-    return [(si, ti) for si, _ in _axis_taps(_snap(ex), S)
-            for ti, _ in _axis_taps(_snap(ey), T)]
-
-
 def render_views(state, poses, stop_level=0, geometry=None,
                  background=(0, 0, 0), device=None, out=None):
     """Render a batch of same-size poses; returns a CUDA uint8 tensor
@@ -226,34 +215,47 @@ def render_views(state, poses, stop_level=0, geometry=None,
     if any((p.width, p.height) != (ow, oh) for p in poses):
         raise ValueError("a batch must share one output size")
     S, T, W, H = hdr.s_count, hdr.t_count, hdr.width, hdr.height
-    geos = geometry if isinstance(geometry, (list, tuple)) and geometry and \
-        isinstance(geometry[0], (PlaneGeometry, type(None))) else [geometry] * n
-    geos = [default_geometry(S, T) if g is None else g for g in geos]
+    per_pose = isinstance(geometry, (list, tuple)) and geometry and \
+        isinstance(geometry[0], (PlaneGeometry, type(None)))
+    if per_pose:
+        geos = [default_geometry(S, T) if g is None else g for g in geometry]
+        gstruct = np.array([_geom_struct(g) for g in geos], dtype=np.float64)
+    else:
+        one = default_geometry(S, T) if geometry is None else geometry
+        geos = None
+        gstruct = np.tile(np.array(_geom_struct(one), dtype=np.float64), (n, 1))
     bgs = np.asarray(background, dtype=np.uint8).reshape(-1, 3)
     bgs = np.broadcast_to(bgs, (n, 3)).copy() if bgs.shape[0] == 1 else bgs
     df = state.device_field(device)
     dev = df.device
     L = _native.lib()
     stream = torch.cuda.current_stream(dev).cuda_stream
-    d_geom = torch.from_numpy(np.array([_geom_struct(g) for g in geos],
-                                       dtype=np.float64)).to(dev)
+    d_geom = torch.from_numpy(gstruct).to(dev)
     d_bg = torch.from_numpy(bgs).to(dev)
     if out is None:
         out = torch.empty((n, oh, ow, 3), dtype=torch.uint8, device=dev)
     if kinds == {SlabPose}:
-        cams = sorted({c for p, g in zip(poses, geos)
-                       for c in _slab_cameras(p, S, T, g)})
         pose_arr = np.array([(p.s, p.t, float(p.focal_z is not None),
                               float(p.focal_z or 0.0)) for p in poses],
                             dtype=np.float64)
-        field, slots = _decode_cameras(state, cams, stop_level, device)
+        # renderer.py:175-176: a focal plane on the camera plane is rejected
+        focal = np.where(pose_arr[:, 2] != 0.0, pose_arr[:, 3], gstruct[:, 1])
+        if np.any(focal == gstruct[:, 0]):
+            raise ValueError("focal plane coincides with the camera plane")
+        cams = _slab_camera_set(pose_arr[:, 0], pose_arr[:, 1], S, T)
+        field, slots, status = _decode_cameras(state, cams, stop_level,
+                                               device)
         d_pose = torch.from_numpy(pose_arr).to(dev)
         with torch.cuda.device(dev):
             _native.check(L.rlfc_render_slab(
                 field.data_ptr(), slots.data_ptr(), S, T, W, H,
                 d_pose.data_ptr(), d_geom.data_ptr(), d_bg.data_ptr(), n, ow,
                 oh, out.data_ptr(), stream), "rlfc_render_slab")
+        if status is not None:
+            decoder._raise_word(status.cpu().item())
         return out
+    if geos is None:
+        geos = [one] * n
     frames = np.stack([_pinhole_basis(p, g) for p, g in zip(poses, geos)])
     d_frames = torch.from_numpy(np.ascontiguousarray(frames)).to(dev)
     need = torch.zeros(S * T, dtype=torch.uint8, device=dev)
@@ -261,9 +263,10 @@ def render_views(state, poses, stop_level=0, geometry=None,
         _native.check(L.rlfc_render_pinhole_needs(
             S, T, W, H, d_frames.data_ptr(), d_geom.data_ptr(), n, ow, oh,
             need.data_ptr(), stream), "rlfc_render_pinhole_needs")
-    idx = np.flatnonzero(need.cpu().numpy())
-    cams = [(int(i) // T, int(i) % T) for i in idx]
-    field, slots = _decode_cameras(state, cams, stop_level, device)
+    cams = np.flatnonzero(need.cpu().numpy())
+    field, slots, dstatus = _decode_cameras(state, cams, stop_level, device)
+    if dstatus is not None:
+        decoder._raise_word(dstatus.cpu().item())
     status = torch.zeros(n, dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
         _native.check(L.rlfc_render_pinhole(
@@ -276,21 +279,35 @@ def render_views(state, poses, stop_level=0, geometry=None,
     return out
 
 
+def _slab_camera_set(ps, pt, S, T):
+    """Serial indices s*T + t of every camera a batch of slab poses can tap:
+    floor and ceil of the clamped eye position along each axis, a superset
+    of renderer.py:119-131 _axis_taps (which may drop a zero-weight tap)."""
+    cs = np.clip(ps, 0.0, S - 1.0)
+    ct = np.clip(pt, 0.0, T - 1.0)
+    sx = np.stack([np.floor(cs), np.ceil(cs)]).astype(np.int64)
+    ty = np.stack([np.floor(ct), np.ceil(ct)]).astype(np.int64)
+    return np.unique((sx[:, None, :] * T + ty[None, :, :]).ravel())
+
+
 def _decode_cameras(state, cams, stop_level, device):
+    """Decode the given cameras (serial indices s*T + t) into a compact
+    field; returns (field, slots, status word tensor or None)."""
     import torch
     hdr = state.header
     S, T = hdr.s_count, hdr.t_count
     df = state.device_field(device)
+    cams = np.asarray(cams, dtype=np.int64)
     slots = np.full(S * T, -1, dtype=np.int32)
-    for i, (s, t) in enumerate(cams):
-        slots[s * T + t] = i
-    if cams:
-        field, _ = decoder.decode_field(state, stop_level, images=cams,
-                                        device=device)
-    else:
-        field = torch.zeros((1, hdr.height, hdr.width, 3), dtype=torch.uint8,
-                            device=df.device)
-    return field, torch.from_numpy(slots).to(df.device)
+    slots[cams] = np.arange(len(cams), dtype=np.int32)
+    d_slots = torch.from_numpy(slots).to(df.device)
+    if len(cams):
+        field, status = decoder.decode_field_slots(state, stop_level, d_slots,
+                                                   len(cams), device=device)
+        return field, d_slots, status
+    field = torch.zeros((1, hdr.height, hdr.width, 3), dtype=torch.uint8,
+                        device=df.device)
+    return field, d_slots, None
 
 
 def render_view(state, pose, stop_level=0, geometry: PlaneGeometry = None,
