@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     if (tid == 0) cnt[0] = 0;
     // ---- records: residual row masks and slot bases of this camera row --------
     for (int r = tid; r < NR; r += BT) {
-        const int c = r / NB, b = r - c * NB;
+        const int c = r >> (__ffs(NB) - 1), b = r & (NB - 1);
         uint32_t fl = 0;
         if (b < nb && nlev > 0 && !(P.debug & 8)) {
             const int64_t blk = (int64_t)by * f.wb + bx0 + b;
@@ -804,19 +804,21 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     // with a warp-aggregated shared-memory atomic (unit order is irrelevant);
     // pairs touching a flagged record are tagged for the reference-order walk
     const int lane = tid & 31;
+    const int lgnb = __ffs(NB) - 1;                  // NB is a power of two (TW / B)
     for (int p0 = 0; p0 < S * NB; p0 += BT) {
         const int pi = p0 + tid;
-        const int s = pi / NB, b = pi - s * NB;
+        const int s = pi >> lgnb, b = pi & (NB - 1);
         bool emit = false, fb = false;
         uint32_t pres = 0;
         if (pi < S * NB && b < nb && (!P.slots || P.slots[s * T + t] >= 0)) {
             fb = (rflag[b] | rflag[NB + b] | rflag[2 * NB + b]) != 0;
             if (!fb) {
-                for (int l = k; l < h; ++l) {
-                    const int x = s >> l;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        pres |= (uint32_t)((mask[(l - k) * NR + c * NB + b] >> x) & 1ull) << (3 * (l - k) + c);
+                const uint64_t* mb = mask + b;
+                for (int li = 0; li < nlev; ++li, mb += NR) {
+                    const int x = s >> (k + li);
+                    pres |= (uint32_t)((mb[0] >> x) & 1ull) << (3 * li) |
+                            (uint32_t)((mb[NB] >> x) & 1ull) << (3 * li + 1) |
+                            (uint32_t)((mb[2 * NB] >> x) & 1ull) << (3 * li + 2);
                 }
             }
             emit = fb || pres != 0;
