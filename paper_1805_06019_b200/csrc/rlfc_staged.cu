@@ -861,7 +861,66 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     // ---- dirty units: root + present residuals, YCoCg-R inverse, clamp, pack ----------
     // one task = two consecutive pixel quad-rows of a unit (8 consecutive
     // values of each payload), so a present residual is one 16-byte gather
-    {
+    if constexpr (B == 4 && sizeof(VT) == 2) {
+        // B = 4: one task per unit (all 16 pixels): the first present level
+        // of each channel is two 16-byte gathers, all issued before any is
+        // consumed, so a thread pays one round trip per unit
+        const int units = (P.debug & 1) ? 0 : cnt[0];
+        const VT* res = static_cast<const VT*>(P.res);
+        for (int u = tid; u < units; u += BT) {
+            const uint2 e = list[u];
+            const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
+            if (e.x >> 16) {
+                unit_fallback<B>(P, stage, s, t, by, bx0 + b, b * B);
+                continue;
+            }
+            auto slot_of = [&](int c, uint32_t pc) -> uint32_t {
+                const int li = (__ffs(pc) - 1) / 3;
+                const int r = li * NR + c * NB + b;
+                const int x = s >> (k + li);
+                return sbase[r] + (uint32_t)__popcll(mask[r] & ((1ull << x) - 1ull));
+            };
+            uint4 raw[3][2];
+            uint32_t pcs[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                pcs[c] = e.y & (0x249249u << c);             // bits 3i + c: levels k + i
+                raw[c][0] = raw[c][1] = make_uint4(0u, 0u, 0u, 0u);
+                if (pcs[c]) {
+                    const uint4* q = reinterpret_cast<const uint4*>(res + (uint64_t)slot_of(c, pcs[c]) * BSQ);
+                    raw[c][0] = __ldg(q);
+                    raw[c][1] = __ldg(q + 1);
+                    pcs[c] &= pcs[c] - 1u;
+                }
+            }
+            const int rx = s >> h;
+            const int px = b * B;
+#pragma unroll
+            for (int row = 0; row < 4; ++row) {
+                int32_t v[3][4];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    load4s<RT>(roots + ((rx * 3 + c) * B + row) * TW + px, v[c]);
+                    const uint4 w = raw[c][row >> 1];
+                    const uint32_t lo = (row & 1) ? w.z : w.x, hi = (row & 1) ? w.w : w.y;
+                    v[c][0] += (int32_t)(int16_t)(lo & 0xFFFFu);
+                    v[c][1] += (int32_t)lo >> 16;
+                    v[c][2] += (int32_t)(int16_t)(hi & 0xFFFFu);
+                    v[c][3] += (int32_t)hi >> 16;
+                    uint32_t pc = pcs[c];
+                    while (pc) {                               // further levels (rare)
+                        int32_t r4[4] = {0, 0, 0, 0};
+                        const VT* q = res + (uint64_t)slot_of(c, pc) * BSQ + row * 4;
+                        add4<VT>(q, r4);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) v[c][i] += r4[i];
+                        pc &= pc - 1u;
+                    }
+                }
+                ycocg4_pack(v, reinterpret_cast<uint32_t*>(stage + stage_off<B>(S, s, row, px)));
+            }
+        }
+    } else {
         constexpr int TP = B * QB / 2;                   // tasks per unit
         const int units = (P.debug & 1) ? 0 : cnt[0];
         const VT* res = static_cast<const VT*>(P.res);
