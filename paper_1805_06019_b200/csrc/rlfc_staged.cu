@@ -650,8 +650,8 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     constexpr int QB = B / 4;                      // pixel quads per block row
     const rlfc_field& f = P.f;
     const int tid = threadIdx.x;
-    const int chunk = blockIdx.x % P.nchunks, t = blockIdx.x / P.nchunks;
-    const int by = P.by_lo + blockIdx.y;
+    const int chunk = blockIdx.x, t = blockIdx.y;
+    const int by = P.by_lo + blockIdx.z;
     const int NB = P.NB, TW = P.TW, NR = 3 * NB;
     const int bx0 = chunk * NB;
     const int nb = min(NB, f.wb - bx0);
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     uint8_t* stage = smem + P.off_stage;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + P.off_mbar);
 #ifdef RLFC_BLEND_TIMING
-    const int64_t bidx = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    const int64_t bidx = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
 #endif
     RLFC_BSTAMP(0);
 
@@ -1204,7 +1204,7 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     }
     auto kern = bt == 256 ? k_blend<B, VT, RT, 256> : k_blend<B, VT, RT, 128>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
-    const dim3 grid((unsigned)(P.nchunks * f.t_count), (unsigned)(by_hi - by_lo));
+    const dim3 grid((unsigned)P.nchunks, (unsigned)f.t_count, (unsigned)(by_hi - by_lo));
     kern<<<grid, bt, pl.smem, stream>>>(P, out_map, rgb_map, root_map);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
