@@ -416,7 +416,20 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     const uint64_t n = min((uint64_t)*w.counter, w.cap);
     const int64_t nblk = (int64_t)f.wb * f.hb;
     VT* res = static_cast<VT*>(w.res);
-    for (uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK; base < n; base += (uint64_t)gridDim.x * PAY_CHUNK) {
+    // the next chunk's entries are loaded while the current chunk decodes
+    constexpr int EPT = PAY_CHUNK / THREADS;                   // entries per thread
+    const uint64_t stride = (uint64_t)gridDim.x * PAY_CHUNK;
+    uint2 ent[EPT];
+    auto load_entries = [&](uint64_t b0) {
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const uint64_t i = b0 + tid + q * THREADS;
+            ent[q] = i < n ? __ldg(w.entries + i) : make_uint2(0u, SKIP);
+        }
+    };
+    uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK;
+    if (base < n) load_entries(base);
+    for (; base < n; base += stride) {
         if (tid < 3) bcount[tid] = 0;
         if (tid == 0) {
             range[0] = ~0u;
@@ -425,8 +438,10 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
         }
         __syncthreads();
         uint32_t lo = ~0u, hi = 0u, cm = 0u;
-        for (int i = tid; i < PAY_CHUNK && base + i < n; i += THREADS) {
-            const uint2 e = w.entries[base + i];
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            const int i = tid + q * THREADS;
+            const uint2 e = ent[q];
             const uint32_t d = e.y & 31u;
             if (d >= (uint32_t)NUM_DESC) continue;
             const int m = desc_mode((int)d);
@@ -437,6 +452,7 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
             hi = max(hi, e.x);
             cm |= 1u << ((e.y >> 5) & 3);
         }
+        if (base + stride < n) load_entries(base + stride);
         if (BSQ == 16) {
             // the chunk's payloads are consecutive nodes of consecutive records
             // of one channel: one contiguous byte range of its SRV section
