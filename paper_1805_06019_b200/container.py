@@ -14,6 +14,7 @@ the GPU (decoder.py).
 """
 
 import io
+import os
 import struct
 from dataclasses import dataclass
 
@@ -251,29 +252,65 @@ def encode_root(plane, codec_id) -> bytes:
     return buf.getvalue()
 
 
-def parse_roots(data, header: RlfcHeader):
-    """All root planes, (rsx, rsy, 3, Hp, Wp) int32 with the bias removed."""
+def parse_roots(data, header: RlfcHeader, threads=None):
+    """All root planes, (rsx, rsy, 3, Hp, Wp) int32 with the bias removed.
+
+    The section layout is walked serially (container.py:355-379); the plane
+    images, Pillow decodes that release the GIL, are decoded on a thread pool.
+    The first failure in stream order is raised, exactly as the reference's
+    plane-by-plane loop meets it: a decode error of an earlier plane before a
+    truncation or trailing bytes found later.
+    """
+    from concurrent.futures import ThreadPoolExecutor
     wp, hp = header.padded_dims
     rsx, rsy = level_dims(header.s_count, header.t_count, header.tree_height)
     starts, _ = section_offsets(header)
     out = np.zeros((rsx, rsy, 3, hp, wp), dtype=np.int32)
+    events = []            # ("plane", (x, y, c), blob) | ("error", exc)
     for c in range(3):
         pos = starts[c][0]
         end = pos + header.section_lengths[c][0]
+        stop = False
         for y in range(rsy):
             for x in range(rsx):
-                if pos + 4 > end:
-                    raise FormatError("root stream truncated")
+                if pos + 4 > end or pos + 4 + struct.unpack_from("<I", data, pos)[0] > end:
+                    events.append(("error", FormatError("root stream truncated")))
+                    stop = True
+                    break
                 (n,) = struct.unpack_from("<I", data, pos)
                 pos += 4
-                if pos + n > end:
-                    raise FormatError("root stream truncated")
-                out[x, y, c] = decode_root(bytes(data[pos:pos + n]),
-                                           header.root_codec_id, wp, hp) \
-                    - CHANNEL_BIAS[c]
+                events.append(("plane", (x, y, c), bytes(data[pos:pos + n])))
                 pos += n
+            if stop:
+                break
+        if stop:
+            break
         if pos != end:
-            raise FormatError("trailing bytes in root stream")
+            events.append(("error", FormatError("trailing bytes in root stream")))
+            break
+    planes = [e for e in events if e[0] == "plane"]
+
+    def dec(e):
+        try:
+            return decode_root(e[2], header.root_codec_id, wp, hp), None
+        except Exception as exc:          # raised below in stream order
+            return None, exc
+
+    nthreads = threads or min(32, os.cpu_count() or 1)
+    if header.root_codec_id == CODEC_RAW or nthreads <= 1 or len(planes) <= 1:
+        results = [dec(e) for e in planes]
+    else:
+        with ThreadPoolExecutor(max_workers=nthreads) as ex:
+            results = list(ex.map(dec, planes))
+    it = iter(results)
+    for e in events:
+        if e[0] == "error":
+            raise e[1]
+        arr, exc = next(it)
+        if exc is not None:
+            raise exc
+        x, y, c = e[1]
+        out[x, y, c] = arr - CHANNEL_BIAS[c]
     return out
 
 

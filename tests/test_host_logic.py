@@ -126,3 +126,45 @@ def test_balanced_bands_partition_rows():
         cost = parallel.row_costs(st)
         per = [cost[lo:hi].sum() for lo, hi in bands]
         assert max(per) <= cost.sum() / n + cost.max() + 1e-6
+
+
+def test_parallel_root_parse_matches_serial():
+    """container.parse_roots decodes the root images on a thread pool; values
+    and the first error in stream order are those of the plane-by-plane walk
+    (container.py:355-379)."""
+    import struct
+    from paper_1805_06019_b200 import container
+    from paper_1805_06019_b200.errors import FormatError
+    data = load_stream("kat8_default")
+    hdr = container.parse_header(data)
+    assert hdr.root_codec_id == container.CODEC_PNG
+    a = container.parse_roots(data, hdr, threads=1)
+    b = container.parse_roots(data, hdr, threads=8)
+    assert np.array_equal(a, b)
+    starts, _ = container.section_offsets(hdr)
+    # corrupt the image bytes of the first root plane of channel 1
+    pos = starts[1][0]
+    n = struct.unpack_from("<I", data, pos)[0]
+    bad = bytearray(data)
+    bad[pos + 4 + 8:pos + 4 + 24] = b"\xff" * 16
+    msgs = []
+    for th in (1, 8):
+        with pytest.raises(FormatError) as ei:
+            container.parse_roots(bytes(bad), hdr, threads=th)
+        msgs.append(str(ei.value))
+    import re
+    strip = [re.sub(r" at 0x[0-9a-f]+", "", m) for m in msgs]      # object addresses
+    assert strip[0] == strip[1] and "decode failed" in strip[0]
+    # ... and also make channel 2's root length run past its section: the
+    # earlier decode error still comes first
+    pos2 = starts[2][0]
+    bad[pos2:pos2 + 4] = struct.pack("<I", 1 << 30)
+    for th in (1, 8):
+        with pytest.raises(FormatError, match="decode failed"):
+            container.parse_roots(bytes(bad), hdr, threads=th)
+    only_trunc = bytearray(data)
+    only_trunc[pos2:pos2 + 4] = struct.pack("<I", 1 << 30)
+    for th in (1, 8):
+        with pytest.raises(FormatError, match="truncated"):
+            container.parse_roots(bytes(only_trunc), hdr, threads=th)
+    assert n > 24
