@@ -145,6 +145,24 @@ __global__ void k_count_present(const __grid_constant__ rlfc_field f, unsigned l
     if ((threadIdx.x & 31) == 0 && n) atomicAdd(out, (unsigned long long)n);
 }
 
+// Node size (descriptor + payload bytes) for B*B = 16 values from three
+// 64-bit immediates (5 bits per descriptor): no memory access in the walk's
+// dependent chain.
+constexpr uint64_t nb16_word(int w) {
+    uint64_t v = 0;
+    for (int i = 0; i < 12; ++i) {
+        const int d = w * 12 + i;
+        if (d < NUM_DESC) v |= (uint64_t)(1 + payload_bytes(d, 16)) << (5 * i);
+    }
+    return v;
+}
+__device__ __forceinline__ uint32_t node_bytes16(int d) {
+    constexpr uint64_t W0 = nb16_word(0), W1 = nb16_word(1), W2 = nb16_word(2);
+    const uint64_t w = d < 12 ? W0 : d < 24 ? W1 : W2;
+    const int i = d < 12 ? d : d < 24 ? d - 12 : d - 24;
+    return (uint32_t)(w >> (5 * i)) & 31u;
+}
+
 // ---- pass 1: index -----------------------------------------------------------------
 // Levels >= k occupy serial nodes [0, node_end) (level h-1 first,
 // container.py:102-145); only those are indexed and decoded.
@@ -189,13 +207,18 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
             while (bits) {
                 bits &= bits - 1u;
                 const int d = cursor < len ? rec[cursor] : NUM_DESC;
-                if (d >= NUM_DESC || cursor + nb.v[d] > len) {
+                if (d >= NUM_DESC) {
+                    flag = 1;
+                    break;
+                }
+                const uint32_t sz = BSQ == 16 ? node_bytes16(d) : (uint32_t)nb.v[d];
+                if (cursor + sz > len) {
                     flag = 1;
                     break;
                 }
                 w.entries[slot0 + rank] =
                     make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
-                cursor += nb.v[d];
+                cursor += sz;
                 ++rank;
             }
         }
