@@ -56,6 +56,8 @@ __device__ __forceinline__ const NodeBytes& node_bytes() {
     return BSQ == 16 ? g_nb4 : BSQ == 64 ? g_nb8 : g_nb16;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 struct Ws {
     unsigned long long* counter;
     uint32_t* rec_base;
@@ -421,16 +423,16 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
 // mode in shared memory, then decodes each bucket with the mode's unrolled
 // code so every warp runs one code path.
 constexpr int PAY_CHUNK = 512;
-constexpr int PAY_BUF = 12 * 1024;       // staged SRV bytes per chunk
+constexpr int PAY_BUF = 12 * 1024;       // staged SRV bytes per chunk (two buffers, dynamic shared memory)
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w) {
     __shared__ uint2 bucket[3][PAY_CHUNK];
     __shared__ uint32_t bslot[3][PAY_CHUNK];
     __shared__ int bcount[3];
-    __shared__ uint32_t range[3];            // min / max payload offset, channel mask
+    __shared__ uint32_t range[2][3];         // per buffer: min / max payload offset, channel mask
     __shared__ uint16_t lut[243 + 125];
     __shared__ VT dq[BSQ == 16 ? 2048 : 1];
-    __shared__ __align__(16) uint32_t cbuf[BSQ == 16 ? PAY_BUF / 4 : 4];
+    extern __shared__ __align__(16) uint32_t cbuf[];    // [2][PAY_BUF / 4] (B = 4 only)
     const int tid = threadIdx.x;
     const int shift = f.quant_shift;
     for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
@@ -439,75 +441,108 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     const uint64_t n = min((uint64_t)*w.counter, w.cap);
     const int64_t nblk = (int64_t)f.wb * f.hb;
     VT* res = static_cast<VT*>(w.res);
-    // the next chunk's entries are loaded while the current chunk decodes
+    // Chunks are software-pipelined: while chunk i decodes, chunk i+1's
+    // entries are in registers and its SRV byte range is on its way into the
+    // other shared buffer (cp.async).  A chunk's payloads are consecutive
+    // nodes of consecutive records of one channel: one contiguous byte range.
     constexpr int EPT = PAY_CHUNK / THREADS;                   // entries per thread
     const uint64_t stride = (uint64_t)gridDim.x * PAY_CHUNK;
-    uint2 ent[EPT];
-    auto load_entries = [&](uint64_t b0) {
+    auto load_entries = [&](uint64_t b0, uint2* e4) {
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
             const uint64_t i = b0 + tid + q * THREADS;
-            ent[q] = i < n ? __ldg(w.entries + i) : make_uint2(0u, SKIP);
+            e4[q] = i < n ? __ldg(w.entries + i) : make_uint2(0u, SKIP);
         }
     };
-    uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK;
-    if (base < n) load_entries(base);
-    for (; base < n; base += stride) {
-        if (tid < 3) bcount[tid] = 0;
-        if (tid == 0) {
-            range[0] = ~0u;
-            range[1] = 0u;
-            range[2] = 0u;
-        }
-        __syncthreads();
+    auto reduce_range = [&](const uint2* e4, int q) {
+        if (BSQ != 16) return;
         uint32_t lo = ~0u, hi = 0u, cm = 0u;
 #pragma unroll
-        for (int q = 0; q < EPT; ++q) {
-            const int i = tid + q * THREADS;
-            const uint2 e = ent[q];
+        for (int k2 = 0; k2 < EPT; ++k2)
+            if ((e4[k2].y & 31u) < (uint32_t)NUM_DESC) {
+                lo = min(lo, e4[k2].x);
+                hi = max(hi, e4[k2].x);
+                cm |= 1u << ((e4[k2].y >> 5) & 3);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            cm |= __shfl_xor_sync(0xffffffffu, cm, o);
+        }
+        if ((tid & 31) == 0 && cm) {
+            atomicMin(&range[q][0], lo);
+            atomicMax(&range[q][1], hi);
+            atomicOr(&range[q][2], cm);
+        }
+    };
+    // staged (one channel, range fits): copy issue into buffer q; every
+    // thread derives the same (staged, lo16) from range[q]
+    auto stage_issue = [&](int q, uint32_t& lo16) -> bool {
+        if (BSQ != 16 || !range[q][2] || __popc(range[q][2]) != 1) return false;
+        const int sc = __ffs(range[q][2]) - 1;
+        lo16 = range[q][0] & ~15u;
+        if ((uint64_t)range[q][1] + 48 - lo16 > (uint64_t)PAY_BUF) return false;
+        const uint64_t end = min((uint64_t)range[q][1] + 48, f.srv_len[sc] + 16);
+        const uint8_t* src = f.srv[sc] + lo16;
+        const uint32_t dst = smem_u32(cbuf + q * (PAY_BUF / 4));
+        const int n16 = (int)((end - lo16) >> 4);
+        for (int k2 = tid; k2 < n16; k2 += THREADS)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * k2), "l"(src + 16 * k2)
+                         : "memory");
+        return true;
+    };
+    uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK;
+    uint2 ent[EPT];
+    bool staged = false;
+    uint32_t lo16 = 0;
+    if (tid == 0) {
+        range[0][0] = ~0u;
+        range[0][1] = 0u;
+        range[0][2] = 0u;
+    }
+    __syncthreads();
+    if (base < n) {
+        load_entries(base, ent);
+        reduce_range(ent, 0);
+    }
+    __syncthreads();
+    if (base < n) staged = stage_issue(0, lo16);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    for (int it = 0; base < n; base += stride, ++it) {
+        const int q = it & 1;
+        if (tid < 3) bcount[tid] = 0;
+        if (tid == 0) {
+            range[q ^ 1][0] = ~0u;
+            range[q ^ 1][1] = 0u;
+            range[q ^ 1][2] = 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k2 = 0; k2 < EPT; ++k2) {
+            const uint2 e = ent[k2];
             const uint32_t d = e.y & 31u;
             if (d >= (uint32_t)NUM_DESC) continue;
             const int m = desc_mode((int)d);
             const int pos = atomicAdd(&bcount[m], 1);
             bucket[m][pos] = e;
-            bslot[m][pos] = (uint32_t)(base + i);
-            lo = min(lo, e.x);
-            hi = max(hi, e.x);
-            cm |= 1u << ((e.y >> 5) & 3);
+            bslot[m][pos] = (uint32_t)(base + tid + k2 * THREADS);
         }
-        if (base + stride < n) load_entries(base + stride);
-        if (BSQ == 16) {
-            // the chunk's payloads are consecutive nodes of consecutive records
-            // of one channel: one contiguous byte range of its SRV section
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-                hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-                cm |= __shfl_xor_sync(0xffffffffu, cm, o);
-            }
-            if ((tid & 31) == 0 && cm) {
-                atomicMin(&range[0], lo);
-                atomicMax(&range[1], hi);
-                atomicOr(&range[2], cm);
-            }
+        const bool has_next = base + stride < n;
+        uint2 entn[EPT];
+        if (has_next) {
+            load_entries(base + stride, entn);
+            reduce_range(entn, q ^ 1);
         }
         __syncthreads();
+        uint32_t lo16n = 0;
+        bool stagedn = false;
+        if (has_next) stagedn = stage_issue(q ^ 1, lo16n);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");     // this chunk's copies
+        __syncthreads();
         const int n0 = bcount[0], n1 = bcount[1], n2 = bcount[2];
-        bool staged = false;
-        uint32_t lo16 = 0;
-        int sc = 0;
-        if (BSQ == 16 && range[2] && __popc(range[2]) == 1) {
-            sc = __ffs(range[2]) - 1;
-            lo16 = range[0] & ~15u;
-            const uint64_t end = min((uint64_t)range[1] + 48, f.srv_len[sc] + 16);
-            staged = (uint64_t)range[1] + 48 - lo16 <= (uint64_t)PAY_BUF;
-            if (staged) {
-                const uint4* src = reinterpret_cast<const uint4*>(f.srv[sc] + lo16);
-                const int n16 = (int)((end - lo16) >> 4);
-                for (int q = tid; q < n16; q += THREADS) reinterpret_cast<uint4*>(cbuf)[q] = __ldg(src + q);
-                __syncthreads();
-            }
-        }
+        const uint32_t* cb = cbuf + q * (PAY_BUF / 4);
         for (int j = tid; j < n0 + n1 + n2; j += THREADS) {
             const int m = j < n0 ? 0 : j < n0 + n1 ? 1 : 2;
             const int jj = j - (m == 0 ? 0 : m == 1 ? n0 : n0 + n1);
@@ -519,7 +554,7 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
             bool bad;
             if constexpr (BSQ == 16) {
                 // payload words from the staged chunk, else straight from HBM
-                const uint32_t* sw = staged ? cbuf + ((e.x - lo16) >> 2)
+                const uint32_t* sw = staged ? cb + ((e.x - lo16) >> 2)
                                             : reinterpret_cast<const uint32_t*>(f.srv[c] + (e.x & ~3u));
                 const uint32_t bit0 = (e.x & 3u) * 8u;
                 if (m == MODE_BITS) bad = decode16<MODE_BITS, VT>(sw, bit0, b, lut, dq, out);
@@ -534,7 +569,12 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
             if (bad) w.rec_flag[(int64_t)c * nblk + (e.y >> 7)] = 1u;   // kernels.py:147-150
         }
         __syncthreads();
+#pragma unroll
+        for (int k2 = 0; k2 < EPT; ++k2) ent[k2] = entn[k2];
+        staged = stagedn;
+        lo16 = lo16n;
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ---- pass 3: blend -------------------------------------------------------------------
@@ -677,7 +717,6 @@ __device__ __noinline__ void unit_fallback(const BlendParams& P, uint8_t* stage,
         }
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int B, typename VT, typename RT, int BT>
 __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__ BlendParams P,
@@ -1239,7 +1278,9 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
         const uint64_t cap_grid = (uint64_t)sms * 8;
         const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
-        k_payloads<BSQ, VT><<<grid, THREADS, 0, stream>>>(f, w);
+        const int pdyn = BSQ == 16 ? 2 * PAY_BUF : 16;
+        cudaFuncSetAttribute(k_payloads<BSQ, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdyn);
+        k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w);
     }
     auto kern = bt == 256 ? k_blend<B, VT, RT, 256> : k_blend<B, VT, RT, 128>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
