@@ -2,33 +2,43 @@
 //
 // The reference decodes image by image and re-walks every record once per
 // image (decoder.py:187-210 -> kernels.py:219-242 -> decode_chain_core
-// kernels.py:162-216).  Here the work is split into three launches, each
-// with full-warp parallelism and no per-camera-row barriers:
+// kernels.py:162-216).  Here the work is split into launches, each with
+// full-warp parallelism and no per-camera-row barriers:
 //
+//   k_root_rgb  RGB8 of every root sample of the band (colorspace.py:27-56).
 //   k_index     one lane per record (channel, block): popcount of the
 //               presence bitmap (kernels.py:181-183) reserves a dense run of
 //               payload slots (one atomic per warp), then the lane walks the
 //               descriptors (kernels.py:185-200) and writes one entry per
-//               present node: payload byte offset, descriptor, channel,
-//               block.  Records with any anomaly are flagged.
-//   k_payloads  one lane per payload: BISE decode (kernels.py:128-159) with
-//               one state machine for all three modes -- a plain-bit payload
-//               is a "group" of one value with no pack -- over a sequential
-//               64-bit bit reader, dequantised (kernels.py:202-211) into the
-//               residual array.  A corrupt pack flags its record.
-//   k_blend     one CTA per (block row, camera row, TW-pixel column chunk),
-//               all S views: residual slots are found by popcount rank in the
-//               record bitmaps, clean (view, block) pairs are RGB(root)
-//               copies, dirty ones add their residuals, YCoCg-R inverse +
-//               clamp (colorspace.py:27-56), and TMA tensor stores write the
+//               present node (payload byte offset, descriptor, channel,
+//               block), plus the record's bitmap words and per-word slot
+//               ranks into word-major tables.  Records with any anomaly are
+//               flagged.
+//   k_payloads  one lane per payload, CTAs bucket 512 entries by BISE mode
+//               so every warp runs one unrolled code path
+//               (kernels.py:128-159); for B = 4 the chunk's contiguous SRV
+//               bytes are staged in shared memory (double-buffered, cp.async)
+//               and each group is one 64-bit window at its closed-form bit
+//               offset; dequantisation (kernels.py:202-211) is a table.  A
+//               corrupt pack flags its record.
+//   k_blend     one 128-thread CTA per (column chunk of 64 pixels, camera
+//               row, block row), all S views.  The last warp issues TMA
+//               tensor loads of every view's RGB(root) rows (the result for
+//               clean pixels) and of the raw roots; the record phase reads
+//               row masks and slot bases from the word-major tables; one
+//               thread per (view, block) pair finds the dirty pairs and
+//               appends them (warp-aggregated atomics); tasks add the
+//               present residuals (16-byte gathers), YCoCg-R inverse + clamp
+//               + pack over the prefilled bytes; TMA tensor stores write the
 //               staged rows straight to HBM.  (view, block) pairs touching a
 //               flagged record run the reference-order walk (walk_chain),
 //               which reproduces the reference's values and failure order.
 //
 // Workspace (caller-owned device memory, rlfc_decode_workspace_bytes):
-//   u64 slot counter | u32 rec_base[3*nblk] | u32 rec_flag[3*nblk] |
-//   uint2 entries[cap] | VT residuals[cap][B*B]   (VT int16 when the
-//   quantisation shift keeps |residual| <= 16392, else int32).
+//   u64 counters | u32 rec_base[3*nblk] | u32 rec_flag[3*nblk] |
+//   uint2 entries[cap] | VT residuals[cap][B*B] (VT int16 when the
+//   quantisation shift keeps |residual| <= 16392, else int32) |
+//   RGB8 root colours | word-major bitmap words and word ranks.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
