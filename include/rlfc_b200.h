@@ -141,8 +141,9 @@ int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
  * intermediates in a caller-owned device workspace of
  * rlfc_decode_workspace_bytes(f, present_total) bytes (256-byte aligned).
  * present_total: the number of present nodes over all records
- * (rlfc_count_present).  Returns RLFC_ERR_ARGUMENT when the geometry is
- * outside this path's envelope (block 4/8/16, S <= 64, h <= 8); the caller
+ * (rlfc_count_present).  Returns RLFC_ERR_ARGUMENT when the stream is
+ * outside this path's envelope (block 4/8/16, S <= 64, h <= 8, level rows of
+ * <= 64 nodes, quantisation shift <= 20, SRV sections < 4 GiB); the caller
  * then uses rlfc_decode_field.  Records with any stream anomaly are decoded
  * by the reference-order walk, so values and the failure word are identical
  * to rlfc_decode_field's. */
