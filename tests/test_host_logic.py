@@ -168,3 +168,12 @@ def test_parallel_root_parse_matches_serial():
         with pytest.raises(FormatError, match="truncated"):
             container.parse_roots(bytes(only_trunc), hdr, threads=th)
     assert n > 24
+
+
+def test_colour_kat():
+    """test_colorspace.py:9-11: (255, 0, 0) <-> YCoCg-R (63, 255, -127)."""
+    from paper_1805_06019_b200 import colorspace
+    y, co, cg = colorspace.rgb_to_ycocgr(np.array([255]), np.array([0]), np.array([0]))
+    assert (int(y[0]), int(co[0]), int(cg[0])) == (63, 255, -127)
+    r, g, b = colorspace.ycocgr_to_rgb(y, co, cg)
+    assert (int(r[0]), int(g[0]), int(b[0])) == (255, 0, 0)
