@@ -393,9 +393,16 @@ __device__ __forceinline__ uint64_t win64(const uint32_t* sw, uint32_t pos) {
     return (uint64_t)__funnelshift_r(a, b, o) | (uint64_t)__funnelshift_r(b, c, o) << 32;
 }
 
+// 16-byte store with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void st16_hint(void* p, uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(x), "r"(y), "r"(z),
+                 "r"(w), "l"(pol)
+                 : "memory");
+}
+
 template <int MODE, typename VT>
 __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint32_t b, const uint16_t* dlut,
-                                         const VT* dq, VT* out) {
+                                         const VT* dq, VT* out, uint64_t pol = 0) {
     const uint32_t lm = (1u << b) - 1u;
     int32_t v[16];
     bool bad = false;
@@ -424,8 +431,17 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
             }
         }
     }
+    if (sizeof(VT) == 2 && pol) {
+        // int16 residuals: two 16-byte stores that stay in L2 for k_blend's gathers
+        uint32_t u[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) store4<VT>(out + 4 * q, v + 4 * q);
+        for (int q = 0; q < 8; ++q) u[q] = ((uint32_t)v[2 * q] & 0xFFFFu) | ((uint32_t)v[2 * q + 1] << 16);
+        st16_hint(out, u[0], u[1], u[2], u[3], pol);
+        st16_hint(out + 8, u[4], u[5], u[6], u[7], pol);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) store4<VT>(out + 4 * q, v + 4 * q);
+    }
     return bad;
 }
 
@@ -435,7 +451,7 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
 constexpr int PAY_CHUNK = 512;
 constexpr int PAY_BUF = 12 * 1024;       // staged SRV bytes per chunk (two buffers, dynamic shared memory)
 template <int BSQ, typename VT>
-__global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w) {
+__global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w, int l2_last) {
     __shared__ uint2 bucket[3][PAY_CHUNK];
     __shared__ uint32_t bslot[3][PAY_CHUNK];
     __shared__ int bcount[3];
@@ -451,6 +467,8 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     const uint64_t n = min((uint64_t)*w.counter, w.cap);
     const int64_t nblk = (int64_t)f.wb * f.hb;
     VT* res = static_cast<VT*>(w.res);
+    uint64_t pol = 0;
+    if (l2_last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     // Chunks are software-pipelined: while chunk i decodes, chunk i+1's
     // entries are in registers and its SRV byte range is on its way into the
     // other shared buffer (cp.async).  A chunk's payloads are consecutive
@@ -567,9 +585,9 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
                 const uint32_t* sw = staged ? cb + ((e.x - lo16) >> 2)
                                             : reinterpret_cast<const uint32_t*>(f.srv[c] + (e.x & ~3u));
                 const uint32_t bit0 = (e.x & 3u) * 8u;
-                if (m == MODE_BITS) bad = decode16<MODE_BITS, VT>(sw, bit0, b, lut, dq, out);
-                else if (m == MODE_TRIT) bad = decode16<MODE_TRIT, VT>(sw, bit0, b, lut, dq, out);
-                else bad = decode16<MODE_QUINT, VT>(sw, bit0, b, lut + 243, dq, out);
+                if (m == MODE_BITS) bad = decode16<MODE_BITS, VT>(sw, bit0, b, lut, dq, out, pol);
+                else if (m == MODE_TRIT) bad = decode16<MODE_TRIT, VT>(sw, bit0, b, lut, dq, out, pol);
+                else bad = decode16<MODE_QUINT, VT>(sw, bit0, b, lut + 243, dq, out, pol);
             } else {
                 const uint8_t* p = f.srv[c] + e.x;
                 if (m == MODE_BITS) bad = decode_payload<1, 0, BSQ, VT>(p, lut, b, shift, out);
@@ -1290,7 +1308,10 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
         const int pdyn = BSQ == 16 ? 2 * PAY_BUF : 16;
         cudaFuncSetAttribute(k_payloads<BSQ, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdyn);
-        k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w);
+        // residual payloads are stored with an L2 evict-last policy so the
+        // blend's gathers hit L2 (RLFC_RES_L2_LAST=0 disables it)
+        const char* l2e = getenv("RLFC_RES_L2_LAST");
+        k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, l2e ? atoi(l2e) : 1);
     }
     auto kern = bt == 256 ? k_blend<B, VT, RT, 256> : k_blend<B, VT, RT, 128>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
