@@ -181,6 +181,7 @@ __device__ __forceinline__ uint32_t node_bytes16(int d) {
 template <int BSQ>
 __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_field f, int k, int by_lo,
                                                    int by_hi, Ws w) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");      // k_root_rgb may run alongside
     const int64_t nblk = (int64_t)f.wb * f.hb;
     const int64_t band = (int64_t)(by_hi - by_lo) * f.wb;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -459,6 +460,7 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     __shared__ uint16_t lut[243 + 125];
     __shared__ VT dq[BSQ == 16 ? 2048 : 1];
     extern __shared__ __align__(16) uint32_t cbuf[];    // [2][PAY_BUF / 4] (B = 4 only)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");      // k_blend's prologue may start
     const int tid = threadIdx.x;
     const int shift = f.quant_shift;
     for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
@@ -703,6 +705,8 @@ __global__ void __launch_bounds__(THREADS) k_root_rgb(const __grid_constant__ rl
         }
         ycocg4_pack(v, reinterpret_cast<uint32_t*>(out + ry * rgb_stride + xq * 12));
     }
+    // launched programmatically behind k_index: do not complete before it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // byte offset of pixel (view s, row, tile column px) in the strip-major
@@ -821,7 +825,6 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         if (b < nb && nlev > 0 && !(P.debug & 8)) {
             const int64_t blk = (int64_t)by * f.wb + bx0 + b;
             const int64_t ri = (int64_t)c * nblk + blk;
-            fl = __ldg(P.rec_flag + ri);
             {
                 // every table word of the first RL levels is loaded before
                 // any is used (one round trip, not one per level); they are
@@ -856,6 +859,13 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                         sbase[li * NR + r] = rkv[li] + __popc(lo[li] & ((1u << o) - 1u));
                     }
                 }
+                // the table words above come from k_index (complete); the flags
+                // are also written by k_payloads, which may still be running
+                // when this grid starts (programmatic launch)
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                // a coherent load the compiler cannot hoist above the wait
+                // (ld.global.nc may be scheduled early)
+                asm volatile("ld.global.u32 %0, [%1];" : "=r"(fl) : "l"(P.rec_flag + ri) : "memory");
                 for (int li = RL; li < nlev; ++li) {             // deeper trees
                     const int l = k + li, sx = f.level_sx[l];
                     const int n0 = f.level_base[l] + (t >> l) * sx;
@@ -873,6 +883,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         }
         rflag[r] = fl;
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");       // residuals (tasks) come from k_payloads
     // ---- manual path: roots of this camera row and their RGB8 -------------------------
     if (!P.tma_in) {
         const int quads = TW / 4;
@@ -1293,16 +1304,38 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (P.tma_in) {
+    // Programmatic dependent launches (RLFC_PDL=0 disables): k_root_rgb runs
+    // alongside k_index's long record walks, and k_blend's CTAs start their
+    // TMA loads and record-table loads while k_payloads drains.
+    const char* pdl_env = getenv("RLFC_PDL");
+    const bool pdl = !pdl_env || atoi(pdl_env) != 0;
+    cudaLaunchAttribute pdl_attr[1];
+    pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+    auto cfg_of = [&](dim3 g, dim3 b, size_t smem, bool programmatic) {
+        cudaLaunchConfig_t c{};
+        c.gridDim = g;
+        c.blockDim = b;
+        c.dynamicSmemBytes = smem;
+        c.stream = stream;
+        c.attrs = programmatic && pdl ? pdl_attr : nullptr;
+        c.numAttrs = programmatic && pdl ? 1 : 0;
+        return c;
+    };
+    auto root_rgb = [&](bool programmatic) {
+        if (!P.tma_in) return;
         const int64_t n = (int64_t)nroot * (by_hi - by_lo) * B * (f.wp / 4);
         const int64_t want = (n + THREADS - 1) / THREADS;
-        k_root_rgb<RT><<<(unsigned)(want < sms * 16 ? want : sms * 16), THREADS, 0, stream>>>(
-            f, w.root_rgb, w.rgb_stride, by_lo * B, by_hi * B);
-    }
+        const cudaLaunchConfig_t c =
+            cfg_of(dim3((unsigned)(want < sms * 16 ? want : sms * 16)), dim3(THREADS), 0, programmatic);
+        cudaLaunchKernelEx(&c, k_root_rgb<RT>, f, w.root_rgb, w.rgb_stride, by_lo * B, by_hi * B);
+    };
+    if (k >= h) root_rgb(false);
     if (k < h) {
         cudaMemsetAsync(w.counter, 0, 8, stream);
         const int64_t nrec = 3ll * (by_hi - by_lo) * f.wb;
         k_index<BSQ><<<(unsigned)((nrec + THREADS - 1) / THREADS), THREADS, 0, stream>>>(f, k, by_lo, by_hi, w);
+        root_rgb(true);
         const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
         const uint64_t cap_grid = (uint64_t)sms * 8;
         const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
@@ -1316,7 +1349,10 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     auto kern = bt == 256 ? k_blend<B, VT, RT, 256> : k_blend<B, VT, RT, 128>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     const dim3 grid((unsigned)P.nchunks, (unsigned)f.t_count, (unsigned)(by_hi - by_lo));
-    kern<<<grid, bt, pl.smem, stream>>>(P, out_map, rgb_map, root_map);
+    {
+        const cudaLaunchConfig_t c = cfg_of(grid, dim3(bt), pl.smem, k < h);
+        cudaLaunchKernelEx(&c, kern, P, out_map, rgb_map, root_map);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "rlfc_b200: staged decode launch error: %s\n", cudaGetErrorString(e));
