@@ -847,6 +847,14 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                         rkv[li] = __ldg(rkr + wi * nrec);
                     }
                 }
+                // the table words above come from k_index (complete); the flags
+                // are also written by k_payloads, which may still be running
+                // when this grid starts (programmatic launch). The flag load is
+                // issued before any table word is consumed, so both share one
+                // round trip. A coherent load the compiler cannot hoist above
+                // the wait (ld.global.nc may be scheduled early).
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                asm volatile("ld.global.u32 %0, [%1];" : "=r"(fl) : "l"(P.rec_flag + ri) : "memory");
 #pragma unroll
                 for (int li = 0; li < RL; ++li) {
                     if (li < nlev) {
@@ -859,13 +867,6 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                         sbase[li * NR + r] = rkv[li] + __popc(lo[li] & ((1u << o) - 1u));
                     }
                 }
-                // the table words above come from k_index (complete); the flags
-                // are also written by k_payloads, which may still be running
-                // when this grid starts (programmatic launch)
-                asm volatile("griddepcontrol.wait;" ::: "memory");
-                // a coherent load the compiler cannot hoist above the wait
-                // (ld.global.nc may be scheduled early)
-                asm volatile("ld.global.u32 %0, [%1];" : "=r"(fl) : "l"(P.rec_flag + ri) : "memory");
                 for (int li = RL; li < nlev; ++li) {             // deeper trees
                     const int l = k + li, sx = f.level_sx[l];
                     const int n0 = f.level_base[l] + (t >> l) * sx;
