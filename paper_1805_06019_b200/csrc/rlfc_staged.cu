@@ -214,26 +214,24 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
         const uint8_t* rec = f.srv[c] + off;
         const NodeBytes& nb = node_bytes<BSQ>();
         uint32_t cursor = (uint32_t)f.bitmap_bytes;
-        for (int n0 = 0; n0 < node_end && !flag; n0 += 32) {
-            uint32_t bits = bitmap_word(rec, n0);
-            if (node_end - n0 < 32) bits &= (1u << (node_end - n0)) - 1u;
-            while (bits) {
-                bits &= bits - 1u;
-                const int d = cursor < len ? rec[cursor] : NUM_DESC;
-                if (d >= NUM_DESC) {
-                    flag = 1;
-                    break;
-                }
-                const uint32_t sz = BSQ == 16 ? node_bytes16(d) : (uint32_t)nb.v[d];
-                if (cursor + sz > len) {
-                    flag = 1;
-                    break;
-                }
-                w.entries[slot0 + rank] =
-                    make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
-                cursor += sz;
-                ++rank;
+        // The present nodes of [0, node_end) are the record's first `count`
+        // nodes in stream order (BFS puts levels >= k first), so the walk is
+        // one flat loop of `count` hops: a warp runs max-over-lanes hops, not
+        // the sum over bitmap words of per-word maxima.
+        for (; rank < count; ++rank) {
+            const int d = cursor < len ? rec[cursor] : NUM_DESC;
+            if (d >= NUM_DESC) {
+                flag = 1;
+                break;
             }
+            const uint32_t sz = BSQ == 16 ? node_bytes16(d) : (uint32_t)nb.v[d];
+            if (cursor + sz > len) {
+                flag = 1;
+                break;
+            }
+            w.entries[slot0 + rank] =
+                make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
+            cursor += sz;
         }
     }
     // every reserved slot below the capacity is written (SKIP when not decoded)
