@@ -93,7 +93,10 @@ int rlfc_decode_blocks(const rlfc_field *f, const int32_t *req, int32_t n,
  * int32) and are copied into host (pinned host memory, B*B+1 int32); with
  * dev NULL the kernel writes them straight into host, which must then be
  * pinned and device-addressable (unified addressing).  The call returns after
- * the result is in host (cudaStreamSynchronize on stream).
+ * the result is in host: with dev == NULL the kernel writes the block into
+ * host, status word last, and the call polls that word (the stream is queried
+ * every 1024 polls, so a failed launch returns RLFC_ERR_CUDA instead of
+ * hanging); with a device buffer it copies and synchronises the stream.
  * Out-of-range requests return RLFC_ERR_ARGUMENT (the host checks them first,
  * decoder.py:51-63). */
 int rlfc_decode_block_sync(const rlfc_field *f, int32_t s, int32_t t,

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <climits>
 
 #include "rlfc_common.cuh"
 #include "rlfc_field.cuh"
@@ -90,7 +92,10 @@ __global__ void __launch_bounds__(32) k_decode_block_one(const rlfc_field f, int
     }
 #pragma unroll
     for (int j = 0; j < B * B; ++j) out[j] = acc[j];
-    out[B * B] = st;
+    // the status word is written last, after a system-scope fence: a host
+    // polling it in mapped memory then sees the complete block
+    __threadfence_system();
+    *reinterpret_cast<volatile int32_t*>(out + B * B) = st;
 }
 
 // One thread per (plane request, block): kernels.py:219-242 decode_plane_core.
@@ -266,8 +271,26 @@ extern "C" int rlfc_decode_block_sync(const rlfc_field* f, int32_t s, int32_t t,
             return RLFC_ERR_CUDA;
     } else {
         // host is pinned, device-addressable memory (unified addressing):
-        // the kernel writes the result straight into it
+        // the kernel writes the result straight into it, status word last.
+        // The host polls that word instead of a stream synchronize (whose
+        // wake-up is most of a single request's latency), checking the
+        // stream every 1024 polls so a failed launch cannot hang the caller.
+        volatile int32_t* flag = host + f->block * f->block;
+        *flag = INT_MIN;                       // never a status value
+        std::atomic_thread_fence(std::memory_order_seq_cst);
         RLFC_DISPATCH_B(f->block, k_decode_block_one<BB><<<1, 32, 0, st>>>(*f, s, t, bx, by, c, stop_level, host));
+        if (cudaGetLastError() != cudaSuccess) return RLFC_ERR_CUDA;
+        for (uint32_t i = 1; *flag == INT_MIN; ++i) {
+            if ((i & 1023u) == 0) {
+                const cudaError_t q = cudaStreamQuery(st);
+                if (q == cudaErrorNotReady) continue;
+                if (q != cudaSuccess) return RLFC_ERR_CUDA;
+                if (*flag == INT_MIN) return RLFC_ERR_CUDA;     // kernel done, no status: cannot happen
+                break;
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return RLFC_OK;
     }
     return cudaStreamSynchronize(st) == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }

@@ -27,3 +27,29 @@ for s, t, bx, by, c in picks:
     rl.decode_block(st, (s, t), (bx, by), c)
 dt = (time.perf_counter() - t0) / len(picks)
 print(f"decode_block latency {dt * 1e6:.2f} us (mean of {len(picks)})")
+
+# breakdown: the native call alone (no Python argument checks / copy)
+from paper_1805_06019_b200 import decoder  # noqa: E402
+sc = decoder._block_scratch(st)
+ref, dev, host, stream = sc.args
+t0 = time.perf_counter()
+for s, t, bx, by, c in picks:
+    sc.fn(ref, s, t, bx, by, c, 0, dev, host, stream)
+dt2 = (time.perf_counter() - t0) / len(picks)
+print(f"native rlfc_decode_block_sync alone {dt2 * 1e6:.2f} us")
+# the same block over and over (record and roots L2-resident)
+s, t, bx, by, c = picks[0]
+t0 = time.perf_counter()
+for _ in range(len(picks)):
+    sc.fn(ref, s, t, bx, by, c, 0, dev, host, stream)
+dt3 = (time.perf_counter() - t0) / len(picks)
+print(f"native call, one block repeated (L2-warm) {dt3 * 1e6:.2f} us")
+import torch  # noqa: E402
+x = torch.zeros(1, device="cuda")
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(len(picks)):
+    x.add_(1)
+    torch.cuda.synchronize()
+dt4 = (time.perf_counter() - t0) / len(picks)
+print(f"torch one-kernel launch + synchronize {dt4 * 1e6:.2f} us")
