@@ -455,15 +455,17 @@ def render_measure(state, args, rl):
     for _ in range(2):
         rl.render_views(state, poses, out=out)
     torch.cuda.synchronize()
-    reps = 3
-    t0 = time.perf_counter()
-    for _ in range(reps):
+    # median of 15 synchronised batches (wall clock, host pose prep included)
+    times = []
+    for _ in range(15):
+        t0 = time.perf_counter()
         rl.render_views(state, poses, out=out)
-    torch.cuda.synchronize()
-    dt = (time.perf_counter() - t0) / reps
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
     return {"views_per_s": n / dt, "batch": n, "ms_per_batch": dt * 1e3,
             "view": "512x512 SlabPose, default focal, k=0, bit-exact",
-            "timing": "wall clock incl. host pose prep, sync per batch"}
+            "timing": "wall clock incl. host pose prep, sync per batch, median of 15 batches"}
 
 
 CFG5 = dict(S=32, T=32, W=2048, H=2048, seed=7, h=3, B=4, shift=4, tp=16,
