@@ -176,6 +176,20 @@ __device__ __forceinline__ uint32_t node_bytes16(int d) {
 }
 
 // ---- pass 1: index -----------------------------------------------------------------
+// Records whose bitmap fits IDX_MAXW - 4 aligned words (bitmap_bytes <= 64,
+// e.g. M = 395 -> 50 bytes) load it once with aligned 16-byte loads, all in
+// flight together, and take the popcount and the blend's word tables from
+// registers: the per-lane bitmap reads (every warp load touching 32 lines)
+// were most of k_index's time.
+constexpr int IDX_MAXW = 20;
+__device__ __forceinline__ uint32_t node_word(const uint32_t* A, int j, uint32_t sh, int node_end) {
+    const int n0 = 32 * j;
+    if (n0 >= node_end) return 0u;
+    uint32_t v = __funnelshift_r(A[j], A[j + 1], sh);
+    if (node_end - n0 < 32) v &= (1u << (node_end - n0)) - 1u;
+    return v;
+}
+
 // Levels >= k occupy serial nodes [0, node_end) (level h-1 first,
 // container.py:102-145); only those are indexed and decoded.
 template <int BSQ>
@@ -191,9 +205,42 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
     const int node_end = f.level_base[k] + f.level_sx[k] * f.level_sy[k];
     uint64_t off = 0, len = 0;
     uint32_t flag = 0, count = 0;
+    const bool fastbm = f.bitmap_bytes + 15 + 4 <= IDX_MAXW * 4;
+    uint32_t A[IDX_MAXW];
+#pragma unroll
+    for (int j = 0; j < IDX_MAXW; ++j) A[j] = 0u;
+    uint32_t sh = 0;
+    int w0 = 0;                               // first aligned word of the bitmap in A
     if (valid) {
-        if (record_span(f, c, blk, off, len)) count = popc_prefix(f.srv[c] + off, node_end);
-        else flag = 1;
+        if (record_span(f, c, blk, off, len)) {
+            if (fastbm) {
+                const uintptr_t ra = reinterpret_cast<uintptr_t>(f.srv[c] + off);
+                const uint4* a = reinterpret_cast<const uint4*>(ra & ~uintptr_t(15));
+                const uint32_t lead = (uint32_t)(ra & 15u);
+                const int nq = (int)((lead + (uint32_t)f.bitmap_bytes + 15u) >> 4);
+#pragma unroll
+                for (int q = 0; q < IDX_MAXW / 4; ++q)
+                    if (q < nq) {
+                        const uint4 v = __ldg(a + q);
+                        A[4 * q] = v.x; A[4 * q + 1] = v.y; A[4 * q + 2] = v.z; A[4 * q + 3] = v.w;
+                    }
+                // shift the words down so A[0] holds the bitmap's first byte's word
+                w0 = (int)(lead >> 2);
+#pragma unroll
+                for (int j = 0; j < IDX_MAXW; ++j) {
+                    const uint32_t x1 = j + 1 < IDX_MAXW ? A[j + 1] : 0u, x2 = j + 2 < IDX_MAXW ? A[j + 2] : 0u,
+                                   x3 = j + 3 < IDX_MAXW ? A[j + 3] : 0u;
+                    A[j] = w0 == 0 ? A[j] : w0 == 1 ? x1 : w0 == 2 ? x2 : x3;
+                }
+                sh = (uint32_t)(ra & 3u) * 8u;
+#pragma unroll
+                for (int j = 0; j + 1 < IDX_MAXW - 3; ++j) count += __popc(node_word(A, j, sh, node_end));
+            } else {
+                count = popc_prefix(f.srv[c] + off, node_end);
+            }
+        } else {
+            flag = 1;
+        }
     }
     // dense slot run per record: warp scan + one atomic per warp
     const int lane = threadIdx.x & 31;
@@ -209,6 +256,27 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
     const uint64_t slot0 = wbase + incl - count;
     if (!valid) return;
     if (slot0 + count > w.cap) flag = 1;
+    const int64_t ri = (int64_t)c * nblk + blk;
+    if (fastbm && !flag) {
+        // bitmap words of levels >= k and the slot at each word start, for
+        // the blend's row masks and ranks (k_blend); a record the walk then
+        // flags never has its words read
+        const int64_t nrec = 3 * nblk;
+        uint32_t run = (uint32_t)slot0;
+#pragma unroll
+        for (int wi = 0; wi + 1 < IDX_MAXW - 3; ++wi) {
+            if (wi < w.nwp) {
+                const uint32_t word = node_word(A, wi, sh, node_end);
+                w.bm[wi * nrec + ri] = word;
+                w.rk[wi * nrec + ri] = run;
+                run += __popc(word);
+            }
+        }
+        for (int wi = IDX_MAXW - 4; wi < w.nwp; ++wi) {
+            w.bm[wi * nrec + ri] = 0u;
+            w.rk[wi * nrec + ri] = run;
+        }
+    }
     uint32_t rank = 0;
     if (!flag && count) {
         const uint8_t* rec = f.srv[c] + off;
@@ -236,8 +304,7 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
     }
     // every reserved slot below the capacity is written (SKIP when not decoded)
     for (uint64_t r = rank; r < count && slot0 + r < w.cap; ++r) w.entries[slot0 + r] = make_uint2(0u, SKIP);
-    const int64_t ri = (int64_t)c * nblk + blk;
-    if (!flag) {
+    if (!fastbm && !flag) {
         // bitmap words of levels >= k and the slot at each word start, for
         // the blend's row masks and ranks (k_blend)
         const uint8_t* rec = f.srv[c] + off;
