@@ -286,6 +286,10 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
         // nodes in stream order (BFS puts levels >= k first), so the walk is
         // one flat loop of `count` hops: a warp runs max-over-lanes hops, not
         // the sum over bitmap words of per-word maxima.
+        // entries go out in 16-byte pairs (an even slot is held until its
+        // odd neighbour exists): half the scattered store sectors
+        uint2 pend = make_uint2(0u, 0u);
+        bool has_pend = false;
         for (; rank < count; ++rank) {
             const int d = cursor < len ? rec[cursor] : NUM_DESC;
             if (d >= NUM_DESC) {
@@ -297,10 +301,20 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
                 flag = 1;
                 break;
             }
-            w.entries[slot0 + rank] =
-                make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
+            const uint2 e = make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
+            const uint64_t sl = slot0 + rank;
+            if (!(sl & 1u)) {
+                pend = e;
+                has_pend = true;
+            } else if (has_pend) {
+                *reinterpret_cast<uint4*>(w.entries + (sl - 1)) = make_uint4(pend.x, pend.y, e.x, e.y);
+                has_pend = false;
+            } else {
+                w.entries[sl] = e;
+            }
             cursor += sz;
         }
+        if (has_pend) w.entries[slot0 + rank - 1] = pend;
     }
     // every reserved slot below the capacity is written (SKIP when not decoded)
     for (uint64_t r = rank; r < count && slot0 + r < w.cap; ++r) w.entries[slot0 + r] = make_uint2(0u, SKIP);
