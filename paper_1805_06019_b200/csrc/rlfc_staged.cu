@@ -286,10 +286,18 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
         // nodes in stream order (BFS puts levels >= k first), so the walk is
         // one flat loop of `count` hops: a warp runs max-over-lanes hops, not
         // the sum over bitmap words of per-word maxima.
-        // entries go out in 16-byte pairs (an even slot is held until its
-        // odd neighbour exists): half the scattered store sectors
-        uint2 pend = make_uint2(0u, 0u);
-        bool has_pend = false;
+        // entries go out as full 32-byte sectors: slots of an aligned quad are
+        // held in registers until its last slot exists (one 256-bit store);
+        // partial quads at the run's ends are stored entry by entry
+        uint2 p0 = make_uint2(0u, 0u), p1 = p0, p2 = p0;
+        uint32_t pm = 0;                                // pending quad positions
+        uint64_t pq = 0;                                // their quad's first slot
+        auto flush = [&]() {
+            if (pm & 1u) w.entries[pq] = p0;
+            if (pm & 2u) w.entries[pq + 1] = p1;
+            if (pm & 4u) w.entries[pq + 2] = p2;
+            pm = 0;
+        };
         for (; rank < count; ++rank) {
             const int d = cursor < len ? rec[cursor] : NUM_DESC;
             if (d >= NUM_DESC) {
@@ -303,18 +311,23 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
             }
             const uint2 e = make_uint2((uint32_t)(off + cursor + 1), (uint32_t)d | (uint32_t)c << 5 | (uint32_t)blk << 7);
             const uint64_t sl = slot0 + rank;
-            if (!(sl & 1u)) {
-                pend = e;
-                has_pend = true;
-            } else if (has_pend) {
-                *reinterpret_cast<uint4*>(w.entries + (sl - 1)) = make_uint4(pend.x, pend.y, e.x, e.y);
-                has_pend = false;
+            const uint32_t pos = (uint32_t)sl & 3u;
+            pq = sl - pos;
+            if (pos == 0) { p0 = e; pm |= 1u; }
+            else if (pos == 1) { p1 = e; pm |= 2u; }
+            else if (pos == 2) { p2 = e; pm |= 4u; }
+            else if (pm == 7u) {
+                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(w.entries + pq),
+                             "r"(p0.x), "r"(p0.y), "r"(p1.x), "r"(p1.y), "r"(p2.x), "r"(p2.y), "r"(e.x), "r"(e.y)
+                             : "memory");
+                pm = 0;
             } else {
+                flush();
                 w.entries[sl] = e;
             }
             cursor += sz;
         }
-        if (has_pend) w.entries[slot0 + rank - 1] = pend;
+        flush();
     }
     // every reserved slot below the capacity is written (SKIP when not decoded)
     for (uint64_t r = rank; r < count && slot0 + r < w.cap; ++r) w.entries[slot0 + r] = make_uint2(0u, SKIP);
