@@ -529,8 +529,11 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
         uint32_t u[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) u[q] = ((uint32_t)v[2 * q] & 0xFFFFu) | ((uint32_t)v[2 * q + 1] << 16);
-        st16_hint(out, u[0], u[1], u[2], u[3], pol);
-        st16_hint(out + 8, u[4], u[5], u[6], u[7], pol);
+        // one 256-bit store: the payload's whole 32-byte sector
+        asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(out),
+                     "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]),
+                     "l"(pol)
+                     : "memory");
     } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) store4<VT>(out + 4 * q, v + 4 * q);
@@ -1097,9 +1100,12 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                 pcs[c] = e.y & (0x249249u << c);             // bits 3i + c: levels k + i
                 raw[c][0] = raw[c][1] = make_uint4(0u, 0u, 0u, 0u);
                 if (pcs[c]) {
-                    const uint4* q = reinterpret_cast<const uint4*>(res + (uint64_t)slot_of(c, pcs[c]) * BSQ);
-                    raw[c][0] = __ldg(q);
-                    raw[c][1] = __ldg(q + 1);
+                    // the payload's 32-byte sector in one 256-bit load
+                    const VT* q = res + (uint64_t)slot_of(c, pcs[c]) * BSQ;
+                    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                 : "=r"(raw[c][0].x), "=r"(raw[c][0].y), "=r"(raw[c][0].z), "=r"(raw[c][0].w),
+                                   "=r"(raw[c][1].x), "=r"(raw[c][1].y), "=r"(raw[c][1].z), "=r"(raw[c][1].w)
+                                 : "l"(q));
                     pcs[c] &= pcs[c] - 1u;
                 }
             }
