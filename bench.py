@@ -147,7 +147,8 @@ class ClockSampler:
 
 NCU_SUMMARY = {"fused": "profiles/r1_decode_ncu_summary.json",
                "staged": "profiles/r1_staged_ncu_summary.json"}
-KERNELS = {"fused": ["k_decode_field_tiled"],
+KERNELS = {"auto": ["k_field_dir"], "dir": ["k_field_dir"],
+           "fused": ["k_decode_field_tiled"],
            "staged": ["k_root_rgb", "k_index", "k_payloads", "k_blend"],
            "simple": ["k_decode_field_simple"]}
 
@@ -237,7 +238,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--kernel", default="staged", choices=["staged", "fused", "simple"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "dir", "staged", "fused", "simple"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--render-batch", type=int, default=256)

@@ -160,6 +160,64 @@ int rlfc_decode_field_staged(const rlfc_field *f, int32_t stop_level,
                              uint64_t workspace_bytes, uint64_t present_total,
                              uint64_t *status, void *stream);
 
+/* Device record directory: the stream-invariant part of the reference's
+ * per-image record walk (kernels.py:162-200), done once per stream and GPU
+ * (the reference keeps its own init-time index, `chains`, decoder.py:40-44).
+ * The present nodes' stream bytes (descriptor + BISE payload, unchanged) are
+ * regrouped into tile-major blobs, one per (block row, 64-pixel chunk, tree
+ * level, node row):
+ *     u32 n | u16 nbits, ntrits | u32 pad[2] | u32 mask[3*nb] | u16 off[n] |
+ *     u16 rot[n] | node bytes (pad 16)
+ * mask[c*nb + b] = presence bits of the node row in record (c, block b of the
+ * chunk) (kernels.py:181-183); off[j] = byte offset of the j-th present node
+ * (rank order c, b, x); rot[] = the ranks ordered by BISE mode (plain bits,
+ * trits, quints), nbits / ntrits the first two counts.  blob_off[i] is blob i's offset in 16-byte units, blob
+ * i = (by * nchunks + chunk) * rows + row_base[l] + tl, with rows = sum of
+ * level_sy over the levels (level 0 first).  root_rgb holds the RGB8 of every
+ * root sample (colorspace.py:27-56), rows of rgb_stride bytes.  Records with
+ * a stream anomaly (descriptor >= 30, a node past the record end,
+ * inconsistent offsets) are not in any blob; they are listed in flagged
+ * (c * wb*hb + block) and decoded by the reference-order walk.
+ *
+ * Build: rlfc_dir_plan fills the geometry and the scratch / root_rgb sizes;
+ * the caller allocates scratch (scratch_bytes), blob_off (n_blobs + 1 u32),
+ * flagged (nrec int32) and root_rgb; rlfc_dir_size (synchronous) sizes the
+ * blobs (blob_bytes, n_flagged); the caller allocates blobs (blob_bytes + 64,
+ * the tail lets 64-bit bit windows read past the last payload);
+ * rlfc_dir_build fills them.  RLFC_ERR_ARGUMENT: outside this path's
+ * envelope (block 4, S <= 32, h <= 8, int16 roots, a blob over 64 KiB). */
+typedef struct rlfc_dir {
+    int32_t tw, nb, nchunks, rows;
+    int64_t n_blobs, nrec;
+    uint64_t scratch_bytes, root_rgb_bytes;
+    int32_t rgb_stride, n_flagged;
+    uint64_t blob_bytes;
+    void *scratch;
+    uint32_t *blob_off;
+    int32_t *flagged;
+    uint8_t *root_rgb;
+    uint8_t *blobs;
+} rlfc_dir;
+
+int rlfc_dir_plan(const rlfc_field *f, rlfc_dir *d);
+int rlfc_dir_size(const rlfc_field *f, rlfc_dir *d, void *stream);
+int rlfc_dir_build(const rlfc_field *f, rlfc_dir *d, void *stream);
+
+/* Full-field decode over the record directory (rlfc_dir_build): same
+ * contract and output as rlfc_decode_field for all S x T images (no slot
+ * table), block rows [by_lo, by_hi).  One persistent kernel per call: TMA
+ * prefill of every view's RGB(root) rows, BISE decode of each dirty unit's
+ * chain payloads from the blobs (kernels.py:128-159, 202-211), YCoCg-R
+ * inverse + clamp (colorspace.py:27-56), TMA store; every payload is
+ * decoded in every call.  Records listed as flagged are then re-decoded by
+ * the reference-order walk, so values and the failure word equal
+ * rlfc_decode_field's.  rgb, img_stride and row_stride must be multiples
+ * of 16 bytes. */
+int rlfc_decode_field_dir(const rlfc_field *f, const rlfc_dir *d,
+                          int32_t stop_level, int32_t by_lo, int32_t by_hi,
+                          uint8_t *rgb, int64_t img_stride, int64_t row_stride,
+                          uint64_t *status, void *stream);
+
 /* BISE payload decode, batched.  Replaces kernels.bise_decode_core
  * (kernels.py:128-159) / bise.bise_decode (bise.py:108-118).  payload i
  * starts at data + offs[i], has descriptor descs[i] and `count` values;

@@ -44,8 +44,27 @@ class RenderGeom(ctypes.Structure):
                 ("cam_z", "img_z", "x0", "y0", "x1", "y1")]
 
 
+class RlfcDir(ctypes.Structure):
+    """Mirror of `rlfc_dir` (the device record directory)."""
+    _fields_ = [("tw", ctypes.c_int32), ("nb", ctypes.c_int32),
+                ("nchunks", ctypes.c_int32), ("rows", ctypes.c_int32),
+                ("n_blobs", ctypes.c_int64), ("nrec", ctypes.c_int64),
+                ("scratch_bytes", ctypes.c_uint64),
+                ("root_rgb_bytes", ctypes.c_uint64),
+                ("rgb_stride", ctypes.c_int32), ("n_flagged", ctypes.c_int32),
+                ("blob_bytes", ctypes.c_uint64),
+                ("scratch", ctypes.c_void_p), ("blob_off", ctypes.c_void_p),
+                ("flagged", ctypes.c_void_p), ("root_rgb", ctypes.c_void_p),
+                ("blobs", ctypes.c_void_p)]
+
+
 _lib = None
 _SIGS = {
+    "rlfc_dir_plan": ["p", "p"],
+    "rlfc_dir_size": ["p", "p", "p"],
+    "rlfc_dir_build": ["p", "p", "p"],
+    "rlfc_decode_field_dir": ["p", "p", "i", "i", "i", "p", "q", "q", "p",
+                              "p"],
     "rlfc_decode_blocks": ["p", "p", "i", "p", "p", "p"],
     "rlfc_decode_block_sync": ["p", "i", "i", "i", "i", "i", "i", "p", "p",
                                "p"],

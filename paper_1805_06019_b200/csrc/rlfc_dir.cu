@@ -1,0 +1,1201 @@
+// rlfc_dir.cu -- record directory + single-pass persistent full-field decode (sm_100a).
+//
+// The reference decodes image by image, re-walking every record once per image
+// (decoder.py:187-210 -> kernels.py:219-242 -> decode_chain_core
+// kernels.py:162-216).  Here the stream-invariant part of that walk -- where
+// each present node's payload sits -- is done ONCE per stream and GPU (the
+// reference's precedent is the init-time `chains` table, decoder.py:40-44):
+//
+//   record directory (built at init, rlfc_dir_build):
+//     the SRV payloads are regrouped into tile-major BLOBS, one per
+//     (block row by, 64-pixel chunk, tree level l, node row tl): the present
+//     nodes of node row tl of level l, for the 3 x NB records (channel c,
+//     block b) of the chunk, in (c, b, x) order.  A blob is
+//         u32 n | u16 nbits, ntrits | u32 pad[2] | u32 mask[3*NB] | u16 off[n] |
+//         u16 rot[n] | node bytes
+//     where mask[c*NB + b] is the record's presence bits of that node row
+//     (kernels.py:181-183) and each node keeps its stream bytes unchanged
+//     (descriptor + BISE payload, container.py:306-323).  blob_off gives
+//     every blob's position (16-byte units); root colours (RGB8 of every root
+//     sample, colorspace.py:27-56) are also computed once.  Records with a
+//     stream anomaly (bad descriptor, truncation, inconsistent offsets) are
+//     listed instead and decoded by the reference-order walk (k_fixup).
+//
+//   decode step (rlfc_decode_field_dir): ONE persistent kernel, k_field_dir.
+//     A CTA owns (block row, chunk) columns and walks their camera rows t.
+//     Warp 0 is the producer: per tile (by, chunk, t) it TMA-loads every
+//     view's RGB(root) rows into the output stage (the result of every clean
+//     pixel) and bulk-copies the tile's blobs (levels k..h-1, rows t >> l);
+//     per root row segment it TMA-loads the raw root planes.  Eight consumer
+//     warps find the dirty (view, block) units from the blob masks, BISE-
+//     decode each unit's chain payloads straight from the blob bytes
+//     (kernels.py:128-159, dequantised kernels.py:202-211), add them to the
+//     root block, apply the YCoCg-R inverse + clamp (colorspace.py:27-56)
+//     over the prefilled stage, and one thread TMA-stores the stage (all S
+//     views of the tile).  Stages form a ring so loads, decode and stores of
+//     consecutive tiles overlap.  Every payload a pixel needs is BISE-decoded
+//     in every step; nothing decoded is cached across steps.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
+#include <cstdio>
+#include <cstring>
+
+#include "rlfc_common.cuh"
+
+namespace rlfc {
+namespace dir {
+
+constexpr int B = 4;                 // block size of this path
+constexpr int TW = 64;               // tile width, pixels (one 192-byte TMA row)
+constexpr int NB = TW / B;           // blocks per tile
+constexpr int NR = 3 * NB;           // records per tile row
+constexpr int MAXL = 8;              // tree levels
+constexpr int MAXS = 32;             // views per camera row (masks are 32-bit)
+constexpr int NG = 6;                // consumer groups (one tile each at a time)
+constexpr int GW = 3;                // warps per group (6 groups x 3 + producer = 19 warps)
+constexpr int GT = GW * 32;
+constexpr int NT = 32 + NG * GT;     // + one producer warp
+constexpr int HDR0 = 16 + 4 * NR;    // blob bytes before the u16 offsets
+
+__device__ const DigitLut g_lut = make_digit_lut();
+__device__ const NodeBytes g_nb16 = make_node_bytes<16>();
+
+// blob bytes before the node bytes: header, masks, off[n], rot[n]
+__host__ __device__ inline uint32_t blob_hdr(uint32_t n) { return (HDR0 + 4 * n + 3) & ~3u; }
+
+// Geometry shared by the build kernels.
+struct Geo {
+    int h, wb, hb, nchunks, R, nblk;
+    int row_base[MAXL];              // first row id of each level (level 0 first)
+};
+
+__device__ __forceinline__ bool span_of(const rlfc_field& f, int c, int64_t blk, uint64_t& off, uint64_t& len) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    off = f.offsets[c][blk];
+    const uint64_t end = blk + 1 < nblk ? f.offsets[c][blk + 1] : f.srv_len[c];
+    if (off > end || end > f.srv_len[c] || end - off < (uint64_t)f.bitmap_bytes) return false;
+    len = end - off;
+    return true;
+}
+
+// Walk the present nodes of one record row by row in serial (stream) order:
+// level h-1 .. 0, node rows ascending, x ascending (container.py:102-145).
+// fn(row_id, mask, cursor_at_row_start) is called for every node row; it
+// returns the bytes the row's nodes occupy (or -1 to stop).  Returns false
+// on an anomaly (descriptor >= 30 or a node past the record end).
+template <typename Fn>
+__device__ __forceinline__ bool walk_rows(const rlfc_field& f, const Geo& g, const uint8_t* rec, uint64_t len,
+                                          Fn fn) {
+    const NodeBytes& nb = g_nb16;
+    uint64_t cursor = (uint64_t)f.bitmap_bytes;
+    for (int l = g.h - 1; l >= 0; --l) {
+        const int sx = f.level_sx[l], sy = f.level_sy[l];
+        for (int tl = 0; tl < sy; ++tl) {
+            const int n0 = f.level_base[l] + tl * sx;
+            uint32_t m = load_bits32<true>(rec, (uint64_t)n0);
+            if (sx < 32) m &= (1u << sx) - 1u;
+            uint64_t cur = cursor;
+            for (uint32_t mm = m; mm; mm &= mm - 1u) {
+                if (cur >= len) return false;
+                const int d = rec[cur];
+                if (d >= NUM_DESC) return false;
+                if (cur + nb.v[d] > len) return false;
+                cur += nb.v[d];
+            }
+            fn(g.row_base[l] + tl, m, cursor, cur);
+            cursor = cur;
+        }
+    }
+    return true;
+}
+
+// ---- build 1: per (record, node row) payload count and bytes ------------------------
+__global__ void k_dir_count(const __grid_constant__ rlfc_field f, Geo g, uint32_t* cnt, uint32_t* byt,
+                            int32_t* flagged, uint32_t* n_flagged) {
+    const int64_t nrec = 3ll * g.nblk;
+    const int64_t ri = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ri >= nrec) return;
+    const int c = (int)(ri / g.nblk);
+    const int64_t blk = ri - (int64_t)c * g.nblk;
+    uint64_t off, len;
+    bool ok = span_of(f, c, blk, off, len);
+    const uint8_t* rec = f.srv[c] + off;
+    if (ok) ok = walk_rows(f, g, rec, len, [](int, uint32_t, uint64_t, uint64_t) {});
+    if (!ok) {
+        flagged[atomicAdd(n_flagged, 1u)] = (int32_t)ri;
+        return;
+    }
+    walk_rows(f, g, rec, len, [&](int row, uint32_t m, uint64_t c0, uint64_t c1) {
+        if (m) {
+            cnt[(int64_t)row * nrec + ri] = __popc(m);
+            byt[(int64_t)row * nrec + ri] = (uint32_t)(c1 - c0);
+        }
+    });
+}
+
+// ---- build 2: per blob size; per-record exclusive prefix inside the blob --------------
+__global__ void k_dir_blob(Geo g, uint32_t* cnt, uint32_t* byt, uint32_t* blob_n, uint32_t* blob_sz,
+                           uint32_t* too_big) {
+    const int64_t nrec = 3ll * g.nblk;
+    const int64_t nblob = (int64_t)g.hb * g.nchunks * g.R;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > nblob) return;
+    if (i == nblob) {                     // sentinel: the exclusive scan's total
+        blob_sz[i] = 0;
+        return;
+    }
+    const int row = (int)(i % g.R);
+    const int64_t col = i / g.R;
+    const int by = (int)(col / g.nchunks), chunk = (int)(col % g.nchunks);
+    uint32_t n = 0, d = 0;
+    for (int c = 0; c < 3; ++c)
+        for (int b = 0; b < NB; ++b) {
+            const int bx = chunk * NB + b;
+            if (bx >= g.wb) break;
+            const int64_t ri = (int64_t)c * g.nblk + (int64_t)by * g.wb + bx;
+            const int64_t a = (int64_t)row * nrec + ri;
+            const uint32_t x = cnt[a], y = byt[a];
+            cnt[a] = n;
+            byt[a] = d;
+            n += x;
+            d += y;
+        }
+    const uint32_t size = (blob_hdr(n) + d + 15u) & ~15u;
+    if (size > 65536u) atomicOr(too_big, 1u);
+    blob_n[i] = n;
+    blob_sz[i] = size >> 4;
+}
+
+// ---- build 3: blob contents ---------------------------------------------------------
+__global__ void k_dir_fill(const __grid_constant__ rlfc_field f, Geo g, const uint32_t* cnt, const uint32_t* byt,
+                           const uint32_t* blob_n, const uint32_t* blob_off, uint8_t* blobs,
+                           const uint8_t* rec_bad) {
+    const int64_t nrec = 3ll * g.nblk;
+    const int64_t ri = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ri >= nrec || rec_bad[ri]) return;
+    const int c = (int)(ri / g.nblk);
+    const int64_t blk = ri - (int64_t)c * g.nblk;
+    const int by = (int)(blk / g.wb), bx = (int)(blk - (int64_t)by * g.wb);
+    const int chunk = bx / NB, b = bx - chunk * NB;
+    uint64_t off, len;
+    span_of(f, c, blk, off, len);
+    const uint8_t* rec = f.srv[c] + off;
+    const int64_t col = (int64_t)by * g.nchunks + chunk;
+    walk_rows(f, g, rec, len, [&](int row, uint32_t m, uint64_t c0, uint64_t c1) {
+        if (!m) return;
+        const int64_t bi = col * g.R + row;
+        uint8_t* base = blobs + (uint64_t)blob_off[bi] * 16u;
+        const uint32_t hdr = blob_hdr(blob_n[bi]);
+        reinterpret_cast<uint32_t*>(base)[4 + c * NB + b] = m;
+        const int64_t a = (int64_t)row * nrec + ri;
+        uint32_t pidx = cnt[a], pos = hdr + byt[a];
+        uint16_t* offs = reinterpret_cast<uint16_t*>(base + HDR0);
+        const NodeBytes& nb = g_nb16;
+        uint64_t cur = c0;
+        for (uint32_t mm = m; mm; mm &= mm - 1u) {
+            const int sz = nb.v[rec[cur]];
+            offs[pidx++] = (uint16_t)pos;
+            for (int j = 0; j < sz; ++j) base[pos + j] = rec[cur + j];
+            pos += sz;
+            cur += sz;
+        }
+    });
+}
+
+// Blob header: the payload count, and rot[] = the payload ranks ordered by
+// BISE mode (plain bits, trits, quints; stable), with the per-mode counts,
+// so the decode step hands warps payloads of one mode.
+__global__ void k_dir_hdr(int64_t nblob, const uint32_t* blob_n, const uint32_t* blob_off, uint8_t* blobs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nblob) return;
+    uint8_t* base = blobs + (uint64_t)blob_off[i] * 16u;
+    const uint32_t n = blob_n[i];
+    const uint16_t* offs = reinterpret_cast<const uint16_t*>(base + HDR0);
+    uint16_t* rot = reinterpret_cast<uint16_t*>(base + HDR0) + n;
+    uint32_t cnt[3] = {0, 0, 0};
+    uint32_t pos = 0;
+    for (int m = 0; m < 3; ++m)
+        for (uint32_t j = 0; j < n; ++j)
+            if (desc_mode(base[offs[j]]) == m) {
+                rot[pos++] = (uint16_t)j;
+                ++cnt[m];
+            }
+    reinterpret_cast<uint32_t*>(base)[0] = n;
+    reinterpret_cast<uint16_t*>(base)[2] = (uint16_t)cnt[0];
+    reinterpret_cast<uint16_t*>(base)[3] = (uint16_t)cnt[1];
+}
+
+__global__ void k_mark_bad(const int32_t* flagged, const uint32_t* n, uint8_t* rec_bad) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < *n) rec_bad[flagged[i]] = 1;
+}
+
+// RGB8 of every root sample (colorspace.py:27-56), rows of rgb_stride bytes.
+__global__ void k_dir_root_rgb(const __grid_constant__ rlfc_field f, uint8_t* out, int rgb_stride) {
+    const int quads = f.wp / 4;
+    const int64_t n = (int64_t)f.rsx * f.rsy * f.hp * quads;
+    const int64_t pl = (int64_t)f.hp * f.wp;
+    const int16_t* R16 = static_cast<const int16_t*>(f.roots);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int xq = (int)(i % quads);
+        const int64_t ry = i / quads;                  // root * hp + y
+        const int64_t r = ry / f.hp;
+        const int y = (int)(ry - r * f.hp);
+        uint8_t* o = out + ry * rgb_stride + xq * 12;
+        for (int j = 0; j < 4; ++j) {
+            int32_t v[3];
+            for (int c = 0; c < 3; ++c) v[c] = R16[(r * 3 + c) * pl + (int64_t)y * f.wp + xq * 4 + j];
+            uint32_t rr, gg, bb;
+            ycocg_to_rgb8(v[0], v[1], v[2], rr, gg, bb);
+            o[3 * j] = (uint8_t)rr;
+            o[3 * j + 1] = (uint8_t)gg;
+            o[3 * j + 2] = (uint8_t)bb;
+        }
+    }
+}
+
+// ---- decode step ----------------------------------------------------------------------
+struct Params {
+    int S, T, h, k, nlev, wb, hb, nchunks, R, rsx, rsy;
+    int by_lo, ncols;
+    int row_base[MAXL];
+    int D;                       // stages
+    int out_bytes, rgb_bytes, blob_cap, stage_bytes;
+    int off_tab, off_grp, grp_bytes, rescap, off_colofs, off_roots, roots_bytes, off_stage;
+    const uint8_t* blobs;
+    const uint32_t* blob_off;
+    const uint8_t* root_rgb;
+    const void* roots;
+    int rgb_stride, hp, wp;
+    uint64_t* status;
+    int shift;
+};
+
+struct StageInfo {
+    uint64_t ptr[MAXL];          // generic address of level (k + i)'s blob
+    int rslot;
+    int copied;                  // the blobs sit in the stage (else in HBM)
+};
+
+// Per consumer group scratch (one tile at a time).
+struct GroupScr {
+    uint32_t smask[MAXL * NR];   // record masks of the tile's node rows
+    uint16_t spst[MAXL * NR];    // residual slot of each record's first node
+    uint16_t list[MAXS * NB];    // dirty units (view | block << 8), view-major
+    int nunits;
+    uint32_t mc[MAXL];           // per level: payloads in plain-bit | trit mode (u16 each)
+    int slbase[MAXL + 1];        // first residual slot of each level; [MAXL] = total
+};
+
+constexpr int RESCAP_MAX = 1024;
+// group scratch | bad-pack bits [rescap / 32] | residual slots (16-byte aligned)
+constexpr int SRES_OFF = ((int)sizeof(GroupScr) + RESCAP_MAX / 8 + 15) & ~15;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+#ifdef RLFC_DIR_TIMING
+// per-tile %globaltimer stamps of the first 16 CTAs (debug build only,
+// tools/dir_timing.py): producer 0-2, consumer 3-8
+__device__ long long g_dtime[16 * 256 * 10];
+#define DSTAMP(q) do { if (blockIdx.x < 16 && ntile < 256) { long long tt; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)); g_dtime[(blockIdx.x * 256 + ntile) * 10 + (q)] = tt; } } while (0)
+#else
+#define DSTAMP(q) do { } while (0)
+#endif
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, int x, int y, int z, int w, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma5(void* dst, const CUtensorMap* map, int x, int y, int z, int w, int v,
+                                     uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(v), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// 16-byte asynchronous copy (zero-filled when src_bytes == 0)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+// arrive on b once this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// named barrier of one consumer group (ids 1..NG)
+__device__ __forceinline__ void gbar(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(GT) : "memory"); }
+
+__device__ __forceinline__ uint32_t pack4_sat(int32_t b0, int32_t b1, int32_t b2, int32_t b3) {
+    uint32_t hi, d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(hi) : "r"(b3), "r"(b2), "r"(0));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(b1), "r"(b0), "r"(hi));
+    return d;
+}
+
+// 64 bits at bit `pos` of the aligned words sw (generic: shared or global).
+__device__ __forceinline__ uint64_t win64(const uint32_t* sw, uint32_t pos) {
+    const uint32_t wi = pos >> 5, o = pos & 31u;
+    const uint32_t a = sw[wi], b = sw[wi + 1], c = sw[wi + 2];
+    return (uint64_t)__funnelshift_r(a, b, o) | (uint64_t)__funnelshift_r(b, c, o) << 32;
+}
+
+// kernels.py:128-159 for one 16-value payload of mode MODE whose bits start
+// at bit bit0 of the aligned words sw, dequantised by table
+// (kernels.py:202-211) into v.  Each BISE group (or plain-bit quad) is one
+// 64-bit window at its closed-form bit offset.  Returns true on a corrupt
+// pack (kernels.py:147-150).
+template <int MODE, typename DQ>
+__device__ __forceinline__ bool dec16(const uint32_t* sw, uint32_t bit0, uint32_t b, const uint16_t* dlut,
+                                      const DQ* dq, int32_t* v) {
+    const uint32_t lm = (1u << b) - 1u;
+    bool bad = false;
+    if (MODE == MODE_BITS) {
+        uint64_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = win64(sw, bit0 + 4u * (uint32_t)q * b);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[4 * q + i] = dq[(uint32_t)(w[q] >> ((uint32_t)i * b)) & lm];
+    } else {
+        constexpr int G = MODE == MODE_TRIT ? 5 : 3, PB = MODE == MODE_TRIT ? 8 : 7;
+        constexpr int NG_ = (16 + G - 1) / G;
+        constexpr uint32_t DB = MODE == MODE_TRIT ? 2u : 3u, DMASK = MODE == MODE_TRIT ? 3u : 7u;
+        constexpr uint32_t PMAX = MODE == MODE_TRIT ? 242u : 124u;
+        const uint32_t gbits = PB + G * b;
+        uint64_t w[NG_];
+#pragma unroll
+        for (int g = 0; g < NG_; ++g) w[g] = win64(sw, bit0 + (uint32_t)g * gbits);
+#pragma unroll
+        for (int g = 0; g < NG_; ++g) {
+            const uint32_t pk = (uint32_t)w[g] & ((1u << PB) - 1u);
+            bad |= pk > PMAX;
+            const uint32_t dg = dlut[pk <= PMAX ? pk : 0u];
+#pragma unroll
+            for (int i = 0; i < G && g * G + i < 16; ++i) {
+                const uint32_t low = (uint32_t)(w[g] >> (PB + (uint32_t)i * b)) & lm;
+                v[g * G + i] = dq[(((dg >> (DB * i)) & DMASK) << b) | low];
+            }
+        }
+    }
+    return bad;
+}
+
+// One payload (descriptor byte at p, validated at build time) added into acc.
+template <typename DQ>
+__device__ __forceinline__ bool add_payload(const uint8_t* p, const uint16_t* lut, const DQ* dq, int32_t* acc) {
+    const int d = p[0];
+    const uint8_t* q = p + 1;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(q) & ~uintptr_t(3));
+    const uint32_t bit0 = (uint32_t)(reinterpret_cast<uintptr_t>(q) & 3u) * 8u;
+    const int m = desc_mode(d);
+    const uint32_t b = (uint32_t)desc_bits(d);
+    int32_t v[16];
+    bool bad;
+    if (m == MODE_BITS) bad = dec16<MODE_BITS>(sw, bit0, b, lut, dq, v);
+    else if (m == MODE_TRIT) bad = dec16<MODE_TRIT>(sw, bit0, b, lut, dq, v);
+    else bad = dec16<MODE_QUINT>(sw, bit0, b, lut + 243, dq, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] += v[i];
+    return bad;
+}
+
+template <typename VT>
+__device__ __forceinline__ void store_res(uint8_t* dst, const int32_t* v) {
+    if (sizeof(VT) == 2) {
+        uint32_t u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) u[q] = ((uint32_t)v[2 * q] & 0xFFFFu) | ((uint32_t)v[2 * q + 1] << 16);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        d4[0] = make_uint4(u[0], u[1], u[2], u[3]);
+        d4[1] = make_uint4(u[4], u[5], u[6], u[7]);
+    } else {
+        int4* d4 = reinterpret_cast<int4*>(dst);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d4[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+}
+// four residuals (one pixel row of a payload) added into acc
+template <typename VT>
+__device__ __forceinline__ void add_res4(const uint8_t* src, int32_t* acc) {
+    if (sizeof(VT) == 2) {
+        const uint2 w = *reinterpret_cast<const uint2*>(src);
+        acc[0] += (int32_t)(int16_t)(w.x & 0xFFFFu);
+        acc[1] += (int32_t)w.x >> 16;
+        acc[2] += (int32_t)(int16_t)(w.y & 0xFFFFu);
+        acc[3] += (int32_t)w.y >> 16;
+    } else {
+        const int4 w = *reinterpret_cast<const int4*>(src);
+        acc[0] += w.x;
+        acc[1] += w.y;
+        acc[2] += w.z;
+        acc[3] += w.w;
+    }
+}
+template <typename VT>
+__device__ __forceinline__ void add_res(const uint8_t* src, int32_t* acc) {
+    if (sizeof(VT) == 2) {
+        const uint4* q4 = reinterpret_cast<const uint4*>(src);
+        const uint4 w0 = q4[0], w1 = q4[1];
+        const uint32_t ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            acc[2 * q] += (int32_t)(int16_t)(ww[q] & 0xFFFFu);
+            acc[2 * q + 1] += (int32_t)ww[q] >> 16;
+        }
+    } else {
+        const int4* q4 = reinterpret_cast<const int4*>(src);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int4 w = q4[q];
+            acc[4 * q] += w.x;
+            acc[4 * q + 1] += w.y;
+            acc[4 * q + 2] += w.z;
+            acc[4 * q + 3] += w.w;
+        }
+    }
+}
+
+// The decode step.  Warp 0 produces (TMA / bulk copies into a ring of D
+// stages); NG consumer groups of GW warps take the tiles round-robin, each
+// group one tile at a time:
+//   A  RGB(root) rows replicated into every view's rows of the output stage
+//      (the clean-pixel result); per level the record masks and payload
+//      ranks; the dirty (view, block) units, view-major;
+//   B1 every payload of the tile's blobs bucketed by BISE mode;
+//   B2 one payload per thread, warps of one mode: decode + dequantise into
+//      the group's shared residual slots (rank order);
+//   C  one dirty unit per thread: root block + chain residuals, YCoCg-R
+//      inverse, clamp, pack into the stage;
+//   then the group leader TMA-stores the stage (all S views of the tile).
+template <typename VT>
+__global__ void __launch_bounds__(NT, 1) k_field_dir(const __grid_constant__ Params P,
+                                                    const __grid_constant__ CUtensorMap out_map) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int S = P.S, T = P.T, h = P.h, k = P.nlev > 0 ? P.k : P.h, nlev = P.nlev, D = P.D;
+    constexpr int RB = 16 * (int)sizeof(VT);           // residual slot bytes
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + D;
+    uint64_t* rfull = empty + D;
+    uint64_t* rempty = rfull + 2;
+    VT* dq = reinterpret_cast<VT*>(smem + P.off_tab);
+    uint16_t* lut = reinterpret_cast<uint16_t*>(dq + 2048);
+    uint32_t* colofs = reinterpret_cast<uint32_t*>(smem + P.off_colofs);
+    uint8_t* roots = smem + P.off_roots;
+    uint8_t* stages = smem + P.off_stage;
+    const int rowbytes = TW * 3;
+    const int rescap = P.rescap;
+
+    if (tid == 0) {
+        for (int i = 0; i < D; ++i) {
+            mbar_init(full + i, 33);          // 32 producer lanes' copies + the info write
+            mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(rfull + i, 32);
+            mbar_init(rempty + i, NG);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int z = tid; z < 2048; z += NT) dq[z] = (VT)dequant((uint32_t)z, P.shift);
+    for (int i = tid; i < 243 + 125; i += NT) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
+    __syncthreads();
+
+    if (tid < 32) {
+        // ---------------- producer warp ----------------
+        // Loads are 16-byte cp.async copies spread over the warp's lanes (the
+        // TMA unit is left to the output stores); each lane's copies arrive
+        // on the stage's barrier when they land (cp.async.mbarrier.arrive).
+        int ntile = 0, nseg = 0;
+        const int rgb_row = P.rgb_stride;
+        for (int col = blockIdx.x; col < P.ncols; col += gridDim.x) {
+            const int by = P.by_lo + col / P.nchunks, chunk = col % P.nchunks;
+            const int64_t gcol = (int64_t)by * P.nchunks + chunk;
+            __syncwarp();
+            for (int j = lane; j <= P.R; j += 32) colofs[j] = __ldg(P.blob_off + gcol * P.R + j);
+            __syncwarp();
+            int cur_ry = -1, rslot = 0;
+            for (int t = 0; t < T; ++t) {
+                const int ry = t >> h;
+                if (nlev > 0 && ry != cur_ry) {
+                    // raw roots of this root row: [rx][c][row][TW] int16
+                    rslot = nseg & 1;
+                    mbar_wait(rempty + rslot, ((nseg >> 1) & 1) ^ 1u);
+                    uint8_t* rdst = roots + rslot * P.roots_bytes;
+                    constexpr int RQ = TW * 2 / 16;                       // 16-byte pieces per root row
+                    const int nq = P.rsx * 3 * B * RQ;
+                    for (int i = lane; i < nq; i += 32) {
+                        const int q = i % RQ, row = (i / RQ) % B, rc = i / (RQ * B);   // rc = rx * 3 + c
+                        const int rx = rc / 3, c = rc - rx * 3;
+                        const int x = chunk * TW + q * 8;
+                        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.roots) +
+                                             ((((int64_t)rx * P.rsy + ry) * 3 + c) * P.hp + by * B + row) * (int64_t)P.wp * 2 +
+                                             (int64_t)x * 2;
+                        cp_async16(rdst + i * 16, src, x < P.wp ? 16 : 0);
+                    }
+                    cp_async_arrive(rfull + rslot);
+                    cur_ry = ry;
+                    ++nseg;
+                }
+                const int st = ntile % D;
+                if (lane == 0) DSTAMP(0);
+                mbar_wait(empty + st, ((ntile / D) & 1) ^ 1u);
+                if (lane == 0) DSTAMP(1);
+                uint8_t* sbase = stages + st * P.stage_bytes;
+                uint8_t* rgbdst = sbase + P.out_bytes;
+                uint8_t* bdst = rgbdst + P.rgb_bytes;
+                StageInfo* info = reinterpret_cast<StageInfo*>(bdst + P.blob_cap);
+                uint32_t total = 0;
+                for (int li = 0; li < nlev; ++li) {
+                    const int row = P.row_base[k + li] + (t >> (k + li));
+                    total += (colofs[row + 1] - colofs[row]) * 16u;
+                }
+                const bool copy = total <= (uint32_t)P.blob_cap;
+                if (lane == 0) {
+                    uint32_t pos = 0;
+                    for (int li = 0; li < nlev; ++li) {
+                        const int row = P.row_base[k + li] + (t >> (k + li));
+                        info->ptr[li] = copy ? reinterpret_cast<uint64_t>(bdst + pos)
+                                             : reinterpret_cast<uint64_t>(P.blobs + (uint64_t)colofs[row] * 16u);
+                        pos += (colofs[row + 1] - colofs[row]) * 16u;
+                    }
+                    info->rslot = rslot;
+                    info->copied = copy;
+                }
+                // RGB(root) rows of the tile: [rx][row][TW * 3]
+                {
+                    constexpr int GQ = TW * 3 / 16;
+                    const int nq = P.rsx * B * GQ;
+                    for (int i = lane; i < nq; i += 32) {
+                        const int q = i % GQ, row = (i / GQ) % B, rx = i / (GQ * B);
+                        const int xb = chunk * TW * 3 + q * 16;
+                        const uint8_t* src = P.root_rgb + (((int64_t)rx * P.rsy + ry) * P.hp + by * B + row) * rgb_row + xb;
+                        cp_async16(rgbdst + i * 16, src, xb < rgb_row ? 16 : 0);
+                    }
+                }
+                if (copy) {
+                    uint32_t pos = 0;
+                    for (int li = 0; li < nlev; ++li) {
+                        const int row = P.row_base[k + li] + (t >> (k + li));
+                        const uint32_t nq = colofs[row + 1] - colofs[row];
+                        const uint8_t* src = P.blobs + (uint64_t)colofs[row] * 16u;
+                        for (uint32_t i = lane; i < nq; i += 32) cp_async16(bdst + pos + i * 16, src + i * 16, 16);
+                        pos += nq * 16u;
+                    }
+                }
+                __syncwarp();
+                cp_async_arrive(full + st);
+                if (lane == 0) mbar_arrive(full + st);       // info written
+                if (lane == 0) DSTAMP(2);
+                ++ntile;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer groups ----------------
+    const int g = (tid - 32) / GT, gt = (tid - 32) % GT, gw = gt >> 5;
+    GroupScr& sc = *reinterpret_cast<GroupScr*>(smem + P.off_grp + g * P.grp_bytes);
+    uint32_t* sbad = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(&sc) + sizeof(GroupScr));
+    uint8_t* sres = reinterpret_cast<uint8_t*>(&sc) + SRES_OFF;
+    uint64_t pol = 0;
+    if (gt == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const uint32_t smask_s = S >= 32 ? 0xFFFFFFFFu : (1u << S) - 1u;
+    const int nsegc = nlev > 0 ? ((T - 1) >> h) + 1 : 0;     // root-row segments per column
+    int prev_st = -1, waited_seg = -1, arrived_seg = -1;
+    // this group's tiles: n = g, g + NG, ... of the CTA's tile sequence
+    // (columns blockIdx.x + i * gridDim.x, camera rows t)
+    for (int n = g;; n += NG) {
+        const int ci = n / T, t = n - ci * T;
+        const int col = blockIdx.x + ci * gridDim.x;
+        if (col >= P.ncols) break;
+        const int by = P.by_lo + col / P.nchunks, chunk = col % P.nchunks;
+        const int ry = t >> h;
+        const int seg = ci * nsegc + ry;
+        const int st = n % D;
+        const int ntile = n;
+        if (nlev > 0) {
+            // segments this group has passed: its share of releasing them
+            if (gt == 0)
+                for (; arrived_seg + 1 < seg; ++arrived_seg) mbar_arrive(rempty + ((arrived_seg + 1) & 1));
+            if (waited_seg != seg) {
+                mbar_wait(rfull + (seg & 1), (seg >> 1) & 1);
+                waited_seg = seg;
+            }
+        }
+        if (gt == 0) DSTAMP(3);
+        mbar_wait(full + st, (n / D) & 1);
+        if (gt == 0) {
+            DSTAMP(4);
+            // the previous tile's store has long been issued: once it has
+            // read its stage, hand the stage back to the producer
+            if (prev_st >= 0) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                mbar_arrive(empty + prev_st);
+            }
+        }
+        uint8_t* sbase = stages + st * P.stage_bytes;
+        const uint8_t* rgbrows = sbase + P.out_bytes;
+        const StageInfo* info = reinterpret_cast<const StageInfo*>(sbase + P.out_bytes + P.rgb_bytes + P.blob_cap);
+        // ---- A: clean pixels (RGB(root) rows -> every view's rows)
+        {
+            constexpr int Q = B * TW * 3 / 16;            // 16-byte quads per view
+            const uint4* src = reinterpret_cast<const uint4*>(rgbrows);
+            uint4* dst = reinterpret_cast<uint4*>(sbase);
+            for (int i = gt; i < S * Q; i += GT) {
+                const int s = i / Q, q = i - s * Q;
+                dst[i] = src[(s >> h) * Q + q];
+            }
+        }
+#ifdef RLFC_DIR_SKIP
+        if (false) {
+#else
+        if (nlev > 0) {
+#endif
+            if (gw < GW - 1) {
+                // per level: record masks, absolute residual slot of each
+                // record's first node, payload counts per BISE mode
+                for (int li = gw; li < nlev; li += GW - 1) {
+                    const uint8_t* bp = reinterpret_cast<const uint8_t*>(info->ptr[li]);
+                    uint32_t base = 0;
+                    for (int l2 = 0; l2 < li; ++l2) base += *reinterpret_cast<const uint32_t*>(info->ptr[l2]);
+                    const uint32_t* mk = reinterpret_cast<const uint32_t*>(bp) + 4;
+                    const int r1 = lane + 32;
+                    const uint32_t m0 = mk[lane], m1 = r1 < NR ? mk[r1] : 0u;
+                    const uint32_t p0 = __popc(m0), p1 = __popc(m1);
+                    uint32_t i0 = p0, i1 = p1;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y0 = __shfl_up_sync(0xffffffffu, i0, o);
+                        const uint32_t y1 = __shfl_up_sync(0xffffffffu, i1, o);
+                        if (lane >= o) {
+                            i0 += y0;
+                            i1 += y1;
+                        }
+                    }
+                    const uint32_t tot0 = __shfl_sync(0xffffffffu, i0, 31);
+                    sc.smask[li * NR + lane] = m0;
+                    sc.spst[li * NR + lane] = (uint16_t)(base + i0 - p0);
+                    if (r1 < NR) {
+                        sc.smask[li * NR + r1] = m1;
+                        sc.spst[li * NR + r1] = (uint16_t)(base + tot0 + i1 - p1);
+                    }
+                    if (lane == 0) {
+                        sc.mc[li] = *reinterpret_cast<const uint32_t*>(bp + 4);      // u16 bits | u16 trits
+                        sc.slbase[li] = (int)base;
+                    }
+                }
+                for (int i = gt; i < rescap / 32; i += (GW - 1) * 32) sbad[i] = 0u;
+            } else {
+                uint32_t dirty = 0;
+                if (lane < NB) {
+                    for (int li = 0; li < nlev; ++li) {
+                        const int l = k + li;
+                        const uint32_t* mk = reinterpret_cast<const uint32_t*>(info->ptr[li]) + 4;
+                        uint32_t m = mk[lane] | mk[NB + lane] | mk[2 * NB + lane];
+                        if (l == 0) {
+                            dirty |= m;
+                        } else {
+                            const int w = 1 << l;
+                            const uint32_t span = w >= 32 ? 0xFFFFFFFFu : (1u << w) - 1u;
+                            for (; m; m &= m - 1u) {
+                                const int sh = (__ffs(m) - 1) << l;
+                                if (sh < 32) dirty |= span << sh;
+                            }
+                        }
+                    }
+                    dirty &= smask_s;
+                }
+                // view-major unit order: consecutive units are different
+                // blocks of one view, so their stage stores spread over the
+                // shared-memory banks
+                const uint32_t below = (1u << lane) - 1u;
+                uint32_t nu = 0;
+                for (int s = 0; s < S; ++s) {
+                    const uint32_t bal = __ballot_sync(0xffffffffu, (dirty >> s) & 1u);
+                    if ((dirty >> s) & 1u) sc.list[nu + __popc(bal & below)] = (uint16_t)(s | lane << 8);
+                    nu += __popc(bal);
+                }
+                uint32_t nt = 0;
+                for (int li = 0; li < nlev; ++li) nt += *reinterpret_cast<const uint32_t*>(info->ptr[li]);
+                if (lane == 0) {
+                    sc.nunits = (int)nu;
+                    sc.slbase[MAXL] = (int)nt;
+                }
+            }
+            gbar(g);
+            if (gt == 0) DSTAMP(5);
+            // ---- B: every payload of the tile's blobs (each is needed by
+            // this tile: level l node x serves views x*2^l .. x*2^l + 2^l - 1
+            // of camera row t) decoded once into the group's residual slots
+            // (rank order), one payload per thread; tasks run level by level
+            // in BISE-mode order (rot[]), so a warp runs one mode's code
+            const int ntask = sc.slbase[MAXL];
+            for (int i = gt; i < ntask; i += GT) {
+                int li = 0;
+                while (li + 1 < nlev && i >= sc.slbase[li + 1]) ++li;
+                const int q = i - sc.slbase[li];
+                const uint8_t* bp = reinterpret_cast<const uint8_t*>(info->ptr[li]);
+                const uint32_t nl = *reinterpret_cast<const uint32_t*>(bp);
+                const uint16_t* offs = reinterpret_cast<const uint16_t*>(bp + HDR0);
+                const uint32_t j = offs[nl + q];                      // rot[q]
+                const int slot = sc.slbase[li] + (int)j;
+                if (slot >= rescap) continue;
+                const uint32_t mc = sc.mc[li];
+                const int mode = (uint32_t)q < (mc & 0xFFFFu) ? MODE_BITS
+                                 : (uint32_t)q < (mc & 0xFFFFu) + (mc >> 16) ? MODE_TRIT : MODE_QUINT;
+                const uint8_t* p = bp + offs[j];
+                const uint32_t bb = (uint32_t)desc_bits(p[0]);
+                const uint8_t* pq = p + 1;
+                const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(pq) & ~uintptr_t(3));
+                const uint32_t bit0 = (uint32_t)(reinterpret_cast<uintptr_t>(pq) & 3u) * 8u;
+                int32_t v[16];
+                bool bad;
+                if (mode == MODE_BITS) bad = dec16<MODE_BITS>(sw, bit0, bb, lut, dq, v);
+                else if (mode == MODE_TRIT) bad = dec16<MODE_TRIT>(sw, bit0, bb, lut, dq, v);
+                else bad = dec16<MODE_QUINT>(sw, bit0, bb, lut + 243, dq, v);
+                if (bad) atomicOr(sbad + (slot >> 5), 1u << (slot & 31));
+                store_res<VT>(sres + slot * RB, v);
+            }
+            gbar(g);
+            if (gt == 0) DSTAMP(6);
+            // ---- C: dirty units, pixel row by pixel row: root samples +
+            // chain residuals, YCoCg-R inverse, clamp, pack over the stage
+            const int units = sc.nunits;
+            const int16_t* rt = reinterpret_cast<const int16_t*>(roots + info->rslot * P.roots_bytes);
+            for (int u = gt; u < units; u += GT) {
+                const uint32_t e = sc.list[u];
+                const int s = (int)(e & 255u), b = (int)(e >> 8);
+                const int rx = s >> h;
+                // chain presence of the unit: bit 3 * li + c
+                uint32_t pres = 0;
+                for (int li = 0; li < nlev; ++li) {
+                    const int x = s >> (k + li);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) pres |= ((sc.smask[li * NR + c * NB + b] >> x) & 1u) << (3 * li + c);
+                }
+                uint32_t badc = 0;
+                uint8_t* o = sbase + s * (B * rowbytes) + b * 12;
+#pragma unroll 1
+                for (int row = 0; row < 4; ++row) {
+                    int32_t v[3][4];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const uint2 w = *reinterpret_cast<const uint2*>(rt + ((rx * 3 + c) * B + row) * TW + b * 4);
+                        v[c][0] = (int32_t)(int16_t)(w.x & 0xFFFFu);
+                        v[c][1] = (int32_t)w.x >> 16;
+                        v[c][2] = (int32_t)(int16_t)(w.y & 0xFFFFu);
+                        v[c][3] = (int32_t)w.y >> 16;
+                        for (uint32_t pc = pres & (0x249249u << c); pc; pc &= pc - 1u) {
+                            const int li = (__ffs(pc) - 1) / 3;
+                            const int r = li * NR + c * NB + b;
+                            const uint32_t m = sc.smask[r];
+                            const int slot = sc.spst[r] + __popc(m & ((1u << (s >> (k + li))) - 1u));
+                            if (slot < rescap) {
+                                if (row == 0 && ((sbad[slot >> 5] >> (slot & 31)) & 1u)) badc |= 1u << c;
+                                add_res4<VT>(sres + slot * RB + row * 4 * (int)sizeof(VT), v[c]);
+                            } else {
+                                // beyond the group's residual slots (dense
+                                // tiles): decode straight from the blob
+                                const uint8_t* bp = reinterpret_cast<const uint8_t*>(info->ptr[li]);
+                                const uint32_t off = reinterpret_cast<const uint16_t*>(bp + HDR0)[slot - sc.slbase[li]];
+                                int32_t full16[16];
+#pragma unroll
+                                for (int q = 0; q < 16; ++q) full16[q] = 0;
+                                if (add_payload(bp + off, lut, dq, full16) && row == 0) badc |= 1u << c;
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    v[c][q] += row == 0 ? full16[q] : row == 1 ? full16[4 + q] : row == 2 ? full16[8 + q] : full16[12 + q];
+                            }
+                        }
+                    }
+                    int32_t r8[12];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int32_t tt = v[0][i] - (v[2][i] >> 1);
+                        const int32_t bb = tt - (v[1][i] >> 1);
+                        r8[3 * i] = bb + v[1][i];
+                        r8[3 * i + 1] = v[2][i] + tt;
+                        r8[3 * i + 2] = bb;
+                    }
+                    uint32_t* o32 = reinterpret_cast<uint32_t*>(o + row * rowbytes);
+                    o32[0] = pack4_sat(r8[0], r8[1], r8[2], r8[3]);
+                    o32[1] = pack4_sat(r8[4], r8[5], r8[6], r8[7]);
+                    o32[2] = pack4_sat(r8[8], r8[9], r8[10], r8[11]);
+                }
+                if (badc) {
+                    const int c = __ffs(badc) - 1;
+                    const int64_t img = (int64_t)s * T + t;
+                    report(P.status, (((uint64_t)img * 3 + c) * P.hb + by) * P.wb + chunk * NB + b, 1);
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        gbar(g);
+        if (gt == 0) {
+            DSTAMP(7);
+            asm volatile(
+                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], "
+                "%6;" ::"l"(&out_map),
+                "r"(chunk * rowbytes), "r"((by - P.by_lo) * B), "r"(t), "r"(0), "r"(smem_u32(sbase)), "l"(pol)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            DSTAMP(8);
+        }
+        prev_st = st;
+    }
+    if (gt == 0) {
+        // release the remaining root segments of this CTA's columns
+        if (nlev > 0) {
+            const int ncol_cta = (P.ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+            for (; arrived_seg + 1 < ncol_cta * nsegc; ++arrived_seg) mbar_arrive(rempty + ((arrived_seg + 1) & 1));
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
+// Units touching a record with a stream anomaly: the reference-order walk
+// (kernels.py:162-216, decode_chain_core) for all three channels of every
+// view's block, written over the blend's output, failures keyed as the
+// reference meets them.
+__global__ void k_fixup(const __grid_constant__ rlfc_field f, const int32_t* flagged, int k, int by_lo, int by_hi,
+                        uint8_t* rgb, int64_t img_stride, int64_t row_stride, uint64_t* status) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t ri = flagged[blockIdx.x];
+    const int64_t blk = ri % nblk;
+    const int by = (int)(blk / f.wb), bx = (int)(blk % f.wb);
+    if (by < by_lo || by >= by_hi) return;
+    const int v = blockIdx.y * blockDim.x + threadIdx.x;
+    if (v >= f.s_count * f.t_count) return;
+    const int s = v / f.t_count, t = v % f.t_count;
+    int32_t acc[3][16];
+    for (int c = 0; c < 3; ++c) {
+        for (int yy = 0; yy < B; ++yy)
+            for (int xx = 0; xx < B; ++xx) acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+        const uint64_t off = f.offsets[c][blk];
+        int st = walk_chain<16>(f, f.srv[c] + off, s, t, k, acc[c], g_lut, g_nb16, srv_avail(f, c, off));
+        if (st == WALK_OOB) st = 2;
+        if (st) {
+            report(status, ((((uint64_t)v) * 3 + c) * f.hb + by) * f.wb + bx, st);
+            return;
+        }
+    }
+    for (int yy = 0; yy < B; ++yy) {
+        const int y = by * B + yy;
+        if (y >= f.height) break;
+        uint8_t* orow = rgb + (int64_t)v * img_stride + (int64_t)(y - by_lo * B) * row_stride;
+        for (int xx = 0; xx < B; ++xx) {
+            const int x = bx * B + xx;
+            if (x >= f.width) break;
+            uint32_t r, g, b;
+            ycocg_to_rgb8(acc[0][yy * B + xx], acc[1][yy * B + xx], acc[2][yy * B + xx], r, g, b);
+            orow[3 * x] = (uint8_t)r;
+            orow[3 * x + 1] = (uint8_t)g;
+            orow[3 * x + 2] = (uint8_t)b;
+        }
+    }
+}
+
+// ---- host helpers ---------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+static bool encode_map(CUtensorMap* map, CUtensorMapDataType dt, cuuint32_t rank, void* base, const cuuint64_t* dims,
+                       const cuuint64_t* strides, const cuuint32_t* box) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
+    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
+    return enc(map, dt, rank, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static Geo geo_of(const rlfc_field& f) {
+    Geo g{};
+    g.h = f.tree_height;
+    g.wb = f.wb;
+    g.hb = f.hb;
+    g.nchunks = (f.wb + NB - 1) / NB;
+    g.nblk = f.wb * f.hb;
+    int r = 0;
+    for (int l = 0; l < MAXL; ++l) {
+        g.row_base[l] = r;
+        if (l < f.tree_height) r += f.level_sy[l];
+    }
+    g.R = r;
+    return g;
+}
+
+static bool in_envelope(const rlfc_field& f) {
+    if (f.block != B || f.tree_height < 1 || f.tree_height > MAXL) return false;
+    if (f.s_count > MAXS || !f.roots_i16) return false;
+    if (f.quant_shift < 0 || f.quant_shift > 20) return false;
+    if ((f.wp * 2) % 16 != 0) return false;                       // raw root rows for TMA
+    if ((int64_t)f.wb * f.hb * 3 >= (1ll << 31)) return false;
+    return true;
+}
+
+// scratch layout: cnt u32[R*nrec] | byt u32[R*nrec] | blob_n u32[nblob] |
+// blob_sz u32[nblob+1] | rec_bad u8[nrec] | counters u32[4] | cub temp
+struct Scratch {
+    uint32_t *cnt, *byt, *blob_n, *blob_sz, *ctr;
+    uint8_t* rec_bad;
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+static uint64_t al256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+static uint64_t carve(const rlfc_field& f, void* base, Scratch* sc) {
+    const Geo g = geo_of(f);
+    const uint64_t nrec = 3ull * g.nblk, nblob = (uint64_t)g.hb * g.nchunks * g.R;
+    size_t cub_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int)(nblob + 1));
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        const uint64_t o = off;
+        off = al256(off + bytes);
+        return o;
+    };
+    const uint64_t o_cnt = take(4ull * g.R * nrec), o_byt = take(4ull * g.R * nrec), o_bn = take(4 * nblob),
+                   o_bs = take(4 * (nblob + 1)), o_bad = take(nrec), o_ctr = take(16), o_cub = take(cub_bytes);
+    if (sc) {
+        uint8_t* b = static_cast<uint8_t*>(base);
+        sc->cnt = reinterpret_cast<uint32_t*>(b + o_cnt);
+        sc->byt = reinterpret_cast<uint32_t*>(b + o_byt);
+        sc->blob_n = reinterpret_cast<uint32_t*>(b + o_bn);
+        sc->blob_sz = reinterpret_cast<uint32_t*>(b + o_bs);
+        sc->rec_bad = b + o_bad;
+        sc->ctr = reinterpret_cast<uint32_t*>(b + o_ctr);
+        sc->cub_tmp = b + o_cub;
+        sc->cub_bytes = cub_bytes;
+    }
+    return off;
+}
+
+}  // namespace dir
+}  // namespace rlfc
+
+using namespace rlfc;
+
+#ifdef RLFC_DIR_TIMING
+extern "C" int rlfc_dir_debug_times(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, dir::g_dtime, sizeof(dir::g_dtime)) == cudaSuccess ? 0 : 4;
+}
+#endif
+
+extern "C" int rlfc_dir_plan(const rlfc_field* f, rlfc_dir* d) {
+    if (!f || !d) return RLFC_ERR_ARGUMENT;
+    memset(d, 0, sizeof(*d));
+    if (!dir::in_envelope(*f)) return RLFC_ERR_ARGUMENT;
+    const dir::Geo g = dir::geo_of(*f);
+    d->tw = dir::TW;
+    d->nb = dir::NB;
+    d->nchunks = g.nchunks;
+    d->rows = g.R;
+    d->n_blobs = (int64_t)g.hb * g.nchunks * g.R;
+    d->nrec = 3ll * g.nblk;
+    d->scratch_bytes = dir::carve(*f, nullptr, nullptr);
+    d->rgb_stride = (f->wp * 3 + 15) & ~15;
+    d->root_rgb_bytes = (uint64_t)f->rsx * f->rsy * f->hp * (uint64_t)d->rgb_stride;
+    return RLFC_OK;
+}
+
+extern "C" int rlfc_dir_size(const rlfc_field* f, rlfc_dir* d, void* stream) {
+    if (!f || !d || !d->scratch || !d->blob_off || !d->flagged) return RLFC_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const dir::Geo g = dir::geo_of(*f);
+    dir::Scratch sc;
+    dir::carve(*f, d->scratch, &sc);
+    const int64_t nrec = d->nrec, nblob = d->n_blobs;
+    cudaMemsetAsync(sc.cnt, 0, 4ull * g.R * nrec, s);
+    cudaMemsetAsync(sc.byt, 0, 4ull * g.R * nrec, s);
+    cudaMemsetAsync(sc.ctr, 0, 16, s);
+    cudaMemsetAsync(sc.rec_bad, 0, nrec, s);
+    if (nrec) {
+        dir::k_dir_count<<<(unsigned)((nrec + 127) / 128), 128, 0, s>>>(*f, g, sc.cnt, sc.byt, d->flagged, sc.ctr);
+        dir::k_mark_bad<<<(unsigned)((nrec + 255) / 256), 256, 0, s>>>(d->flagged, sc.ctr, sc.rec_bad);
+    }
+    dir::k_dir_blob<<<(unsigned)((nblob + 1 + 255) / 256), 256, 0, s>>>(g, sc.cnt, sc.byt, sc.blob_n, sc.blob_sz,
+                                                                       sc.ctr + 1);
+    size_t cb = sc.cub_bytes;
+    if (cub::DeviceScan::ExclusiveSum(sc.cub_tmp, cb, sc.blob_sz, d->blob_off, (int)(nblob + 1), s) != cudaSuccess)
+        return RLFC_ERR_CUDA;
+    uint32_t host[2] = {0, 0}, total = 0;
+    cudaMemcpyAsync(host, sc.ctr, 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&total, d->blob_off + nblob, 4, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return RLFC_ERR_CUDA;
+    d->n_flagged = (int32_t)host[0];
+    d->blob_bytes = (uint64_t)total * 16u;
+    return host[1] ? RLFC_ERR_ARGUMENT : RLFC_OK;       // a blob over 64 KiB: outside the envelope
+}
+
+extern "C" int rlfc_dir_build(const rlfc_field* f, rlfc_dir* d, void* stream) {
+    if (!f || !d || !d->scratch || !d->blob_off || !d->blobs || !d->root_rgb) return RLFC_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const dir::Geo g = dir::geo_of(*f);
+    dir::Scratch sc;
+    dir::carve(*f, d->scratch, &sc);
+    const int64_t nrec = d->nrec, nblob = d->n_blobs;
+    cudaMemsetAsync(d->blobs, 0, d->blob_bytes + 64, s);
+    if (nrec)
+        dir::k_dir_fill<<<(unsigned)((nrec + 127) / 128), 128, 0, s>>>(*f, g, sc.cnt, sc.byt, sc.blob_n, d->blob_off,
+                                                                       d->blobs, sc.rec_bad);
+    if (nblob)
+        dir::k_dir_hdr<<<(unsigned)((nblob + 255) / 256), 256, 0, s>>>(nblob, sc.blob_n, d->blob_off, d->blobs);
+    dir::k_dir_root_rgb<<<1184, 256, 0, s>>>(*f, d->root_rgb, d->rgb_stride);
+    return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
+extern "C" int rlfc_decode_field_dir(const rlfc_field* f, const rlfc_dir* d, int32_t stop_level, int32_t by_lo,
+                                     int32_t by_hi, uint8_t* rgb, int64_t img_stride, int64_t row_stride,
+                                     uint64_t* status, void* stream) {
+    using namespace dir;
+    if (!f || !d || !rgb || !status || !d->blobs || !d->blob_off || !d->root_rgb) return RLFC_ERR_ARGUMENT;
+    if (!in_envelope(*f)) return RLFC_ERR_ARGUMENT;
+    if (stop_level < 0 || stop_level > f->tree_height || by_lo < 0 || by_hi > f->hb || by_lo > by_hi)
+        return RLFC_ERR_ARGUMENT;
+    if (by_lo == by_hi) return RLFC_OK;
+    if (((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride) & 15) != 0)
+        return RLFC_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const Geo g = geo_of(*f);
+    Params P{};
+    P.S = f->s_count;
+    P.T = f->t_count;
+    P.h = f->tree_height;
+    P.k = stop_level;
+    P.nlev = f->tree_height - stop_level;
+    P.wb = f->wb;
+    P.hb = f->hb;
+    P.nchunks = g.nchunks;
+    P.R = g.R;
+    P.rsx = f->rsx;
+    P.rsy = f->rsy;
+    P.by_lo = by_lo;
+    P.ncols = (by_hi - by_lo) * g.nchunks;
+    for (int l = 0; l < MAXL; ++l) P.row_base[l] = g.row_base[l];
+    P.blobs = d->blobs;
+    P.blob_off = d->blob_off;
+    P.root_rgb = d->root_rgb;
+    P.roots = f->roots;
+    P.rgb_stride = d->rgb_stride;
+    P.hp = f->hp;
+    P.wp = f->wp;
+    P.status = status;
+    P.shift = f->quant_shift;
+    // shared memory plan (one CTA per SM)
+    const bool r16 = f->quant_shift <= 4;                  // |residual| <= 16392 fits int16
+    const int vt = r16 ? 2 : 4;
+    auto al = [](int x) { return (x + 127) & ~127; };
+    int off = al(8 * (2 * 32 + 4));                          // barriers (<= 32 stages)
+    P.off_tab = off;
+    off = al(off + 2048 * vt + 368 * 2);
+    P.off_colofs = off;
+    off = al(off + 4 * (g.R + 1));
+    P.off_roots = off;
+    P.roots_bytes = f->rsx * 3 * B * TW * 2;
+    off = al(off + 2 * P.roots_bytes);
+    P.out_bytes = f->s_count * B * TW * 3;
+    P.rgb_bytes = f->rsx * B * TW * 3;
+    P.blob_cap = 3072;
+    P.stage_bytes = al(P.out_bytes + P.rgb_bytes + P.blob_cap + (int)sizeof(StageInfo));
+    static int smem_max = 0, sms = 0;
+    if (!smem_max) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // stages first (2 per group, at least one more than the groups), the rest
+    // to the groups' residual slots
+    const int fixed_grp = SRES_OFF;
+    int rescap = 0;
+    for (P.D = NG + 3; P.D > NG; --P.D) {
+        const int left = smem_max - off - P.D * P.stage_bytes;
+        rescap = left > 0 ? ((left / NG - fixed_grp) / (16 * vt)) & ~31 : 0;
+        if (rescap >= 256) break;
+    }
+    if (rescap > RESCAP_MAX) rescap = RESCAP_MAX;
+    if (rescap < 64) return RLFC_ERR_ARGUMENT;
+    P.rescap = rescap;
+    P.grp_bytes = al(fixed_grp + rescap * 16 * vt);
+    P.off_grp = off;
+    off = al(off + NG * P.grp_bytes);
+    P.off_stage = off;
+    const int smem = off + P.D * P.stage_bytes;
+    if (smem > smem_max) return RLFC_ERR_ARGUMENT;
+    // tensor maps: output (x bytes, rows of the band, t, s), RGB(root) rows,
+    // raw root planes
+    const int nrows = min(by_hi * B, f->height) - by_lo * B;
+    CUtensorMap out_map;
+    memset(&out_map, 0, sizeof(out_map));
+    {
+        const cuuint64_t dims[4] = {(cuuint64_t)f->width * 3, (cuuint64_t)nrows, (cuuint64_t)f->t_count,
+                                    (cuuint64_t)f->s_count};
+        const cuuint64_t strides[3] = {(cuuint64_t)row_stride, (cuuint64_t)img_stride,
+                                       (cuuint64_t)img_stride * f->t_count};
+        const cuuint32_t box[4] = {(cuuint32_t)(TW * 3), (cuuint32_t)B, 1u, (cuuint32_t)f->s_count};
+        if (!encode_map(&out_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, rgb, dims, strides, box)) return RLFC_ERR_ARGUMENT;
+    }
+    auto kern = r16 ? k_field_dir<int16_t> : k_field_dir<int32_t>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int grid = min(P.ncols, sms);
+    kern<<<grid, NT, smem, s>>>(P, out_map);
+    if (d->n_flagged > 0 && d->flagged) {
+        const int nv = f->s_count * f->t_count;
+        k_fixup<<<dim3((unsigned)d->n_flagged, (unsigned)((nv + 127) / 128)), 128, 0, s>>>(
+            *f, d->flagged, stop_level, by_lo, by_hi, rgb, img_stride, row_stride, status);
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "rlfc_b200: directory decode launch error: %s\n", cudaGetErrorString(e));
+        return RLFC_ERR_CUDA;
+    }
+    return RLFC_OK;
+}

@@ -18,6 +18,7 @@ functions raise `_native.NativeUnavailable`.
 
 import ctypes
 import threading
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -89,9 +90,62 @@ class DeviceField:
         self.cfield = f
         self.ref = ctypes.byref(f)
         self._ws_lock = threading.Lock()
+        # the staged path's workspace is shared by every caller enqueueing on
+        # the same CUDA stream: its whole launch sequence is enqueued under
+        # this lock so two threads' sequences never interleave
+        self.enqueue_lock = threading.Lock()
         self._ws = {}
         self._ws_bytes = 0
         self._present = None
+        self._dir = None
+
+    def directory(self):
+        """The device record directory (rlfc_b200.h rlfc_dir: tile-major
+        payload blobs, blob offsets, root colours, anomaly list), built on
+        the GPU on first use; None outside its envelope."""
+        torch = _torch()
+        with self._ws_lock:
+            if self._dir is not None:
+                return self._dir or None
+            L = _native.lib()
+            d = _native.RlfcDir()
+            if L.rlfc_dir_plan(self.ref, ctypes.byref(d)) != _native.RLFC_OK:
+                self._dir = False
+                return None
+            t0 = time.perf_counter()
+            dev = self.device
+            with torch.cuda.device(dev):
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                scratch = torch.empty(d.scratch_bytes, dtype=torch.uint8,
+                                      device=dev)
+                blob_off = torch.empty(d.n_blobs + 1, dtype=torch.int32,
+                                       device=dev)
+                flagged = torch.empty(max(1, d.nrec), dtype=torch.int32,
+                                      device=dev)
+                root_rgb = torch.empty(max(16, d.root_rgb_bytes),
+                                       dtype=torch.uint8, device=dev)
+                d.scratch = scratch.data_ptr()
+                d.blob_off = blob_off.data_ptr()
+                d.flagged = flagged.data_ptr()
+                d.root_rgb = root_rgb.data_ptr()
+                rc = L.rlfc_dir_size(self.ref, ctypes.byref(d), _stream())
+                if rc == _native.RLFC_ERR_ARGUMENT:
+                    self._dir = False
+                    return None
+                _native.check(rc, "rlfc_dir_size")
+                blobs = torch.empty(d.blob_bytes + 64, dtype=torch.uint8,
+                                    device=dev)
+                d.blobs = blobs.data_ptr()
+                _native.check(L.rlfc_dir_build(self.ref, ctypes.byref(d),
+                                               _stream()), "rlfc_dir_build")
+                torch.cuda.synchronize(dev)
+                build_ms = (time.perf_counter() - t0) * 1e3
+            d.scratch = None
+            del scratch
+            self._dir = Directory(d, blobs, blob_off, flagged, root_rgb,
+                                  build_ms)
+            return self._dir
 
     def staged_workspace(self, stream_handle):
         """(tensor, bytes, present_total) for the staged decode on one CUDA
@@ -127,6 +181,30 @@ class DeviceField:
     def hbm_bytes(self):
         return sum(t.numel() * t.element_size()
                    for t in self.srv + self.offsets + [self.roots])
+
+
+class Directory:
+    """Device record directory of one DeviceField (rlfc_dir_build)."""
+
+    def __init__(self, c, blobs, blob_off, flagged, root_rgb, build_ms):
+        self.c = c
+        self.ref = ctypes.byref(c)
+        self.blobs, self.blob_off = blobs, blob_off
+        self.flagged, self.root_rgb = flagged, root_rgb
+        self.build_ms = build_ms
+
+    @property
+    def n_flagged(self):
+        return int(self.c.n_flagged)
+
+    @property
+    def blob_bytes(self):
+        return int(self.c.blob_bytes)
+
+    @property
+    def hbm_bytes(self):
+        return sum(t.numel() * t.element_size() for t in
+                   (self.blobs, self.blob_off, self.flagged, self.root_rgb))
 
 
 def tile_bytes_max(header, offsets):
@@ -281,17 +359,23 @@ def decode_planes(state, planes, stop_level=0, device=None):
     return out
 
 
+KERNELS = ("auto", "dir", "staged", "fused", "simple")
+
+
 def decode_field(state, stop_level=0, images=None, rows=None, out=None,
-                 device=None, kernel="staged", check=True):
+                 device=None, kernel="auto", check=True):
     """Decode many camera images straight into an RGB8 CUDA tensor.
 
     images: None for the whole (S, T) grid -- the result is (S, T, H, W, 3)
     -- or a sequence of (s, t) pairs -- the result is (n, H, W, 3) in that
     order.  rows: optional block-row band (by_lo, by_hi); the result then
-    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "staged"
-    (index -> payload decode -> blend, rlfc_staged.cu; falls back to
-    "fused" outside its envelope), "fused" (the single tiled kernel,
-    rlfc_field.cu) or "simple" (per-block kernel).  With check, a
+    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "auto"
+    ("dir" when the stream is inside its envelope and the whole grid is
+    decoded, else "staged"), "dir" (one persistent kernel over the device
+    record directory, rlfc_dir.cu), "staged" (index -> payload decode ->
+    blend, rlfc_staged.cu; falls back to "fused" outside its envelope),
+    "fused" (the single tiled kernel, rlfc_field.cu) or "simple" (per-block
+    kernel).  With check, a
     corrupt stream raises the FormatError the reference raises first.
     Returns (tensor, status) where status is the device status word tensor.
     """
@@ -327,22 +411,33 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
             not out.is_contiguous():
         raise ValueError(f"out must be a contiguous uint8 tensor {shape}")
     status = torch.zeros(1, dtype=torch.int64, device=df.device)
-    if kernel not in ("staged", "fused", "simple"):
+    if kernel not in KERNELS:
         raise ValueError(f"unknown decode kernel {kernel!r}")
     if nimg and nrows:
         L = _native.lib()
         slots_p = None if slots_t is None else slots_t.data_ptr()
         with torch.cuda.device(df.device):
             done = False
-            if kernel == "staged":
+            if kernel in ("auto", "dir") and slots_t is None:
+                dr = df.directory()
+                if dr is not None:
+                    rc = L.rlfc_decode_field_dir(
+                        df.ref, dr.ref, stop_level, by_lo, by_hi,
+                        out.data_ptr(), nrows * W * 3, W * 3,
+                        status.data_ptr(), _stream())
+                    if rc != _native.RLFC_ERR_ARGUMENT:
+                        _native.check(rc, "rlfc_decode_field_dir")
+                        done = True
+            if not done and kernel in ("auto", "dir", "staged"):
                 stream = _stream()
                 ws = df.staged_workspace(stream)
                 if ws is not None:
-                    rc = L.rlfc_decode_field_staged(
-                        df.ref, stop_level, slots_p, by_lo, by_hi,
-                        out.data_ptr(), nrows * W * 3, W * 3,
-                        ws[0].data_ptr(), ws[1], ws[2], status.data_ptr(),
-                        stream)
+                    with df.enqueue_lock:
+                        rc = L.rlfc_decode_field_staged(
+                            df.ref, stop_level, slots_p, by_lo, by_hi,
+                            out.data_ptr(), nrows * W * 3, W * 3,
+                            ws[0].data_ptr(), ws[1], ws[2], status.data_ptr(),
+                            stream)
                     if rc != _native.RLFC_ERR_ARGUMENT:
                         _native.check(rc, "rlfc_decode_field_staged")
                         done = True
@@ -375,10 +470,11 @@ def decode_field_slots(state, stop_level, slots, n, device=None):
         ws = df.staged_workspace(stream)
         rc = _native.RLFC_ERR_ARGUMENT
         if ws is not None:
-            rc = L.rlfc_decode_field_staged(
-                df.ref, stop_level, slots.data_ptr(), 0, hb, out.data_ptr(),
-                H * W * 3, W * 3, ws[0].data_ptr(), ws[1], ws[2],
-                status.data_ptr(), stream)
+            with df.enqueue_lock:
+                rc = L.rlfc_decode_field_staged(
+                    df.ref, stop_level, slots.data_ptr(), 0, hb,
+                    out.data_ptr(), H * W * 3, W * 3, ws[0].data_ptr(), ws[1],
+                    ws[2], status.data_ptr(), stream)
         if rc == _native.RLFC_ERR_ARGUMENT:
             rc = L.rlfc_decode_field(df.ref, stop_level, slots.data_ptr(), 0,
                                      hb, out.data_ptr(), H * W * 3, W * 3,
