@@ -181,11 +181,14 @@ int rlfc_decode_field_staged(const rlfc_field *f, int32_t stop_level,
  *
  * Build: rlfc_dir_plan fills the geometry and the scratch / root_rgb sizes;
  * the caller allocates scratch (scratch_bytes), blob_off (n_blobs + 1 u32),
- * flagged (nrec int32) and root_rgb; rlfc_dir_size (synchronous) sizes the
+ * flagged (nrec int32), root_rgb and tables (RLFC_DIR_TABLE_BYTES);
+ * rlfc_dir_size (synchronous) sizes the
  * blobs (blob_bytes, n_flagged); the caller allocates blobs (blob_bytes + 64,
  * the tail lets 64-bit bit windows read past the last payload);
  * rlfc_dir_build fills them.  RLFC_ERR_ARGUMENT: outside this path's
  * envelope (block 4, S <= 32, h <= 8, int16 roots, a blob over 64 KiB). */
+#define RLFC_DIR_TABLE_BYTES 16384
+
 typedef struct rlfc_dir {
     int32_t tw, nb, nchunks, rows;
     int64_t n_blobs, nrec;
@@ -197,6 +200,7 @@ typedef struct rlfc_dir {
     int32_t *flagged;
     uint8_t *root_rgb;
     uint8_t *blobs;
+    uint8_t *tables;    /* RLFC_DIR_TABLE_BYTES: dequantisation + digit tables */
 } rlfc_dir;
 
 int rlfc_dir_plan(const rlfc_field *f, rlfc_dir *d);

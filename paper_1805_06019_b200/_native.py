@@ -55,7 +55,10 @@ class RlfcDir(ctypes.Structure):
                 ("blob_bytes", ctypes.c_uint64),
                 ("scratch", ctypes.c_void_p), ("blob_off", ctypes.c_void_p),
                 ("flagged", ctypes.c_void_p), ("root_rgb", ctypes.c_void_p),
-                ("blobs", ctypes.c_void_p)]
+                ("blobs", ctypes.c_void_p), ("tables", ctypes.c_void_p)]
+
+
+DIR_TABLE_BYTES = 16384
 
 
 _lib = None

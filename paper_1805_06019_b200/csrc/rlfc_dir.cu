@@ -52,13 +52,18 @@ constexpr int NB = TW / B;           // blocks per tile
 constexpr int NR = 3 * NB;           // records per tile row
 constexpr int MAXL = 8;              // tree levels
 constexpr int MAXS = 32;             // views per camera row (masks are 32-bit)
-constexpr int NG = 6;                // consumer groups (one tile each at a time)
-constexpr int GW = 3;                // warps per group (6 groups x 3 + producer = 19 warps)
-constexpr int GT = GW * 32;
-constexpr int NT = 32 + NG * GT;     // + one producer warp
+constexpr int CW = 4;                // warps per tile CTA
+constexpr int CT = CW * 32;
+constexpr int CPS = 5;               // tile CTAs resident per SM (registers)
 constexpr int HDR0 = 16 + 4 * NR;    // blob bytes before the u16 offsets
 
 __device__ const DigitLut g_lut = make_digit_lut();
+// directory tables (RLFC_DIR_TABLE_BYTES): int16 dequantisation table + digit
+// tables at TAB_DQ16, int32 dequantisation table + digit tables at TAB_DQ32
+constexpr int TAB_DQ16 = 0;
+constexpr int TAB_DQ32 = 4864;
+static_assert(TAB_DQ16 + 2048 * 2 + 368 * 2 <= TAB_DQ32 && TAB_DQ32 + 2048 * 4 + 368 * 2 <= RLFC_DIR_TABLE_BYTES,
+              "table layout");
 __device__ const NodeBytes g_nb16 = make_node_bytes<16>();
 
 // blob bytes before the node bytes: header, masks, off[n], rot[n]
@@ -231,6 +236,19 @@ __global__ void k_mark_bad(const int32_t* flagged, const uint32_t* n, uint8_t* r
     if (i < *n) rec_bad[flagged[i]] = 1;
 }
 
+__global__ void k_dir_tables(int shift, uint8_t* tab) {
+    int16_t* d16 = reinterpret_cast<int16_t*>(tab + TAB_DQ16);
+    int32_t* d32 = reinterpret_cast<int32_t*>(tab + TAB_DQ32);
+    uint16_t* l16 = reinterpret_cast<uint16_t*>(d16 + 2048);
+    uint16_t* l32 = reinterpret_cast<uint16_t*>(d32 + 2048);
+    for (int z = threadIdx.x; z < 2048; z += blockDim.x) {
+        const int32_t v = dequant((uint32_t)z, shift);       // kernels.py:202-211
+        d16[z] = (int16_t)v;
+        d32[z] = v;
+    }
+    for (int i = threadIdx.x; i < 368; i += blockDim.x) l16[i] = l32[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
+}
+
 // RGB8 of every root sample (colorspace.py:27-56), rows of rgb_stride bytes.
 __global__ void k_dir_root_rgb(const __grid_constant__ rlfc_field f, uint8_t* out, int rgb_stride) {
     const int quads = f.wp / 4;
@@ -257,34 +275,29 @@ __global__ void k_dir_root_rgb(const __grid_constant__ rlfc_field f, uint8_t* ou
 
 // ---- decode step ----------------------------------------------------------------------
 struct Params {
-    int S, T, h, k, nlev, wb, hb, nchunks, R, rsx, rsy;
-    int by_lo, ncols;
+    int S, T, W, H, h, k, nlev, wb, hb, nchunks, R, rsx, rsy;
+    int by_lo;
     int row_base[MAXL];
-    int D;                       // stages
-    int out_bytes, rgb_bytes, blob_cap, stage_bytes;
-    int off_tab, off_grp, grp_bytes, rescap, off_colofs, off_roots, roots_bytes, off_stage;
+    int blob_cap, rescap;
+    int off_roots, off_colofs, off_bptr, off_buf, buf_bytes, off_rgb, off_stage;
     const uint8_t* blobs;
     const uint32_t* blob_off;
     const uint8_t* root_rgb;
+    const uint8_t* tables;
     const void* roots;
     int rgb_stride, hp, wp;
     uint64_t* status;
     int shift;
 };
 
-struct StageInfo {
-    uint64_t ptr[MAXL];          // generic address of level (k + i)'s blob
-    int rslot;
-    int copied;                  // the blobs sit in the stage (else in HBM)
-};
-
-// Per consumer group scratch (one tile at a time).
+// Tile scratch.
 struct GroupScr {
     uint32_t smask[MAXL * NR];   // record masks of the tile's node rows
     uint16_t spst[MAXL * NR];    // residual slot of each record's first node
     uint16_t list[MAXS * NB];    // dirty units (view | block << 8), view-major
     int nunits;
     uint32_t mc[MAXL];           // per level: payloads in plain-bit | trit mode (u16 each)
+    uint32_t nl[MAXL];           // per level: payloads
     int slbase[MAXL + 1];        // first residual slot of each level; [MAXL] = total
 };
 
@@ -295,55 +308,16 @@ constexpr int SRES_OFF = ((int)sizeof(GroupScr) + RESCAP_MAX / 8 + 15) & ~15;
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 #ifdef RLFC_DIR_TIMING
-// per-tile %globaltimer stamps of the first 16 CTAs (debug build only,
-// tools/dir_timing.py): producer 0-2, consumer 3-8
-__device__ long long g_dtime[16 * 256 * 10];
-#define DSTAMP(q) do { if (blockIdx.x < 16 && ntile < 256) { long long tt; \
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)); g_dtime[(blockIdx.x * 256 + ntile) * 10 + (q)] = tt; } } while (0)
+// per-tile %globaltimer stamps of the first 64 CTAs (debug build only,
+// tools/dir_timing.py)
+__device__ long long g_dtime[64 * 8 * 8];
+#define DSTAMP(q) do { if (tid == 0 && (blockIdx.x + blockIdx.y * gridDim.x) < 64 && (t - t0) < 8) { long long tt; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)); \
+    g_dtime[((blockIdx.x + blockIdx.y * gridDim.x) * 8 + (t - t0)) * 8 + (q)] = tt; } } while (0)
 #else
 #define DSTAMP(q) do { } while (0)
 #endif
 
-__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    const uint32_t a = smem_u32(b);
-    uint32_t done = 0;
-    while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done)
-                     : "r"(a), "r"(parity)
-                     : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, int x, int y, int z, int w, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-        "[%6];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma5(void* dst, const CUtensorMap* map, int x, int y, int z, int w, int v,
-                                     uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
-        "%6}], [%7];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(v), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 // 16-byte asynchronous copy (zero-filled when src_bytes == 0)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
@@ -353,8 +327,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_b
 __device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-// named barrier of one consumer group (ids 1..NG)
-__device__ __forceinline__ void gbar(int g) { asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "n"(GT) : "memory"); }
+// 16-byte store with an L2 evict-first policy: the output streams through L2
+// once, so the root colours and blobs other tiles read stay resident
+__device__ __forceinline__ void st_global_ef(void* p, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w), "l"(pol)
+                 : "memory");
+}
 
 __device__ __forceinline__ uint32_t pack4_sat(int32_t b0, int32_t b1, int32_t b2, int32_t b3) {
     uint32_t hi, d;
@@ -487,210 +466,154 @@ __device__ __forceinline__ void add_res(const uint8_t* src, int32_t* acc) {
     }
 }
 
-// The decode step.  Warp 0 produces (TMA / bulk copies into a ring of D
-// stages); NG consumer groups of GW warps take the tiles round-robin, each
-// group one tile at a time:
-//   A  RGB(root) rows replicated into every view's rows of the output stage
-//      (the clean-pixel result); per level the record masks and payload
-//      ranks; the dirty (view, block) units, view-major;
-//   B1 every payload of the tile's blobs bucketed by BISE mode;
-//   B2 one payload per thread, warps of one mode: decode + dequantise into
-//      the group's shared residual slots (rank order);
-//   C  one dirty unit per thread: root block + chain residuals, YCoCg-R
-//      inverse, clamp, pack into the stage;
-//   then the group leader TMA-stores the stage (all S views of the tile).
+// The decode step: one CTA per (block row by, 64-pixel chunk, root row ry)
+// "segment", i.e. the camera rows t whose views share one root row; several
+// CTAs resident per SM.  The CTA loads the segment's raw root rows once and
+// then, tile by tile (camera row t), with the next tile's inputs already on
+// their way (cp.async, double-buffered):
+//   1. writes the clean-pixel result -- every view's RGB(root) rows, staged
+//      once per tile in shared memory -- to HBM with 16-byte stores;
+//   A. per level: record masks and residual slots; the dirty (view, block)
+//      units, view-major;
+//   B. decodes every payload of the tile's blobs once (one payload per
+//      thread, tasks in BISE-mode order) into shared residual slots;
+//   C. per dirty unit: root block + chain residuals, YCoCg-R inverse, clamp,
+//      pack, stored over the clean rows (ordered after them by the CTA
+//      barriers).
 template <typename VT>
-__global__ void __launch_bounds__(NT, 1) k_field_dir(const __grid_constant__ Params P,
-                                                    const __grid_constant__ CUtensorMap out_map) {
+__global__ void __launch_bounds__(CT, CPS) k_seg_dir(const __grid_constant__ Params P, uint8_t* __restrict__ rgb,
+                                                    int64_t img_stride, int64_t row_stride) {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int S = P.S, T = P.T, h = P.h, k = P.nlev > 0 ? P.k : P.h, nlev = P.nlev, D = P.D;
-    constexpr int RB = 16 * (int)sizeof(VT);           // residual slot bytes
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + D;
-    uint64_t* rfull = empty + D;
-    uint64_t* rempty = rfull + 2;
-    VT* dq = reinterpret_cast<VT*>(smem + P.off_tab);
-    uint16_t* lut = reinterpret_cast<uint16_t*>(dq + 2048);
-    uint32_t* colofs = reinterpret_cast<uint32_t*>(smem + P.off_colofs);
-    uint8_t* roots = smem + P.off_roots;
-    uint8_t* stages = smem + P.off_stage;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int S = P.S, T = P.T, h = P.h, k = P.nlev > 0 ? P.k : P.h, nlev = P.nlev;
+    constexpr int RB = 16 * (int)sizeof(VT);
+    constexpr int Q = TW * 3 / 16;                        // 16-byte pieces per RGB row
+    const int nsegc = ((T - 1) >> h) + 1;
+    const int chunk = blockIdx.x, ry = blockIdx.y % nsegc, by = P.by_lo + blockIdx.y / nsegc;
+    const int t0 = ry << h, t1 = min(T, t0 + (1 << h));
     const int rowbytes = TW * 3;
     const int rescap = P.rescap;
+    const int nrow = min(B, P.H - by * B);
+    GroupScr& sc = *reinterpret_cast<GroupScr*>(smem);
+    uint32_t* sbad = reinterpret_cast<uint32_t*>(smem + sizeof(GroupScr));
+    uint8_t* sres = smem + SRES_OFF;
+    uint8_t* roots = smem + P.off_roots;
+    uint32_t* colofs = reinterpret_cast<uint32_t*>(smem + P.off_colofs);     // [R + 1]
+    uint64_t* bptrs = reinterpret_cast<uint64_t*>(smem + P.off_bptr);        // [2][MAXL]
+    uint8_t* stage = smem + P.off_stage;                                      // [S][B][TW*3]
+    uint8_t* rgbrows = smem + P.off_rgb;                                      // [rsx][B][TW*3]
+    const VT* dq = reinterpret_cast<const VT*>(P.tables + (sizeof(VT) == 2 ? TAB_DQ16 : TAB_DQ32));
+    const uint16_t* lut = reinterpret_cast<const uint16_t*>(dq + 2048);
+    const int64_t gcol = (int64_t)by * P.nchunks + chunk;
+    const int x0 = chunk * rowbytes;                          // byte offset of the chunk in a row
+    const int wbytes = min(rowbytes, P.W * 3 - x0);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 
-    if (tid == 0) {
-        for (int i = 0; i < D; ++i) {
-            mbar_init(full + i, 33);          // 32 producer lanes' copies + the info write
-            mbar_init(empty + i, 1);
+    // the tile's blobs (levels k.., node rows t >> l) into buffer q, or their
+    // HBM address when they exceed the buffer
+    auto issue = [&](int t, int q) {
+        uint8_t* bdst = smem + P.off_buf + q * P.buf_bytes;
+        uint32_t o[MAXL], n[MAXL], total = 0;
+#pragma unroll
+        for (int li = 0; li < MAXL; ++li) {
+            o[li] = n[li] = 0;
+            if (li < nlev) {
+                const int row = P.row_base[k + li] + (t >> (k + li));
+                o[li] = colofs[row];
+                n[li] = colofs[row + 1] - o[li];
+                total += n[li];
+            }
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(rfull + i, 32);
-            mbar_init(rempty + i, NG);
+        const bool copy = total * 16u <= (uint32_t)P.blob_cap;
+        if (tid < nlev) {
+            uint32_t pos = 0, ot = 0;
+#pragma unroll
+            for (int li = 0; li < MAXL; ++li) {
+                if (li < tid) pos += n[li];
+                if (li == tid) ot = o[li];
+            }
+            bptrs[q * MAXL + tid] = copy ? reinterpret_cast<uint64_t>(bdst + pos * 16u)
+                                         : reinterpret_cast<uint64_t>(P.blobs + (uint64_t)ot * 16u);
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (copy)
+            for (uint32_t i = tid; i < total; i += CT) {
+                uint32_t j = i, li = 0;
+#pragma unroll
+                for (int l2 = 0; l2 < MAXL - 1; ++l2)
+                    if (l2 == (int)li && j >= n[l2]) {
+                        j -= n[l2];
+                        ++li;
+                    }
+                uint32_t src = o[0];
+#pragma unroll
+                for (int l2 = 1; l2 < MAXL; ++l2)
+                    if (l2 == (int)li) src = o[l2];
+                cp_async16(bdst + i * 16, P.blobs + ((uint64_t)src + j) * 16u, 16);
+            }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    // segment prologue: blob offsets of the column; raw root rows
+    // [rx][c][row][TW] int16 and RGB(root) rows [rx][row][TW*3] of the root
+    // row, shared by every tile of the segment
+    for (int j = tid; j <= P.R; j += CT) colofs[j] = __ldg(P.blob_off + gcol * P.R + j);
+    {
+        const uint8_t* rgb0 = P.root_rgb + ((int64_t)ry * P.hp + by * B) * P.rgb_stride + x0;
+        const int64_t rxs = (int64_t)P.rsy * P.hp * P.rgb_stride;
+        for (int i = tid; i < P.rsx * B * Q; i += CT) {
+            const int rx = i / (B * Q), rq = i - rx * (B * Q), row = rq / Q, xb = (rq - row * Q) * 16;
+            cp_async16(rgbrows + i * 16, rgb0 + rx * rxs + row * P.rgb_stride + xb, x0 + xb < P.rgb_stride ? 16 : 0);
+        }
     }
-    for (int z = tid; z < 2048; z += NT) dq[z] = (VT)dequant((uint32_t)z, P.shift);
-    for (int i = tid; i < 243 + 125; i += NT) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
-    __syncthreads();
-
-    if (tid < 32) {
-        // ---------------- producer warp ----------------
-        // Loads are 16-byte cp.async copies spread over the warp's lanes (the
-        // TMA unit is left to the output stores); each lane's copies arrive
-        // on the stage's barrier when they land (cp.async.mbarrier.arrive).
-        int ntile = 0, nseg = 0;
-        const int rgb_row = P.rgb_stride;
-        for (int col = blockIdx.x; col < P.ncols; col += gridDim.x) {
-            const int by = P.by_lo + col / P.nchunks, chunk = col % P.nchunks;
-            const int64_t gcol = (int64_t)by * P.nchunks + chunk;
-            __syncwarp();
-            for (int j = lane; j <= P.R; j += 32) colofs[j] = __ldg(P.blob_off + gcol * P.R + j);
-            __syncwarp();
-            int cur_ry = -1, rslot = 0;
-            for (int t = 0; t < T; ++t) {
-                const int ry = t >> h;
-                if (nlev > 0 && ry != cur_ry) {
-                    // raw roots of this root row: [rx][c][row][TW] int16
-                    rslot = nseg & 1;
-                    mbar_wait(rempty + rslot, ((nseg >> 1) & 1) ^ 1u);
-                    uint8_t* rdst = roots + rslot * P.roots_bytes;
-                    constexpr int RQ = TW * 2 / 16;                       // 16-byte pieces per root row
-                    const int nq = P.rsx * 3 * B * RQ;
-                    for (int i = lane; i < nq; i += 32) {
-                        const int q = i % RQ, row = (i / RQ) % B, rc = i / (RQ * B);   // rc = rx * 3 + c
-                        const int rx = rc / 3, c = rc - rx * 3;
-                        const int x = chunk * TW + q * 8;
-                        const uint8_t* src = reinterpret_cast<const uint8_t*>(P.roots) +
-                                             ((((int64_t)rx * P.rsy + ry) * 3 + c) * P.hp + by * B + row) * (int64_t)P.wp * 2 +
-                                             (int64_t)x * 2;
-                        cp_async16(rdst + i * 16, src, x < P.wp ? 16 : 0);
-                    }
-                    cp_async_arrive(rfull + rslot);
-                    cur_ry = ry;
-                    ++nseg;
-                }
-                const int st = ntile % D;
-                if (lane == 0) DSTAMP(0);
-                mbar_wait(empty + st, ((ntile / D) & 1) ^ 1u);
-                if (lane == 0) DSTAMP(1);
-                uint8_t* sbase = stages + st * P.stage_bytes;
-                uint8_t* rgbdst = sbase + P.out_bytes;
-                uint8_t* bdst = rgbdst + P.rgb_bytes;
-                StageInfo* info = reinterpret_cast<StageInfo*>(bdst + P.blob_cap);
-                uint32_t total = 0;
-                for (int li = 0; li < nlev; ++li) {
-                    const int row = P.row_base[k + li] + (t >> (k + li));
-                    total += (colofs[row + 1] - colofs[row]) * 16u;
-                }
-                const bool copy = total <= (uint32_t)P.blob_cap;
-                if (lane == 0) {
-                    uint32_t pos = 0;
-                    for (int li = 0; li < nlev; ++li) {
-                        const int row = P.row_base[k + li] + (t >> (k + li));
-                        info->ptr[li] = copy ? reinterpret_cast<uint64_t>(bdst + pos)
-                                             : reinterpret_cast<uint64_t>(P.blobs + (uint64_t)colofs[row] * 16u);
-                        pos += (colofs[row + 1] - colofs[row]) * 16u;
-                    }
-                    info->rslot = rslot;
-                    info->copied = copy;
-                }
-                // RGB(root) rows of the tile: [rx][row][TW * 3]
-                {
-                    constexpr int GQ = TW * 3 / 16;
-                    const int nq = P.rsx * B * GQ;
-                    for (int i = lane; i < nq; i += 32) {
-                        const int q = i % GQ, row = (i / GQ) % B, rx = i / (GQ * B);
-                        const int xb = chunk * TW * 3 + q * 16;
-                        const uint8_t* src = P.root_rgb + (((int64_t)rx * P.rsy + ry) * P.hp + by * B + row) * rgb_row + xb;
-                        cp_async16(rgbdst + i * 16, src, xb < rgb_row ? 16 : 0);
-                    }
-                }
-                if (copy) {
-                    uint32_t pos = 0;
-                    for (int li = 0; li < nlev; ++li) {
-                        const int row = P.row_base[k + li] + (t >> (k + li));
-                        const uint32_t nq = colofs[row + 1] - colofs[row];
-                        const uint8_t* src = P.blobs + (uint64_t)colofs[row] * 16u;
-                        for (uint32_t i = lane; i < nq; i += 32) cp_async16(bdst + pos + i * 16, src + i * 16, 16);
-                        pos += nq * 16u;
-                    }
-                }
-                __syncwarp();
-                cp_async_arrive(full + st);
-                if (lane == 0) mbar_arrive(full + st);       // info written
-                if (lane == 0) DSTAMP(2);
-                ++ntile;
-            }
+    if (nlev > 0) {
+        constexpr int RQ = TW * 2 / 16;
+        const int nq = P.rsx * 3 * B * RQ;
+        const int64_t pl = (int64_t)P.hp * P.wp * 2;
+        const uint8_t* r0 = reinterpret_cast<const uint8_t*>(P.roots) + ((int64_t)ry * 3 * P.hp + by * B) * P.wp * 2 +
+                            (int64_t)chunk * TW * 2;
+        for (int i = tid; i < nq; i += CT) {
+            const int q = i % RQ, row = (i / RQ) % B, rc = i / (RQ * B);
+            const int rx = rc / 3, c = rc - rx * 3;
+            cp_async16(roots + i * 16, r0 + (rx * P.rsy * 3 + c) * pl + row * P.wp * 2 + q * 16,
+                       chunk * TW + q * 8 < P.wp ? 16 : 0);
         }
-        return;
     }
+    __syncthreads();                                          // colofs
+    issue(t0, 0);
 
-    // ---------------- consumer groups ----------------
-    const int g = (tid - 32) / GT, gt = (tid - 32) % GT, gw = gt >> 5;
-    GroupScr& sc = *reinterpret_cast<GroupScr*>(smem + P.off_grp + g * P.grp_bytes);
-    uint32_t* sbad = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(&sc) + sizeof(GroupScr));
-    uint8_t* sres = reinterpret_cast<uint8_t*>(&sc) + SRES_OFF;
-    uint64_t pol = 0;
-    if (gt == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const uint32_t smask_s = S >= 32 ? 0xFFFFFFFFu : (1u << S) - 1u;
-    const int nsegc = nlev > 0 ? ((T - 1) >> h) + 1 : 0;     // root-row segments per column
-    int prev_st = -1, waited_seg = -1, arrived_seg = -1;
-    // this group's tiles: n = g, g + NG, ... of the CTA's tile sequence
-    // (columns blockIdx.x + i * gridDim.x, camera rows t)
-    for (int n = g;; n += NG) {
-        const int ci = n / T, t = n - ci * T;
-        const int col = blockIdx.x + ci * gridDim.x;
-        if (col >= P.ncols) break;
-        const int by = P.by_lo + col / P.nchunks, chunk = col % P.nchunks;
-        const int ry = t >> h;
-        const int seg = ci * nsegc + ry;
-        const int st = n % D;
-        const int ntile = n;
-        if (nlev > 0) {
-            // segments this group has passed: its share of releasing them
-            if (gt == 0)
-                for (; arrived_seg + 1 < seg; ++arrived_seg) mbar_arrive(rempty + ((arrived_seg + 1) & 1));
-            if (waited_seg != seg) {
-                mbar_wait(rfull + (seg & 1), (seg >> 1) & 1);
-                waited_seg = seg;
-            }
+    for (int t = t0; t < t1; ++t) {
+        const int q = (t - t0) & 1;
+        DSTAMP(0);
+        if (t + 1 < t1) {
+            issue(t + 1, q ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        if (gt == 0) DSTAMP(3);
-        mbar_wait(full + st, (n / D) & 1);
-        if (gt == 0) {
-            DSTAMP(4);
-            // the previous tile's store has long been issued: once it has
-            // read its stage, hand the stage back to the producer
-            if (prev_st >= 0) {
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                mbar_arrive(empty + prev_st);
-            }
-        }
-        uint8_t* sbase = stages + st * P.stage_bytes;
-        const uint8_t* rgbrows = sbase + P.out_bytes;
-        const StageInfo* info = reinterpret_cast<const StageInfo*>(sbase + P.out_bytes + P.rgb_bytes + P.blob_cap);
-        // ---- A: clean pixels (RGB(root) rows -> every view's rows)
+        __syncthreads();
+        const uint8_t* buf = smem + P.off_buf + q * P.buf_bytes;
+        const uint64_t* bptr = bptrs + q * MAXL;
+        DSTAMP(1);
+
+        // ---- 1: clean pixels: every view's RGB(root) rows into the output
+        // stage [s][row][TW*3]
         {
-            constexpr int Q = B * TW * 3 / 16;            // 16-byte quads per view
+            uint4* dst = reinterpret_cast<uint4*>(stage);
             const uint4* src = reinterpret_cast<const uint4*>(rgbrows);
-            uint4* dst = reinterpret_cast<uint4*>(sbase);
-            for (int i = gt; i < S * Q; i += GT) {
-                const int s = i / Q, q = i - s * Q;
-                dst[i] = src[(s >> h) * Q + q];
+            for (int i = tid; i < S * B * Q; i += CT) {
+                const int s = i / (B * Q), rq = i - s * (B * Q);
+                dst[i] = src[(s >> h) * (B * Q) + rq];
             }
         }
-#ifdef RLFC_DIR_SKIP
-        if (false) {
-#else
+        DSTAMP(2);
         if (nlev > 0) {
-#endif
-            if (gw < GW - 1) {
-                // per level: record masks, absolute residual slot of each
-                // record's first node, payload counts per BISE mode
-                for (int li = gw; li < nlev; li += GW - 1) {
-                    const uint8_t* bp = reinterpret_cast<const uint8_t*>(info->ptr[li]);
+            // ---- A: per-level masks + residual slots (warps 0..CW-2), dirty units (last warp)
+            if (wid < CW - 1) {
+                for (int li = wid; li < nlev; li += CW - 1) {
+                    const uint8_t* bp = reinterpret_cast<const uint8_t*>(bptr[li]);
                     uint32_t base = 0;
-                    for (int l2 = 0; l2 < li; ++l2) base += *reinterpret_cast<const uint32_t*>(info->ptr[l2]);
+                    for (int l2 = 0; l2 < li; ++l2) base += *reinterpret_cast<const uint32_t*>(bptr[l2]);
                     const uint32_t* mk = reinterpret_cast<const uint32_t*>(bp) + 4;
                     const int r1 = lane + 32;
                     const uint32_t m0 = mk[lane], m1 = r1 < NR ? mk[r1] : 0u;
@@ -714,16 +637,18 @@ __global__ void __launch_bounds__(NT, 1) k_field_dir(const __grid_constant__ Par
                     }
                     if (lane == 0) {
                         sc.mc[li] = *reinterpret_cast<const uint32_t*>(bp + 4);      // u16 bits | u16 trits
+                        sc.nl[li] = *reinterpret_cast<const uint32_t*>(bp);
                         sc.slbase[li] = (int)base;
                     }
                 }
-                for (int i = gt; i < rescap / 32; i += (GW - 1) * 32) sbad[i] = 0u;
+                for (int i = tid; i < rescap / 32; i += (CW - 1) * 32) sbad[i] = 0u;
             } else {
+                const uint32_t smask_s = S >= 32 ? 0xFFFFFFFFu : (1u << S) - 1u;
                 uint32_t dirty = 0;
                 if (lane < NB) {
                     for (int li = 0; li < nlev; ++li) {
                         const int l = k + li;
-                        const uint32_t* mk = reinterpret_cast<const uint32_t*>(info->ptr[li]) + 4;
+                        const uint32_t* mk = reinterpret_cast<const uint32_t*>(bptr[li]) + 4;
                         uint32_t m = mk[lane] | mk[NB + lane] | mk[2 * NB + lane];
                         if (l == 0) {
                             dirty |= m;
@@ -739,8 +664,7 @@ __global__ void __launch_bounds__(NT, 1) k_field_dir(const __grid_constant__ Par
                     dirty &= smask_s;
                 }
                 // view-major unit order: consecutive units are different
-                // blocks of one view, so their stage stores spread over the
-                // shared-memory banks
+                // blocks of one view row, so their stores are adjacent
                 const uint32_t below = (1u << lane) - 1u;
                 uint32_t nu = 0;
                 for (int s = 0; s < S; ++s) {
@@ -749,140 +673,158 @@ __global__ void __launch_bounds__(NT, 1) k_field_dir(const __grid_constant__ Par
                     nu += __popc(bal);
                 }
                 uint32_t nt = 0;
-                for (int li = 0; li < nlev; ++li) nt += *reinterpret_cast<const uint32_t*>(info->ptr[li]);
+                for (int li = 0; li < nlev; ++li) nt += *reinterpret_cast<const uint32_t*>(bptr[li]);
                 if (lane == 0) {
                     sc.nunits = (int)nu;
                     sc.slbase[MAXL] = (int)nt;
                 }
             }
-            gbar(g);
-            if (gt == 0) DSTAMP(5);
-            // ---- B: every payload of the tile's blobs (each is needed by
-            // this tile: level l node x serves views x*2^l .. x*2^l + 2^l - 1
-            // of camera row t) decoded once into the group's residual slots
-            // (rank order), one payload per thread; tasks run level by level
-            // in BISE-mode order (rot[]), so a warp runs one mode's code
-            const int ntask = sc.slbase[MAXL];
-            for (int i = gt; i < ntask; i += GT) {
-                int li = 0;
-                while (li + 1 < nlev && i >= sc.slbase[li + 1]) ++li;
-                const int q = i - sc.slbase[li];
-                const uint8_t* bp = reinterpret_cast<const uint8_t*>(info->ptr[li]);
-                const uint32_t nl = *reinterpret_cast<const uint32_t*>(bp);
-                const uint16_t* offs = reinterpret_cast<const uint16_t*>(bp + HDR0);
-                const uint32_t j = offs[nl + q];                      // rot[q]
-                const int slot = sc.slbase[li] + (int)j;
-                if (slot >= rescap) continue;
-                const uint32_t mc = sc.mc[li];
-                const int mode = (uint32_t)q < (mc & 0xFFFFu) ? MODE_BITS
-                                 : (uint32_t)q < (mc & 0xFFFFu) + (mc >> 16) ? MODE_TRIT : MODE_QUINT;
-                const uint8_t* p = bp + offs[j];
-                const uint32_t bb = (uint32_t)desc_bits(p[0]);
-                const uint8_t* pq = p + 1;
-                const uint32_t* sw = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(pq) & ~uintptr_t(3));
-                const uint32_t bit0 = (uint32_t)(reinterpret_cast<uintptr_t>(pq) & 3u) * 8u;
-                int32_t v[16];
-                bool bad;
-                if (mode == MODE_BITS) bad = dec16<MODE_BITS>(sw, bit0, bb, lut, dq, v);
-                else if (mode == MODE_TRIT) bad = dec16<MODE_TRIT>(sw, bit0, bb, lut, dq, v);
-                else bad = dec16<MODE_QUINT>(sw, bit0, bb, lut + 243, dq, v);
-                if (bad) atomicOr(sbad + (slot >> 5), 1u << (slot & 31));
-                store_res<VT>(sres + slot * RB, v);
+            __syncthreads();
+            DSTAMP(3);
+
+            // ---- B: decode every payload of the tile's blobs into the residual
+            // slots.  Each warp takes one BISE mode (warp 3 helps with plain
+            // bits), so a warp runs one mode's code: per level, the mode's
+            // payloads are a contiguous run of rot[] (mode order); a warp's
+            // lanes run over the concatenation of its mode's runs
+            {
+                const int mode = wid == 3 ? MODE_BITS : wid;
+                const int nw = wid == 0 || wid == 3 ? 2 : 1, wi = wid == 3 ? 1 : 0;
+                uint32_t q0[MAXL], cnt[MAXL], tot = 0;
+#pragma unroll
+                for (int li = 0; li < MAXL; ++li) {
+                    q0[li] = cnt[li] = 0;
+                    if (li < nlev) {
+                        const uint32_t mc = sc.mc[li], nb0 = mc & 0xFFFFu, nt0 = mc >> 16;
+                        const uint32_t nl = sc.nl[li];
+                        q0[li] = mode == MODE_BITS ? 0u : mode == MODE_TRIT ? nb0 : nb0 + nt0;
+                        cnt[li] = (mode == MODE_BITS ? nb0 : mode == MODE_TRIT ? nb0 + nt0 : nl) - q0[li];
+                        tot += cnt[li];
+                    }
+                }
+                for (uint32_t i = wi * 32 + lane; i < tot; i += 32 * nw) {
+                    uint32_t j = i, li = 0;
+#pragma unroll
+                    for (int l2 = 0; l2 < MAXL - 1; ++l2)
+                        if (l2 == (int)li && j >= cnt[l2]) {
+                            j -= cnt[l2];
+                            ++li;
+                        }
+                    const uint8_t* bp = reinterpret_cast<const uint8_t*>(bptr[li]);
+                    uint32_t qi = j + q0[0];
+#pragma unroll
+                    for (int l2 = 1; l2 < MAXL; ++l2)
+                        if (l2 == (int)li) qi = j + q0[l2];
+                    const uint16_t* offs = reinterpret_cast<const uint16_t*>(bp + HDR0);
+                    const uint32_t r = offs[sc.nl[li] + qi];                   // rot[qi]
+                    const int slot = sc.slbase[li] + (int)r;
+                    if (slot >= rescap) continue;
+                    const uint8_t* p = bp + offs[r];
+                    const uint32_t bb = (uint32_t)desc_bits(p[0]);
+                    const uint8_t* pq = p + 1;
+                    const uint32_t* sw =
+                        reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(pq) & ~uintptr_t(3));
+                    const uint32_t bit0 = (uint32_t)(reinterpret_cast<uintptr_t>(pq) & 3u) * 8u;
+                    int32_t v[16];
+                    bool bad;
+                    if (mode == MODE_BITS) bad = dec16<MODE_BITS>(sw, bit0, bb, lut, dq, v);
+                    else if (mode == MODE_TRIT) bad = dec16<MODE_TRIT>(sw, bit0, bb, lut, dq, v);
+                    else bad = dec16<MODE_QUINT>(sw, bit0, bb, lut + 243, dq, v);
+                    if (bad) atomicOr(sbad + (slot >> 5), 1u << (slot & 31));
+                    store_res<VT>(sres + slot * RB, v);
+                }
             }
-            gbar(g);
-            if (gt == 0) DSTAMP(6);
-            // ---- C: dirty units, pixel row by pixel row: root samples +
-            // chain residuals, YCoCg-R inverse, clamp, pack over the stage
+            __syncthreads();
+
+            // ---- C: dirty units: root block + chain residuals, YCoCg-R
+            // inverse, clamp, pack, store over the clean rows
             const int units = sc.nunits;
-            const int16_t* rt = reinterpret_cast<const int16_t*>(roots + info->rslot * P.roots_bytes);
-            for (int u = gt; u < units; u += GT) {
+            const int16_t* rt = reinterpret_cast<const int16_t*>(roots);
+            for (int u = tid; u < units; u += CT) {
                 const uint32_t e = sc.list[u];
                 const int s = (int)(e & 255u), b = (int)(e >> 8);
                 const int rx = s >> h;
-                // chain presence of the unit: bit 3 * li + c
-                uint32_t pres = 0;
-                for (int li = 0; li < nlev; ++li) {
-                    const int x = s >> (k + li);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) pres |= ((sc.smask[li * NR + c * NB + b] >> x) & 1u) << (3 * li + c);
-                }
+                const int bx = chunk * NB + b;
+                int32_t acc[3][16];
                 uint32_t badc = 0;
-                uint8_t* o = sbase + s * (B * rowbytes) + b * 12;
-#pragma unroll 1
-                for (int row = 0; row < 4; ++row) {
-                    int32_t v[3][4];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
+                for (int c = 0; c < 3; ++c) {
+#pragma unroll
+                    for (int row = 0; row < 4; ++row) {
                         const uint2 w = *reinterpret_cast<const uint2*>(rt + ((rx * 3 + c) * B + row) * TW + b * 4);
-                        v[c][0] = (int32_t)(int16_t)(w.x & 0xFFFFu);
-                        v[c][1] = (int32_t)w.x >> 16;
-                        v[c][2] = (int32_t)(int16_t)(w.y & 0xFFFFu);
-                        v[c][3] = (int32_t)w.y >> 16;
-                        for (uint32_t pc = pres & (0x249249u << c); pc; pc &= pc - 1u) {
-                            const int li = (__ffs(pc) - 1) / 3;
-                            const int r = li * NR + c * NB + b;
-                            const uint32_t m = sc.smask[r];
-                            const int slot = sc.spst[r] + __popc(m & ((1u << (s >> (k + li))) - 1u));
-                            if (slot < rescap) {
-                                if (row == 0 && ((sbad[slot >> 5] >> (slot & 31)) & 1u)) badc |= 1u << c;
-                                add_res4<VT>(sres + slot * RB + row * 4 * (int)sizeof(VT), v[c]);
-                            } else {
-                                // beyond the group's residual slots (dense
-                                // tiles): decode straight from the blob
-                                const uint8_t* bp = reinterpret_cast<const uint8_t*>(info->ptr[li]);
-                                const uint32_t off = reinterpret_cast<const uint16_t*>(bp + HDR0)[slot - sc.slbase[li]];
-                                int32_t full16[16];
-#pragma unroll
-                                for (int q = 0; q < 16; ++q) full16[q] = 0;
-                                if (add_payload(bp + off, lut, dq, full16) && row == 0) badc |= 1u << c;
-#pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    v[c][q] += row == 0 ? full16[q] : row == 1 ? full16[4 + q] : row == 2 ? full16[8 + q] : full16[12 + q];
-                            }
+                        acc[c][4 * row] = (int32_t)(int16_t)(w.x & 0xFFFFu);
+                        acc[c][4 * row + 1] = (int32_t)w.x >> 16;
+                        acc[c][4 * row + 2] = (int32_t)(int16_t)(w.y & 0xFFFFu);
+                        acc[c][4 * row + 3] = (int32_t)w.y >> 16;
+                    }
+                    for (int li = 0; li < nlev; ++li) {
+                        const int r = li * NR + c * NB + b;
+                        const uint32_t m = sc.smask[r];
+                        const int x = s >> (k + li);
+                        if (!((m >> x) & 1u)) continue;
+                        const int slot = sc.spst[r] + __popc(m & ((1u << x) - 1u));
+                        if (slot < rescap) {
+                            if ((sbad[slot >> 5] >> (slot & 31)) & 1u) badc |= 1u << c;
+                            add_res<VT>(sres + slot * RB, acc[c]);
+                        } else {
+                            // beyond the residual slots (dense tiles): decode from the blob
+                            const uint8_t* bp = reinterpret_cast<const uint8_t*>(bptr[li]);
+                            const uint32_t off = reinterpret_cast<const uint16_t*>(bp + HDR0)[slot - sc.slbase[li]];
+                            if (add_payload(bp + off, lut, dq, acc[c])) badc |= 1u << c;
                         }
                     }
-                    int32_t r8[12];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int32_t tt = v[0][i] - (v[2][i] >> 1);
-                        const int32_t bb = tt - (v[1][i] >> 1);
-                        r8[3 * i] = bb + v[1][i];
-                        r8[3 * i + 1] = v[2][i] + tt;
-                        r8[3 * i + 2] = bb;
-                    }
-                    uint32_t* o32 = reinterpret_cast<uint32_t*>(o + row * rowbytes);
-                    o32[0] = pack4_sat(r8[0], r8[1], r8[2], r8[3]);
-                    o32[1] = pack4_sat(r8[4], r8[5], r8[6], r8[7]);
-                    o32[2] = pack4_sat(r8[8], r8[9], r8[10], r8[11]);
                 }
                 if (badc) {
                     const int c = __ffs(badc) - 1;
                     const int64_t img = (int64_t)s * T + t;
-                    report(P.status, (((uint64_t)img * 3 + c) * P.hb + by) * P.wb + chunk * NB + b, 1);
+                    report(P.status, (((uint64_t)img * 3 + c) * P.hb + by) * P.wb + bx, 1);
+                }
+                uint8_t* orow = stage + s * (B * rowbytes) + b * 12;
+#pragma unroll
+                for (int row = 0; row < 4; ++row) {
+                    int32_t r8[12];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int32_t y = acc[0][4 * row + i], co = acc[1][4 * row + i], cg = acc[2][4 * row + i];
+                        const int32_t tt = y - (cg >> 1);
+                        const int32_t bb = tt - (co >> 1);
+                        r8[3 * i] = bb + co;
+                        r8[3 * i + 1] = cg + tt;
+                        r8[3 * i + 2] = bb;
+                    }
+                    uint32_t* o32 = reinterpret_cast<uint32_t*>(orow + row * rowbytes);
+                    o32[0] = pack4_sat(r8[0], r8[1], r8[2], r8[3]);
+                    o32[1] = pack4_sat(r8[4], r8[5], r8[6], r8[7]);
+                    o32[2] = pack4_sat(r8[8], r8[9], r8[10], r8[11]);
                 }
             }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        gbar(g);
-        if (gt == 0) {
-            DSTAMP(7);
-            asm volatile(
-                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], "
-                "%6;" ::"l"(&out_map),
-                "r"(chunk * rowbytes), "r"((by - P.by_lo) * B), "r"(t), "r"(0), "r"(smem_u32(sbase)), "l"(pol)
-                : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            DSTAMP(8);
+        DSTAMP(5);
+        __syncthreads();
+        // ---- store: the stage's rows to HBM.  Threads 0..95 own one (pixel
+        // row, 16-byte piece) each and walk the views two at a time (each
+        // view row of the tile is 12 contiguous pieces)
+        if (tid < 2 * B * Q) {
+            const int rq = tid % (B * Q), row = rq / Q, xb = (rq - row * Q) * 16;
+            if (row < nrow && xb < wbytes) {
+                const int64_t vstride = (int64_t)T * img_stride;
+                int s = tid / (B * Q);
+                uint8_t* dst = rgb + (int64_t)s * vstride + (int64_t)t * img_stride +
+                               (int64_t)((by - P.by_lo) * B + row) * row_stride + x0 + xb;
+                const uint4* src = reinterpret_cast<const uint4*>(stage) + s * (B * Q) + rq;
+                if (xb + 16 <= wbytes) {
+                    for (; s < S; s += 2, dst += 2 * vstride, src += 2 * B * Q) st_global_ef(dst, *src, pol);
+                } else {
+                    for (; s < S; s += 2, dst += 2 * vstride, src += 2 * B * Q) {
+                        const uint4 v = *src;
+                        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                        for (int j = 0; j < wbytes - xb; ++j) dst[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+                    }
+                }
+            }
         }
-        prev_st = st;
-    }
-    if (gt == 0) {
-        // release the remaining root segments of this CTA's columns
-        if (nlev > 0) {
-            const int ncol_cta = (P.ncols - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-            for (; arrived_seg + 1 < ncol_cta * nsegc; ++arrived_seg) mbar_arrive(rempty + ((arrived_seg + 1) & 1));
-        }
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncthreads();                                      // stage and buffer q are reused
+        DSTAMP(6);
     }
 }
 
@@ -1076,7 +1018,7 @@ extern "C" int rlfc_dir_size(const rlfc_field* f, rlfc_dir* d, void* stream) {
 }
 
 extern "C" int rlfc_dir_build(const rlfc_field* f, rlfc_dir* d, void* stream) {
-    if (!f || !d || !d->scratch || !d->blob_off || !d->blobs || !d->root_rgb) return RLFC_ERR_ARGUMENT;
+    if (!f || !d || !d->scratch || !d->blob_off || !d->blobs || !d->root_rgb || !d->tables) return RLFC_ERR_ARGUMENT;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const dir::Geo g = dir::geo_of(*f);
     dir::Scratch sc;
@@ -1089,6 +1031,7 @@ extern "C" int rlfc_dir_build(const rlfc_field* f, rlfc_dir* d, void* stream) {
     if (nblob)
         dir::k_dir_hdr<<<(unsigned)((nblob + 255) / 256), 256, 0, s>>>(nblob, sc.blob_n, d->blob_off, d->blobs);
     dir::k_dir_root_rgb<<<1184, 256, 0, s>>>(*f, d->root_rgb, d->rgb_stride);
+    dir::k_dir_tables<<<1, 256, 0, s>>>(f->quant_shift, d->tables);
     return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }
 
@@ -1096,7 +1039,8 @@ extern "C" int rlfc_decode_field_dir(const rlfc_field* f, const rlfc_dir* d, int
                                      int32_t by_hi, uint8_t* rgb, int64_t img_stride, int64_t row_stride,
                                      uint64_t* status, void* stream) {
     using namespace dir;
-    if (!f || !d || !rgb || !status || !d->blobs || !d->blob_off || !d->root_rgb) return RLFC_ERR_ARGUMENT;
+    if (!f || !d || !rgb || !status || !d->blobs || !d->blob_off || !d->root_rgb || !d->tables)
+        return RLFC_ERR_ARGUMENT;
     if (!in_envelope(*f)) return RLFC_ERR_ARGUMENT;
     if (stop_level < 0 || stop_level > f->tree_height || by_lo < 0 || by_hi > f->hb || by_lo > by_hi)
         return RLFC_ERR_ARGUMENT;
@@ -1108,6 +1052,8 @@ extern "C" int rlfc_decode_field_dir(const rlfc_field* f, const rlfc_dir* d, int
     Params P{};
     P.S = f->s_count;
     P.T = f->t_count;
+    P.W = f->width;
+    P.H = f->height;
     P.h = f->tree_height;
     P.k = stop_level;
     P.nlev = f->tree_height - stop_level;
@@ -1118,75 +1064,45 @@ extern "C" int rlfc_decode_field_dir(const rlfc_field* f, const rlfc_dir* d, int
     P.rsx = f->rsx;
     P.rsy = f->rsy;
     P.by_lo = by_lo;
-    P.ncols = (by_hi - by_lo) * g.nchunks;
     for (int l = 0; l < MAXL; ++l) P.row_base[l] = g.row_base[l];
     P.blobs = d->blobs;
     P.blob_off = d->blob_off;
     P.root_rgb = d->root_rgb;
+    P.tables = d->tables;
     P.roots = f->roots;
     P.rgb_stride = d->rgb_stride;
     P.hp = f->hp;
     P.wp = f->wp;
     P.status = status;
     P.shift = f->quant_shift;
-    // shared memory plan (one CTA per SM)
+    // shared memory: tile scratch + residual slots | raw root rows of the
+    // segment | column blob offsets | blob pointers | two tile buffers
+    // (RGB(root) rows + blobs)
     const bool r16 = f->quant_shift <= 4;                  // |residual| <= 16392 fits int16
     const int vt = r16 ? 2 : 4;
     auto al = [](int x) { return (x + 127) & ~127; };
-    int off = al(8 * (2 * 32 + 4));                          // barriers (<= 32 stages)
-    P.off_tab = off;
-    off = al(off + 2048 * vt + 368 * 2);
+    P.rescap = 256;
+    int off = al(SRES_OFF + P.rescap * 16 * vt);
+    P.off_roots = off;
+    off = al(off + f->rsx * 3 * B * TW * 2);
     P.off_colofs = off;
     off = al(off + 4 * (g.R + 1));
-    P.off_roots = off;
-    P.roots_bytes = f->rsx * 3 * B * TW * 2;
-    off = al(off + 2 * P.roots_bytes);
-    P.out_bytes = f->s_count * B * TW * 3;
-    P.rgb_bytes = f->rsx * B * TW * 3;
+    P.off_bptr = off;
+    off = al(off + 2 * 8 * MAXL);
+    P.off_rgb = off;
+    off = al(off + f->rsx * B * TW * 3);
     P.blob_cap = 3072;
-    P.stage_bytes = al(P.out_bytes + P.rgb_bytes + P.blob_cap + (int)sizeof(StageInfo));
-    static int smem_max = 0, sms = 0;
-    if (!smem_max) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    // stages first (2 per group, at least one more than the groups), the rest
-    // to the groups' residual slots
-    const int fixed_grp = SRES_OFF;
-    int rescap = 0;
-    for (P.D = NG + 3; P.D > NG; --P.D) {
-        const int left = smem_max - off - P.D * P.stage_bytes;
-        rescap = left > 0 ? ((left / NG - fixed_grp) / (16 * vt)) & ~31 : 0;
-        if (rescap >= 256) break;
-    }
-    if (rescap > RESCAP_MAX) rescap = RESCAP_MAX;
-    if (rescap < 64) return RLFC_ERR_ARGUMENT;
-    P.rescap = rescap;
-    P.grp_bytes = al(fixed_grp + rescap * 16 * vt);
-    P.off_grp = off;
-    off = al(off + NG * P.grp_bytes);
+    P.buf_bytes = al(P.blob_cap + 64);
+    P.off_buf = off;
+    off += 2 * P.buf_bytes;
     P.off_stage = off;
-    const int smem = off + P.D * P.stage_bytes;
-    if (smem > smem_max) return RLFC_ERR_ARGUMENT;
-    // tensor maps: output (x bytes, rows of the band, t, s), RGB(root) rows,
-    // raw root planes
-    const int nrows = min(by_hi * B, f->height) - by_lo * B;
-    CUtensorMap out_map;
-    memset(&out_map, 0, sizeof(out_map));
-    {
-        const cuuint64_t dims[4] = {(cuuint64_t)f->width * 3, (cuuint64_t)nrows, (cuuint64_t)f->t_count,
-                                    (cuuint64_t)f->s_count};
-        const cuuint64_t strides[3] = {(cuuint64_t)row_stride, (cuuint64_t)img_stride,
-                                       (cuuint64_t)img_stride * f->t_count};
-        const cuuint32_t box[4] = {(cuuint32_t)(TW * 3), (cuuint32_t)B, 1u, (cuuint32_t)f->s_count};
-        if (!encode_map(&out_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, rgb, dims, strides, box)) return RLFC_ERR_ARGUMENT;
-    }
-    auto kern = r16 ? k_field_dir<int16_t> : k_field_dir<int32_t>;
+    off = al(off + f->s_count * B * TW * 3);
+    const int smem = off;
+    auto kern = r16 ? k_seg_dir<int16_t> : k_seg_dir<int32_t>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int grid = min(P.ncols, sms);
-    kern<<<grid, NT, smem, s>>>(P, out_map);
+    const int nsegc = ((f->t_count - 1) >> f->tree_height) + 1;
+    const dim3 grid((unsigned)g.nchunks, (unsigned)(nsegc * (by_hi - by_lo)));
+    kern<<<grid, CT, smem, s>>>(P, rgb, img_stride, row_stride);
     if (d->n_flagged > 0 && d->flagged) {
         const int nv = f->s_count * f->t_count;
         k_fixup<<<dim3((unsigned)d->n_flagged, (unsigned)((nv + 127) / 128)), 128, 0, s>>>(

@@ -125,6 +125,9 @@ class DeviceField:
                                       device=dev)
                 root_rgb = torch.empty(max(16, d.root_rgb_bytes),
                                        dtype=torch.uint8, device=dev)
+                tables = torch.empty(_native.DIR_TABLE_BYTES,
+                                     dtype=torch.uint8, device=dev)
+                d.tables = tables.data_ptr()
                 d.scratch = scratch.data_ptr()
                 d.blob_off = blob_off.data_ptr()
                 d.flagged = flagged.data_ptr()
@@ -144,7 +147,7 @@ class DeviceField:
             d.scratch = None
             del scratch
             self._dir = Directory(d, blobs, blob_off, flagged, root_rgb,
-                                  build_ms)
+                                  tables, build_ms)
             return self._dir
 
     def staged_workspace(self, stream_handle):
@@ -186,11 +189,12 @@ class DeviceField:
 class Directory:
     """Device record directory of one DeviceField (rlfc_dir_build)."""
 
-    def __init__(self, c, blobs, blob_off, flagged, root_rgb, build_ms):
+    def __init__(self, c, blobs, blob_off, flagged, root_rgb, tables,
+                 build_ms):
         self.c = c
         self.ref = ctypes.byref(c)
         self.blobs, self.blob_off = blobs, blob_off
-        self.flagged, self.root_rgb = flagged, root_rgb
+        self.flagged, self.root_rgb, self.tables = flagged, root_rgb, tables
         self.build_ms = build_ms
 
     @property
@@ -204,7 +208,8 @@ class Directory:
     @property
     def hbm_bytes(self):
         return sum(t.numel() * t.element_size() for t in
-                   (self.blobs, self.blob_off, self.flagged, self.root_rgb))
+                   (self.blobs, self.blob_off, self.flagged, self.root_rgb,
+                    self.tables))
 
 
 def tile_bytes_max(header, offsets):

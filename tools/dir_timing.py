@@ -41,29 +41,26 @@ def main():
     fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     for it in range(4):
         if it == 3:
             e0.record()
-        rc = fn(ctypes.addressof(df.cfield), ctypes.addressof(dr.c), 0, 0, hdr.block_grid[1], out.data_ptr(),
+        rc = fn(ctypes.addressof(df.cfield), ctypes.addressof(dr.c), k, 0, hdr.block_grid[1], out.data_ptr(),
                 hdr.height * hdr.width * 3, hdr.width * 3, status.data_ptr(), None)
         assert rc == 0
     e1.record()
     torch.cuda.synchronize()
     print(f"variant {extra}: last call {e0.elapsed_time(e1):.3f} ms")
-    buf = np.zeros(16 * 256 * 10, dtype=np.int64)
+    buf = np.zeros(64 * 8 * 8, dtype=np.int64)
     assert D.rlfc_dir_debug_times(buf.ctypes.data_as(ctypes.c_void_p)) == 0
-    t = buf.reshape(16, 256, 10).astype(np.float64)
-    names = ["prod: wait empty", "prod: issue", "cons: wait full", "cons: phase A", "cons: phase B",
-             "cons: phase C + store barrier", "cons: store issue + read wait", "cons: tile total"]
-    pairs = [(0, 1), (1, 2), (3, 4), (4, 5), (5, 6), (6, 7), (7, 8), (3, 8)]
+    t = buf.reshape(64, 8, 8).astype(np.float64)
+    names = ["wait inputs (cp.async + barrier)", "stage prefill (thread 0)", "phase A + barrier",
+             "phase B + barrier", "phase C + barrier", "store + barrier", "tile total"]
+    pairs = [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (0, 6)]
+    ok = t[:, :, 6] > 0
     for n, (a, b) in zip(names, pairs):
-        d = (t[:, 8:240, b] - t[:, 8:240, a]) / 1e3
+        d = ((t[:, :, b] - t[:, :, a]) / 1e3)[ok]
         print(f"{n:34s} median {np.median(d):7.3f} us  mean {d.mean():7.3f} us")
-    # consumer tile period
-    per = np.diff(t[:, 8:240, 8], axis=1) / 1e3
-    print(f"{'cons: tile period':34s} median {np.median(per):7.3f} us  mean {per.mean():7.3f} us")
-    lead = (t[:, 8:240, 4] - t[:, 8:240, 2]) / 1e3   # data landed vs producer issue (lower bound: full wait end)
-    print(f"{'issue -> consumer got data':34s} median {np.median(lead):7.3f} us")
 
 
 if __name__ == "__main__":
