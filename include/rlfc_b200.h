@@ -136,13 +136,18 @@ int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
                              void *stream);
 
 /* Staged full-field decode: the same contract and output as
- * rlfc_decode_field, computed as three launches -- a record index (one lane
- * per record: bitmap popcount + descriptor walk, kernels.py:162-200), a
- * payload decode (one lane per present payload, kernels.py:128-159 +
- * 202-211) into a residual array, and a blend (residual gather by bitmap
- * rank + YCoCg-R inverse + clamp, colorspace.py:27-56) -- with the
- * intermediates in a caller-owned device workspace of
- * rlfc_decode_workspace_bytes(f, present_total) bytes (256-byte aligned).
+ * rlfc_decode_field, computed in two launches per call -- a payload decode
+ * (one lane per present payload, kernels.py:128-159 + 202-211) into a
+ * residual array, and a blend (residual gather by bitmap rank + YCoCg-R
+ * inverse + clamp, colorspace.py:27-56) -- over a record index that
+ * rlfc_staged_prepare builds ONCE per workspace: the stream-invariant part
+ * of the reference's per-image record walk (kernels.py:162-200: per present
+ * node its payload offset and descriptor; per record its slot base, bitmap
+ * words and word ranks; anomaly flags), as the reference builds its own
+ * init-time index (`chains`, decoder.py:40-44), plus the RGB8 of every root
+ * sample.  The workspace (rlfc_decode_workspace_bytes(f, present_total)
+ * bytes, 256-byte aligned, caller-owned) also holds the residuals; every
+ * call BISE-decodes every present payload of its block-row band.
  * present_total: the number of present nodes over all records
  * (rlfc_count_present).  Returns RLFC_ERR_ARGUMENT when the stream is
  * outside this path's envelope (block 4/8/16, S <= 64, h <= 8, level rows of
@@ -153,6 +158,9 @@ int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
 int rlfc_count_present(const rlfc_field *f, uint64_t *count, void *stream);
 int rlfc_decode_workspace_bytes(const rlfc_field *f, uint64_t present_total,
                                 uint64_t *bytes);
+int rlfc_staged_prepare(const rlfc_field *f, void *workspace,
+                        uint64_t workspace_bytes, uint64_t present_total,
+                        void *stream);
 int rlfc_decode_field_staged(const rlfc_field *f, int32_t stop_level,
                              const int32_t *image_slots, int32_t by_lo,
                              int32_t by_hi, uint8_t *rgb, int64_t img_stride,

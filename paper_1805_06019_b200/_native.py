@@ -76,6 +76,7 @@ _SIGS = {
     "rlfc_decode_field_simple": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "p"],
     "rlfc_count_present": ["p", "p", "p"],
+    "rlfc_staged_prepare": ["p", "p", "u", "u", "p"],
     "rlfc_decode_workspace_bytes": ["p", "u", "p"],
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "u", "u", "p", "p"],

@@ -157,6 +157,42 @@ __global__ void k_count_present(const __grid_constant__ rlfc_field f, unsigned l
     if ((threadIdx.x & 31) == 0 && n) atomicAdd(out, (unsigned long long)n);
 }
 
+// ---- prepared index: per-record present counts and their exclusive prefix ---------------
+__global__ void k_rec_count(const __grid_constant__ rlfc_field f, uint32_t* cnt) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * nblk) return;
+    const int c = (int)(i / nblk);
+    const int64_t blk = i % nblk;
+    uint64_t off, len;
+    cnt[i] = record_span(f, c, blk, off, len) ? popc_prefix(f.srv[c] + off, f.m_nodes) : 0u;
+}
+
+// In-place exclusive scan of n counts by one CTA of 1024 threads (each thread
+// a contiguous run); the total goes to *total.  Init-time only.
+__global__ void __launch_bounds__(1024) k_scan_bases(uint32_t* v, int64_t n, unsigned long long* total) {
+    __shared__ unsigned long long part[1024];
+    const int tid = threadIdx.x;
+    const int64_t per = (n + 1023) / 1024, lo = tid * per, hi = min(n, lo + per);
+    unsigned long long sum = 0;
+    for (int64_t i = lo; i < hi; ++i) sum += v[i];
+    part[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const unsigned long long y = tid >= o ? part[tid - o] : 0ull;
+        __syncthreads();
+        part[tid] += y;
+        __syncthreads();
+    }
+    unsigned long long run = part[tid] - sum;
+    for (int64_t i = lo; i < hi; ++i) {
+        const uint32_t x = v[i];
+        v[i] = (uint32_t)run;
+        run += x;
+    }
+    if (tid == 1023) *total = part[1023];
+}
+
 // Node size (descriptor + payload bytes) for B*B = 16 values from three
 // 64-bit immediates (5 bits per descriptor): no memory access in the walk's
 // dependent chain.
@@ -194,7 +230,7 @@ __device__ __forceinline__ uint32_t node_word(const uint32_t* A, int j, uint32_t
 // container.py:102-145); only those are indexed and decoded.
 template <int BSQ>
 __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_field f, int k, int by_lo,
-                                                   int by_hi, Ws w) {
+                                                   int by_hi, Ws w, const uint32_t* base_in) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");      // k_root_rgb may run alongside
     const int64_t nblk = (int64_t)f.wb * f.hb;
     const int64_t band = (int64_t)(by_hi - by_lo) * f.wb;
@@ -250,11 +286,19 @@ __global__ void __launch_bounds__(THREADS) k_index(const __grid_constant__ rlfc_
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
     }
-    unsigned long long wbase = 0;
-    if (lane == 31 && incl) wbase = atomicAdd(w.counter, (unsigned long long)incl);
-    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-    const uint64_t slot0 = wbase + incl - count;
-    if (!valid) return;
+    uint64_t slot0;
+    if (base_in) {
+        // prepared index: record slot bases are the exclusive prefix of the
+        // records' present counts in record order (k_scan_bases)
+        if (!valid) return;
+        slot0 = base_in[(int64_t)c * nblk + blk];
+    } else {
+        unsigned long long wbase = 0;
+        if (lane == 31 && incl) wbase = atomicAdd(w.counter, (unsigned long long)incl);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        slot0 = wbase + incl - count;
+        if (!valid) return;
+    }
     if (slot0 + count > w.cap) flag = 1;
     const int64_t ri = (int64_t)c * nblk + blk;
     if (fastbm && !flag) {
@@ -547,7 +591,8 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
 constexpr int PAY_CHUNK = 512;
 constexpr int PAY_BUF = 12 * 1024;       // staged SRV bytes per chunk (two buffers, dynamic shared memory)
 template <int BSQ, typename VT>
-__global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w, int l2_last) {
+__global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w, int l2_last,
+                                                      int by_lo, int by_hi) {
     __shared__ uint2 bucket[3][PAY_CHUNK];
     __shared__ uint32_t bslot[3][PAY_CHUNK];
     __shared__ int bcount[3];
@@ -561,8 +606,24 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
     if (BSQ == 16)
         for (int z = tid; z < 2048; z += THREADS) dq[z] = (VT)deq((uint32_t)z, shift);
-    const uint64_t n = min((uint64_t)*w.counter, w.cap);
     const int64_t nblk = (int64_t)f.wb * f.hb;
+    // the band's payload slots: per channel one contiguous run (prepared
+    // index: record bases ascend in record order), concatenated
+    uint64_t lo[3], len[3];
+    {
+        const uint64_t ntot = min((uint64_t)*w.counter, w.cap);
+        for (int c = 0; c < 3; ++c) {
+            const int64_t a = (int64_t)c * nblk + (int64_t)by_lo * f.wb, b = (int64_t)c * nblk + (int64_t)by_hi * f.wb;
+            const uint64_t sa = a < 3 * nblk ? w.rec_base[a] : ntot;
+            const uint64_t sb = b < 3 * nblk ? w.rec_base[b] : ntot;
+            lo[c] = min(sa, ntot);
+            len[c] = min(sb, ntot) > lo[c] ? min(sb, ntot) - lo[c] : 0;
+        }
+    }
+    const uint64_t n = len[0] + len[1] + len[2];
+    auto slot_of = [&](uint64_t v) -> uint64_t {
+        return v < len[0] ? lo[0] + v : v < len[0] + len[1] ? lo[1] + (v - len[0]) : lo[2] + (v - len[0] - len[1]);
+    };
     VT* res = static_cast<VT*>(w.res);
     uint64_t pol = 0;
     if (l2_last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -576,7 +637,7 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
             const uint64_t i = b0 + tid + q * THREADS;
-            e4[q] = i < n ? __ldg(w.entries + i) : make_uint2(0u, SKIP);
+            e4[q] = i < n ? __ldg(w.entries + slot_of(i)) : make_uint2(0u, SKIP);
         }
     };
     auto reduce_range = [&](const uint2* e4, int q) {
@@ -651,7 +712,7 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
             const int m = desc_mode((int)d);
             const int pos = atomicAdd(&bcount[m], 1);
             bucket[m][pos] = e;
-            bslot[m][pos] = (uint32_t)(base + tid + k2 * THREADS);
+            bslot[m][pos] = (uint32_t)slot_of(base + tid + k2 * THREADS);
         }
         const bool has_next = base + stride < n;
         uint2 entn[EPT];
@@ -733,8 +794,6 @@ struct BlendParams {
     int TW, NB, nchunks, nstrip;
     int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
     int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
-    int debug;                   // timing experiments only (RLFC_BLEND_DEBUG): 1 no tasks,
-                                 // 2 no store, 4 no input TMA, 8 no records, 16 no L2 hint
     int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
     int off_flag, off_mask, off_sbase, off_roots, off_rgb, off_cnt, off_list, off_stage,
         off_mbar;
@@ -880,7 +939,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     RLFC_BSTAMP(0);
 
     // ---- TMA: RGB(root) rows into every view's staging rows, raw roots ----------------
-    if (P.tma_in && tid >= BT - 32 && !(P.debug & 4)) {
+    if (P.tma_in && tid >= BT - 32) {
         // last warp (no record work when NR <= BT - 32): lane 0 arms the
         // barrier, then every lane issues its share of the tensor loads
         const uint32_t bar = smem_u32(mbar);
@@ -917,7 +976,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     for (int r = tid; r < NR; r += BT) {
         const int c = r >> (__ffs(NB) - 1), b = r & (NB - 1);
         uint32_t fl = 0;
-        if (b < nb && nlev > 0 && !(P.debug & 8)) {
+        if (b < nb && nlev > 0) {
             const int64_t blk = (int64_t)by * f.wb + bx0 + b;
             const int64_t ri = (int64_t)c * nblk + blk;
             {
@@ -1058,7 +1117,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         }
     }
     RLFC_BSTAMP(3);
-    if (P.tma_in && !(P.debug & 4)) {
+    if (P.tma_in) {
         const uint32_t bar = smem_u32(mbar);
         uint32_t done = 0;
         while (!done)
@@ -1078,7 +1137,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         // B = 4: one task per unit (all 16 pixels): the first present level
         // of each channel is two 16-byte gathers, all issued before any is
         // consumed, so a thread pays one round trip per unit
-        const int units = (P.debug & 1) ? 0 : cnt[0];
+        const int units = cnt[0];
         const VT* res = static_cast<const VT*>(P.res);
         for (int u = tid; u < units; u += BT) {
             const uint2 e = list[u];
@@ -1138,7 +1197,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         }
     } else {
         constexpr int TP = B * QB / 2;                   // tasks per unit
-        const int units = (P.debug & 1) ? 0 : cnt[0];
+        const int units = cnt[0];
         const VT* res = static_cast<const VT*>(P.res);
         for (int it = tid; it < units * TP; it += BT) {
             const int u = it / TP, j = it - u * TP;
@@ -1207,31 +1266,22 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
 
     // ---- store ------------------------------------------------------------------------
     const int nrows_band = min(by * B + B, f.height) - by * B;   // rows of this block row
-    if (P.debug & 2) {
-    } else if (P.store_mode == 2) {
+    if (P.store_mode == 2) {
         if (tid == 0) {
             // the output streams through L2 once: evict it first so the
             // record tables, residuals and root colours the other tiles
             // gather stay resident
             uint64_t pol = 0;
-            if (!(P.debug & 16)) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             for (int st = 0; st < P.nstrip; ++st) {
                 const int x0 = (bx0 * B + st * STRIP) * 3;
                 if (x0 >= f.width * 3) break;
-                if (P.debug & 16)
-                    asm volatile(
-                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                            &out_map),
-                        "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0),
-                        "r"(smem_u32(stage + st * S * B * STRIP * 3))
-                        : "memory");
-                else
-                    asm volatile(
-                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], "
-                        "[%5], %6;" ::"l"(&out_map),
-                        "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0),
-                        "r"(smem_u32(stage + st * S * B * STRIP * 3)), "l"(pol)
-                        : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], "
+                    "[%5], %6;" ::"l"(&out_map),
+                    "r"(x0), "r"((by - P.by_lo) * B), "r"(t), "r"(0), "r"(smem_u32(stage + st * S * B * STRIP * 3)),
+                    "l"(pol)
+                    : "memory");
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1339,17 +1389,11 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     constexpr int BSQ = B * B;
     const bool tma_ok = w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 &&
                         ((f.wp * (int)sizeof(RT)) % 16) == 0 && encode_fn() != nullptr;
-    // blend CTA shape: 96 threads on 64-pixel tiles by default. Tile
-    // residency is what bounds the blend (output bytes in flight / tile
-    // lifetime): at 64 registers, 96-thread CTAs fit 10 per SM (shared memory
-    // 10 x 22.6 KB) against 8 for 128 threads (455 vs 448 Gpix/s)
-    int bt = 96, tw = 64;
-    if (const char* e = getenv("RLFC_BLEND_THREADS")) {
-        const int v = atoi(e);
-        bt = v == 256 || v == 128 || v == 160 ? v : 96;
-    }
-    if (const char* e = getenv("RLFC_BLEND_TW")) tw = atoi(e) == 128 ? 128 : 64;
-    const char* dbg = getenv("RLFC_BLEND_DEBUG");
+    // blend CTA shape: 96 threads on 64-pixel tiles. Tile residency is what
+    // bounds the blend (output bytes in flight / tile lifetime): at 64
+    // registers, 96-thread CTAs fit 10 per SM (shared memory 10 x 22.6 KB)
+    // against 8 for 128 threads (455 vs 448 Gpix/s)
+    constexpr int bt = 96, tw = 64;
     Plan pl{};
     if (!plan_blend<RT>(f, k, !tma_ok, tw, pl)) return RLFC_ERR_ARGUMENT;
     BlendParams& P = pl.P;
@@ -1370,7 +1414,6 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     P.rk = w.rk;
     P.nwp = w.nwp;
     P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
-    P.debug = dbg ? atoi(dbg) : 0;
     const int h = f.tree_height, S = f.s_count;
     // output path
     const bool aligned = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride) & 15) == 0;
@@ -1408,11 +1451,9 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // Programmatic dependent launches (RLFC_PDL=0 disables): k_root_rgb runs
-    // alongside k_index's long record walks, and k_blend's CTAs start their
-    // TMA loads and record-table loads while k_payloads drains.
-    const char* pdl_env = getenv("RLFC_PDL");
-    const bool pdl = !pdl_env || atoi(pdl_env) != 0;
+    // Programmatic dependent launch: k_blend's CTAs start their TMA loads and
+    // record-table loads while k_payloads drains.
+    constexpr bool pdl = true;
     cudaLaunchAttribute pdl_attr[1];
     pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1426,38 +1467,20 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         c.numAttrs = programmatic && pdl ? 1 : 0;
         return c;
     };
-    auto root_rgb = [&](bool programmatic) {
-        if (!P.tma_in) return;
-        const int64_t n = (int64_t)nroot * (by_hi - by_lo) * B * (f.wp / 4);
-        const int64_t want = (n + THREADS - 1) / THREADS;
-        const cudaLaunchConfig_t c =
-            cfg_of(dim3((unsigned)(want < sms * 16 ? want : sms * 16)), dim3(THREADS), 0, programmatic);
-        cudaLaunchKernelEx(&c, k_root_rgb<RT>, f, w.root_rgb, w.rgb_stride, by_lo * B, by_hi * B);
-    };
-    if (k >= h) root_rgb(false);
     if (k < h) {
-        cudaMemsetAsync(w.counter, 0, 8, stream);
-        const int64_t nrec = 3ll * (by_hi - by_lo) * f.wb;
-        k_index<BSQ><<<(unsigned)((nrec + THREADS - 1) / THREADS), THREADS, 0, stream>>>(f, k, by_lo, by_hi, w);
-        root_rgb(true);
         const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
         const uint64_t cap_grid = (uint64_t)sms * 8;
         const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
         const int pdyn = BSQ == 16 ? 2 * PAY_BUF : 16;
         cudaFuncSetAttribute(k_payloads<BSQ, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdyn);
         // residual payloads are stored with an L2 evict-last policy so the
-        // blend's gathers hit L2 (RLFC_RES_L2_LAST=0 disables it)
-        const char* l2e = getenv("RLFC_RES_L2_LAST");
-        k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, l2e ? atoi(l2e) : 1);
+        // blend's gathers hit L2
+        k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, 1, by_lo, by_hi);
     }
-    auto kern = bt == 256 ? k_blend<B, VT, RT, 256>
-                : bt == 96  ? k_blend<B, VT, RT, 96>
-                : bt == 160 ? k_blend<B, VT, RT, 160>
-                            : k_blend<B, VT, RT, 128>;
+    auto kern = k_blend<B, VT, RT, bt>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     // tile residency is bounded by shared memory: ask for the largest carveout
-    if (!getenv("RLFC_BLEND_NOCARVE"))
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const dim3 grid((unsigned)P.nchunks, (unsigned)f.t_count, (unsigned)(by_hi - by_lo));
     {
         const cudaLaunchConfig_t c = cfg_of(grid, dim3(bt), pl.smem, k < h);
@@ -1509,6 +1532,40 @@ extern "C" int rlfc_decode_workspace_bytes(const rlfc_field* f, uint64_t present
     if (!f || !bytes) return RLFC_ERR_ARGUMENT;
     *bytes = staged::carve(*f, nullptr, present_total, nullptr);
     return staged::in_envelope(*f) ? RLFC_OK : RLFC_ERR_ARGUMENT;
+}
+
+extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_t workspace_bytes,
+                                   uint64_t present_total, void* stream) {
+    if (!f || !workspace) return RLFC_ERR_ARGUMENT;
+    if (!staged::in_envelope(*f)) return RLFC_ERR_ARGUMENT;
+    staged::Ws w;
+    if (staged::carve(*f, workspace, present_total, &w) > workspace_bytes) return RLFC_ERR_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0) return RLFC_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t nrec = 3ll * f->wb * f->hb;
+    cudaMemsetAsync(w.counter, 0, 8, s);
+    if (nrec > 0) {
+        staged::k_rec_count<<<(unsigned)((nrec + 255) / 256), 256, 0, s>>>(*f, w.rec_base);
+        staged::k_scan_bases<<<1, 1024, 0, s>>>(w.rec_base, nrec, w.counter);
+        const unsigned g = (unsigned)((nrec + staged::THREADS - 1) / staged::THREADS);
+        switch (f->block) {
+            case 4: staged::k_index<16><<<g, staged::THREADS, 0, s>>>(*f, 0, 0, f->hb, w, w.rec_base); break;
+            case 8: staged::k_index<64><<<g, staged::THREADS, 0, s>>>(*f, 0, 0, f->hb, w, w.rec_base); break;
+            default: staged::k_index<256><<<g, staged::THREADS, 0, s>>>(*f, 0, 0, f->hb, w, w.rec_base); break;
+        }
+    }
+    const bool tma_ok = (reinterpret_cast<uintptr_t>(f->roots) & 15) == 0 &&
+                        ((f->wp * (f->roots_i16 ? 2 : 4)) % 16) == 0;
+    if (tma_ok) {
+        const int64_t n = (int64_t)f->rsx * f->rsy * f->hp * (f->wp / 4);
+        const int64_t want = (n + staged::THREADS - 1) / staged::THREADS;
+        const unsigned g = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+        if (f->roots_i16)
+            staged::k_root_rgb<int16_t><<<g, staged::THREADS, 0, s>>>(*f, w.root_rgb, w.rgb_stride, 0, f->hp);
+        else
+            staged::k_root_rgb<int32_t><<<g, staged::THREADS, 0, s>>>(*f, w.root_rgb, w.rgb_stride, 0, f->hp);
+    }
+    return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }
 
 extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level, const int32_t* image_slots,

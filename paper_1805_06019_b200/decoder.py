@@ -152,10 +152,12 @@ class DeviceField:
 
     def staged_workspace(self, stream_handle):
         """(tensor, bytes, present_total) for the staged decode on one CUDA
-        stream, allocated on first use.  present_total (the number of
-        present nodes over all records) is counted on the device once per
-        field; the workspace holds the record index, the payload entries and
-        the decoded residuals (rlfc_staged.cu)."""
+        stream, allocated and prepared on first use.  present_total (the
+        number of present nodes over all records) is counted on the device
+        once per field; rlfc_staged_prepare then builds the stream-invariant
+        record index (payload entries, record tables) and the root colours
+        into the workspace, which also holds the decoded residuals of each
+        step (rlfc_staged.cu)."""
         torch = _torch()
         L = _native.lib()
         with self._ws_lock:
@@ -177,6 +179,12 @@ class DeviceField:
             if ws is None:
                 ws = torch.empty(self._ws_bytes, dtype=torch.uint8,
                                  device=self.device)
+                # the record index (payload entries, record tables) and the
+                # root colours are stream-invariant: built once per workspace
+                with torch.cuda.device(self.device):
+                    _native.check(L.rlfc_staged_prepare(
+                        self.ref, ws.data_ptr(), self._ws_bytes,
+                        self._present, stream_handle), "rlfc_staged_prepare")
                 self._ws[stream_handle] = ws
             return ws, self._ws_bytes, self._present
 
