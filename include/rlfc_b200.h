@@ -152,21 +152,25 @@ int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
  * (rlfc_count_present).  Returns RLFC_ERR_ARGUMENT when the stream is
  * outside this path's envelope (block 4/8/16, S <= 64, h <= 8, level rows of
  * <= 64 nodes, quantisation shift <= 20, SRV sections < 4 GiB); the caller
- * then uses rlfc_decode_field.  Records with any stream anomaly are decoded
- * by the reference-order walk, so values and the failure word are identical
- * to rlfc_decode_field's. */
+ * then uses rlfc_decode_field.  rlfc_staged_prepare (synchronous) also
+ * decodes every payload once and lists the records with any stream anomaly
+ * (bad descriptor, truncation, corrupt pack); it returns their number in
+ * *n_flagged, which each decode call takes back: units touching them are
+ * redone by the reference-order walk after the blend, so values and the
+ * failure word are identical to rlfc_decode_field's. */
 int rlfc_count_present(const rlfc_field *f, uint64_t *count, void *stream);
 int rlfc_decode_workspace_bytes(const rlfc_field *f, uint64_t present_total,
                                 uint64_t *bytes);
 int rlfc_staged_prepare(const rlfc_field *f, void *workspace,
                         uint64_t workspace_bytes, uint64_t present_total,
-                        void *stream);
+                        int32_t *n_flagged, void *stream);
 int rlfc_decode_field_staged(const rlfc_field *f, int32_t stop_level,
                              const int32_t *image_slots, int32_t by_lo,
                              int32_t by_hi, uint8_t *rgb, int64_t img_stride,
                              int64_t row_stride, void *workspace,
                              uint64_t workspace_bytes, uint64_t present_total,
-                             uint64_t *status, void *stream);
+                             int32_t n_flagged, uint64_t *status,
+                             void *stream);
 
 /* Device record directory: the stream-invariant part of the reference's
  * per-image record walk (kernels.py:162-200), done once per stream and GPU

@@ -76,10 +76,10 @@ _SIGS = {
     "rlfc_decode_field_simple": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "p"],
     "rlfc_count_present": ["p", "p", "p"],
-    "rlfc_staged_prepare": ["p", "p", "u", "u", "p"],
+    "rlfc_staged_prepare": ["p", "p", "u", "u", "p", "p"],
     "rlfc_decode_workspace_bytes": ["p", "u", "p"],
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
-                                 "u", "u", "p", "p"],
+                                 "u", "u", "i", "p", "p"],
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
     "rlfc_render_slab": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
                          "i", "i", "p", "p"],

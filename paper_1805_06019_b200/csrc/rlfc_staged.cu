@@ -79,6 +79,7 @@ struct Ws {
     uint32_t* bm;          // [nwp][3*nblk] record bitmaps as aligned 32-bit words (word-major:
                            // one level row's words of consecutive records are contiguous)
     uint32_t* rk;          // [nwp][3*nblk] slot of the first present node of each word
+    uint32_t* flist;       // [3*nblk + 1] records with a stream anomaly (prepare-time), count first
     int nwp;
     uint64_t cap;
 };
@@ -102,7 +103,8 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
     const uint64_t o_cnt = take(8), o_base = take(4 * nrec), o_flag = take(4 * nrec), o_ent = take(8 * cap),
                    o_res = take(cap * bsq * (uint64_t)value_bytes(f)),
                    o_rgb = take((uint64_t)f.rsx * f.rsy * f.hp * (uint64_t)rgb_stride),
-                   o_bm = take(4 * nrec * (uint64_t)nwp), o_rk = take(4 * nrec * (uint64_t)nwp);
+                   o_bm = take(4 * nrec * (uint64_t)nwp), o_rk = take(4 * nrec * (uint64_t)nwp),
+                   o_fl = take(4 * (nrec + 1));
     if (w) {
         uint8_t* b = static_cast<uint8_t*>(base);
         w->counter = reinterpret_cast<unsigned long long*>(b + o_cnt);
@@ -114,6 +116,7 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
         w->rgb_stride = rgb_stride;
         w->bm = reinterpret_cast<uint32_t*>(b + o_bm);
         w->rk = reinterpret_cast<uint32_t*>(b + o_rk);
+        w->flist = reinterpret_cast<uint32_t*>(b + o_fl);
         w->nwp = nwp;
         w->cap = cap;
     }
@@ -870,39 +873,58 @@ __device__ __forceinline__ int stage_off(int S, int s, int row, int px) {
     return (((px / STRIP) * S + s) * B + row) * (STRIP * 3) + (px % STRIP) * 3;
 }
 
-// Reference-order decode of one (view, block) whose records carry an anomaly:
-// walk_chain per channel (kernels.py:162-216) into the staging buffer, or the
-// failure word with the reference's key.
+// (view, block) units touching a record with a stream anomaly (bad
+// descriptor, truncation, corrupt pack: listed by rlfc_staged_prepare) are
+// skipped by the blend and redone afterwards by the reference-order walk
+// (kernels.py:162-216, decode_chain_core) for all three channels, over the
+// blend's output, with the failure word keyed as the reference meets it.
 template <int B>
-__device__ __noinline__ void unit_fallback(const BlendParams& P, uint8_t* stage, int s, int t, int by, int bx,
-                                           int px0) {
-    const rlfc_field& f = P.f;
+__global__ void k_fixup(const __grid_constant__ rlfc_field f, const uint32_t* flist, int k, const int32_t* slots,
+                        int by_lo, int by_hi, uint8_t* rgb, int64_t img_stride, int64_t row_stride,
+                        uint64_t* status) {
     constexpr int BSQ = B * B;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t ri = flist[1 + blockIdx.x];
+    const int64_t blk = ri % nblk;
+    const int by = (int)(blk / f.wb), bx = (int)(blk % f.wb);
+    if (by < by_lo || by >= by_hi) return;
+    const int v = blockIdx.y * blockDim.x + threadIdx.x;
+    if (v >= f.s_count * f.t_count) return;
+    const int slot = slots ? slots[v] : v;
+    if (slot < 0) return;
+    const int s = v / f.t_count, t = v % f.t_count;
     int32_t acc[3][BSQ];
-    const int img = s * f.t_count + t;
     for (int c = 0; c < 3; ++c) {
         for (int yy = 0; yy < B; ++yy)
             for (int xx = 0; xx < B; ++xx) acc[c][yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
-        const uint64_t off = f.offsets[c][(int64_t)by * f.wb + bx];
-        int st = walk_chain<BSQ>(f, f.srv[c] + off, s, t, P.k, acc[c], g_lut, node_bytes<BSQ>(), srv_avail(f, c, off));
+        const uint64_t off = f.offsets[c][blk];
+        int st = walk_chain<BSQ>(f, f.srv[c] + off, s, t, k, acc[c], g_lut, node_bytes<BSQ>(), srv_avail(f, c, off));
         if (st == WALK_OOB) st = 2;
         if (st) {
-            report(P.status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
+            report(status, ((((uint64_t)v) * 3 + c) * f.hb + by) * f.wb + bx, st);
             return;
         }
     }
-    for (int yy = 0; yy < B; ++yy)
+    for (int yy = 0; yy < B; ++yy) {
+        const int y = by * B + yy;
+        if (y >= f.height) break;
+        uint8_t* orow = rgb + (int64_t)slot * img_stride + (int64_t)(y - by_lo * B) * row_stride;
         for (int xx = 0; xx < B; ++xx) {
+            const int x = bx * B + xx;
+            if (x >= f.width) break;
             uint32_t r, g, b;
-            const int j = yy * B + xx;
-            ycocg_to_rgb8(acc[0][j], acc[1][j], acc[2][j], r, g, b);
-            uint8_t* o = stage + stage_off<B>(f.s_count, s, yy, px0 + xx);
-            o[0] = (uint8_t)r;
-            o[1] = (uint8_t)g;
-            o[2] = (uint8_t)b;
+            ycocg_to_rgb8(acc[0][yy * B + xx], acc[1][yy * B + xx], acc[2][yy * B + xx], r, g, b);
+            orow[3 * x] = (uint8_t)r;
+            orow[3 * x + 1] = (uint8_t)g;
+            orow[3 * x + 2] = (uint8_t)b;
         }
+    }
 }
 
+__global__ void k_flag_list(const uint32_t* rec_flag, int64_t nrec, uint32_t* flist) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nrec && rec_flag[i]) flist[1 + atomicAdd(flist, 1u)] = (uint32_t)i;
+}
 
 template <int B, typename VT, typename RT, int BT>
 __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__ BlendParams P,
@@ -1142,10 +1164,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         for (int u = tid; u < units; u += BT) {
             const uint2 e = list[u];
             const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
-            if (e.x >> 16) {
-                unit_fallback<B>(P, stage, s, t, by, bx0 + b, b * B);
-                continue;
-            }
+            if (e.x >> 16) continue;                 // anomalous record: k_fixup
             auto slot_of = [&](int c, uint32_t pc) -> uint32_t {
                 const int li = (__ffs(pc) - 1) / 3;
                 const int r = li * NR + c * NB + b;
@@ -1203,10 +1222,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
             const int u = it / TP, j = it - u * TP;
             const uint2 e = list[u];
             const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
-            if (e.x >> 16) {
-                if (j == 0) unit_fallback<B>(P, stage, s, t, by, bx0 + b, b * B);
-                continue;
-            }
+            if (e.x >> 16) continue;                 // anomalous record: k_fixup
             const int rx = s >> h;
             int row[2], px[2];
 #pragma unroll
@@ -1383,9 +1399,22 @@ static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_fir
     return false;
 }
 
+template <int BSQ, typename VT>
+static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi, int sms, cudaStream_t stream) {
+    const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
+    const uint64_t cap_grid = (uint64_t)sms * 8;
+    const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
+    const int pdyn = BSQ == 16 ? 2 * PAY_BUF : 16;
+    cudaFuncSetAttribute(k_payloads<BSQ, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdyn);
+    // residual payloads are stored with an L2 evict-last policy so the
+    // blend's gathers hit L2
+    k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, 1, by_lo, by_hi);
+}
+
 template <int B, typename VT, typename RT>
 static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
-                  int64_t img_stride, int64_t row_stride, const Ws& w, uint64_t* status, cudaStream_t stream) {
+                  int64_t img_stride, int64_t row_stride, const Ws& w, int n_flagged, uint64_t* status,
+                  cudaStream_t stream) {
     constexpr int BSQ = B * B;
     const bool tma_ok = w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 &&
                         ((f.wp * (int)sizeof(RT)) % 16) == 0 && encode_fn() != nullptr;
@@ -1467,16 +1496,7 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         c.numAttrs = programmatic && pdl ? 1 : 0;
         return c;
     };
-    if (k < h) {
-        const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
-        const uint64_t cap_grid = (uint64_t)sms * 8;
-        const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
-        const int pdyn = BSQ == 16 ? 2 * PAY_BUF : 16;
-        cudaFuncSetAttribute(k_payloads<BSQ, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdyn);
-        // residual payloads are stored with an L2 evict-last policy so the
-        // blend's gathers hit L2
-        k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, 1, by_lo, by_hi);
-    }
+    if (k < h) run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream);
     auto kern = k_blend<B, VT, RT, bt>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     // tile residency is bounded by shared memory: ask for the largest carveout
@@ -1485,6 +1505,11 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     {
         const cudaLaunchConfig_t c = cfg_of(grid, dim3(bt), pl.smem, k < h);
         cudaLaunchKernelEx(&c, kern, P, out_map, rgb_map, root_map);
+    }
+    if (n_flagged > 0 && k < h) {
+        const int nv = f.s_count * f.t_count;
+        k_fixup<B><<<dim3((unsigned)n_flagged, (unsigned)((nv + 63) / 64)), 64, 0, stream>>>(
+            f, w.flist, k, slots, by_lo, by_hi, rgb, img_stride, row_stride, status);
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -1535,7 +1560,7 @@ extern "C" int rlfc_decode_workspace_bytes(const rlfc_field* f, uint64_t present
 }
 
 extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_t workspace_bytes,
-                                   uint64_t present_total, void* stream) {
+                                   uint64_t present_total, int32_t* n_flagged, void* stream) {
     if (!f || !workspace) return RLFC_ERR_ARGUMENT;
     if (!staged::in_envelope(*f)) return RLFC_ERR_ARGUMENT;
     staged::Ws w;
@@ -1554,6 +1579,26 @@ extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_
             default: staged::k_index<256><<<g, staged::THREADS, 0, s>>>(*f, 0, 0, f->hb, w, w.rec_base); break;
         }
     }
+    // every payload decoded once here too: corrupt packs flag their records
+    // (kernels.py:147-150), so the anomaly list below is complete
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const bool small = f->quant_shift <= 4;
+        switch (f->block) {
+            case 4: small ? staged::run_payloads<16, int16_t>(*f, w, 0, f->hb, sms, s)
+                          : staged::run_payloads<16, int32_t>(*f, w, 0, f->hb, sms, s); break;
+            case 8: small ? staged::run_payloads<64, int16_t>(*f, w, 0, f->hb, sms, s)
+                          : staged::run_payloads<64, int32_t>(*f, w, 0, f->hb, sms, s); break;
+            default: small ? staged::run_payloads<256, int16_t>(*f, w, 0, f->hb, sms, s)
+                           : staged::run_payloads<256, int32_t>(*f, w, 0, f->hb, sms, s); break;
+        }
+    }
+    cudaMemsetAsync(w.flist, 0, 4, s);
+    if (nrec > 0) staged::k_flag_list<<<(unsigned)((nrec + 255) / 256), 256, 0, s>>>(w.rec_flag, nrec, w.flist);
+    uint32_t nf = 0;
+    cudaMemcpyAsync(&nf, w.flist, 4, cudaMemcpyDeviceToHost, s);
     const bool tma_ok = (reinterpret_cast<uintptr_t>(f->roots) & 15) == 0 &&
                         ((f->wp * (f->roots_i16 ? 2 : 4)) % 16) == 0;
     if (tma_ok) {
@@ -1565,13 +1610,16 @@ extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_
         else
             staged::k_root_rgb<int32_t><<<g, staged::THREADS, 0, s>>>(*f, w.root_rgb, w.rgb_stride, 0, f->hp);
     }
+    if (cudaStreamSynchronize(s) != cudaSuccess) return RLFC_ERR_CUDA;
+    if (n_flagged) *n_flagged = (int32_t)nf;
     return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }
 
 extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level, const int32_t* image_slots,
                                         int32_t by_lo, int32_t by_hi, uint8_t* rgb, int64_t img_stride,
                                         int64_t row_stride, void* workspace, uint64_t workspace_bytes,
-                                        uint64_t present_total, uint64_t* status, void* stream) {
+                                        uint64_t present_total, int32_t n_flagged, uint64_t* status,
+                                        void* stream) {
     if (!f || !rgb || !status || !workspace) return RLFC_ERR_ARGUMENT;
     if (stop_level < 0 || stop_level > f->tree_height || by_lo < 0 || by_hi > f->hb || by_lo > by_hi)
         return RLFC_ERR_ARGUMENT;
@@ -1585,15 +1633,15 @@ extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level,
 #define RLFC_STAGED(B_)                                                                                            \
     if (small && r16)                                                                                              \
         return staged::launch<B_, int16_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, status, s);                                     \
+                                                    row_stride, w, n_flagged, status, s);                                     \
     if (small)                                                                                                     \
         return staged::launch<B_, int16_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, status, s);                                     \
+                                                    row_stride, w, n_flagged, status, s);                                     \
     if (r16)                                                                                                       \
         return staged::launch<B_, int32_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, status, s);                                     \
+                                                    row_stride, w, n_flagged, status, s);                                     \
     return staged::launch<B_, int32_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,       \
-                                                row_stride, w, status, s);
+                                                row_stride, w, n_flagged, status, s);
     switch (f->block) {
         case 4: { RLFC_STAGED(4) }
         case 8: { RLFC_STAGED(8) }

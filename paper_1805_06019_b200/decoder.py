@@ -151,7 +151,7 @@ class DeviceField:
             return self._dir
 
     def staged_workspace(self, stream_handle):
-        """(tensor, bytes, present_total) for the staged decode on one CUDA
+        """(tensor, bytes, present_total, n_flagged) for the staged decode on one CUDA
         stream, allocated and prepared on first use.  present_total (the
         number of present nodes over all records) is counted on the device
         once per field; rlfc_staged_prepare then builds the stream-invariant
@@ -179,14 +179,18 @@ class DeviceField:
             if ws is None:
                 ws = torch.empty(self._ws_bytes, dtype=torch.uint8,
                                  device=self.device)
-                # the record index (payload entries, record tables) and the
-                # root colours are stream-invariant: built once per workspace
+                # the record index (payload entries, record tables), the
+                # anomaly list and the root colours are stream-invariant:
+                # built once per workspace
+                nflag = ctypes.c_int32(0)
                 with torch.cuda.device(self.device):
                     _native.check(L.rlfc_staged_prepare(
                         self.ref, ws.data_ptr(), self._ws_bytes,
-                        self._present, stream_handle), "rlfc_staged_prepare")
+                        self._present, ctypes.byref(nflag), stream_handle),
+                        "rlfc_staged_prepare")
+                ws = (ws, int(nflag.value))
                 self._ws[stream_handle] = ws
-            return ws, self._ws_bytes, self._present
+            return ws[0], self._ws_bytes, self._present, ws[1]
 
     @property
     def hbm_bytes(self):
@@ -449,8 +453,8 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
                         rc = L.rlfc_decode_field_staged(
                             df.ref, stop_level, slots_p, by_lo, by_hi,
                             out.data_ptr(), nrows * W * 3, W * 3,
-                            ws[0].data_ptr(), ws[1], ws[2], status.data_ptr(),
-                            stream)
+                            ws[0].data_ptr(), ws[1], ws[2], ws[3],
+                            status.data_ptr(), stream)
                     if rc != _native.RLFC_ERR_ARGUMENT:
                         _native.check(rc, "rlfc_decode_field_staged")
                         done = True
@@ -487,7 +491,7 @@ def decode_field_slots(state, stop_level, slots, n, device=None):
                 rc = L.rlfc_decode_field_staged(
                     df.ref, stop_level, slots.data_ptr(), 0, hb,
                     out.data_ptr(), H * W * 3, W * 3, ws[0].data_ptr(), ws[1],
-                    ws[2], status.data_ptr(), stream)
+                    ws[2], ws[3], status.data_ptr(), stream)
         if rc == _native.RLFC_ERR_ARGUMENT:
             rc = L.rlfc_decode_field(df.ref, stop_level, slots.data_ptr(), 0,
                                      hb, out.data_ptr(), H * W * 3, W * 3,
@@ -768,7 +772,7 @@ class HostPipeline:
                 if ws is not None:
                     rc = L.rlfc_decode_field_staged(
                         df.ref, 0, None, lo, hi, dst, img, W * 3,
-                        ws[0].data_ptr(), ws[1], ws[2],
+                        ws[0].data_ptr(), ws[1], ws[2], ws[3],
                         self.status.data_ptr(), s_dec.cuda_stream)
                 if rc == _native.RLFC_ERR_ARGUMENT:
                     rc = L.rlfc_decode_field(

@@ -146,7 +146,7 @@ def test_staged_path_taken(rl, name):
     from paper_1805_06019_b200 import _native
     st = state_for(rl, name)
     df = st.device_field()
-    ws, nbytes, present = df.staged_workspace(0)
+    ws, nbytes, present, nflag = df.staged_workspace(0)
     hdr = st.header
     out = torch.empty((hdr.s_count, hdr.t_count, hdr.height, hdr.width, 3),
                       dtype=torch.uint8, device="cuda")
@@ -154,7 +154,7 @@ def test_staged_path_taken(rl, name):
     rc = _native.lib().rlfc_decode_field_staged(
         df.ref, 0, None, 0, hdr.block_grid[1], out.data_ptr(),
         hdr.height * hdr.width * 3, hdr.width * 3, ws.data_ptr(), nbytes,
-        present, status.data_ptr(), 0)
+        present, nflag, status.data_ptr(), 0)
     assert rc == _native.RLFC_OK
     torch.cuda.synchronize()
     assert status.item() == 0
