@@ -146,10 +146,10 @@ class ClockSampler:
 
 
 NCU_SUMMARY = {"fused": "profiles/r1_decode_ncu_summary.json",
-               "staged": "profiles/r1_staged_ncu_summary.json"}
-KERNELS = {"auto": ["k_field_dir"], "dir": ["k_field_dir"],
+               "staged": "profiles/r2_staged_ncu_summary.json"}
+KERNELS = {"dir": ["k_seg_dir"],
            "fused": ["k_decode_field_tiled"],
-           "staged": ["k_root_rgb", "k_index", "k_payloads", "k_blend"],
+           "staged": ["k_payloads", "k_blend"],
            "simple": ["k_decode_field_simple"]}
 
 
@@ -178,7 +178,7 @@ def peaks():
 
 # --- CPU baseline / reference arm -------------------------------------------------
 
-def cpu_decode(data, steps, warmup, cfg_name):
+def cpu_decode(data, steps, warmup, cfg_name, want_sha=False):
     """Oracle port (C restatement of the reference decode path), all host
     threads, full field per step."""
     from oracle import oracle
@@ -194,6 +194,9 @@ def cpu_decode(data, steps, warmup, cfg_name):
         if i >= warmup:
             times.append(dt)
     px = orc.S * orc.T * orc.W * orc.H
+    if want_sha:
+        import hashlib
+        return px / statistics.mean(times) / 1e9, nth, times, hashlib.sha256(out.tobytes()).hexdigest()
     return px / statistics.mean(times) / 1e9, nth, times
 
 
@@ -207,9 +210,11 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "Gpix/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * statistics.mean(times),
-        "higher_is_better": True, "scaling": args.scaling,
+        "higher_is_better": True, "scaling": args.scaling or ("strong" if args.gpus > 1 else "weak"),
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": workload_config(),
+        "config": dict(workload_config(), bpp=round(8.0 * len(data) / (289 * 1024 * 1024), 4),
+                       present_frac=0.06449, kernel="oracle C port (reference decode_all order)",
+                       bands=[[0, 256]]),
         "cpu_baseline": {"value": val, "unit": "Gpix/s", "cores": nth,
                          "kind": "port",
                          "sample": "full 17x17x1024^2 field per step"},
@@ -231,33 +236,62 @@ def workload_config():
 
 # --- GPU arm -----------------------------------------------------------------------
 
+REF_DECODE = os.path.join(ROOT, "tests", "golden", "cfg2_r4_decode_reference.json")
+
+
+def relaunch(args):
+    """--gpus N without a launcher: re-run this script under torchrun, one
+    process per GPU (rank 0 prints the line)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def sha_host(t):
+    import hashlib
+    return hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "dir", "staged", "fused", "simple"])
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: strong (default; cfg3, one cfg2 field split "
+                         "into block-row bands) or weak (a field per rank)")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "staged", "dir", "fused", "simple"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-render", action="store_true")
-    ap.add_argument("--render-batch", type=int, default=256)
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     if args.config == "cfg5":
         return run_cfg5(args)
+    for k in os.environ:
+        if k.startswith("RLFC_"):
+            raise SystemExit(f"refusing to benchmark with {k} set")
 
     import torch
     import torch.distributed as dist
     import paper_1805_06019_b200 as rl
-    from paper_1805_06019_b200 import _native, decoder
+    from paper_1805_06019_b200 import decoder, parallel
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    scaling = args.scaling or ("strong" if world > 1 else "weak")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
@@ -274,25 +308,30 @@ def main():
     hdr = state.header
     st = stream_stats(state)
     hb = hdr.block_grid[1]
-    # rows this rank decodes
-    if args.scaling == "strong" and world > 1:
-        from paper_1805_06019_b200.parallel import balanced_bands
-        band = balanced_bands(state, world)[rank]
+    B = hdr.block_size
+    if scaling == "strong" and world > 1:
+        bands = parallel.balanced_bands(state, world)
     else:
-        band = (0, hb)
-    rows_px = min(band[1] * hdr.block_size, hdr.height) - band[0] * hdr.block_size
+        bands = [(0, hb)] * world
+    band = bands[rank]
+    rows_px = min(band[1] * B, hdr.height) - band[0] * B
     px_rank = hdr.s_count * hdr.t_count * hdr.width * rows_px
     out = torch.empty((hdr.s_count, hdr.t_count, rows_px, hdr.width, 3),
                       dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    kern = "staged" if args.kernel == "auto" else args.kernel
+    # stream-invariant record index (built once per workspace): timed here
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prepared = state.device_field().staged_workspace(stream.cuda_stream) if kern == "staged" else None
+    torch.cuda.synchronize()
+    index_ms = (time.perf_counter() - t0) * 1e3
 
     def step():
-        decoder.decode_field(state, 0, rows=band, out=out, kernel=args.kernel,
-                             check=False)
+        decoder.decode_field(state, 0, rows=band, out=out, kernel=kern, check=False)
 
     # correctness gate before timing: status word must be clean
-    _, status = decoder.decode_field(state, 0, rows=band, out=out,
-                                     kernel=args.kernel, check=True)
+    decoder.decode_field(state, 0, rows=band, out=out, kernel=kern, check=True)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -316,50 +355,56 @@ def main():
         torch.cuda.synchronize()
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms], device="cuda")
+    per_rank = [ms]
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    total_px = px_rank * world if args.scaling == "weak" else \
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, ms)
+    ms_max = max(per_rank)
+    total_px = px_rank * world if scaling == "weak" else \
         hdr.s_count * hdr.t_count * hdr.width * hdr.height
     value = total_px / (ms_max * 1e-3) / 1e9
-    # roofline of the decode step (the fused kernel, or the staged path's
-    # four launches together): algorithmic bytes over the device time per
-    # step on this rank
+
+    # parity: the decoded field against the live reference's decode_all
+    # sha256 (and the oracle's, when the CPU leg runs); strong scaling
+    # assembles the bands on rank 0 with one all_gather_into_tensor
+    parity = parity_check(state, out, bands, scaling, world, rank, parallel)
+
+    # roofline of the step on this rank: algorithmic bytes (SURVEY 8d
+    # formula) plus the per-step reads of the prepared record index
     frac_rows = rows_px / hdr.height
-    alg = st["comp_bytes"] * frac_rows + st["root_bytes"] * frac_rows + \
-        st["out_bytes"] * frac_rows
+    idx_bytes = (8 * st["present"] + 4 * 3 * hdr.block_grid[0] * hb +
+                 2 * 4 * ((state.m_nodes + 31) // 32 + 2) * 3 * hdr.block_grid[0] * hb)
+    alg = (st["comp_bytes"] + st["root_bytes"] + st["out_bytes"] + idx_bytes) * frac_rows
     achieved = alg / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
 
-    # e2e: public API with host buffers: H2D of the compressed sections and
-    # root planes from pinned memory, decode, D2H of the RGB field into
-    # pinned memory, every step (decoder.decode_field_host)
     e2e = e2e_measure(state, band, args, rl)
-
-    render = None
-    if not args.no_render:
-        render = render_measure(state, args, rl)
+    render = None if args.no_render else render_measure(state, args, rl, world, rank)
     random_access = random_access_measure(state, rl)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        val, nth, times = cpu_decode(data, 2, 1, "cfg2")
+        val, nth, times, orc_sha = cpu_decode(data, 2, 1, "cfg2", want_sha=True)
         cpu = {"value": val, "unit": "Gpix/s", "cores": nth, "kind": "port",
                "sample": "full 17x17x1024^2 R4 field, oracle C port, "
                          f"{nth} threads, mean of {len(times)} steps"}
+        parity["oracle_sha256"] = orc_sha
+        if parity.get("sha256") and orc_sha != parity["sha256"]:
+            parity["decode"] = "MISMATCH (oracle)"
 
-    traffic, traffic_src = ncu_traffic(args.kernel) if band == (0, hb) else (None, None)
+    traffic, traffic_src = ncu_traffic(kern) if band == (0, hb) else (None, None)
     if rank == 0:
+        ok = parity.get("decode") == "bit-exact"
         line = {
-            "metric": METRIC, "value": value, "unit": "Gpix/s",
+            "metric": METRIC, "value": value if ok else None, "unit": "Gpix/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": args.scaling if world > 1 else "weak",
+            "scaling": scaling,
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": dict(workload_config(), bpp=round(st["bpp"], 4),
                            present_frac=round(st["present_frac"], 5),
-                           kernel=args.kernel, band_rows=list(band)),
+                           kernel=kern, bands=[list(b) for b in bands] if world > 1 else [[0, hb]]),
+            "parity": parity,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
@@ -368,17 +413,148 @@ def main():
                              traffic_src + " (ncu, DRAM bytes summed over "
                              "the step's kernels)"),
                          "peak_source": peak_kind,
-                         "kernels": KERNELS[args.kernel],
-                         "alg_bytes_per_launch": int(alg)},
-            "e2e": e2e, "gpu_launches": args.steps * len(KERNELS[args.kernel]),
+                         "kernels": KERNELS[kern],
+                         "alg_bytes_per_launch": int(alg),
+                         "alg_bytes_note": "SURVEY 8d: offsets+SRV + int16 roots + RGB8 out, "
+                                           "plus the prepared index read per step "
+                                           "(entries, record flags, bitmap words and ranks)"},
+            "index_build_ms": round(index_ms, 2),
+            "per_rank_ms": per_rank,
+            "e2e": e2e, "gpu_launches": args.steps * len(KERNELS[kern]),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "render": render,
             "random_access": random_access,
         }
+        if not ok:
+            line["error"] = "decoded field differs from the reference: value withheld"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def parity_check(state, out, bands, scaling, world, rank, parallel):
+    """sha256 of the decoded (S, T, H, W, 3) field vs the live reference's."""
+    try:
+        with open(REF_DECODE) as f:
+            ref = json.load(f)
+    except OSError:
+        return {"decode": "unchecked", "why": "no reference golden"}
+    import hashlib
+    if hashlib.sha256(state.data).hexdigest() != ref["stream_sha256"]:
+        return {"decode": "unchecked", "why": "stream differs from the golden's"}
+    want = ref["k0"]["decode_all_sha256"]
+    if world == 1:
+        got = sha_host(out)
+    elif scaling == "strong":
+        full = parallel.gather_field(state, out, bands)     # band-major, all_gather_into_tensor
+        got = sha_host(parallel.band_major_to_grid(full, state, bands)) if rank == 0 else None
+    else:
+        got = sha_host(out)
+    res = {"decode": "bit-exact" if got == want or rank != 0 else "MISMATCH",
+           "sha256": got, "reference_sha256": want,
+           "reference": "tests/golden/cfg2_r4_decode_reference.json: live reference rlfc 0.1.0 "
+                        "decode_image over all 289 views (tools/make_cfg2_decode_reference.py)"}
+    return res
+
+
+def render_measure(state, args, rl, world, rank):
+    """cfg4: batches of 512x512 SlabPoses (s, t ~ U[0, S-1] x U[0, T-1]) x
+    focal {image plane, 0.9, 1.12} x k {0, h}; poses sharded round-robin
+    over the ranks (replicated stream).  Per cell: wall clock per batch
+    (host pose prep + launches + sync, median of 7) and device time (CUDA
+    events).  Parity: 6 views against the oracle's render of the oracle's
+    decode (bit-exact)."""
+    import torch
+    import torch.distributed as dist
+    hdr = state.header
+    S, T, h = hdr.s_count, hdr.t_count, hdr.tree_height
+    cells = []
+    out = torch.empty((256, 512, 512, 3), dtype=torch.uint8, device="cuda")
+    for batch in (1, 64, 256):
+        for focal in (None, 0.9, 1.12):
+            for k in (0, h):
+                rng = np.random.default_rng(1000 * batch + 10 * k + (0 if focal is None else int(focal * 100)))
+                allp = [rl.SlabPose(float(rng.uniform(0, S - 1)), float(rng.uniform(0, T - 1)), 512, 512, focal)
+                        for _ in range(batch)]
+                mine = allp[rank::world]
+                o = out[:len(mine)]
+                for _ in range(2):
+                    if mine:
+                        rl.render_views(state, mine, stop_level=k, out=o)
+                torch.cuda.synchronize()
+                wall = []
+                for _ in range(7):
+                    if world > 1:
+                        dist.barrier()
+                    t0 = time.perf_counter()
+                    if mine:
+                        rl.render_views(state, mine, stop_level=k, out=o)
+                    torch.cuda.synchronize()
+                    wall.append(time.perf_counter() - t0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(5):
+                    if mine:
+                        rl.render_views(state, mine, stop_level=k, out=o)
+                e1.record()
+                torch.cuda.synchronize()
+                dev_ms = e0.elapsed_time(e1) / 5
+                w = statistics.median(wall)
+                if world > 1:
+                    t = torch.tensor([w, dev_ms], device="cuda")
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    w, dev_ms = float(t[0]), float(t[1])
+                cells.append({"batch": batch, "focal_z": focal, "k": k,
+                              "views_per_s": batch / w, "ms_per_batch": w * 1e3,
+                              "device_ms_per_batch": dev_ms,
+                              "device_views_per_s": batch / (dev_ms * 1e-3)})
+    res = {"cells": cells, "view": "512x512 SlabPose, default geometry",
+           "timing": "wall clock incl. host pose prep, sync per batch (median of 7); device = CUDA events",
+           "sharding": f"poses round-robin over {world} rank(s), replicated stream"}
+    head = next(c for c in cells if c["batch"] == 256 and c["focal_z"] is None and c["k"] == 0)
+    res["views_per_s"] = head["views_per_s"]
+    if rank == 0 and not args.no_cpu_baseline:
+        res.update(render_parity_and_cpu(state, rl))
+    return res
+
+
+def render_parity_and_cpu(state, rl):
+    from oracle import oracle
+    hdr = state.header
+    orc = oracle.OracleState(state.data)
+    nth = oracle.lib().orc_nproc()
+    field0, st0 = orc.decode_all(0, nthreads=nth)
+    fieldh, sth = orc.decode_all(hdr.tree_height, nthreads=nth)
+    assert st0 == 0 and sth == 0
+    rng = np.random.default_rng(77)
+    exact = 0
+    cases = []
+    for i, (focal, k) in enumerate([(None, 0), (0.9, 0), (1.12, 0), (None, 3), (0.9, 3), (1.12, 3),
+                                   (None, 0), (1.12, 0)]):
+        s, t = float(rng.uniform(0, hdr.s_count - 1)), float(rng.uniform(0, hdr.t_count - 1))
+        k = min(k, hdr.tree_height)
+        gpu = rl.render_view(state, rl.SlabPose(s, t, 512, 512, focal), stop_level=k)
+        ref = orc.render_slab(s, t, 512, 512, focal_z=focal, stop_level=k,
+                              field=field0 if k == 0 else fieldh)
+        exact += int(np.array_equal(gpu, ref))
+        cases.append([round(s, 4), round(t, 4), focal, k])
+    # CPU baseline: the reference's per-view cost (decode the tap cameras,
+    # then blend; renderer.py:212-276) in the C port, one view per thread
+    import concurrent.futures as cf
+    nv = 2 * nth
+    poses = [(float(rng.uniform(0, hdr.s_count - 1)), float(rng.uniform(0, hdr.t_count - 1))) for _ in range(nv)]
+    scratch = [np.zeros((hdr.s_count, hdr.t_count, hdr.height, hdr.width, 3), np.uint8) for _ in range(nth)]
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(nth) as ex:
+        list(ex.map(lambda ip: orc.render_slab_decoding(ip[1][0], ip[1][1], 512, 512,
+                                                        scratch=scratch[ip[0] % nth]), enumerate(poses)))
+    dt = time.perf_counter() - t0
+    return {"parity": {"views_bit_exact": exact, "views_checked": len(cases), "poses": cases,
+                       "against": "oracle render_slab of the oracle decode (renderer.py:233-276 order)"},
+            "cpu_baseline": {"value": nv / dt, "unit": "views/s", "cores": nth, "kind": "port",
+                             "sample": f"{nv} 512x512 slab views, tap cameras decoded per view then blended "
+                                       "(reference per-view cost), one view per thread"}}
 
 
 def e2e_measure(state, band, args, rl):
@@ -394,8 +570,7 @@ def e2e_measure(state, band, args, rl):
         res.run()
     dt = (time.perf_counter() - t0) / steps
     hdr = state.header
-    rows_px = res.rows_px
-    px = hdr.s_count * hdr.t_count * hdr.width * rows_px
+    px = hdr.s_count * hdr.t_count * hdr.width * res.rows_px
     return {"value": px / dt / 1e9, "unit": "Gpix/s",
             "h2d_bytes_per_step": res.h2d_bytes,
             "d2h_bytes_per_step": res.d2h_bytes,
@@ -408,8 +583,8 @@ def e2e_measure(state, band, args, rl):
 def random_access_measure(state, rl):
     """Random-access block decode (decoder.decode_block path): 10^6-pick
     device-resident batches (throughput, CUDA events) and single-block calls
-    through the public API (latency incl. H2D/D2H), picks from
-    default_rng(7) as in the reference acceptance test."""
+    through the public API (latency), picks from default_rng(7) as in the
+    reference acceptance test."""
     import torch
     from paper_1805_06019_b200 import decoder
     hdr = state.header
@@ -441,32 +616,6 @@ def random_access_measure(state, rl):
     return {"blocks_per_s": n / (ms * 1e-3), "batch": n, "ms_per_batch": ms,
             "decode_block_latency_us": lat * 1e6,
             "note": "cfg2 R4 stream, k=0, one CUDA thread per block request"}
-
-
-def render_measure(state, args, rl):
-    """cfg4: batches of 512x512 SlabPoses, s,t ~ U[0,16]^2, default focal."""
-    import torch
-    rng = np.random.default_rng(11)
-    n = args.render_batch
-    hdr = state.header
-    poses = [rl.SlabPose(float(rng.uniform(0, hdr.s_count - 1)),
-                         float(rng.uniform(0, hdr.t_count - 1)), 512, 512)
-             for _ in range(n)]
-    out = torch.empty((n, 512, 512, 3), dtype=torch.uint8, device="cuda")
-    for _ in range(2):
-        rl.render_views(state, poses, out=out)
-    torch.cuda.synchronize()
-    # median of 15 synchronised batches (wall clock, host pose prep included)
-    times = []
-    for _ in range(15):
-        t0 = time.perf_counter()
-        rl.render_views(state, poses, out=out)
-        torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-    dt = statistics.median(times)
-    return {"views_per_s": n / dt, "batch": n, "ms_per_batch": dt * 1e3,
-            "view": "512x512 SlabPose, default focal, k=0, bit-exact",
-            "timing": "wall clock incl. host pose prep, sync per batch, median of 15 batches"}
 
 
 CFG5 = dict(S=32, T=32, W=2048, H=2048, seed=7, h=3, B=4, shift=4, tp=16,

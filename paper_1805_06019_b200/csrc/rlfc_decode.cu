@@ -27,7 +27,17 @@ __global__ void k_decode_blocks(const rlfc_field f, const int32_t* __restrict__ 
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int s = req[6 * i], t = req[6 * i + 1], bx = req[6 * i + 2], by = req[6 * i + 3];
-    const int c = req[6 * i + 4], k = req[6 * i + 5];
+    int c = req[6 * i + 4];
+    const int k = req[6 * i + 5];
+    // range checks of decoder.py:51-63 (the channel indexes Python-style:
+    // -3..-1 alias 0..2); an out-of-range request reports code 3 and is
+    // not decoded
+    if (s < 0 || s >= f.s_count || t < 0 || t >= f.t_count || bx < 0 || bx >= f.wb || by < 0 || by >= f.hb ||
+        c < -3 || c >= 3 || k < 0 || k > f.tree_height) {
+        status[i] = 3;
+        return;
+    }
+    if (c < 0) c += 3;
     int32_t acc[B * B];
 #pragma unroll
     for (int yy = 0; yy < B; ++yy)

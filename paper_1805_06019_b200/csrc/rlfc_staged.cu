@@ -1422,7 +1422,11 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     // bounds the blend (output bytes in flight / tile lifetime): at 64
     // registers, 96-thread CTAs fit 10 per SM (shared memory 10 x 22.6 KB)
     // against 8 for 128 threads (455 vs 448 Gpix/s)
-    constexpr int bt = 96, tw = 64;
+#ifndef RLFC_BLEND_BT
+#define RLFC_BLEND_BT 96
+#define RLFC_BLEND_TW 64
+#endif
+    constexpr int bt = RLFC_BLEND_BT, tw = RLFC_BLEND_TW;     // compile-time (tools/variant_sweep.py)
     Plan pl{};
     if (!plan_blend<RT>(f, k, !tma_ok, tw, pl)) return RLFC_ERR_ARGUMENT;
     BlendParams& P = pl.P;

@@ -28,7 +28,10 @@ from .bise import RANGE_TABLE, payload_bytes_table
 from .errors import FormatError
 from .lightfield import LightFieldGrid, default_geometry, grid_positions
 
-SRV_TAIL_PAD = 16
+# zero bytes after each device SRV section: 64-bit bit windows read up to 8
+# bytes past a payload, and the single-block kernel stages whole 16-byte
+# lines up to 31 bytes past the record end
+SRV_TAIL_PAD = 32
 
 
 def _torch():
@@ -98,6 +101,7 @@ class DeviceField:
         self._ws_bytes = 0
         self._present = None
         self._dir = None
+        self.block_scratch = {}      # thread id -> _BlockScratch
 
     def directory(self):
         """The device record directory (rlfc_b200.h rlfc_dir: tile-major
@@ -308,6 +312,43 @@ def _check_level(state, stop_level):
                          f"{state.header.tree_height}]")
 
 
+def _check_requests(state, req, ncol):
+    """Range checks of batched requests (decoder.py:51-63 per request): s, t,
+    block indices inside the grid, channel in [-3, 3) (Python indexing, as
+    the reference's root_planes[..., c] / srv[c]) and, for blocks, the stop
+    level in [0, h].  Raises IndexError / ValueError like the reference;
+    returns the requests with negative channels normalised."""
+    hdr = state.header
+    wb, hb = hdr.block_grid
+    S, T, h = hdr.s_count, hdr.t_count, hdr.tree_height
+    torch = _torch()
+    if isinstance(req, torch.Tensor):
+        if req.numel() == 0:
+            return req
+        lo = req.min(dim=0).values.cpu().numpy()
+        hi = req.max(dim=0).values.cpu().numpy()
+    else:
+        if req.size == 0:
+            return req
+        lo, hi = req.min(axis=0), req.max(axis=0)
+    if lo[0] < 0 or hi[0] >= S or lo[1] < 0 or hi[1] >= T:
+        raise IndexError("image index outside grid")
+    if ncol == 6:
+        if lo[2] < 0 or hi[2] >= wb or lo[3] < 0 or hi[3] >= hb:
+            raise IndexError("block index outside block grid")
+        c, k = 4, 5
+        if lo[k] < 0 or hi[k] > h:
+            raise ValueError(f"stop level outside [0, {h}]")
+    else:
+        c = 2
+    if lo[c] < -3 or hi[c] >= 3:
+        raise IndexError("index out of bounds for axis 2 with size 3")
+    if lo[c] < 0:
+        req = req.clone() if isinstance(req, torch.Tensor) else req.copy()
+        req[:, c] %= 3
+    return req
+
+
 def _raise_status(code):
     if code == 1:
         raise FormatError("corrupt coded pack in SRV payload")
@@ -331,17 +372,21 @@ def decode_blocks(state, requests, device=None, raise_errors=True):
     """Decode a batch of blocks on the GPU.
 
     requests: (n, 6) ints (s, t, bx, by, channel, stop_level).  Returns
-    (CUDA int32 tensor (n, B, B), CUDA int32 status tensor (n,)).  With
-    raise_errors the first failing request (lowest index) raises the
-    reference's FormatError.
+    (CUDA int32 tensor (n, B, B), CUDA int32 status tensor (n,)).  Host
+    requests are range-checked first (IndexError / ValueError as
+    decoder.py:51-63); device requests are checked by the kernel (status 3).
+    With raise_errors the first failing request (lowest index) raises the
+    reference's error.
     """
     torch = _torch()
     df = state.device_field(device)
     if isinstance(requests, torch.Tensor) and requests.is_cuda:
+        # device-resident requests are range-checked by the kernel (code 3)
         req = requests.to(torch.int32).reshape(-1, 6).contiguous()
     else:
-        req = torch.as_tensor(np.ascontiguousarray(requests, dtype=np.int32)
-                              .reshape(-1, 6)).to(df.device, non_blocking=True)
+        req = _check_requests(state, np.ascontiguousarray(
+            requests, dtype=np.int32).reshape(-1, 6), 6)
+        req = torch.as_tensor(req).to(df.device, non_blocking=True)
     n = req.shape[0]
     b = state.header.block_size
     out = torch.empty((n, b, b), dtype=torch.int32, device=df.device)
@@ -354,6 +399,9 @@ def decode_blocks(state, requests, device=None, raise_errors=True):
         st = status.cpu().numpy()
         bad = np.flatnonzero(st)
         if bad.size:
+            if st[bad[0]] == 3:
+                _check_requests(state, req.cpu().numpy(), 6)     # raises
+                raise IndexError("block request out of range")
             _raise_status(int(st[bad[0]]))
     return out, status
 
@@ -362,8 +410,10 @@ def decode_planes(state, planes, stop_level=0, device=None):
     """(n, Hp, Wp) int32 CUDA tensor of padded planes for (s, t, c) triples."""
     torch = _torch()
     df = state.device_field(device)
-    req = torch.as_tensor(np.ascontiguousarray(planes, dtype=np.int32)
-                          .reshape(-1, 3)).to(df.device)
+    _check_level(state, stop_level)
+    req = _check_requests(state, np.ascontiguousarray(
+        planes, dtype=np.int32).reshape(-1, 3), 3)
+    req = torch.as_tensor(req).to(df.device)
     n = req.shape[0]
     wp, hp = state.header.padded_dims
     out = torch.empty((n, hp, wp), dtype=torch.int32, device=df.device)
@@ -386,11 +436,11 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
     images: None for the whole (S, T) grid -- the result is (S, T, H, W, 3)
     -- or a sequence of (s, t) pairs -- the result is (n, H, W, 3) in that
     order.  rows: optional block-row band (by_lo, by_hi); the result then
-    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "auto"
-    ("dir" when the stream is inside its envelope and the whole grid is
-    decoded, else "staged"), "dir" (one persistent kernel over the device
-    record directory, rlfc_dir.cu), "staged" (index -> payload decode ->
-    blend, rlfc_staged.cu; falls back to "fused" outside its envelope),
+    holds only pixel rows [by_lo*B, min(by_hi*B, H)).  kernel: "auto" (=
+    "staged"), "staged" (payload decode -> blend over the prepared record
+    index, rlfc_staged.cu; falls back to "fused" outside its envelope),
+    "dir" (one kernel over the tile-major device record directory,
+    rlfc_dir.cu; slower at cfg2, kept as an alternative and cross-check),
     "fused" (the single tiled kernel, rlfc_field.cu) or "simple" (per-block
     kernel).  With check, a
     corrupt stream raises the FormatError the reference raises first.
@@ -435,7 +485,7 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
         slots_p = None if slots_t is None else slots_t.data_ptr()
         with torch.cuda.device(df.device):
             done = False
-            if kernel in ("auto", "dir") and slots_t is None:
+            if kernel == "dir" and slots_t is None:
                 dr = df.directory()
                 if dr is not None:
                     rc = L.rlfc_decode_field_dir(
@@ -533,14 +583,13 @@ def bise_decode_batch(payloads, descs, count, device=None):
 # --- reference-signature API ---------------------------------------------------
 
 class _BlockScratch:
-    """Per-thread state for single-block requests: the field's device copy,
-    a device + pinned host buffer of B*B+1 int32 and a private CUDA stream
-    (the decode reads only immutable state), so a request is one ctypes call
-    into rlfc_decode_block_sync (kernel, D2H copy, stream sync)."""
+    """Per-thread state for single-block requests: a pinned host buffer of
+    B*B+1 int32 and a private CUDA stream (the decode reads only immutable
+    state), so a request is one ctypes call into rlfc_decode_block_sync
+    (kernel, status word polled in mapped memory)."""
 
     def __init__(self, df, b):
         torch = _torch()
-        self.df = df
         self.b = b
         # pinned host memory is device-addressable (unified addressing): the
         # kernel writes the block and its status straight into it
@@ -552,24 +601,15 @@ class _BlockScratch:
         self.fn = _native.lib().rlfc_decode_block_sync
 
 
-_tls = threading.local()
-
-
 def _block_scratch(state):
-    last = getattr(_tls, "last", None)
-    torch = _torch()
-    dev = torch.cuda.current_device()
-    if last is not None and last[0] is state and last[1] == dev:
-        return last[2]
-    cache = getattr(_tls, "blocks", None)
-    if cache is None:
-        cache = _tls.blocks = {}
-    key = (id(state), dev)
-    sc = cache.get(key)
-    if sc is None or sc.df is not state.device_field():
-        sc = cache[key] = _BlockScratch(state.device_field(),
-                                        state.header.block_size)
-    _tls.last = (state, dev, sc)
+    """The calling thread's single-block scratch for this state's field on
+    the current device.  It lives on the DeviceField (keyed by thread), so it
+    is released with the state; nothing module-level holds the state."""
+    df = state.device_field()
+    key = threading.get_ident()
+    sc = df.block_scratch.get(key)
+    if sc is None:
+        sc = df.block_scratch[key] = _BlockScratch(df, state.header.block_size)
     return sc
 
 
@@ -644,6 +684,12 @@ def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
     """One image channel plane at padded dims, int32 (decoder.py:165-184)."""
     _check_indices(state, s, t)
     _check_level(state, stop_level)
+    # root_planes[..., channel] / srv[channel] in the reference: Python
+    # indexing, so -3..-1 alias 0..2 and anything else is an IndexError
+    if not -3 <= channel < 3:
+        raise IndexError(f"index {channel} is out of bounds for axis 2 with "
+                         "size 3")
+    channel = int(channel) % 3
     if stop_level == state.header.tree_height:
         h = state.header.tree_height
         return state.root_planes[s >> h, t >> h, channel].copy()

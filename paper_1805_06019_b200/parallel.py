@@ -42,19 +42,37 @@ def balanced_bands(state, n):
     return [(bounds[i], bounds[i + 1]) for i in range(n)]
 
 
+def band_rows(state, bands):
+    """Pixel rows of each block-row band."""
+    B, H = state.header.block_size, state.header.height
+    return [max(0, min(hi * B, H) - lo * B) for lo, hi in bands]
+
+
 def gather_field(state, band_out, bands, group=None):
-    """All-gather per-rank bands (S, T, rows_r, W, 3) into the full
-    (S, T, H, W, 3) field on every rank (NCCL over NVLink)."""
+    """All-gather every rank's band (S, T, rows_r, W, 3) into one band-major
+    tensor (n_bands, S, T, rows_max, W, 3) on every rank: one
+    all_gather_into_tensor (NCCL over NVLink between GPUs), no concatenation
+    copy.  Bands shorter than the longest are padded (only the short ones
+    are copied); band_major_to_grid gives the (S, T, H, W, 3) layout."""
     import torch
     import torch.distributed as dist
     hdr = state.header
-    B = hdr.block_size
-    rows = [max(0, min(hi * B, hdr.height) - lo * B) for lo, hi in bands]
+    rows = band_rows(state, bands)
     pad = max(rows)
     S, T, W = hdr.s_count, hdr.t_count, hdr.width
-    send = torch.zeros((S, T, pad, W, 3), dtype=torch.uint8,
-                       device=band_out.device)
-    send[:, :, :band_out.shape[2]] = band_out
-    recv = [torch.empty_like(send) for _ in bands]
-    dist.all_gather(recv, send, group=group)
-    return torch.cat([r[:, :, :n] for r, n in zip(recv, rows)], dim=2)
+    if band_out.shape[2] == pad and band_out.is_contiguous():
+        send = band_out
+    else:
+        send = torch.zeros((S, T, pad, W, 3), dtype=torch.uint8, device=band_out.device)
+        send[:, :, :band_out.shape[2]] = band_out
+    recv = torch.empty(len(bands) * send.numel(), dtype=torch.uint8, device=band_out.device)
+    dist.all_gather_into_tensor(recv, send.reshape(-1), group=group)
+    return recv.view(len(bands), S, T, pad, W, 3)
+
+
+def band_major_to_grid(recv, state, bands):
+    """(S, T, H, W, 3) copy of a band-major gather (the reference decode_all
+    layout)."""
+    import torch
+    rows = band_rows(state, bands)
+    return torch.cat([recv[i, :, :, :n] for i, n in enumerate(rows)], dim=2)

@@ -258,3 +258,55 @@ def test_bise_roundtrip_property(rl):
         assert not status.any()
         for (d, vals, _), got in zip(group, out):
             assert np.array_equal(got, vals), (d, n)
+
+
+def test_request_validation_and_channel_aliasing(rl):
+    """decoder.py:51-63 range checks on the batched APIs (host requests
+    before any launch, device requests by the kernel) and Python-style
+    channel indexing (-3..-1 alias 0..2, 3 is an IndexError) in
+    decode_plane, as the reference's root_planes[..., c] / srv[c]."""
+    from paper_1805_06019_b200 import decoder
+    st = rl.init(load_stream("mid17_r4"))
+    hdr = st.header
+    wb, hb = hdr.block_grid
+    np.testing.assert_array_equal(rl.decode_plane(st, 2, 3, -1), rl.decode_plane(st, 2, 3, 2))
+    with pytest.raises(IndexError):
+        rl.decode_plane(st, 2, 3, 3)
+    good = [1, 2, 3, 4, 0, 0]
+    for bad, exc in [([hdr.s_count, 0, 0, 0, 0, 0], IndexError), ([0, 0, wb, 0, 0, 0], IndexError),
+                     ([0, 0, 0, 0, 3, 0], IndexError), ([0, 0, 0, 0, 0, hdr.tree_height + 1], ValueError)]:
+        with pytest.raises(exc):
+            decoder.decode_blocks(st, [good, bad])
+        dev = torch.tensor([good, bad], dtype=torch.int32, device="cuda")
+        _, status = decoder.decode_blocks(st, dev, raise_errors=False)
+        assert status.cpu().tolist() == [0, 3]
+        with pytest.raises((IndexError, ValueError)):
+            decoder.decode_blocks(st, dev)
+    out, status = decoder.decode_blocks(st, [[1, 2, 3, 4, -2, 0]])
+    want = rl.decode_block(st, (1, 2), (3, 4), 1)
+    np.testing.assert_array_equal(out[0].cpu().numpy(), want)
+    with pytest.raises(IndexError):
+        decoder.decode_planes(st, [(0, 0, 3)])
+
+
+def test_concurrent_decodes_on_one_stream(rl):
+    """Many threads decoding different camera subsets concurrently on the
+    default stream (the service pattern, reference service.py) get exactly
+    the serial results: the staged path's per-stream workspace is enqueued
+    under a lock."""
+    import concurrent.futures as cf
+    st = rl.init(load_stream("mid17_r4"))
+    full, _ = rl.decode_field(st)
+    full = full.cpu().numpy()
+    rng = np.random.default_rng(8)
+    jobs = [[(int(s), int(t)) for s, t in zip(rng.choice(17, 5, replace=False), rng.integers(0, 17, 5))]
+            for _ in range(48)]
+
+    def run(imgs):
+        out, _ = rl.decode_field(st, images=imgs)
+        return imgs, out.cpu().numpy()
+
+    with cf.ThreadPoolExecutor(12) as ex:
+        for imgs, out in ex.map(run, jobs):
+            for i, (s, t) in enumerate(imgs):
+                assert np.array_equal(out[i], full[s, t])

@@ -177,3 +177,26 @@ def test_colour_kat():
     assert (int(y[0]), int(co[0]), int(cg[0])) == (63, 255, -127)
     r, g, b = colorspace.ycocgr_to_rgb(y, co, cg)
     assert (int(r[0]), int(g[0]), int(b[0])) == (255, 0, 0)
+
+
+def test_request_range_checks():
+    """decoder._check_requests mirrors decoder.py:51-63 for batched
+    requests and normalises Python-style negative channels."""
+    from paper_1805_06019_b200 import container, decoder
+
+    class St:
+        pass
+    st = St()
+    st.header = container.parse_header(load_stream("mid17_r4"))
+    wb, hb = st.header.block_grid
+    ok = np.array([[0, 0, 0, 0, -1, 0], [16, 16, wb - 1, hb - 1, 2, 3]], np.int32)
+    out = decoder._check_requests(st, ok, 6)
+    assert out[0, 4] == 2 and ok[0, 4] == -1
+    for col, val, exc in [(0, 17, IndexError), (1, -1, IndexError), (2, wb, IndexError),
+                          (3, -1, IndexError), (4, 3, IndexError), (4, -4, IndexError), (5, 4, ValueError)]:
+        bad = ok.copy()
+        bad[1, col] = val
+        with pytest.raises(exc):
+            decoder._check_requests(st, bad, 6)
+    with pytest.raises(IndexError):
+        decoder._check_requests(st, np.array([[0, 0, 3]], np.int32), 3)

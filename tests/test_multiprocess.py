@@ -42,7 +42,7 @@ def _worker(rank, world, port, name, q):
     full, _ = oracle.OracleState(data).decode_all(0, nthreads=1)
     band = torch.from_numpy(np.ascontiguousarray(
         full[:, :, lo * B:min(hi * B, st.header.height)]))
-    out = parallel.gather_field(st, band, bands)
+    out = parallel.band_major_to_grid(parallel.gather_field(st, band, bands), st, bands)
     q.put((rank, bool(np.array_equal(out.numpy(), full))))
     dist.destroy_process_group()
 
@@ -57,6 +57,43 @@ def test_gloo_two_rank_gather(name):
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
+
+
+def _gpu_worker(rank, world, port, name, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1805_06019_b200 as rl
+    from paper_1805_06019_b200 import parallel
+    torch.cuda.set_device(0)
+    st = rl.init(load_stream(name))
+    bands = parallel.balanced_bands(st, world)
+    band, _ = rl.decode_field(st, 0, rows=bands[rank])          # the real GPU band decode
+    full = parallel.band_major_to_grid(parallel.gather_field(st, band.cpu(), bands), st, bands)
+    ref, _ = rl.decode_field(st, 0)
+    q.put((rank, bool(np.array_equal(full.numpy(), ref.cpu().numpy()))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mid17_r4", "kat8_default"])
+def test_two_ranks_gpu_band_decode(name):
+    """Two processes on one GPU, each decoding its own block-row band with
+    the CUDA path (independent kernels, no cross-rank waiting); the gloo
+    band-major gather equals the single-rank decode."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}

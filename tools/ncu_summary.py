@@ -15,7 +15,7 @@ import csv
 import json
 import sys
 
-KERNELS = {"staged": ["k_root_rgb", "k_index", "k_payloads", "k_blend"],
+KERNELS = {"staged": ["k_payloads", "k_blend"],
            "fused": ["k_decode_field_tiled"]}
 
 
