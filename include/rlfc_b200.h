@@ -234,6 +234,18 @@ int rlfc_decode_field_dir(const rlfc_field *f, const rlfc_dir *d,
                           uint8_t *rgb, int64_t img_stride, int64_t row_stride,
                           uint64_t *status, void *stream);
 
+/* Random-access block decode over a workspace prepared by
+ * rlfc_staged_prepare: same requests, outputs and per-request codes as
+ * rlfc_decode_blocks (out-of-range requests report 3), but each chain
+ * payload is found from its record's bitmap word and word rank and its
+ * index entry instead of a walk over the record's earlier nodes
+ * (kernels.py:162-216 early-exit walk); anomalous records take the
+ * reference-order walk. */
+int rlfc_decode_blocks_indexed(const rlfc_field *f, void *workspace,
+                               uint64_t workspace_bytes, uint64_t present_total,
+                               const int32_t *req, int32_t n, int32_t *out,
+                               int32_t *status, void *stream);
+
 /* BISE payload decode, batched.  Replaces kernels.bise_decode_core
  * (kernels.py:128-159) / bise.bise_decode (bise.py:108-118).  payload i
  * starts at data + offs[i], has descriptor descs[i] and `count` values;

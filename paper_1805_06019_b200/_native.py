@@ -77,6 +77,7 @@ _SIGS = {
                                  "p"],
     "rlfc_count_present": ["p", "p", "p"],
     "rlfc_staged_prepare": ["p", "p", "u", "u", "p", "p"],
+    "rlfc_decode_blocks_indexed": ["p", "p", "u", "u", "p", "i", "p", "p", "p"],
     "rlfc_decode_workspace_bytes": ["p", "u", "p"],
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "u", "u", "i", "p", "p"],

@@ -921,6 +921,75 @@ __global__ void k_fixup(const __grid_constant__ rlfc_field f, const uint32_t* fl
     }
 }
 
+// Random-access block decode over the prepared record index (decoder.py:
+// 81-106 / kernels.py:162-216): per chain level, the node's presence bit and
+// payload slot come from the record's bitmap word and word rank (one round
+// trip for all levels), the slot's entry gives the payload's byte offset
+// and descriptor, and only the chain payloads are read and BISE-decoded -- no
+// walk over the record's earlier nodes.  Records with a stream anomaly take
+// the reference-order walk.  Out-of-range requests report code 3.
+template <int B>
+__global__ void k_blocks_indexed(const __grid_constant__ rlfc_field f, Ws w, const int32_t* __restrict__ req, int n,
+                                 int32_t* __restrict__ out, int32_t* __restrict__ status) {
+    constexpr int BSQ = B * B;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = req[6 * i], t = req[6 * i + 1], bx = req[6 * i + 2], by = req[6 * i + 3];
+    int c = req[6 * i + 4];
+    const int k = req[6 * i + 5];
+    if (s < 0 || s >= f.s_count || t < 0 || t >= f.t_count || bx < 0 || bx >= f.wb || by < 0 || by >= f.hb ||
+        c < -3 || c >= 3 || k < 0 || k > f.tree_height) {
+        status[i] = 3;
+        return;
+    }
+    if (c < 0) c += 3;
+    const int64_t nblk = (int64_t)f.wb * f.hb, nrec = 3 * nblk;
+    const int64_t blk = (int64_t)by * f.wb + bx, ri = (int64_t)c * nblk + blk;
+    int32_t acc[BSQ];
+#pragma unroll
+    for (int yy = 0; yy < B; ++yy)
+#pragma unroll
+        for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+    int st = 0;
+    if (__ldg(w.rec_flag + ri)) {
+        const uint64_t off = f.offsets[c][blk];
+        st = walk_chain<BSQ>(f, f.srv[c] + off, s, t, k, acc, g_lut, node_bytes<BSQ>(), srv_avail(f, c, off));
+        if (st == WALK_OOB) st = 2;
+    } else {
+        const int h = f.tree_height;
+        uint32_t words[MAXH], ranks[MAXH];
+#pragma unroll
+        for (int l = 0; l < MAXH; ++l) {
+            words[l] = ranks[l] = 0u;
+            if (l >= k && l < h) {
+                const int nd = chain_node(f, l, s, t);
+                words[l] = __ldg(w.bm + (int64_t)(nd >> 5) * nrec + ri);
+                ranks[l] = __ldg(w.rk + (int64_t)(nd >> 5) * nrec + ri);
+            }
+        }
+        uint2 ent[MAXH];
+#pragma unroll
+        for (int l = 0; l < MAXH; ++l) {
+            ent[l] = make_uint2(0u, SKIP);
+            if (l >= k && l < h) {
+                const int bit = chain_node(f, l, s, t) & 31;
+                if ((words[l] >> bit) & 1u)
+                    ent[l] = __ldg(w.entries + ranks[l] + __popc(words[l] & ((1u << bit) - 1u)));
+            }
+        }
+        // chain order h-1 .. k, as the reference decodes its targets
+#pragma unroll
+        for (int l = MAXH - 1; l >= 0; --l) {
+            if ((ent[l].y & 31u) < (uint32_t)NUM_DESC && !st)
+                st = decode_payload_acc<BSQ>(f.srv[c] + ent[l].x, (int)(ent[l].y & 31u), f.quant_shift, acc, g_lut);
+        }
+    }
+    status[i] = st;
+    int32_t* o = out + (int64_t)i * BSQ;
+#pragma unroll
+    for (int j = 0; j < BSQ; ++j) o[j] = acc[j];
+}
+
 __global__ void k_flag_list(const uint32_t* rec_flag, int64_t nrec, uint32_t* flist) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nrec && rec_flag[i]) flist[1 + atomicAdd(flist, 1u)] = (uint32_t)i;
@@ -1616,6 +1685,25 @@ extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_
     }
     if (cudaStreamSynchronize(s) != cudaSuccess) return RLFC_ERR_CUDA;
     if (n_flagged) *n_flagged = (int32_t)nf;
+    return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
+extern "C" int rlfc_decode_blocks_indexed(const rlfc_field* f, void* workspace, uint64_t workspace_bytes,
+                                          uint64_t present_total, const int32_t* req, int32_t n, int32_t* out,
+                                          int32_t* status, void* stream) {
+    if (!f || !workspace || n < 0) return RLFC_ERR_ARGUMENT;
+    if (!staged::in_envelope(*f)) return RLFC_ERR_ARGUMENT;
+    staged::Ws w;
+    if (staged::carve(*f, workspace, present_total, &w) > workspace_bytes) return RLFC_ERR_ARGUMENT;
+    if (n == 0) return RLFC_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned g = (unsigned)((n + 127) / 128);
+    switch (f->block) {
+        case 4: staged::k_blocks_indexed<4><<<g, 128, 0, s>>>(*f, w, req, n, out, status); break;
+        case 8: staged::k_blocks_indexed<8><<<g, 128, 0, s>>>(*f, w, req, n, out, status); break;
+        case 16: staged::k_blocks_indexed<16><<<g, 128, 0, s>>>(*f, w, req, n, out, status); break;
+        default: return RLFC_ERR_ARGUMENT;
+    }
     return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }
 

@@ -392,9 +392,19 @@ def decode_blocks(state, requests, device=None, raise_errors=True):
     out = torch.empty((n, b, b), dtype=torch.int32, device=df.device)
     status = torch.zeros(n, dtype=torch.int32, device=df.device)
     with torch.cuda.device(df.device):
-        _native.check(_native.lib().rlfc_decode_blocks(
-            df.ref, req.data_ptr(), n, out.data_ptr(), status.data_ptr(),
-            _stream()), "rlfc_decode_blocks")
+        stream = _stream()
+        ws = df.staged_workspace(stream) if n >= 4096 else None
+        rc = _native.RLFC_ERR_ARGUMENT
+        if ws is not None:
+            # large batches: the prepared record index (no record walks)
+            rc = _native.lib().rlfc_decode_blocks_indexed(
+                df.ref, ws[0].data_ptr(), ws[1], ws[2], req.data_ptr(), n,
+                out.data_ptr(), status.data_ptr(), stream)
+        if rc == _native.RLFC_ERR_ARGUMENT:
+            rc = _native.lib().rlfc_decode_blocks(
+                df.ref, req.data_ptr(), n, out.data_ptr(), status.data_ptr(),
+                stream)
+        _native.check(rc, "rlfc_decode_blocks")
     if raise_errors and n:
         st = status.cpu().numpy()
         bad = np.flatnonzero(st)

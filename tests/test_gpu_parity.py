@@ -347,3 +347,27 @@ def test_corrupt_offsets_never_fault(rl, name):
         except rl.FormatError:
             pass
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name", ["mid17_r4", "b8_h2", "b16_h4", "grid32", "mid17_dense"])
+def test_indexed_random_access_matches_walk(rl, name):
+    """Batches >= 4096 go through the prepared record index
+    (rlfc_decode_blocks_indexed); values and codes equal the record walk's
+    (rlfc_decode_blocks) for random picks at every stop level."""
+    from paper_1805_06019_b200 import _native
+    st = state_for(rl, name)
+    hdr = st.header
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(17)
+    n = 6000
+    req = np.stack([rng.integers(0, hdr.s_count, n), rng.integers(0, hdr.t_count, n),
+                    rng.integers(0, wb, n), rng.integers(0, hb, n), rng.integers(-3, 3, n),
+                    rng.integers(0, hdr.tree_height + 1, n)], 1).astype(np.int32)
+    got, gst = rl.decode_blocks(st, req)
+    df = st.device_field()
+    dreq = torch.from_numpy(req % np.array([1 << 30] * 4 + [3, 1 << 30], np.int32)).cuda()
+    want = torch.empty_like(got)
+    wst = torch.zeros(n, dtype=torch.int32, device="cuda")
+    assert _native.lib().rlfc_decode_blocks(df.ref, dreq.data_ptr(), n, want.data_ptr(), wst.data_ptr(), 0) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(got, want) and torch.equal(gst, wst)
