@@ -80,6 +80,8 @@ struct Ws {
                            // one level row's words of consecutive records are contiguous)
     uint32_t* rk;          // [nwp][3*nblk] slot of the first present node of each word
     uint32_t* flist;       // [3*nblk + 1] records with a stream anomaly (prepare-time), count first
+    uint32_t* units;       // [tile][1 + ucap] prepared dirty-unit lists of the B = 4 blend (count first)
+    int ucap;
     int nwp;
     uint64_t cap;
 };
@@ -105,6 +107,12 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
                    o_rgb = take((uint64_t)f.rsx * f.rsy * f.hp * (uint64_t)rgb_stride),
                    o_bm = take(4 * nrec * (uint64_t)nwp), o_rk = take(4 * nrec * (uint64_t)nwp),
                    o_fl = take(4 * (nrec + 1));
+    // prepared dirty-unit lists (B = 4, 64-pixel blend tiles, h <= 6): per
+    // tile (block row, camera row, chunk) a count and up to S * 16 entries
+    const bool ul = f.block == 4 && f.tree_height <= 6;
+    const uint64_t ucap = (uint64_t)f.s_count * 16;
+    const uint64_t ntiles = (uint64_t)f.hb * f.t_count * ((f.wb + 15) / 16);
+    const uint64_t o_ul = take(ul ? 4 * ntiles * (1 + ucap) : 0);
     if (w) {
         uint8_t* b = static_cast<uint8_t*>(base);
         w->counter = reinterpret_cast<unsigned long long*>(b + o_cnt);
@@ -117,6 +125,8 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
         w->bm = reinterpret_cast<uint32_t*>(b + o_bm);
         w->rk = reinterpret_cast<uint32_t*>(b + o_rk);
         w->flist = reinterpret_cast<uint32_t*>(b + o_fl);
+        w->units = ul ? reinterpret_cast<uint32_t*>(b + o_ul) : nullptr;
+        w->ucap = (int)ucap;
         w->nwp = nwp;
         w->cap = cap;
     }
@@ -798,6 +808,9 @@ struct BlendParams {
     int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
     int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
     int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
+    uint32_t* units;             // prepared dirty-unit lists (B = 4), or null
+    int ucap;
+    int build_units;             // 1: this launch writes the lists (prepare, k = 0)
     int off_flag, off_mask, off_sbase, off_roots, off_rgb, off_cnt, off_list, off_stage,
         off_mbar;
 };
@@ -1063,6 +1076,18 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     }
 
     if (tid == 0) cnt[0] = 0;
+    // prepared dirty-unit list of this tile (B = 4): its count and this
+    // thread's first two entries are loaded with the record tables (one round
+    // trip); the pair scan below is then skipped
+    const bool use_list = B == 4 && P.units && !P.build_units;
+    const uint32_t* ulist = nullptr;
+    uint32_t ucount = 0, ue0 = 0, ue1 = 0;
+    if (use_list) {
+        ulist = P.units + ((uint64_t)((int64_t)by * T + t) * P.nchunks + chunk) * (uint64_t)(1 + P.ucap);
+        ucount = __ldg(ulist);
+        if (tid < P.ucap) ue0 = __ldg(ulist + 1 + tid);
+        if (tid + BT < P.ucap) ue1 = __ldg(ulist + 1 + tid + BT);
+    }
     // ---- records: residual row masks and slot bases of this camera row --------
     for (int r = tid; r < NR; r += BT) {
         const int c = r >> (__ffs(NB) - 1), b = r & (NB - 1);
@@ -1131,7 +1156,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");       // residuals (tasks) come from k_payloads
     // ---- manual path: roots of this camera row and their RGB8 -------------------------
-    if (!P.tma_in) {
+    if (!P.tma_in && !P.build_units) {
         const int quads = TW / 4;
         const int64_t pl = (int64_t)f.hp * f.wp;
         for (int it = tid; it < f.rsx * B * quads; it += BT) {
@@ -1168,7 +1193,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     // pairs touching a flagged record are tagged for the reference-order walk
     const int lane = tid & 31;
     const int lgnb = __ffs(NB) - 1;                  // NB is a power of two (TW / B)
-    for (int p0 = 0; p0 < S * NB; p0 += BT) {
+    for (int p0 = use_list ? S * NB : 0; p0 < S * NB; p0 += BT) {
         const int pi = p0 + tid;
         const int s = pi >> lgnb, b = pi & (NB - 1);
         bool emit = false, fb = false;
@@ -1195,6 +1220,15 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
                 list[base + __popc(bal & ((1u << lane) - 1u))] =
                     make_uint2((uint32_t)s | (uint32_t)b << 8 | (fb ? 1u << 16 : 0u), pres);
         }
+    }
+    if (P.build_units) {
+        // prepare (k = 0): this tile's dirty units (s | b << 8 | presence << 14)
+        __syncthreads();
+        uint32_t* ul = P.units + ((uint64_t)((int64_t)by * T + t) * P.nchunks + chunk) * (uint64_t)(1 + P.ucap);
+        const int n = cnt[0];
+        if (tid == 0) ul[0] = (uint32_t)n;
+        for (int u = tid; u < n; u += BT) ul[1 + u] = list[u].x & 0xFFFFu | list[u].y << 14;
+        return;
     }
     if (!P.tma_in) {
         // staging[strip][s][row] <- root_rgb[strip][s >> h][row]: one warp per
@@ -1228,10 +1262,23 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         // B = 4: one task per unit (all 16 pixels): the first present level
         // of each channel is two 16-byte gathers, all issued before any is
         // consumed, so a thread pays one round trip per unit
-        const int units = cnt[0];
+        const int units = use_list ? (int)ucount : cnt[0];
         const VT* res = static_cast<const VT*>(P.res);
         for (int u = tid; u < units; u += BT) {
-            const uint2 e = list[u];
+            uint2 e;
+            if (use_list) {
+                // prepared entry (k = 0): keep levels >= k, skip views outside
+                // the slot table, units of anomalous records (k_fixup) and
+                // units clean at this stop level
+                const uint32_t q = u == tid ? ue0 : u == tid + BT ? ue1 : __ldg(ulist + 1 + u);
+                const int s = (int)(q & 255u), b = (int)((q >> 8) & 63u);
+                const uint32_t pres = (q >> 14 >> (3 * k)) & ((1u << (3 * nlev)) - 1u);
+                if (rflag[b] | rflag[NB + b] | rflag[2 * NB + b]) continue;
+                if (!pres || (P.slots && P.slots[s * T + t] < 0)) continue;
+                e = make_uint2((uint32_t)s | (uint32_t)b << 8, pres);
+            } else {
+                e = list[u];
+            }
             const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
             if (e.x >> 16) continue;                 // anomalous record: k_fixup
             auto slot_of = [&](int c, uint32_t pc) -> uint32_t {
@@ -1483,7 +1530,7 @@ static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi,
 template <int B, typename VT, typename RT>
 static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
                   int64_t img_stride, int64_t row_stride, const Ws& w, int n_flagged, uint64_t* status,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, bool build_units = false) {
     constexpr int BSQ = B * B;
     const bool tma_ok = w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 &&
                         ((f.wp * (int)sizeof(RT)) % 16) == 0 && encode_fn() != nullptr;
@@ -1516,6 +1563,10 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     P.rk = w.rk;
     P.nwp = w.nwp;
     P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
+    P.units = B == 4 && P.NB == 16 ? w.units : nullptr;
+    P.ucap = w.ucap;
+    P.build_units = build_units && P.units ? 1 : 0;
+    if (build_units && !P.units) return RLFC_OK;
     const int h = f.tree_height, S = f.s_count;
     // output path
     const bool aligned = ((reinterpret_cast<uintptr_t>(rgb) | (uintptr_t)img_stride | (uintptr_t)row_stride) & 15) == 0;
@@ -1569,17 +1620,18 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         c.numAttrs = programmatic && pdl ? 1 : 0;
         return c;
     };
-    if (k < h) run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream);
+    if (P.build_units) P.tma_in = 0;
+    if (k < h && !P.build_units) run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream);
     auto kern = k_blend<B, VT, RT, bt>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     // tile residency is bounded by shared memory: ask for the largest carveout
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     const dim3 grid((unsigned)P.nchunks, (unsigned)f.t_count, (unsigned)(by_hi - by_lo));
     {
-        const cudaLaunchConfig_t c = cfg_of(grid, dim3(bt), pl.smem, k < h);
+        const cudaLaunchConfig_t c = cfg_of(grid, dim3(bt), pl.smem, k < h && !P.build_units);
         cudaLaunchKernelEx(&c, kern, P, out_map, rgb_map, root_map);
     }
-    if (n_flagged > 0 && k < h) {
+    if (n_flagged > 0 && k < h && !P.build_units) {
         const int nv = f.s_count * f.t_count;
         k_fixup<B><<<dim3((unsigned)n_flagged, (unsigned)((nv + 63) / 64)), 64, 0, stream>>>(
             f, w.flist, k, slots, by_lo, by_hi, rgb, img_stride, row_stride, status);
@@ -1672,6 +1724,19 @@ extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_
     if (nrec > 0) staged::k_flag_list<<<(unsigned)((nrec + 255) / 256), 256, 0, s>>>(w.rec_flag, nrec, w.flist);
     uint32_t nf = 0;
     cudaMemcpyAsync(&nf, w.flist, 4, cudaMemcpyDeviceToHost, s);
+    // the B = 4 blend's dirty-unit lists (stream-invariant: presence bits and
+    // anomaly flags only), built by the blend's own record phase and pair scan
+    if (f->block == 4 && w.units) {
+        const int rc = f->roots_i16 ? (f->quant_shift <= 4 ? staged::launch<4, int16_t, int16_t>(
+                                           *f, 0, nullptr, 0, f->hb, nullptr, 0, 0, w, 0, nullptr, s, true)
+                                                           : staged::launch<4, int32_t, int16_t>(
+                                           *f, 0, nullptr, 0, f->hb, nullptr, 0, 0, w, 0, nullptr, s, true))
+                                    : (f->quant_shift <= 4 ? staged::launch<4, int16_t, int32_t>(
+                                           *f, 0, nullptr, 0, f->hb, nullptr, 0, 0, w, 0, nullptr, s, true)
+                                                           : staged::launch<4, int32_t, int32_t>(
+                                           *f, 0, nullptr, 0, f->hb, nullptr, 0, 0, w, 0, nullptr, s, true));
+        if (rc != RLFC_OK) return rc;
+    }
     const bool tma_ok = (reinterpret_cast<uintptr_t>(f->roots) & 15) == 0 &&
                         ((f->wp * (f->roots_i16 ? 2 : 4)) % 16) == 0;
     if (tma_ok) {
