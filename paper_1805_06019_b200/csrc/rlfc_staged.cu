@@ -73,6 +73,7 @@ struct Ws {
     uint32_t* rec_base;
     uint32_t* rec_flag;
     uint2* entries;
+    uint2* sorted;         // [cap rounded to PAY_CHUNK] entries of each 512-slot chunk ordered by BISE mode
     void* res;
     uint8_t* root_rgb;     // RGB8 of every root sample, rows of rgb_stride bytes
     int rgb_stride;
@@ -103,6 +104,7 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
     const int rgb_stride = (f.wp * 3 + 15) & ~15;
     const int nwp = (f.m_nodes + 31) / 32 + 2;
     const uint64_t o_cnt = take(8), o_base = take(4 * nrec), o_flag = take(4 * nrec), o_ent = take(8 * cap),
+                   o_sort = take(8 * ((cap + 511) / 512) * 512),
                    o_res = take(cap * bsq * (uint64_t)value_bytes(f)),
                    o_rgb = take((uint64_t)f.rsx * f.rsy * f.hp * (uint64_t)rgb_stride),
                    o_bm = take(4 * nrec * (uint64_t)nwp), o_rk = take(4 * nrec * (uint64_t)nwp),
@@ -119,6 +121,7 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
         w->rec_base = reinterpret_cast<uint32_t*>(b + o_base);
         w->rec_flag = reinterpret_cast<uint32_t*>(b + o_flag);
         w->entries = reinterpret_cast<uint2*>(b + o_ent);
+        w->sorted = reinterpret_cast<uint2*>(b + o_sort);
         w->res = b + o_res;
         w->root_rgb = b + o_rgb;
         w->rgb_stride = rgb_stride;
@@ -598,17 +601,73 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
     return bad;
 }
 
-// One CTA takes PAY_CHUNK consecutive slots, buckets their entries by BISE
-// mode in shared memory, then decodes each bucket with the mode's unrolled
-// code so every warp runs one code path.
+// Payload decode over the prepared index.  Slots form chunks of PAY_CHUNK
+// consecutive payloads (consecutive nodes of consecutive records: one
+// contiguous SRV byte range per channel), and rlfc_staged_prepare stores each
+// chunk's entries ordered by BISE mode (k_sort_chunks), so a warp runs one
+// mode's unrolled code (kernels.py:128-159).  A CTA takes chunks of the
+// band's slot ranges, software-pipelined: while chunk i decodes, chunk i+1's
+// entries are in registers and its SRV byte range is on its way into the
+// other shared buffer (cp.async).  Dequantisation (kernels.py:202-211) is a
+// table.  A corrupt pack flags its record (kernels.py:147-150).
 constexpr int PAY_CHUNK = 512;
 constexpr int PAY_BUF = 12 * 1024;       // staged SRV bytes per chunk (two buffers, dynamic shared memory)
+
+// record of a payload slot (slot bases ascend in record order)
+__device__ int64_t record_of_slot(const uint32_t* rec_base, int64_t nrec, uint64_t slot) {
+    int64_t lo = 0, hi = nrec - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (rec_base[mid] <= slot) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// prepare: each chunk's entries stably ordered by mode (plain bits, trits,
+// quints, undecoded); entry.y = descriptor | channel << 5 | index in chunk << 7
+__global__ void __launch_bounds__(THREADS) k_sort_chunks(Ws w, uint64_t ntot) {
+    __shared__ int part[4][THREADS + 1];
+    const int tid = threadIdx.x;
+    const uint64_t c0 = (uint64_t)blockIdx.x * PAY_CHUNK;
+    constexpr int EPT = PAY_CHUNK / THREADS;
+    uint2 e[EPT];
+    int m[EPT];
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+        const uint64_t i = c0 + tid * EPT + q;
+        e[q] = i < ntot ? w.entries[i] : make_uint2(0u, SKIP);
+        const uint32_t d = e[q].y & 31u;
+        m[q] = d < (uint32_t)NUM_DESC ? desc_mode((int)d) : 3;
+    }
+    for (int mm = 0; mm < 4; ++mm) {
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) cnt += m[q] == mm;
+        part[mm][tid + 1] = cnt;
+    }
+    if (tid == 0)
+        for (int mm = 0; mm < 4; ++mm) part[mm][0] = 0;
+    __syncthreads();
+    if (tid < 4)
+        for (int i = 1; i <= THREADS; ++i) part[tid][i] += part[tid][i - 1];
+    __syncthreads();
+    int base[4];
+    base[0] = 0;
+    for (int mm = 1; mm < 4; ++mm) base[mm] = base[mm - 1] + part[mm - 1][THREADS];
+    int seen[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+        const int mm = m[q];
+        const int pos = base[mm] + part[mm][tid] + seen[mm]++;
+        const uint32_t local = (uint32_t)(tid * EPT + q);
+        w.sorted[c0 + pos] = make_uint2(e[q].x, (e[q].y & 127u) | local << 7);
+    }
+}
+
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w, int l2_last,
                                                       int by_lo, int by_hi) {
-    __shared__ uint2 bucket[3][PAY_CHUNK];
-    __shared__ uint32_t bslot[3][PAY_CHUNK];
-    __shared__ int bcount[3];
     __shared__ uint32_t range[2][3];         // per buffer: min / max payload offset, channel mask
     __shared__ uint16_t lut[243 + 125];
     __shared__ VT dq[BSQ == 16 ? 2048 : 1];
@@ -620,58 +679,61 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     if (BSQ == 16)
         for (int z = tid; z < 2048; z += THREADS) dq[z] = (VT)deq((uint32_t)z, shift);
     const int64_t nblk = (int64_t)f.wb * f.hb;
-    // the band's payload slots: per channel one contiguous run (prepared
-    // index: record bases ascend in record order), concatenated
-    uint64_t lo[3], len[3];
-    {
-        const uint64_t ntot = min((uint64_t)*w.counter, w.cap);
-        for (int c = 0; c < 3; ++c) {
-            const int64_t a = (int64_t)c * nblk + (int64_t)by_lo * f.wb, b = (int64_t)c * nblk + (int64_t)by_hi * f.wb;
-            const uint64_t sa = a < 3 * nblk ? w.rec_base[a] : ntot;
-            const uint64_t sb = b < 3 * nblk ? w.rec_base[b] : ntot;
-            lo[c] = min(sa, ntot);
-            len[c] = min(sb, ntot) > lo[c] ? min(sb, ntot) - lo[c] : 0;
-        }
+    const uint64_t ntot = min((uint64_t)*w.counter, w.cap);
+    // the band's payload slots: per channel one contiguous run [lo, hi)
+    // (record bases ascend in record order); the chunks covering them
+    uint64_t lo[3], hi[3], ch0[3], nch[3];
+    for (int c = 0; c < 3; ++c) {
+        const int64_t a = (int64_t)c * nblk + (int64_t)by_lo * f.wb, b = (int64_t)c * nblk + (int64_t)by_hi * f.wb;
+        lo[c] = min(a < 3 * nblk ? (uint64_t)w.rec_base[a] : ntot, ntot);
+        hi[c] = max(lo[c], min(b < 3 * nblk ? (uint64_t)w.rec_base[b] : ntot, ntot));
+        ch0[c] = lo[c] / PAY_CHUNK;
+        nch[c] = hi[c] > lo[c] ? (hi[c] + PAY_CHUNK - 1) / PAY_CHUNK - ch0[c] : 0;
     }
-    const uint64_t n = len[0] + len[1] + len[2];
-    auto slot_of = [&](uint64_t v) -> uint64_t {
-        return v < len[0] ? lo[0] + v : v < len[0] + len[1] ? lo[1] + (v - len[0]) : lo[2] + (v - len[0] - len[1]);
+    const uint64_t n = nch[0] + nch[1] + nch[2];             // chunks to visit (virtual index)
+    auto chunk_of = [&](uint64_t v) -> uint64_t {
+        return v < nch[0] ? ch0[0] + v : v < nch[0] + nch[1] ? ch0[1] + (v - nch[0]) : ch0[2] + (v - nch[0] - nch[1]);
     };
     VT* res = static_cast<VT*>(w.res);
     uint64_t pol = 0;
     if (l2_last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    // Chunks are software-pipelined: while chunk i decodes, chunk i+1's
-    // entries are in registers and its SRV byte range is on its way into the
-    // other shared buffer (cp.async).  A chunk's payloads are consecutive
-    // nodes of consecutive records of one channel: one contiguous byte range.
     constexpr int EPT = PAY_CHUNK / THREADS;                   // entries per thread
-    const uint64_t stride = (uint64_t)gridDim.x * PAY_CHUNK;
-    auto load_entries = [&](uint64_t b0, uint2* e4) {
+    // entry j of chunk cc for this thread (j = tid + q * THREADS); slots
+    // outside the band are skipped
+    auto load_entries = [&](uint64_t v, uint2* e4, uint32_t* sl) {
+        const uint64_t cc = chunk_of(v);
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
-            const uint64_t i = b0 + tid + q * THREADS;
-            e4[q] = i < n ? __ldg(w.entries + slot_of(i)) : make_uint2(0u, SKIP);
+            const uint64_t i = cc * PAY_CHUNK + tid + q * THREADS;
+            uint2 e = i < ntot ? __ldg(w.sorted + i) : make_uint2(0u, SKIP);
+            const uint64_t slot = cc * PAY_CHUNK + ((e.y >> 7) & (PAY_CHUNK - 1));
+            const int c = (int)(e.y >> 5) & 3;
+            const uint64_t lc = c == 0 ? lo[0] : c == 1 ? lo[1] : lo[2];
+            const uint64_t hc = c == 0 ? hi[0] : c == 1 ? hi[1] : hi[2];
+            if (slot < lc || slot >= hc) e.y = SKIP;
+            e4[q] = e;
+            sl[q] = (uint32_t)slot;
         }
     };
     auto reduce_range = [&](const uint2* e4, int q) {
         if (BSQ != 16) return;
-        uint32_t lo = ~0u, hi = 0u, cm = 0u;
+        uint32_t rlo = ~0u, rhi = 0u, cm = 0u;
 #pragma unroll
         for (int k2 = 0; k2 < EPT; ++k2)
             if ((e4[k2].y & 31u) < (uint32_t)NUM_DESC) {
-                lo = min(lo, e4[k2].x);
-                hi = max(hi, e4[k2].x);
+                rlo = min(rlo, e4[k2].x);
+                rhi = max(rhi, e4[k2].x);
                 cm |= 1u << ((e4[k2].y >> 5) & 3);
             }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            rlo = min(rlo, __shfl_xor_sync(0xffffffffu, rlo, o));
+            rhi = max(rhi, __shfl_xor_sync(0xffffffffu, rhi, o));
             cm |= __shfl_xor_sync(0xffffffffu, cm, o);
         }
         if ((tid & 31) == 0 && cm) {
-            atomicMin(&range[q][0], lo);
-            atomicMax(&range[q][1], hi);
+            atomicMin(&range[q][0], rlo);
+            atomicMax(&range[q][1], rhi);
             atomicOr(&range[q][2], cm);
         }
     };
@@ -691,8 +753,9 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
                          : "memory");
         return true;
     };
-    uint64_t base = (uint64_t)blockIdx.x * PAY_CHUNK;
+    uint64_t v = blockIdx.x;
     uint2 ent[EPT];
+    uint32_t sl[EPT];
     bool staged = false;
     uint32_t lo16 = 0;
     if (tid == 0) {
@@ -701,36 +764,26 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
         range[0][2] = 0u;
     }
     __syncthreads();
-    if (base < n) {
-        load_entries(base, ent);
+    if (v < n) {
+        load_entries(v, ent, sl);
         reduce_range(ent, 0);
     }
     __syncthreads();
-    if (base < n) staged = stage_issue(0, lo16);
+    if (v < n) staged = stage_issue(0, lo16);
     asm volatile("cp.async.commit_group;" ::: "memory");
-    for (int it = 0; base < n; base += stride, ++it) {
+    for (int it = 0; v < n; v += gridDim.x, ++it) {
         const int q = it & 1;
-        if (tid < 3) bcount[tid] = 0;
         if (tid == 0) {
             range[q ^ 1][0] = ~0u;
             range[q ^ 1][1] = 0u;
             range[q ^ 1][2] = 0u;
         }
         __syncthreads();
-#pragma unroll
-        for (int k2 = 0; k2 < EPT; ++k2) {
-            const uint2 e = ent[k2];
-            const uint32_t d = e.y & 31u;
-            if (d >= (uint32_t)NUM_DESC) continue;
-            const int m = desc_mode((int)d);
-            const int pos = atomicAdd(&bcount[m], 1);
-            bucket[m][pos] = e;
-            bslot[m][pos] = (uint32_t)slot_of(base + tid + k2 * THREADS);
-        }
-        const bool has_next = base + stride < n;
+        const bool has_next = v + gridDim.x < n;
         uint2 entn[EPT];
+        uint32_t sln[EPT];
         if (has_next) {
-            load_entries(base + stride, entn);
+            load_entries(v + gridDim.x, entn, sln);
             reduce_range(entn, q ^ 1);
         }
         __syncthreads();
@@ -740,15 +793,16 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 1;" ::: "memory");     // this chunk's copies
         __syncthreads();
-        const int n0 = bcount[0], n1 = bcount[1], n2 = bcount[2];
         const uint32_t* cb = cbuf + q * (PAY_BUF / 4);
-        for (int j = tid; j < n0 + n1 + n2; j += THREADS) {
-            const int m = j < n0 ? 0 : j < n0 + n1 ? 1 : 2;
-            const int jj = j - (m == 0 ? 0 : m == 1 ? n0 : n0 + n1);
-            const uint2 e = bucket[m][jj];
-            const uint64_t slot = bslot[m][jj];
+#pragma unroll
+        for (int k2 = 0; k2 < EPT; ++k2) {
+            const uint2 e = ent[k2];
+            const uint32_t d = e.y & 31u;
+            if (d >= (uint32_t)NUM_DESC) continue;
+            const int m = desc_mode((int)d);
+            const uint64_t slot = sl[k2];
             const int c = (int)(e.y >> 5) & 3;
-            const uint32_t b = (uint32_t)desc_bits((int)(e.y & 31u));
+            const uint32_t b = (uint32_t)desc_bits((int)d);
             VT* out = res + slot * BSQ;
             bool bad;
             if constexpr (BSQ == 16) {
@@ -765,11 +819,14 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
                 else if (m == MODE_TRIT) bad = decode_payload<5, 8, BSQ, VT>(p, lut, b, shift, out);
                 else bad = decode_payload<3, 7, BSQ, VT>(p, lut + 243, b, shift, out);
             }
-            if (bad) w.rec_flag[(int64_t)c * nblk + (e.y >> 7)] = 1u;   // kernels.py:147-150
+            if (bad) w.rec_flag[record_of_slot(w.rec_base, 3 * nblk, slot)] = 1u;   // kernels.py:147-150
         }
         __syncthreads();
 #pragma unroll
-        for (int k2 = 0; k2 < EPT; ++k2) ent[k2] = entn[k2];
+        for (int k2 = 0; k2 < EPT; ++k2) {
+            ent[k2] = entn[k2];
+            sl[k2] = sln[k2];
+        }
         staged = stagedn;
         lo16 = lo16n;
     }
@@ -1517,7 +1574,7 @@ static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_fir
 
 template <int BSQ, typename VT>
 static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi, int sms, cudaStream_t stream) {
-    const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK;
+    const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK + 3;
     const uint64_t cap_grid = (uint64_t)sms * 8;
     const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
     const int pdyn = BSQ == 16 ? 2 * PAY_BUF : 16;
@@ -1704,6 +1761,9 @@ extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_
             default: staged::k_index<256><<<g, staged::THREADS, 0, s>>>(*f, 0, 0, f->hb, w, w.rec_base); break;
         }
     }
+    if (present_total > 0)
+        staged::k_sort_chunks<<<(unsigned)((present_total + staged::PAY_CHUNK - 1) / staged::PAY_CHUNK),
+                                staged::THREADS, 0, s>>>(w, present_total);
     // every payload decoded once here too: corrupt packs flag their records
     // (kernels.py:147-150), so the anomaly list below is complete
     {
