@@ -246,6 +246,29 @@ int rlfc_decode_blocks_indexed(const rlfc_field *f, void *workspace,
                                const int32_t *req, int32_t n, int32_t *out,
                                int32_t *status, void *stream);
 
+/* The reference kernel module's decode entry points with their own
+ * arguments (INTEGRATION.md Route 2, paper_1805_06019_b200/kernels_b200.py):
+ * rlfc_chain_core is kernels.decode_chain_core (kernels.py:162-216) for n
+ * records at once -- SRV bytes (device, srv_len bytes + >= 32 readable pad),
+ * record offsets rec_offs[n], the ascending target list (the ancestor
+ * chain), out[n][bsq] pre-filled with the root blocks (in/out), status[n]
+ * 0 / 1 / 2.  rlfc_plane_core is kernels.decode_plane_core
+ * (kernels.py:219-242) for one plane: root_plane / out_plane int32
+ * (blocks_y*block, blocks_x*block); *status (caller initialises to
+ * UINT64_MAX) becomes (first failing block index << 2) | code, blocks in
+ * row-major order, as the reference returns at its first failure. */
+int rlfc_chain_core(const uint8_t *srv, uint64_t srv_len,
+                    const uint64_t *rec_offs, int32_t n, int32_t m_nodes,
+                    int32_t bsq, const int64_t *targets, int32_t nt,
+                    int32_t shift, int32_t *out, int32_t *status,
+                    void *stream);
+int rlfc_plane_core(const uint8_t *srv, uint64_t srv_len,
+                    const uint64_t *offsets, int32_t blocks_x,
+                    int32_t blocks_y, int32_t m_nodes, int32_t block,
+                    const int64_t *targets, int32_t nt, int32_t shift,
+                    const int32_t *root_plane, int32_t *out_plane,
+                    uint64_t *status, void *stream);
+
 /* BISE payload decode, batched.  Replaces kernels.bise_decode_core
  * (kernels.py:128-159) / bise.bise_decode (bise.py:108-118).  payload i
  * starts at data + offs[i], has descriptor descs[i] and `count` values;
@@ -295,6 +318,23 @@ int rlfc_render_pinhole_needs(int32_t S, int32_t T, int32_t W, int32_t H,
                               const rlfc_render_geom *geoms, int32_t n,
                               int32_t ow, int32_t oh, uint8_t *need,
                               void *stream);
+
+/* Root-view decode at init (container.py:175-195, PNG roots): raw holds
+ * nplanes inflated IDAT streams (each height rows of 1 + 2*width filtered
+ * bytes, raw_plane bytes apart); rlfc_png_unfilter undoes the PNG scanline
+ * filters (None / Sub / Up / Average / Paeth, 2 bytes per pixel) into
+ * big-endian 16-bit samples out[plane][height][width] (out_plane apart);
+ * *bad becomes 1 on a filter type above 4.  rlfc_root_planes removes the
+ * channel bias (0, 256, 256) and scatters plane p (decode order: channel,
+ * root row, root column) into the root tensor (rsx, rsy, 3, hp, wp) as int16
+ * (i16 = 1) or int32; minmax (nullable, int32[2], caller initialises to
+ * {INT_MAX-ish, INT_MIN-ish}) receives the value range. */
+int rlfc_png_unfilter(const uint8_t *raw, int64_t raw_plane, int32_t nplanes,
+                      int32_t width, int32_t height, uint16_t *out,
+                      int64_t out_plane, int32_t *bad, void *stream);
+int rlfc_root_planes(const uint16_t *samples, int32_t nplanes, int32_t rsx,
+                     int32_t rsy, int32_t hp, int32_t wp, int32_t i16,
+                     void *dst, int32_t *minmax, void *stream);
 
 /* Host plumbing for band-pipelined host-buffer decodes (decoder.HostPipeline):
  * an asynchronous strided copy (cudaMemcpy2DAsync), kind 0 host->device,

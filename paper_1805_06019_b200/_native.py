@@ -82,6 +82,10 @@ _SIGS = {
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "u", "u", "i", "p", "p"],
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
+    "rlfc_chain_core": ["p", "u", "p", "i", "i", "i", "p", "i", "i", "p", "p",
+                        "p"],
+    "rlfc_plane_core": ["p", "u", "p", "i", "i", "i", "i", "p", "i", "i", "p",
+                        "p", "p", "p"],
     "rlfc_render_slab": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
                          "i", "i", "p", "p"],
     "rlfc_render_pinhole": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
@@ -89,6 +93,8 @@ _SIGS = {
     "rlfc_render_pinhole_needs": ["i", "i", "i", "i", "p", "p", "i", "i", "i",
                                   "p", "p"],
     "rlfc_copy2d": ["p", "q", "p", "q", "q", "q", "i", "p"],
+    "rlfc_png_unfilter": ["p", "q", "i", "i", "i", "p", "q", "p", "p"],
+    "rlfc_root_planes": ["p", "i", "i", "i", "i", "i", "i", "p", "p", "p"],
     "rlfc_version": ["p", "i"],
 }
 _CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64,

@@ -314,6 +314,118 @@ def parse_roots(data, header: RlfcHeader, threads=None):
     return out
 
 
+_PNG_SIG = b"\x89PNG\r\n\x1a\n"
+
+
+def _png_idat(blob, width, height):
+    """The zlib stream of a 16-bit greyscale, non-interlaced PNG of the
+    header's dims with valid chunk CRCs, or None (anything else goes to
+    Pillow, which raises the reference's errors)."""
+    import zlib
+    if blob[:8] != _PNG_SIG:
+        return None
+    pos, idat, seen_end, ihdr_ok = 8, [], False, False
+    while pos + 12 <= len(blob):
+        (n,) = struct.unpack_from(">I", blob, pos)
+        typ = blob[pos + 4:pos + 8]
+        if pos + 12 + n > len(blob):
+            return None
+        body = blob[pos + 8:pos + 8 + n]
+        if zlib.crc32(typ + body) != struct.unpack_from(">I", blob, pos + 8 + n)[0]:
+            return None
+        if typ == b"IHDR":
+            if n != 13 or struct.unpack(">IIBBBBB", body) != (width, height, 16, 0, 0, 0, 0):
+                return None
+            ihdr_ok = True
+        elif typ == b"IDAT":
+            idat.append(body)
+        elif typ == b"IEND":
+            seen_end = True
+            break
+        elif typ[0] & 0x20 == 0:            # unknown critical chunk
+            return None
+        pos += 12 + n
+    if not (ihdr_ok and seen_end and idat):
+        return None
+    return b"".join(idat)
+
+
+def parse_roots_device(data, header: RlfcHeader, device, threads=None):
+    """Root planes decoded on the GPU (container.py:175-195 for PNG roots):
+    the host walks the sections and inflates each plane's IDAT stream on a
+    thread pool; the PNG scanline filters are undone by rlfc_png_unfilter
+    and the channel bias removed by rlfc_root_planes straight into the
+    device root tensor (rsx, rsy, 3, Hp, Wp) (int16 when every sample fits,
+    else int32).  Returns the device tensor, or None when
+    the stream is not a plain 16-bit PNG-root stream; the caller then takes
+    parse_roots (Pillow), which raises exactly the reference's errors."""
+    import zlib
+    from concurrent.futures import ThreadPoolExecutor
+    import torch
+    from . import _native
+    if header.root_codec_id != CODEC_PNG:
+        return None
+    wp, hp = header.padded_dims
+    rsx, rsy = level_dims(header.s_count, header.t_count, header.tree_height)
+    starts, _ = section_offsets(header)
+    blobs = []
+    for c in range(3):
+        pos = starts[c][0]
+        end = pos + header.section_lengths[c][0]
+        for _ in range(rsy * rsx):
+            if pos + 4 > end:
+                return None
+            (n,) = struct.unpack_from("<I", data, pos)
+            if pos + 4 + n > end:
+                return None
+            blobs.append(bytes(data[pos + 4:pos + 4 + n]))
+            pos += 4 + n
+        if pos != end:
+            return None
+    stride = hp * (1 + 2 * wp)
+
+    def inflate(b):
+        z = _png_idat(b, wp, hp)
+        if z is None:
+            return None
+        try:
+            raw = zlib.decompress(z)
+        except zlib.error:
+            return None
+        return raw if len(raw) == stride else None
+
+    nthreads = threads or min(32, os.cpu_count() or 1)
+    with ThreadPoolExecutor(max_workers=nthreads) as ex:
+        raws = list(ex.map(inflate, blobs))
+    if any(r is None for r in raws):
+        return None
+    L = _native.lib()
+    dev = torch.device(device)
+    host = torch.empty((len(raws), stride), dtype=torch.uint8).pin_memory()
+    hv = host.numpy()
+    for i, r in enumerate(raws):
+        hv[i] = np.frombuffer(r, dtype=np.uint8)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        raw_d = host.to(dev, non_blocking=True)
+        samples = torch.empty((len(raws), hp, wp), dtype=torch.int16, device=dev)
+        bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        _native.check(L.rlfc_png_unfilter(raw_d.data_ptr(), stride, len(raws), wp, hp, samples.data_ptr(),
+                                          hp * wp, bad.data_ptr(), stream), "rlfc_png_unfilter")
+        roots = torch.empty((rsx, rsy, 3, hp, wp), dtype=torch.int16, device=dev)
+        mm = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=dev)
+        _native.check(L.rlfc_root_planes(samples.data_ptr(), len(raws), rsx, rsy, hp, wp, 1, roots.data_ptr(),
+                                         mm.data_ptr(), stream), "rlfc_root_planes")
+        lo, hi = mm.cpu().tolist()
+        if bad.item():
+            return None
+        if lo < -32768 or hi > 32767:
+            roots = torch.empty((rsx, rsy, 3, hp, wp), dtype=torch.int32, device=dev)
+            _native.check(L.rlfc_root_planes(samples.data_ptr(), len(raws), rsx, rsy, hp, wp, 0, roots.data_ptr(),
+                                             None, stream), "rlfc_root_planes")
+    return roots
+
+
 def parse_offsets(data, header: RlfcHeader, channel):
     wb, hb = header.block_grid
     starts, _ = section_offsets(header)

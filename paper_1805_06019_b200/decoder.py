@@ -48,7 +48,7 @@ class DeviceField:
     (rsx, rsy, 3, Hp, Wp) int16 tensor (int32 if any sample needs it).
     """
 
-    def __init__(self, header, srv, offsets, root_planes, device):
+    def __init__(self, header, srv, offsets, root_planes, device, roots_dev=None):
         torch = _torch()
         self.device = torch.device(device)
         self.header = header
@@ -64,10 +64,15 @@ class DeviceField:
             self.srv.append(buf.to(self.device))
             off = np.ascontiguousarray(offsets[c]).view(np.int64)
             self.offsets.append(torch.from_numpy(off.copy()).to(self.device))
-        i16 = bool(root_planes.size == 0 or (root_planes.min() >= -32768 and
-                                             root_planes.max() <= 32767))
-        rp = root_planes.astype(np.int16 if i16 else np.int32)
-        self.roots = torch.from_numpy(np.ascontiguousarray(rp)).to(self.device)
+        if roots_dev is not None and roots_dev.device == self.device:
+            # decoded on this GPU at init (container.parse_roots_device)
+            self.roots = roots_dev
+            i16 = roots_dev.dtype == torch.int16
+        else:
+            i16 = bool(root_planes.size == 0 or (root_planes.min() >= -32768 and
+                                                 root_planes.max() <= 32767))
+            rp = root_planes.astype(np.int16 if i16 else np.int32)
+            self.roots = torch.from_numpy(np.ascontiguousarray(rp)).to(self.device)
         f = _native.RlfcField()
         wp, hp = header.padded_dims
         wb, hb = header.block_grid
@@ -251,14 +256,25 @@ class DecoderState:
     per-GPU device copies."""
     header: container.RlfcHeader
     data: bytes
-    root_planes: np.ndarray      # (rsx, rsy, 3, Hp, Wp) int32, unbiased
+    _root_host: object           # (rsx, rsy, 3, Hp, Wp) int32, unbiased, or None (on the GPU)
     offsets: tuple               # per channel u64 array, one per block
     srv: tuple                   # per channel uint8 view of the SRV stream
     chains: np.ndarray           # (S, T, h) ascending serial ancestor indices
     m_nodes: int
     _devices: dict = field(default_factory=dict, compare=False, repr=False)
+    _roots_dev: dict = field(default_factory=dict, compare=False, repr=False)
     _lock: object = field(default_factory=threading.Lock, compare=False,
                           repr=False)
+
+    @property
+    def root_planes(self) -> np.ndarray:
+        """(rsx, rsy, 3, Hp, Wp) int32 root planes, bias removed (reference
+        DecoderState.root_planes).  When the roots were decoded on the GPU at
+        init, the host copy is made on first use."""
+        if self._root_host is None:
+            t = next(iter(self._roots_dev.values()))
+            object.__setattr__(self, "_root_host", t.cpu().numpy().astype(np.int32))
+        return self._root_host
 
     def device_field(self, device=None) -> DeviceField:
         """The stream's HBM copy on `device` (default: current CUDA device),
@@ -271,8 +287,10 @@ class DecoderState:
         with self._lock:
             df = self._devices.get(key)
             if df is None:
+                rd = self._roots_dev.get(key)
                 df = DeviceField(self.header, self.srv, self.offsets,
-                                 self.root_planes, dev)
+                                 None if rd is not None else self.root_planes,
+                                 dev, roots_dev=rd)
                 self._devices[key] = df
         return df
 
@@ -282,16 +300,27 @@ def init(stream: bytes, device=None) -> DecoderState:
     header = container.parse_header(stream)
     container.check_stream_length(header, stream)
     data = bytes(stream)
-    roots = container.parse_roots(data, header)
+    torch = _torch()
+    _native.lib()                       # no CUDA device: NativeUnavailable
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if device is None else torch.device(device)
+    # PNG roots: inflated on host threads, unfiltered on the GPU; anything
+    # unusual goes through Pillow (the reference's decoder and errors)
+    got = container.parse_roots_device(data, header, dev)
+    roots_dev, roots = got, None
+    if got is None:
+        roots = container.parse_roots(data, header)
     offsets = tuple(container.parse_offsets(data, header, c) for c in range(3))
     srv = tuple(container.srv_section(data, header, c) for c in range(3))
     chains = container.all_chains(header.s_count, header.t_count,
                                   header.tree_height)
     m = container.total_srv_nodes(header.s_count, header.t_count,
                                   header.tree_height)
-    state = DecoderState(header=header, data=data, root_planes=roots,
+    state = DecoderState(header=header, data=data, _root_host=roots,
                          offsets=offsets, srv=srv, chains=chains, m_nodes=m)
-    state.device_field(device)
+    if roots_dev is not None:
+        state._roots_dev[dev.index] = roots_dev
+    state.device_field(dev)
     return state
 
 
