@@ -157,7 +157,9 @@ int rlfc_decode_field_simple(const rlfc_field *f, int32_t stop_level,
  * (bad descriptor, truncation, corrupt pack); it returns their number in
  * *n_flagged, which each decode call takes back: units touching them are
  * redone by the reference-order walk after the blend, so values and the
- * failure word are identical to rlfc_decode_field's. */
+ * failure word are identical to rlfc_decode_field's.  t_rows (device,
+ * n_trows entries; NULL = every camera row) restricts the blend to the camera
+ * rows holding requested views (with an image slot table). */
 int rlfc_count_present(const rlfc_field *f, uint64_t *count, void *stream);
 int rlfc_decode_workspace_bytes(const rlfc_field *f, uint64_t present_total,
                                 uint64_t *bytes);
@@ -169,7 +171,8 @@ int rlfc_decode_field_staged(const rlfc_field *f, int32_t stop_level,
                              int32_t by_hi, uint8_t *rgb, int64_t img_stride,
                              int64_t row_stride, void *workspace,
                              uint64_t workspace_bytes, uint64_t present_total,
-                             int32_t n_flagged, uint64_t *status,
+                             int32_t n_flagged, const int32_t *t_rows,
+                             int32_t n_trows, uint64_t *status,
                              void *stream);
 
 /* Device record directory: the stream-invariant part of the reference's

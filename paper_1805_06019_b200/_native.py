@@ -80,7 +80,7 @@ _SIGS = {
     "rlfc_decode_blocks_indexed": ["p", "p", "u", "u", "p", "i", "p", "p", "p"],
     "rlfc_decode_workspace_bytes": ["p", "u", "p"],
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
-                                 "u", "u", "i", "p", "p"],
+                                 "u", "u", "i", "p", "i", "p", "p"],
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
     "rlfc_chain_core": ["p", "u", "p", "i", "i", "i", "p", "i", "i", "p", "p",
                         "p"],

@@ -865,6 +865,7 @@ struct BlendParams {
     int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
     int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
     int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
+    const int32_t* trows;        // camera rows to decode (grid.y indexes it), or null = all
     uint32_t* units;             // prepared dirty-unit lists (B = 4), or null
     int ucap;
     int build_units;             // 1: this launch writes the lists (prepare, k = 0)
@@ -1075,7 +1076,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
     constexpr int QB = B / 4;                      // pixel quads per block row
     const rlfc_field& f = P.f;
     const int tid = threadIdx.x;
-    const int chunk = blockIdx.x, t = blockIdx.y;
+    const int chunk = blockIdx.x, t = P.trows ? P.trows[blockIdx.y] : (int)blockIdx.y;
     const int by = P.by_lo + blockIdx.z;
     const int NB = P.NB, TW = P.TW, NR = 3 * NB;
     const int bx0 = chunk * NB;
@@ -1104,11 +1105,20 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         // last warp (no record work when NR <= BT - 32): lane 0 arms the
         // barrier, then every lane issues its share of the tensor loads
         const uint32_t bar = smem_u32(mbar);
+        // with a slot table only the requested views of this camera row are
+        // prefilled (their count sets the barrier's byte count)
+        const int ln = tid - (BT - 32);
+        uint32_t need = 0;
+        for (int s0 = 0; s0 < S; s0 += 32) {
+            const int s = s0 + ln;
+            const bool want = s < S && (!P.slots || P.slots[s * T + t] >= 0);
+            need += __popc(__ballot_sync(0xffffffffu, want));
+        }
         if (tid == BT - 32) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             const uint32_t bytes =
-                (uint32_t)(P.nstrip * S * B * STRIP * 3) + (uint32_t)(f.rsx * 3 * B * TW * (int)sizeof(RT));
+                (uint32_t)(P.nstrip * need * B * STRIP * 3) + (uint32_t)(f.rsx * 3 * B * TW * (int)sizeof(RT));
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
         }
         __syncwarp();
@@ -1116,6 +1126,7 @@ __global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__
         for (int i = tid - (BT - 32); i < nrgb + f.rsx * 3; i += 32) {
             if (i < nrgb) {
                 const int st = i / S, s = i - st * S;
+                if (P.slots && P.slots[s * T + t] < 0) continue;
                 asm volatile(
                     "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
                     "%4}], [%5];" ::"r"(smem_u32(stage + ((st * S + s) * B) * (STRIP * 3))),
@@ -1587,7 +1598,7 @@ static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi,
 template <int B, typename VT, typename RT>
 static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
                   int64_t img_stride, int64_t row_stride, const Ws& w, int n_flagged, uint64_t* status,
-                  cudaStream_t stream, bool build_units = false) {
+                  cudaStream_t stream, bool build_units = false, const int32_t* trows = nullptr, int ntrows = 0) {
     constexpr int BSQ = B * B;
     const bool tma_ok = w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 &&
                         ((f.wp * (int)sizeof(RT)) % 16) == 0 && encode_fn() != nullptr;
@@ -1620,6 +1631,7 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     P.rk = w.rk;
     P.nwp = w.nwp;
     P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
+    P.trows = trows && !build_units ? trows : nullptr;
     P.units = B == 4 && P.NB == 16 ? w.units : nullptr;
     P.ucap = w.ucap;
     P.build_units = build_units && P.units ? 1 : 0;
@@ -1683,7 +1695,8 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     // tile residency is bounded by shared memory: ask for the largest carveout
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    const dim3 grid((unsigned)P.nchunks, (unsigned)f.t_count, (unsigned)(by_hi - by_lo));
+    const dim3 grid((unsigned)P.nchunks, (unsigned)(P.trows ? ntrows : f.t_count), (unsigned)(by_hi - by_lo));
+    if (grid.y == 0) return RLFC_OK;
     {
         const cudaLaunchConfig_t c = cfg_of(grid, dim3(bt), pl.smem, k < h && !P.build_units);
         cudaLaunchKernelEx(&c, kern, P, out_map, rgb_map, root_map);
@@ -1835,8 +1848,8 @@ extern "C" int rlfc_decode_blocks_indexed(const rlfc_field* f, void* workspace, 
 extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level, const int32_t* image_slots,
                                         int32_t by_lo, int32_t by_hi, uint8_t* rgb, int64_t img_stride,
                                         int64_t row_stride, void* workspace, uint64_t workspace_bytes,
-                                        uint64_t present_total, int32_t n_flagged, uint64_t* status,
-                                        void* stream) {
+                                        uint64_t present_total, int32_t n_flagged, const int32_t* t_rows,
+                                        int32_t n_trows, uint64_t* status, void* stream) {
     if (!f || !rgb || !status || !workspace) return RLFC_ERR_ARGUMENT;
     if (stop_level < 0 || stop_level > f->tree_height || by_lo < 0 || by_hi > f->hb || by_lo > by_hi)
         return RLFC_ERR_ARGUMENT;
@@ -1850,15 +1863,15 @@ extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level,
 #define RLFC_STAGED(B_)                                                                                            \
     if (small && r16)                                                                                              \
         return staged::launch<B_, int16_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, n_flagged, status, s);                                     \
+                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows);                                     \
     if (small)                                                                                                     \
         return staged::launch<B_, int16_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, n_flagged, status, s);                                     \
+                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows);                                     \
     if (r16)                                                                                                       \
         return staged::launch<B_, int32_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, n_flagged, status, s);                                     \
+                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows);                                     \
     return staged::launch<B_, int32_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,       \
-                                                row_stride, w, n_flagged, status, s);
+                                                row_stride, w, n_flagged, status, s, false, t_rows, n_trows);
     switch (f->block) {
         case 4: { RLFC_STAGED(4) }
         case 8: { RLFC_STAGED(8) }

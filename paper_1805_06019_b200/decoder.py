@@ -496,7 +496,7 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
     if not 0 <= by_lo <= by_hi <= hb:
         raise ValueError(f"block-row band {rows} outside [0, {hb}]")
     nrows = max(0, min(by_hi * B, H) - by_lo * B)
-    slots_t = None
+    slots_t = trows_t = None
     if images is None:
         shape = (S, T, nrows, W, 3)
         nimg = S * T
@@ -511,6 +511,8 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
         shape = (len(pairs), nrows, W, 3)
         nimg = len(pairs)
         slots_t = torch.from_numpy(slots).to(df.device)
+        trows_t = torch.tensor(sorted({t for _, t in pairs}), dtype=torch.int32,
+                               device=df.device)
     if out is None:
         out = torch.empty(shape, dtype=torch.uint8, device=df.device)
     elif tuple(out.shape) != shape or out.dtype != torch.uint8 or \
@@ -543,6 +545,8 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
                             df.ref, stop_level, slots_p, by_lo, by_hi,
                             out.data_ptr(), nrows * W * 3, W * 3,
                             ws[0].data_ptr(), ws[1], ws[2], ws[3],
+                            None if trows_t is None else trows_t.data_ptr(),
+                            0 if trows_t is None else trows_t.numel(),
                             status.data_ptr(), stream)
                     if rc != _native.RLFC_ERR_ARGUMENT:
                         _native.check(rc, "rlfc_decode_field_staged")
@@ -559,13 +563,17 @@ def decode_field(state, stop_level=0, images=None, rows=None, out=None,
     return out, status
 
 
-def decode_field_slots(state, stop_level, slots, n, device=None):
+def decode_field_slots(state, stop_level, slots, n, device=None, rows=None):
     """decode_field for a prebuilt device slot table (slots[s*T + t] = output
-    index or -1, n outputs): the renderer's tap-camera decode.  Returns
-    (field (n, H, W, 3), status word tensor) without synchronising."""
+    index or -1, n outputs): the renderer's tap-camera decode.  rows: the
+    camera rows holding requested views (host ints; None = all rows).
+    Returns (field (n, H, W, 3), status word tensor) without
+    synchronising."""
     torch = _torch()
     hdr = state.header
     df = state.device_field(device)
+    trows = None if rows is None else torch.tensor(sorted(set(int(r) for r in rows)),
+                                                   dtype=torch.int32, device=df.device)
     W, H = hdr.width, hdr.height
     out = torch.empty((n, H, W, 3), dtype=torch.uint8, device=df.device)
     status = torch.zeros(1, dtype=torch.int64, device=df.device)
@@ -580,7 +588,9 @@ def decode_field_slots(state, stop_level, slots, n, device=None):
                 rc = L.rlfc_decode_field_staged(
                     df.ref, stop_level, slots.data_ptr(), 0, hb,
                     out.data_ptr(), H * W * 3, W * 3, ws[0].data_ptr(), ws[1],
-                    ws[2], ws[3], status.data_ptr(), stream)
+                    ws[2], ws[3], None if trows is None else trows.data_ptr(),
+                    0 if trows is None else trows.numel(), status.data_ptr(),
+                    stream)
         if rc == _native.RLFC_ERR_ARGUMENT:
             rc = L.rlfc_decode_field(df.ref, stop_level, slots.data_ptr(), 0,
                                      hb, out.data_ptr(), H * W * 3, W * 3,
@@ -857,7 +867,7 @@ class HostPipeline:
                 if ws is not None:
                     rc = L.rlfc_decode_field_staged(
                         df.ref, 0, None, lo, hi, dst, img, W * 3,
-                        ws[0].data_ptr(), ws[1], ws[2], ws[3],
+                        ws[0].data_ptr(), ws[1], ws[2], ws[3], None, 0,
                         self.status.data_ptr(), s_dec.cuda_stream)
                 if rc == _native.RLFC_ERR_ARGUMENT:
                     rc = L.rlfc_decode_field(

@@ -303,7 +303,8 @@ def _decode_cameras(state, cams, stop_level, device):
     d_slots = torch.from_numpy(slots).to(df.device)
     if len(cams):
         field, status = decoder.decode_field_slots(state, stop_level, d_slots,
-                                                   len(cams), device=device)
+                                                   len(cams), device=device,
+                                                   rows=cams % T)
         return field, d_slots, status
     field = torch.zeros((1, hdr.height, hdr.width, 3), dtype=torch.uint8,
                         device=df.device)

@@ -154,7 +154,7 @@ def test_staged_path_taken(rl, name):
     rc = _native.lib().rlfc_decode_field_staged(
         df.ref, 0, None, 0, hdr.block_grid[1], out.data_ptr(),
         hdr.height * hdr.width * 3, hdr.width * 3, ws.data_ptr(), nbytes,
-        present, nflag, status.data_ptr(), 0)
+        present, nflag, None, 0, status.data_ptr(), 0)
     assert rc == _native.RLFC_OK
     torch.cuda.synchronize()
     assert status.item() == 0

@@ -51,7 +51,7 @@ def main():
         def call():
             return L.rlfc_decode_field_staged(df.ref, 0, None, 0, hdr.block_grid[1], out.data_ptr(),
                                               hdr.height * hdr.width * 3, hdr.width * 3, w2.data_ptr(), ws[1],
-                                              ws[2], nf.value, status.data_ptr(), stream)
+                                              ws[2], nf.value, None, 0, status.data_ptr(), stream)
         for _ in range(3):
             assert call() == 0
         torch.cuda.synchronize()
