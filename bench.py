@@ -42,7 +42,8 @@ def log(*a):
 
 
 def make_stream(cfg, cache_dir=os.path.join(ROOT, "data")):
-    """Produce (or reuse) the benchmark stream with the native producer."""
+    """Produce (or reuse) the benchmark stream: RKV/SRV trees built on the
+    GPU (producer.encode_gpu), byte-identical to the reference encoder."""
     import hashlib
     from paper_1805_06019_b200 import encoder, lightfield
     key = hashlib.sha1(json.dumps(cfg, sort_keys=True).encode()).hexdigest()[:12]
@@ -57,7 +58,9 @@ def make_stream(cfg, cache_dir=os.path.join(ROOT, "data")):
         tree_height=cfg["h"], block_size=cfg["B"], quant_shift=cfg["shift"],
         pixel_threshold=cfg["tp"], block_threshold=cfg["tb"],
         root_codec=cfg["codec"])
-    data, rep = encoder.compress(lf, params)
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else None
+    data, rep = encoder.compress(lf, params, device=dev)
     log(f"produced stream {len(data)} B ({rep.bpp_total:.3f} bpp) in "
         f"{time.time() - t0:.1f}s; present per level {rep.present_blocks}")
     os.makedirs(cache_dir, exist_ok=True)

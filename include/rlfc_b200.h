@@ -339,6 +339,41 @@ int rlfc_root_planes(const uint16_t *samples, int32_t nplanes, int32_t rsx,
                      int32_t rsy, int32_t hp, int32_t wp, int32_t i16,
                      void *dst, int32_t *minmax, void *stream);
 
+/* Producer side on the GPU (hierarchy.py:182-298 RKV/SRV tree construction,
+ * container.py:300-323 records; csrc/rlfc_encode.cu).  rlfc_enc_planes:
+ * YCoCg-R of rgb (nimg, h_valid, W, 3) into planes (nimg, 3, hp, wp) int32,
+ * zero padded.  rlfc_enc_pyramid: parent (px, py, 3, hp, wp) = floor((sum of
+ * weights[cell][m] * member m + 128) / 256) over the <= 4 children of each
+ * cell (members x outer, y inner; weights int64 (px*py, 4)).
+ * rlfc_enc_srv_level: one tree level top-down -- residual against the
+ * reconstructed parent `above`, thresholds, quantise, zigzag, range choice,
+ * closed-loop reconstruction written over `planes`; desc [3][nblk][M]
+ * (caller fills 0xFF) and zv [3][nblk][M][B*B] receive the coded blocks of
+ * the level's nodes (serial index level_base + y*sx + x), *present counts
+ * them, *err = 1 when a block exceeds the range table.
+ * rlfc_enc_record_sizes / rlfc_enc_records: per record (c*nblk + block)
+ * its byte size, then its bytes at rec_off (bitmap, descriptor + BISE
+ * payload per present node in BFS order, kernels.py:92-125). */
+int rlfc_enc_planes(const uint8_t *rgb, int64_t nimg, int32_t W,
+                    int32_t h_valid, int32_t hp, int32_t wp, int32_t *planes,
+                    void *stream);
+int rlfc_enc_pyramid(const int32_t *child, int32_t sx, int32_t sy,
+                     int32_t *parent, int32_t px, int32_t py,
+                     const int64_t *weights, int32_t hp, int32_t wp,
+                     void *stream);
+int rlfc_enc_srv_level(int32_t *planes, const int32_t *above, int32_t sx,
+                       int32_t sy, int32_t psy, int32_t hp, int32_t wp,
+                       int32_t block, int32_t pixel_threshold,
+                       int64_t block_threshold, int32_t shift,
+                       int32_t level_base, int32_t m_nodes, uint8_t *desc,
+                       uint16_t *zv, uint64_t *present, int32_t *err,
+                       void *stream);
+int rlfc_enc_record_sizes(const uint8_t *desc, int64_t nrec, int32_t m_nodes,
+                          int32_t bsq, uint64_t *size, void *stream);
+int rlfc_enc_records(const uint8_t *desc, const uint16_t *zv, int64_t nrec,
+                     int32_t m_nodes, int32_t bsq, const uint64_t *rec_off,
+                     uint8_t *out, void *stream);
+
 /* Host plumbing for band-pipelined host-buffer decodes (decoder.HostPipeline):
  * an asynchronous strided copy (cudaMemcpy2DAsync), kind 0 host->device,
  * 1 device->host, 2 device->device.  Not part of the reference interface. */

@@ -94,6 +94,12 @@ _SIGS = {
                                   "p", "p"],
     "rlfc_copy2d": ["p", "q", "p", "q", "q", "q", "i", "p"],
     "rlfc_png_unfilter": ["p", "q", "i", "i", "i", "p", "q", "p", "p"],
+    "rlfc_enc_planes": ["p", "q", "i", "i", "i", "i", "p", "p"],
+    "rlfc_enc_pyramid": ["p", "i", "i", "p", "i", "i", "p", "i", "i", "p"],
+    "rlfc_enc_srv_level": ["p", "p", "i", "i", "i", "i", "i", "i", "i", "q",
+                           "i", "i", "i", "p", "p", "p", "p", "p"],
+    "rlfc_enc_record_sizes": ["p", "q", "i", "i", "p", "p"],
+    "rlfc_enc_records": ["p", "p", "q", "i", "i", "p", "p", "p"],
     "rlfc_root_planes": ["p", "i", "i", "i", "i", "i", "i", "p", "p", "p"],
     "rlfc_version": ["p", "i"],
 }

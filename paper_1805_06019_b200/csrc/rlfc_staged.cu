@@ -1067,7 +1067,10 @@ __global__ void k_flag_list(const uint32_t* rec_flag, int64_t nrec, uint32_t* fl
 }
 
 template <int B, typename VT, typename RT, int BT>
-__global__ void __launch_bounds__(BT, 1024 / BT) k_blend(const __grid_constant__ BlendParams P,
+#ifndef RLFC_BLEND_MINB
+#define RLFC_BLEND_MINB (1024 / BT)
+#endif
+__global__ void __launch_bounds__(BT, RLFC_BLEND_MINB) k_blend(const __grid_constant__ BlendParams P,
                                                    const __grid_constant__ CUtensorMap out_map,
                                                    const __grid_constant__ CUtensorMap rgb_map,
                                                    const __grid_constant__ CUtensorMap root_map) {
@@ -1551,7 +1554,7 @@ struct Plan {
 
 // Blend geometry and shared-memory layout; false when outside the envelope.
 template <typename RT>
-static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_first, Plan& pl) {
+static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_first, Plan& pl, bool no_list = false) {
     const int B = f.block, S = f.s_count, h = f.tree_height;
     BlendParams& P = pl.P;
     auto al = [](int x) { return (x + 127) & ~127; };
@@ -1569,7 +1572,7 @@ static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_fir
         P.off_roots = off; off = al(off + f.rsx * 3 * B * TW * (int)sizeof(RT));
         P.off_rgb = off;   off = al(off + (manual_roots ? f.rsx * B * TW * 3 : 0));
         P.off_cnt = off;   off = al(off + 16);
-        P.off_list = off;  off = al(off + S * NB * 8);
+        P.off_list = off;  off = al(off + (no_list ? 0 : S * NB * 8));
         P.off_stage = off; off = al(off + S * B * TW * 3);
         if (off <= 100 * 1024) {
             P.TW = TW;
@@ -1612,7 +1615,11 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
 #endif
     constexpr int bt = RLFC_BLEND_BT, tw = RLFC_BLEND_TW;     // compile-time (tools/variant_sweep.py)
     Plan pl{};
-    if (!plan_blend<RT>(f, k, !tma_ok, tw, pl)) return RLFC_ERR_ARGUMENT;
+    // with the prepared dirty-unit lists (B = 4, 64-pixel tiles) the shared
+    // pair list is not needed: a smaller tile fits more CTAs per SM
+    const bool lists = B == 4 && w.units && !build_units;
+    if (!plan_blend<RT>(f, k, !tma_ok, tw, pl, lists)) return RLFC_ERR_ARGUMENT;
+    if (lists && pl.P.NB != 16 && !plan_blend<RT>(f, k, !tma_ok, tw, pl, false)) return RLFC_ERR_ARGUMENT;
     BlendParams& P = pl.P;
     P.f = f;
     P.k = k;

@@ -69,13 +69,21 @@ class EncodeReport:
     encode_seconds: float
 
 
-def compress(lf, params: EncodingParams = None, threads=0):
-    """Encode a LightFieldGrid; returns (stream bytes, EncodeReport)."""
+def compress(lf, params: EncodingParams = None, threads=0, device=None):
+    """Encode a LightFieldGrid; returns (stream bytes, EncodeReport).
+
+    device=None runs the native C++ producer on `threads` host threads;
+    a CUDA device ("cuda", "cuda:1") builds the RKV/SRV trees and the
+    records there (producer.encode_gpu).  Both are byte-identical to the
+    reference encoder (tests/test_producer.py, tests/test_gpu_encoder.py)."""
     from . import producer
     from .container import parse_header
     params = params or EncodingParams()
     t0 = time.perf_counter()
-    stream, present = producer.encode(lf, params, threads=threads)
+    if device is None:
+        stream, present = producer.encode(lf, params, threads=threads)
+    else:
+        stream, present = producer.encode_gpu(lf, params, device=device)
     elapsed = time.perf_counter() - t0
     pixels = lf.s_count * lf.t_count * lf.width * lf.height
     hdr = parse_header(stream)

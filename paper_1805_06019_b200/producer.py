@@ -158,16 +158,25 @@ def _encode_rows(rgb, S, T, W, h_valid, hp_rows, params, weights):
 
 def _assemble(S, T, W, H, params, roots, srvs, offs, present):
     """Root streams + header + sections (container.py:269-339 layout)."""
+    from concurrent.futures import ThreadPoolExecutor
     rsx, rsy = container.level_dims(S, T, params.tree_height)
     codec = container.CODEC_IDS[params.root_codec]
+    # root planes are coded independently (Pillow releases the GIL while it
+    # compresses); the stream order stays channel, y, x
+    keys = [(c, y, x) for c in range(3) for y in range(rsy) for x in range(rsx)]
+
+    def one(key):
+        c, y, x = key
+        return container.encode_root(
+            roots[x, y, c].astype(np.int64) + container.CHANNEL_BIAS[c], codec)
+    with ThreadPoolExecutor(max_workers=min(len(keys), os.cpu_count() or 1)) as ex:
+        blobs = dict(zip(keys, ex.map(one, keys)))
     sections, lengths = [], []
     for c in range(3):
         chunks = []
         for y in range(rsy):
             for x in range(rsx):
-                blob = container.encode_root(
-                    roots[x, y, c].astype(np.int64) + container.CHANNEL_BIAS[c],
-                    codec)
+                blob = blobs[(c, y, x)]
                 chunks.append(len(blob).to_bytes(4, "little"))
                 chunks.append(blob)
         root_sec = b"".join(chunks)
@@ -187,6 +196,91 @@ def _assemble(S, T, W, H, params, roots, srvs, offs, present):
         root_codec_id=codec, section_lengths=tuple(lengths))
     return container.pack_header(header) + b"".join(sections), \
         tuple(int(v) for v in present)
+
+
+def _encode_rows_gpu(rgb, S, T, W, h_valid, hp_rows, params, weights,
+                     device="cuda"):
+    """_encode_rows on the GPU (csrc/rlfc_encode.cu): the same outputs --
+    (roots band, [srv_c], [offsets_c], present per level) -- from the RKV
+    pyramid, the top-down SRV pass with closed-loop reconstruction and the
+    record serialisation run as CUDA kernels."""
+    import torch
+    from . import _native
+    L = _native.lib()
+    dev = torch.device(device)
+    B, h = params.block_size, params.tree_height
+    bsq = B * B
+    wp = -(-W // B) * B
+    hp = hp_rows
+    wb, hb = wp // B, hp // B
+    nblk = wb * hb
+    plane = hp * wp
+    ldim = lambda n, l: -(-n // (1 << l))                          # noqa: E731
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        d_rgb = torch.from_numpy(np.ascontiguousarray(rgb, dtype=np.uint8)).to(dev)
+        lv = [torch.empty(S * T * 3 * plane, dtype=torch.int32, device=dev)]
+        _native.check(L.rlfc_enc_planes(d_rgb.data_ptr(), S * T, W, h_valid, hp, wp, lv[0].data_ptr(), stream),
+                      "rlfc_enc_planes")
+        del d_rgb
+        d_w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.int64)).to(dev)
+        woff = 0
+        for l in range(1, h + 1):
+            sx, sy, px, py = ldim(S, l - 1), ldim(T, l - 1), ldim(S, l), ldim(T, l)
+            lv.append(torch.empty(px * py * 3 * plane, dtype=torch.int32, device=dev))
+            _native.check(L.rlfc_enc_pyramid(lv[l - 1].data_ptr(), sx, sy, lv[l].data_ptr(), px, py,
+                                             d_w.data_ptr() + 8 * woff, hp, wp, stream), "rlfc_enc_pyramid")
+            woff += px * py * 4
+        rsx, rsy = ldim(S, h), ldim(T, h)
+        roots = lv[h].view(rsx, rsy, 3, hp, wp).cpu().numpy()
+        base, M = {}, 0
+        for l in range(h - 1, -1, -1):
+            base[l] = M
+            M += ldim(S, l) * ldim(T, l)
+        desc = torch.full((3 * nblk * M,), 0xFF, dtype=torch.uint8, device=dev)
+        zv = torch.empty(3 * nblk * M * bsq, dtype=torch.int16, device=dev)
+        present = torch.zeros(h, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        above = lv[h]
+        for l in range(h - 1, -1, -1):
+            sx, sy, psy = ldim(S, l), ldim(T, l), ldim(T, l + 1)
+            _native.check(L.rlfc_enc_srv_level(
+                lv[l].data_ptr(), above.data_ptr(), sx, sy, psy, hp, wp, B, params.pixel_threshold,
+                params.block_threshold, params.quant_shift, base[l], M, desc.data_ptr(), zv.data_ptr(),
+                present.data_ptr() + 8 * l, err.data_ptr(), stream), "rlfc_enc_srv_level")
+            above = lv[l]
+        if err.item():
+            raise FormatError("residual value outside the range table")
+        nrec = 3 * nblk
+        size = torch.empty(nrec, dtype=torch.int64, device=dev)
+        _native.check(L.rlfc_enc_record_sizes(desc.data_ptr(), nrec, M, bsq, size.data_ptr(), stream),
+                      "rlfc_enc_record_sizes")
+        ends = torch.cumsum(size, 0)
+        starts = ends - size
+        total = int(ends[-1].item()) if nrec else 0
+        out = torch.empty(max(1, total), dtype=torch.uint8, device=dev)
+        _native.check(L.rlfc_enc_records(desc.data_ptr(), zv.data_ptr(), nrec, M, bsq, starts.data_ptr(),
+                                         out.data_ptr(), stream), "rlfc_enc_records")
+        starts_h = starts.cpu().numpy()
+        out_h = out.cpu().numpy()
+        srvs, offs = [], []
+        for c in range(3):
+            c0 = int(starts_h[c * nblk]) if nblk else 0
+            c1 = int(starts_h[(c + 1) * nblk]) if c < 2 else total
+            offs.append((starts_h[c * nblk:(c + 1) * nblk] - c0).astype("<u8"))
+            srvs.append(out_h[c0:c1].copy())
+        return roots.astype(np.int32), srvs, offs, present.cpu().numpy()
+
+
+def encode_gpu(lf, params, device="cuda"):
+    """encode() with the RKV/SRV trees and the records built on the GPU;
+    root views are still coded by Pillow on the host (container.py:152-172)."""
+    S, T, W, H = lf.s_count, lf.t_count, lf.width, lf.height
+    w = np.ascontiguousarray(pyramid_weights(lf.camera_positions,
+                                             params.tree_height, params.filter))
+    hp = -(-H // params.block_size) * params.block_size
+    roots, srvs, offs, present = _encode_rows_gpu(lf.rgb, S, T, W, H, hp, params, w, device)
+    return _assemble(S, T, W, H, params, roots, srvs, offs, present)
 
 
 def encode(lf, params, threads=0):
