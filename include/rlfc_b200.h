@@ -265,6 +265,15 @@ int rlfc_chain_core(const uint8_t *srv, uint64_t srv_len,
                     int32_t bsq, const int64_t *targets, int32_t nt,
                     int32_t shift, int32_t *out, int32_t *status,
                     void *stream);
+/* rlfc_chain_core for ONE request on the latency path (decoder.py:101-104
+ * calls decode_chain_core per block): targets (nt <= 16) are read on the
+ * host, io is pinned host memory of bsq + 1 int32 -- the root block in, the
+ * target residuals out, status (kernels.py:165-171 codes) in io[bsq] written
+ * last.  Synchronous: returns after polling that word. */
+int rlfc_chain_core_sync(const uint8_t *srv, uint64_t srv_len,
+                         uint64_t rec_off, int32_t m_nodes, int32_t bsq,
+                         const int64_t *targets, int32_t nt, int32_t shift,
+                         int32_t *io, void *stream);
 int rlfc_plane_core(const uint8_t *srv, uint64_t srv_len,
                     const uint64_t *offsets, int32_t blocks_x,
                     int32_t blocks_y, int32_t m_nodes, int32_t block,

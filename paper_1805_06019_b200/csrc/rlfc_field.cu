@@ -76,9 +76,8 @@ struct Params {
                                // cp.async.bulk, 0: byte stores (unaligned rows)
     int roots_all;             // 1: every root of the tile is staged at setup
     int roots_vec;             // 1: root rows are 16-byte aligned in HBM
-    int no_prefill;            // debug knob (RLFC_TILED_NO_PREFILL=1): every view dirty
+    int no_prefill;            // tuning build only (RLFC_TUNING): every view dirty
     int specialized;           // 1: dedicated walker warps (named-barrier handoff)
-    int debug;                 // debug bits (RLFC_TILED_DEBUG): 1 skip copies, 2 all dirty
 };
 
 // One decode job: payload byte offset in the staged tile (16 bits), descriptor
@@ -904,12 +903,14 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     const int plane = 3 * B * TW;
     const int root_row_bytes = f.rsx * plane * (int)sizeof(RT);
     P.roots_all = f.rsy * root_row_bytes <= 16 * 1024;
+    P.no_prefill = 0;
+#ifdef RLFC_TUNING
+    // experiment knobs exist only in a tuning build (never the shipped .so)
     {
         const char* e = getenv("RLFC_TILED_NO_PREFILL");
         P.no_prefill = e && e[0] == '1';
-        const char* d = getenv("RLFC_TILED_DEBUG");
-        P.debug = d ? atoi(d) : 0;
     }
+#endif
     P.roots_vec = ((f.wp * (int)sizeof(RT)) % 16) == 0 && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0;
     auto al = [](int x) { return (x + 127) & ~127; };
     int off = al((int)sizeof(DigitLut));
@@ -960,14 +961,16 @@ int launch(const rlfc_field& f, int stop_level, const int32_t* slots, int by_lo,
     auto kern = k_decode_field_tiled<B, TW, VT, RT>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int threads = 128;                               // measured best (profiles/)
+    P.specialized = 0;
+#ifdef RLFC_TUNING
     if (const char* e = getenv("RLFC_TILED_THREADS")) threads = atoi(e) == 256 ? 256 : 128;
     {
-        // dedicated walker warps measured slower (152 vs 199 Gpix/s, cfg2 R4):
-        // opt-in only
+        // dedicated walker warps measured slower (152 vs 199 Gpix/s, cfg2 R4)
         const char* e = getenv("RLFC_TILED_SPEC");
         P.specialized = e && e[0] == '1';
         if (P.specialized) threads += 64;            // + two dedicated walker warps
     }
+#endif
     const int grid = P.tiles_x * (by_hi - by_lo);
     kern<<<grid, threads, smem, stream>>>(P, map);  // P.specialized set above
     cudaError_t e = cudaGetLastError();

@@ -10,6 +10,8 @@
 // 2 on a bad descriptor).  Reads stay inside the SRV section: a descriptor
 // or payload past its end reports 2 (the reference has no bounds checks).
 #include <cuda_runtime.h>
+#include <atomic>
+#include <climits>
 #include <cstdint>
 
 #include "rlfc_common.cuh"
@@ -73,6 +75,23 @@ __global__ void k_chain_core(const uint8_t* srv, uint64_t srv_len, const uint64_
     for (int j = 0; j < bsq; ++j) out[(int64_t)i * bsq + j] = acc[j];
 }
 
+// One request, latency path: the targets ride in the kernel parameters and
+// the block lives in the caller's pinned host buffer (io[0..bsq) = the root
+// block in, the result out), status word io[bsq] written last.
+struct ChainOne {
+    int64_t targets[16];
+};
+
+__global__ void k_chain_core_one(const uint8_t* srv, uint64_t srv_len, uint64_t rec_off, int m_nodes, int bsq,
+                                 const __grid_constant__ ChainOne tg, int nt, int shift, volatile int32_t* io) {
+    int32_t acc[256];
+    for (int j = 0; j < bsq; ++j) acc[j] = io[j];
+    const int st = walk_targets(srv, srv_len, rec_off, m_nodes, bsq, tg.targets, nt, shift, acc);
+    for (int j = 0; j < bsq; ++j) io[j] = acc[j];
+    __threadfence_system();
+    io[bsq] = st;
+}
+
 // kernels.py:219-242: every block of one plane; the failure word keeps the
 // first failing block in row-major order (the reference returns there).
 __global__ void k_plane_core(const uint8_t* srv, uint64_t srv_len, const uint64_t* offsets, int bxn, int byn,
@@ -125,4 +144,34 @@ extern "C" int rlfc_plane_core(const uint8_t* srv, uint64_t srv_len, const uint6
         srv, srv_len, offsets, blocks_x, blocks_y, m_nodes, block, targets, nt, shift, root_plane, out_plane,
         reinterpret_cast<unsigned long long*>(status));
     return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
+extern "C" int rlfc_chain_core_sync(const uint8_t* srv, uint64_t srv_len, uint64_t rec_off, int32_t m_nodes,
+                                    int32_t bsq, const int64_t* targets, int32_t nt, int32_t shift, int32_t* io,
+                                    void* stream) {
+    if (!srv || !io || nt < 0 || nt > 16 || (nt && !targets) || m_nodes < 1 ||
+        (bsq != 4 && bsq != 16 && bsq != 64 && bsq != 256) || shift < 0 || shift > 30)
+        return RLFC_ERR_ARGUMENT;
+    kabi::ChainOne tg{};
+    for (int i = 0; i < nt; ++i) tg.targets[i] = targets[i];
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    volatile int32_t* flag = io + bsq;
+    *flag = INT_MIN;                           // never a status value
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    kabi::k_chain_core_one<<<1, 1, 0, st>>>(srv, srv_len, rec_off, m_nodes, bsq, tg, nt, shift, io);
+    if (cudaGetLastError() != cudaSuccess) return RLFC_ERR_CUDA;
+    // poll the status word (a stream synchronize's wake-up is most of one
+    // request's latency); query the stream every 1024 polls so a failed
+    // launch cannot hang the caller
+    for (uint32_t i = 1; *flag == INT_MIN; ++i) {
+        if ((i & 1023u) == 0) {
+            const cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaErrorNotReady) continue;
+            if (q != cudaSuccess) return RLFC_ERR_CUDA;
+            if (*flag == INT_MIN) return RLFC_ERR_CUDA;
+            break;
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return RLFC_OK;
 }
