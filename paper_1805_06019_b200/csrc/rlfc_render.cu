@@ -97,13 +97,13 @@ __global__ void __launch_bounds__(256) k_render_slab(const uint8_t* __restrict__
                                                      const double* __restrict__ poses,
                                                      const rlfc_render_geom* __restrict__ geoms,
                                                      const uint8_t* __restrict__ bgs, int ow, int oh,
-                                                     uint8_t* __restrict__ out) {
+                                                     uint8_t* __restrict__ out, int rb) {
     extern __shared__ __align__(16) uint8_t rsm[];
     AxisTap* cols = reinterpret_cast<AxisTap*>(rsm);          // [ow]
-    AxisTap* rows = cols + ow;                                 // [RB]
+    AxisTap* rows = cols + ow;                                 // [rb]
     const int v = blockIdx.y;
-    const int j0 = blockIdx.x * RB;
-    const int nrow = min(RB, oh - j0);
+    const int j0 = blockIdx.x * rb;
+    const int nrow = min(rb, oh - j0);
     const rlfc_render_geom g = geoms[v];
     const double ps = poses[4 * v], pt = poses[4 * v + 1];
     const double focal = poses[4 * v + 2] != 0.0 ? poses[4 * v + 3] : g.img_z;
@@ -278,11 +278,20 @@ extern "C" int rlfc_render_slab(const uint8_t* field, const int32_t* slots, int3
                                 int32_t ow, int32_t oh, uint8_t* out, void* stream) {
     if (S < 1 || T < 1 || W < 1 || H < 1 || n < 0 || ow < 1 || oh < 1 || n > 65535) return RLFC_ERR_ARGUMENT;
     if (n == 0) return RLFC_OK;
-    const size_t smem = (size_t)(ow + RB) * sizeof(AxisTap);
+    // rows per CTA: RB when the batch fills the GPU, fewer for small batches
+    // (a single 512-row view is 32 CTAs at RB = 16: under a quarter of the SMs)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want_ctas = 4ll * sms;
+    int rb = RB;
+    while (rb > 1 && (int64_t)n * ((oh + rb - 1) / rb) < want_ctas) rb >>= 1;
+    const size_t smem = (size_t)(ow + rb) * sizeof(AxisTap);
     if (smem > 200 * 1024) return RLFC_ERR_ARGUMENT;
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_render_slab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((unsigned)((oh + RB - 1) / RB), (unsigned)n);
-    k_render_slab<<<grid, 256, smem, (cudaStream_t)stream>>>(field, slots, S, T, W, H, poses, geoms, bg, ow, oh, out);
+    dim3 grid((unsigned)((oh + rb - 1) / rb), (unsigned)n);
+    k_render_slab<<<grid, 256, smem, (cudaStream_t)stream>>>(field, slots, S, T, W, H, poses, geoms, bg, ow, oh, out,
+                                                             rb);
     return launch_status();
 }
 

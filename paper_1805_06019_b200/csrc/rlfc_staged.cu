@@ -54,6 +54,7 @@ constexpr int MAXH = 8;
 constexpr int MAXS = 64;
 constexpr int THREADS = 256;
 constexpr uint32_t SKIP = 31;       // entry descriptor: slot not decoded
+constexpr int SEL_MAX = 64;         // slot-mode decodes needing at most this many chain nodes decode only those
 constexpr int STRIP = 64;           // pixels per TMA box column (192 bytes)
 
 __device__ const DigitLut g_lut = make_digit_lut();
@@ -82,6 +83,7 @@ struct Ws {
     uint32_t* rk;          // [nwp][3*nblk] slot of the first present node of each word
     uint32_t* flist;       // [3*nblk + 1] records with a stream anomaly (prepare-time), count first
     uint32_t* units;       // [tile][1 + ucap] prepared dirty-unit lists of the B = 4 blend (count first)
+    uint32_t* sel;         // [1 + SEL_MAX] chain nodes of a slot-mode decode (count first)
     int ucap;
     int nwp;
     uint64_t cap;
@@ -115,6 +117,7 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
     const uint64_t ucap = (uint64_t)f.s_count * 16;
     const uint64_t ntiles = (uint64_t)f.hb * f.t_count * ((f.wb + 15) / 16);
     const uint64_t o_ul = take(ul ? 4 * ntiles * (1 + ucap) : 0);
+    const uint64_t o_sel = take(4 * (1 + SEL_MAX));
     if (w) {
         uint8_t* b = static_cast<uint8_t*>(base);
         w->counter = reinterpret_cast<unsigned long long*>(b + o_cnt);
@@ -129,6 +132,7 @@ static uint64_t carve(const rlfc_field& f, void* base, uint64_t cap, Ws* w) {
         w->rk = reinterpret_cast<uint32_t*>(b + o_rk);
         w->flist = reinterpret_cast<uint32_t*>(b + o_fl);
         w->units = ul ? reinterpret_cast<uint32_t*>(b + o_ul) : nullptr;
+        w->sel = reinterpret_cast<uint32_t*>(b + o_sel);
         w->ucap = (int)ucap;
         w->nwp = nwp;
         w->cap = cap;
@@ -667,7 +671,8 @@ __global__ void __launch_bounds__(THREADS) k_sort_chunks(Ws w, uint64_t ntot) {
 
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rlfc_field f, Ws w, int l2_last,
-                                                      int by_lo, int by_hi) {
+                                                      int by_lo, int by_hi, const uint32_t* sel) {
+    if (sel && __ldg(sel) <= (uint32_t)SEL_MAX) return;     // k_payloads_sel decoded what the slots need
     __shared__ uint32_t range[2][3];         // per buffer: min / max payload offset, channel mask
     __shared__ uint16_t lut[243 + 125];
     __shared__ VT dq[BSQ == 16 ? 2048 : 1];
@@ -831,6 +836,145 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
         lo16 = lo16n;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// ---- pass 2b: slot-mode payloads (small view sets) -------------------------------------
+// A decode of a few views (the renderer's tap cameras) needs only the chain
+// nodes of those views at levels >= k: for each, one node per record.
+// k_sel_nodes collects them (ascending serial index; count first, SEL_MAX + 1
+// when there are more); k_payloads_sel then tests each (record, node) pair
+// against the prepared bitmap words, and decodes the present ones into their
+// slots -- the same residual layout k_payloads writes, so k_blend is unchanged.
+__global__ void __launch_bounds__(256) k_sel_nodes(const __grid_constant__ rlfc_field f, const int32_t* slots, int k,
+                                                   uint32_t* sel) {
+    constexpr int MW = 512;                        // mask words: up to 16384 nodes
+    __shared__ uint32_t mask[MW];
+    __shared__ uint32_t wcnt[MW + 1];
+    const int tid = threadIdx.x;
+    if (f.m_nodes > MW * 32) {
+        if (tid == 0) sel[0] = SEL_MAX + 1;
+        return;
+    }
+    const int nw = (f.m_nodes + 31) / 32;
+    for (int i = tid; i < MW; i += 256) mask[i] = 0u;
+    __syncthreads();
+    const int T = f.t_count, nv = f.s_count * T;
+    for (int v = tid; v < nv; v += 256) {
+        if (slots[v] < 0) continue;
+        const int s = v / T, t = v - s * T;
+        for (int l = k; l < f.tree_height; ++l) {
+            const int n = chain_node(f, l, s, t);
+            atomicOr(&mask[n >> 5], 1u << (n & 31));
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t run = 0;
+        for (int i = 0; i < nw; ++i) {
+            wcnt[i] = run;
+            run += __popc(mask[i]);
+        }
+        wcnt[nw] = run;
+        sel[0] = run <= (uint32_t)SEL_MAX ? run : (uint32_t)SEL_MAX + 1;
+    }
+    __syncthreads();
+    if (wcnt[nw] > (uint32_t)SEL_MAX) return;
+    for (int i = tid; i < nw; i += 256) {
+        uint32_t m = mask[i], o = wcnt[i];
+        while (m) {
+            sel[1 + o++] = (uint32_t)(32 * i + __ffs(m) - 1);
+            m &= m - 1u;
+        }
+    }
+}
+
+template <int BSQ, typename VT>
+__global__ void __launch_bounds__(THREADS) k_payloads_sel(const __grid_constant__ rlfc_field f, Ws w, int by_lo,
+                                                          int by_hi) {
+    constexpr int G8 = 8;                                  // nodes per round
+    __shared__ uint16_t lut[243 + 125];
+    __shared__ VT dq[BSQ == 16 ? 2048 : 1];
+    __shared__ uint32_t nodes[SEL_MAX];
+    __shared__ uint2 qe[THREADS * G8];                     // present payloads of the round: entry,
+    __shared__ uint32_t qs[THREADS * G8];                  // slot,
+    __shared__ uint32_t qr[THREADS * G8];                  // record
+    __shared__ int qn;
+    const uint32_t cnt = __ldg(w.sel);
+    if (cnt > (uint32_t)SEL_MAX || cnt == 0) return;
+    const int tid = threadIdx.x;
+    const int shift = f.quant_shift;
+    for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
+    if (BSQ == 16)
+        for (int z = tid; z < 2048; z += THREADS) dq[z] = (VT)deq((uint32_t)z, shift);
+    for (int i = tid; i < (int)cnt; i += THREADS) nodes[i] = __ldg(w.sel + 1 + i);
+    // one thread per record finds the round's present nodes (bitmap word and
+    // slot rank loads issued together); the CTA then decodes the compacted
+    // payloads with every lane busy (present nodes are sparse: decoding in
+    // place left ~6 active lanes per warp)
+    const int64_t nblk = (int64_t)f.wb * f.hb, nrec = 3 * nblk;
+    const int64_t nb = (int64_t)(by_hi - by_lo) * f.wb;
+    const int64_t r = (int64_t)blockIdx.x * THREADS + tid;
+    const bool valid = r < 3 * nb;
+    const int c = valid ? (int)(r / nb) : 0;
+    const int64_t ri = valid ? (int64_t)c * nblk + (int64_t)by_lo * f.wb + (r - (int64_t)c * nb) : 0;
+    const bool live = valid && !__ldg(w.rec_flag + ri);       // anomalous records: k_fixup
+    VT* res = static_cast<VT*>(w.res);
+    for (int j0 = 0; j0 < (int)cnt; j0 += G8) {
+        if (tid == 0) qn = 0;
+        __syncthreads();
+        if (live) {
+            uint32_t word[G8], rk[G8];
+#pragma unroll
+            for (int q = 0; q < G8; ++q) {
+                word[q] = 0u;
+                rk[q] = 0u;
+                if (j0 + q < (int)cnt) {
+                    const int64_t o = (int64_t)(nodes[j0 + q] >> 5) * nrec + ri;
+                    word[q] = __ldg(w.bm + o);
+                    rk[q] = __ldg(w.rk + o);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < G8; ++q) {
+                const uint32_t n = j0 + q < (int)cnt ? nodes[j0 + q] : 0u;
+                if (j0 + q < (int)cnt && ((word[q] >> (n & 31u)) & 1u)) {
+                    const uint32_t slot = rk[q] + (uint32_t)__popc(word[q] & ((1u << (n & 31u)) - 1u));
+                    if (slot < w.cap) {
+                        const int pos = atomicAdd(&qn, 1);
+                        qe[pos] = __ldg(w.entries + slot);
+                        qs[pos] = slot;
+                        qr[pos] = (uint32_t)ri;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const int n = qn;
+        for (int i = tid; i < n; i += THREADS) {
+            const uint2 e = qe[i];
+            const uint32_t d = e.y & 31u;
+            if (d >= (uint32_t)NUM_DESC) continue;
+            const int m = desc_mode((int)d);
+            const int cc = (int)(e.y >> 5) & 3;
+            const uint32_t b = (uint32_t)desc_bits((int)d);
+            VT* out = res + (uint64_t)qs[i] * BSQ;
+            bool bad;
+            if constexpr (BSQ == 16) {
+                const uint32_t* sw = reinterpret_cast<const uint32_t*>(f.srv[cc] + (e.x & ~3u));
+                const uint32_t bit0 = (e.x & 3u) * 8u;
+                if (m == MODE_BITS) bad = decode16<MODE_BITS, VT>(sw, bit0, b, lut, dq, out);
+                else if (m == MODE_TRIT) bad = decode16<MODE_TRIT, VT>(sw, bit0, b, lut, dq, out);
+                else bad = decode16<MODE_QUINT, VT>(sw, bit0, b, lut + 243, dq, out);
+            } else {
+                const uint8_t* p = f.srv[cc] + e.x;
+                if (m == MODE_BITS) bad = decode_payload<1, 0, BSQ, VT>(p, lut, b, shift, out);
+                else if (m == MODE_TRIT) bad = decode_payload<5, 8, BSQ, VT>(p, lut, b, shift, out);
+                else bad = decode_payload<3, 7, BSQ, VT>(p, lut + 243, b, shift, out);
+            }
+            if (bad) w.rec_flag[qr[i]] = 1u;                     // kernels.py:147-150
+        }
+        __syncthreads();
+    }
 }
 
 // ---- pass 3: blend -------------------------------------------------------------------
@@ -1403,11 +1547,22 @@ __global__ void __launch_bounds__(BT, RLFC_BLEND_MINB) k_blend(const __grid_cons
         }
     } else {
         constexpr int TP = B * QB / 2;                   // tasks per unit
-        const int units = cnt[0];
+        const int units = use_list ? (int)ucount : cnt[0];
         const VT* res = static_cast<const VT*>(P.res);
         for (int it = tid; it < units * TP; it += BT) {
             const int u = it / TP, j = it - u * TP;
-            const uint2 e = list[u];
+            uint2 e;
+            if (use_list) {
+                // prepared entry (B = 4, 32-bit residuals): filtered as above
+                const uint32_t q = __ldg(ulist + 1 + u);
+                const int s = (int)(q & 255u), b = (int)((q >> 8) & 63u);
+                const uint32_t pres = (q >> 14 >> (3 * k)) & ((1u << (3 * nlev)) - 1u);
+                if (rflag[b] | rflag[NB + b] | rflag[2 * NB + b]) continue;
+                if (!pres || (P.slots && P.slots[s * T + t] < 0)) continue;
+                e = make_uint2((uint32_t)s | (uint32_t)b << 8, pres);
+            } else {
+                e = list[u];
+            }
             const int s = (int)(e.x & 255u), b = (int)((e.x >> 8) & 255u);
             if (e.x >> 16) continue;                 // anomalous record: k_fixup
             const int rx = s >> h;
@@ -1587,7 +1742,8 @@ static bool plan_blend(const rlfc_field& f, int k, bool manual_roots, int tw_fir
 }
 
 template <int BSQ, typename VT>
-static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi, int sms, cudaStream_t stream) {
+static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi, int sms, cudaStream_t stream,
+                         const uint32_t* sel = nullptr) {
     const uint64_t want = (w.cap + PAY_CHUNK - 1) / PAY_CHUNK + 3;
     const uint64_t cap_grid = (uint64_t)sms * 8;
     const unsigned grid = (unsigned)(want < 1 ? 1 : want < cap_grid ? want : cap_grid);
@@ -1595,7 +1751,7 @@ static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi,
     cudaFuncSetAttribute(k_payloads<BSQ, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, pdyn);
     // residual payloads are stored with an L2 evict-last policy so the
     // blend's gathers hit L2
-    k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, 1, by_lo, by_hi);
+    k_payloads<BSQ, VT><<<grid, THREADS, pdyn, stream>>>(f, w, 1, by_lo, by_hi, sel);
 }
 
 template <int B, typename VT, typename RT>
@@ -1697,7 +1853,19 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         return c;
     };
     if (P.build_units) P.tma_in = 0;
-    if (k < h && !P.build_units) run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream);
+    if (k < h && !P.build_units) {
+        // a slot-mode decode of few views decodes only their chain nodes;
+        // the full pass then exits at once (and runs when there are more)
+        const bool sel = slots != nullptr && w.sel != nullptr;
+        if (sel) {
+            k_sel_nodes<<<1, 256, 0, stream>>>(f, slots, k, w.sel);
+            const int64_t nrb = 3ll * (by_hi - by_lo) * f.wb;
+            if (nrb > 0)
+                k_payloads_sel<BSQ, VT><<<(unsigned)((nrb + THREADS - 1) / THREADS), THREADS, 0, stream>>>(
+                    f, w, by_lo, by_hi);
+        }
+        run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream, sel ? w.sel : nullptr);
+    }
     auto kern = k_blend<B, VT, RT, bt>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     // tile residency is bounded by shared memory: ask for the largest carveout

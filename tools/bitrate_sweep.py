@@ -2,7 +2,7 @@
 decode throughput of the staged and fused paths per preset, with achieved
 bpp, present fraction and the roofline fraction by algorithmic bytes.
 
-    python tools/bitrate_sweep.py [--out profiles/r1_bitrate_sweep.json]
+    python tools/bitrate_sweep.py [--out profiles/r2_bitrate_sweep.json]
 
 Streams come from the native producer (byte-identical to the reference
 encoder) and are cached under data/.  Each preset's staged and fused outputs
@@ -47,7 +47,7 @@ def time_decode(st, out, kernel, iters=10):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_bitrate_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_bitrate_sweep.json"))
     ap.add_argument("--presets", default="R1,R2,R3,R4,R5,R6")
     a = ap.parse_args()
     peak, peak_kind = bench.peaks()

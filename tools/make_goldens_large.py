@@ -37,6 +37,11 @@ CASES = {
     "w512_b8": (dict(s_count=8, t_count=8, width=512, height=512, seed=3), dict(block_size=8, tree_height=3)),
     "w512_b16": (dict(s_count=8, t_count=8, width=512, height=512, seed=5),
                  dict(block_size=16, tree_height=3, quant_shift=2, pixel_threshold=4, block_threshold=60)),
+    # B = 4 with quant_shift > 4: residuals exceed int16, the blend's 32-bit path
+    "w256_b4_s5": (dict(s_count=9, t_count=9, width=256, height=256, seed=17),
+                   dict(tree_height=3, block_size=4, quant_shift=5, pixel_threshold=24, block_threshold=2000)),
+    "w256_b4_s6_dense": (dict(s_count=9, t_count=9, width=256, height=256, seed=19),
+                         dict(tree_height=3, block_size=4, quant_shift=6, pixel_threshold=2, block_threshold=40)),
 }
 _st = None
 
@@ -56,8 +61,15 @@ def sha(b):
 
 
 def main():
+    import sys
+    only = sys.argv[1].split(",") if len(sys.argv) > 1 else None   # add / redo these, keep the rest
     res = {}
+    if only and os.path.exists(OUT):
+        with open(OUT) as f:
+            res = json.load(f)
     for name, (spec, params) in CASES.items():
+        if only and name not in only:
+            continue
         t0 = time.time()
         lf = synthesize_lightfield(SyntheticSpec(**spec))
         data, rep = encoder.compress(lf, EncodingParams(**params))
