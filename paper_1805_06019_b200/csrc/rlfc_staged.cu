@@ -1210,11 +1210,23 @@ __global__ void k_flag_list(const uint32_t* rec_flag, int64_t nrec, uint32_t* fl
     if (i < nrec && rec_flag[i]) flist[1 + atomicAdd(flist, 1u)] = (uint32_t)i;
 }
 
-template <int B, typename VT, typename RT, int BT>
+// NL: present chain levels per unit held in registers (1; RLFC_DENSE_NL for
+// dense streams, whose units often carry several present levels, at fewer
+// CTAs per SM); further levels are read row by row.
+template <int B, typename VT, typename RT, int BT, int NL = 1>
 #ifndef RLFC_BLEND_MINB
 #define RLFC_BLEND_MINB (1024 / BT)
 #endif
-__global__ void __launch_bounds__(BT, RLFC_BLEND_MINB) k_blend(const __grid_constant__ BlendParams P,
+// dense variant: two levels in registers at 8 CTAs per SM measured best
+// (cfg2 R6: 1.40 ms vs 1.84 ms one level, 1.45 ms three levels at 6 CTAs;
+// R5: 0.94 vs 1.09 ms; R4 is faster with one level: 0.438 vs 0.488 ms)
+#ifndef RLFC_DENSE_MINB
+#define RLFC_DENSE_MINB 8
+#endif
+#ifndef RLFC_DENSE_NL
+#define RLFC_DENSE_NL 2
+#endif
+__global__ void __launch_bounds__(BT, NL == 1 ? RLFC_BLEND_MINB : RLFC_DENSE_MINB) k_blend(const __grid_constant__ BlendParams P,
                                                    const __grid_constant__ CUtensorMap out_map,
                                                    const __grid_constant__ CUtensorMap rgb_map,
                                                    const __grid_constant__ CUtensorMap root_map) {
@@ -1502,20 +1514,24 @@ __global__ void __launch_bounds__(BT, RLFC_BLEND_MINB) k_blend(const __grid_cons
                 const int x = s >> (k + li);
                 return sbase[r] + (uint32_t)__popcll(mask[r] & ((1ull << x) - 1ull));
             };
-            uint4 raw[3][2];
+            uint4 raw[NL][3][2];
             uint32_t pcs[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 pcs[c] = e.y & (0x249249u << c);             // bits 3i + c: levels k + i
-                raw[c][0] = raw[c][1] = make_uint4(0u, 0u, 0u, 0u);
-                if (pcs[c]) {
-                    // the payload's 32-byte sector in one 256-bit load
-                    const VT* q = res + (uint64_t)slot_of(c, pcs[c]) * BSQ;
-                    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                                 : "=r"(raw[c][0].x), "=r"(raw[c][0].y), "=r"(raw[c][0].z), "=r"(raw[c][0].w),
-                                   "=r"(raw[c][1].x), "=r"(raw[c][1].y), "=r"(raw[c][1].z), "=r"(raw[c][1].w)
-                                 : "l"(q));
-                    pcs[c] &= pcs[c] - 1u;
+#pragma unroll
+                for (int lv = 0; lv < NL; ++lv) {
+                    raw[lv][c][0] = raw[lv][c][1] = make_uint4(0u, 0u, 0u, 0u);
+                    if (pcs[c]) {
+                        // the payload's 32-byte sector in one 256-bit load
+                        const VT* q = res + (uint64_t)slot_of(c, pcs[c]) * BSQ;
+                        asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                            : "=r"(raw[lv][c][0].x), "=r"(raw[lv][c][0].y), "=r"(raw[lv][c][0].z),
+                              "=r"(raw[lv][c][0].w), "=r"(raw[lv][c][1].x), "=r"(raw[lv][c][1].y),
+                              "=r"(raw[lv][c][1].z), "=r"(raw[lv][c][1].w)
+                            : "l"(q));
+                        pcs[c] &= pcs[c] - 1u;
+                    }
                 }
             }
             const int rx = s >> h;
@@ -1526,12 +1542,15 @@ __global__ void __launch_bounds__(BT, RLFC_BLEND_MINB) k_blend(const __grid_cons
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     load4s<RT>(roots + ((rx * 3 + c) * B + row) * TW + px, v[c]);
-                    const uint4 w = raw[c][row >> 1];
-                    const uint32_t lo = (row & 1) ? w.z : w.x, hi = (row & 1) ? w.w : w.y;
-                    v[c][0] += (int32_t)(int16_t)(lo & 0xFFFFu);
-                    v[c][1] += (int32_t)lo >> 16;
-                    v[c][2] += (int32_t)(int16_t)(hi & 0xFFFFu);
-                    v[c][3] += (int32_t)hi >> 16;
+#pragma unroll
+                    for (int lv = 0; lv < NL; ++lv) {
+                        const uint4 w = raw[lv][c][row >> 1];
+                        const uint32_t lo = (row & 1) ? w.z : w.x, hi = (row & 1) ? w.w : w.y;
+                        v[c][0] += (int32_t)(int16_t)(lo & 0xFFFFu);
+                        v[c][1] += (int32_t)lo >> 16;
+                        v[c][2] += (int32_t)(int16_t)(hi & 0xFFFFu);
+                        v[c][3] += (int32_t)hi >> 16;
+                    }
                     uint32_t pc = pcs[c];
                     while (pc) {                               // further levels (rare)
                         int32_t r4[4] = {0, 0, 0, 0};
@@ -1765,6 +1784,9 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     // bounds the blend (output bytes in flight / tile lifetime): at 64
     // registers, 96-thread CTAs fit 10 per SM (shared memory 10 x 22.6 KB)
     // against 8 for 128 threads (455 vs 448 Gpix/s)
+#ifndef RLFC_DENSE_FRAC
+#define RLFC_DENSE_FRAC 0.12      // present nodes / (records x nodes): R4 0.064, R5 0.21, R6 0.40
+#endif
 #ifndef RLFC_BLEND_BT
 #define RLFC_BLEND_BT 96
 #define RLFC_BLEND_TW 64
@@ -1866,7 +1888,11 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
         }
         run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream, sel ? w.sel : nullptr);
     }
-    auto kern = k_blend<B, VT, RT, bt>;
+    // dense streams (many units with several present levels): the variant
+    // holding three levels per unit in registers
+    const double density = (double)w.cap / ((double)3 * f.wb * f.hb * f.m_nodes);
+    auto kern = B == 4 && sizeof(VT) == 2 && density > RLFC_DENSE_FRAC ? k_blend<B, VT, RT, bt, RLFC_DENSE_NL>
+                                                                        : k_blend<B, VT, RT, bt, 1>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem);
     // tile residency is bounded by shared memory: ask for the largest carveout
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

@@ -5,10 +5,12 @@ with extra -D flags into scratch/, loaded with ctypes beside the product
 library (device memory is shared, so the DeviceField / workspace come from
 the product path) and timed with CUDA events over the same call.
 
-    python tools/variant_sweep.py "-DRLFC_BLEND_BT=128 -DRLFC_BLEND_TW=128" ...
+    python tools/variant_sweep.py [--preset R6] "-DRLFC_BLEND_BT=128 -DRLFC_BLEND_TW=128" ...
+
+--preset picks a cfg2 bitrate preset (tools/bitrate_sweep.py PRESETS; the
+stream is produced if missing), default R4 (the bench stream).
 """
 import ctypes
-import glob
 import hashlib
 import os
 import subprocess
@@ -16,6 +18,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
 def build(flags):
@@ -32,8 +35,15 @@ def main():
     import torch
     import paper_1805_06019_b200 as rl
     from paper_1805_06019_b200 import _native
-    path = glob.glob(os.path.join(ROOT, "data", "bench_*.rlfc"))[0]
-    st = rl.init(open(path, "rb").read())
+    import bench
+    from bitrate_sweep import PRESETS
+    args = sys.argv[1:]
+    preset = "R4"
+    if args[:1] == ["--preset"]:
+        preset, args = args[1], args[2:]
+    h, B, sh, tp, tb = PRESETS[preset]
+    data, _ = bench.make_stream(dict(bench.CFG, h=h, B=B, shift=sh, tp=tp, tb=tb))
+    st = rl.init(data)
     df = st.device_field()
     hdr = st.header
     out = torch.empty((hdr.s_count, hdr.t_count, hdr.height, hdr.width, 3), dtype=torch.uint8, device="cuda")
@@ -41,7 +51,7 @@ def main():
     stream = torch.cuda.current_stream().cuda_stream
     ws = df.staged_workspace(stream)
     ref = rl.decode_field(st, 0, kernel="simple")[0].cpu()
-    for flags in [""] + sys.argv[1:]:
+    for flags in [""] + args:
         L = _native.load_library(build(flags)) if flags else _native.lib()
         # the variant library prepares its own copy of the workspace layout
         w2 = torch.empty_like(ws[0])
