@@ -14,6 +14,7 @@ they are identical to the reference's bit for bit.
 """
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -230,8 +231,6 @@ def render_views(state, poses, stop_level=0, geometry=None,
     dev = df.device
     L = _native.lib()
     stream = torch.cuda.current_stream(dev).cuda_stream
-    d_geom = torch.from_numpy(gstruct).to(dev)
-    d_bg = torch.from_numpy(bgs).to(dev)
     if out is None:
         out = torch.empty((n, oh, ow, 3), dtype=torch.uint8, device=dev)
     if kinds == {SlabPose}:
@@ -243,17 +242,10 @@ def render_views(state, poses, stop_level=0, geometry=None,
         if np.any(focal == gstruct[:, 0]):
             raise ValueError("focal plane coincides with the camera plane")
         cams = _slab_camera_set(pose_arr[:, 0], pose_arr[:, 1], S, T)
-        field, slots, status = _decode_cameras(state, cams, stop_level,
-                                               device)
-        d_pose = torch.from_numpy(pose_arr).to(dev)
-        with torch.cuda.device(dev):
-            _native.check(L.rlfc_render_slab(
-                field.data_ptr(), slots.data_ptr(), S, T, W, H,
-                d_pose.data_ptr(), d_geom.data_ptr(), d_bg.data_ptr(), n, ow,
-                oh, out.data_ptr(), stream), "rlfc_render_slab")
-        if status is not None:
-            decoder._raise_word(status.cpu().item())
-        return out
+        return _render_slab_batch(state, df, stop_level, cams, pose_arr,
+                                  gstruct, bgs, ow, oh, out, stream)
+    d_geom = torch.from_numpy(gstruct).to(dev)
+    d_bg = torch.from_numpy(bgs).to(dev)
     if geos is None:
         geos = [one] * n
     frames = np.stack([_pinhole_basis(p, g) for p, g in zip(poses, geos)])
@@ -276,6 +268,104 @@ def render_views(state, poses, stop_level=0, geometry=None,
             "rlfc_render_pinhole")
     if (status.cpu().numpy() == -2).any():
         raise ValueError("ray parallel to the light-slab planes")
+    return out
+
+
+class _Staging:
+    """Per-thread, per-device staging of a slab render's small inputs (status
+    word, poses, geometries, slot table, camera rows, backgrounds): one pinned
+    host buffer and one device buffer, so a call makes a single host-to-device
+    copy and reads its status back with a single small copy."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.cap = 0
+
+    def buffers(self, nbytes):
+        import torch
+        if nbytes > self.cap:
+            cap = max(4096, 1 << (nbytes - 1).bit_length())
+            self.host = torch.empty(cap, dtype=torch.uint8).pin_memory()
+            self.hnp = self.host.numpy()
+            self.devbuf = torch.empty(cap, dtype=torch.uint8, device=self.dev)
+            self.stat = torch.empty(8, dtype=torch.uint8).pin_memory()
+            self.cap = cap
+        return self.host, self.hnp, self.devbuf
+
+
+_tls = threading.local()
+
+
+def _staging(dev):
+    d = getattr(_tls, "staging", None)
+    if d is None:
+        d = _tls.staging = {}
+    st = d.get(dev.index)
+    if st is None:
+        st = d[dev.index] = _Staging(dev)
+    return st
+
+
+def _render_slab_batch(state, df, stop_level, cams, pose_arr, gstruct, bgs,
+                       ow, oh, out, stream):
+    """Decode the batch's tap cameras (staged path in slot mode) and render
+    every slab pose in one k_render_slab launch."""
+    import torch
+    with torch.cuda.device(df.device):
+        return _render_slab_on(state, df, stop_level, cams, pose_arr, gstruct,
+                               bgs, ow, oh, out, stream)
+
+
+def _render_slab_on(state, df, stop_level, cams, pose_arr, gstruct, bgs, ow,
+                    oh, out, stream):
+    import torch
+    hdr = state.header
+    S, T, W, H = hdr.s_count, hdr.t_count, hdr.width, hdr.height
+    n = pose_arr.shape[0]
+    ncam = len(cams)
+    rows = sorted({int(c) % T for c in cams})
+    al = lambda x: (x + 15) & ~15                                 # noqa: E731
+    o_pose = 16
+    o_geom = al(o_pose + 32 * n)
+    o_slot = al(o_geom + 48 * n)
+    o_rows = al(o_slot + 4 * S * T)
+    o_bg = al(o_rows + 4 * len(rows))
+    total = al(o_bg + 3 * n)
+    stg = _staging(df.device)
+    host, hnp, dbuf = stg.buffers(total)
+    hnp[:16] = 0
+    hnp[o_pose:o_pose + 32 * n].view(np.float64)[:] = pose_arr.ravel()
+    hnp[o_geom:o_geom + 48 * n].view(np.float64)[:] = gstruct.ravel()
+    slots = hnp[o_slot:o_slot + 4 * S * T].view(np.int32)
+    slots[:] = -1
+    slots[np.asarray(cams, dtype=np.int64)] = np.arange(ncam, dtype=np.int32)
+    hnp[o_rows:o_rows + 4 * len(rows)].view(np.int32)[:] = rows
+    hnp[o_bg:o_bg + 3 * n] = bgs.ravel()
+    dbuf[:total].copy_(host[:total], non_blocking=True)
+    base = dbuf.data_ptr()
+    field = torch.empty((ncam, H, W, 3), dtype=torch.uint8, device=df.device)
+    L = _native.lib()
+    hb = hdr.block_grid[1]
+    ws = df.staged_workspace(stream)
+    rc = _native.RLFC_ERR_ARGUMENT
+    if ws is not None:
+        with df.enqueue_lock:
+            rc = L.rlfc_decode_field_staged(
+                df.ref, stop_level, base + o_slot, 0, hb, field.data_ptr(),
+                H * W * 3, W * 3, ws[0].data_ptr(), ws[1], ws[2], ws[3],
+                base + o_rows, len(rows), base, stream)
+    if rc == _native.RLFC_ERR_ARGUMENT:
+        rc = L.rlfc_decode_field(df.ref, stop_level, base + o_slot, 0, hb,
+                                 field.data_ptr(), H * W * 3, W * 3, base,
+                                 stream)
+    _native.check(rc, "rlfc_decode_field")
+    _native.check(L.rlfc_render_slab(
+        field.data_ptr(), base + o_slot, S, T, W, H, base + o_pose,
+        base + o_geom, base + o_bg, n, ow, oh, out.data_ptr(), stream),
+        "rlfc_render_slab")
+    stg.stat.copy_(dbuf[:8], non_blocking=True)
+    torch.cuda.current_stream(df.device).synchronize()
+    decoder._raise_word(int(stg.stat.numpy().view(np.int64)[0]))
     return out
 
 
