@@ -104,6 +104,33 @@ int rlfc_decode_block_sync(const rlfc_field *f, int32_t s, int32_t t,
                            int32_t stop_level, int32_t *dev, int32_t *host,
                            void *stream);
 
+/* Single-block requests through a resident server kernel: the latency path
+ * of decoder.decode_block / decode_block_progressive (decoder.py:73-112)
+ * under a stream of requests.  The mailbox lives in pinned host memory
+ * (device-addressable, zero-filled before first use) and belongs to one host
+ * thread and one CUDA stream.  rlfc_block_server_request writes the request,
+ * launches the server kernel on `stream` when the stream is idle (first
+ * request, or the server exited after idle_ns ns without work) and returns
+ * once the result is complete in the mailbox, copied to out: out[0 .. B*B)
+ * the block, out[B*B] the status (0 / 1 / 2, kernels.py:165-171).  The result
+ * arrives as 16-byte chunks {3 values, request number}.  Out-of-range
+ * requests return RLFC_ERR_ARGUMENT.  rlfc_block_server_stop makes a running
+ * server exit and waits for it (before the mailbox or the field is
+ * released). */
+#define RLFC_MAILBOX_STOP 0xFFFFFFFFu
+typedef struct rlfc_mailbox {
+    uint32_t req_seq;      /* host: request number (written after req) */
+    int32_t req[6];        /* s, t, bx, by, channel, stop_level */
+    uint32_t req_seq2;     /* host: the request number again, written last */
+    uint32_t _pad[8];      /* the host-written words keep their own 64-byte line */
+    uint32_t out[88][4];   /* device: result chunks {v[3q], v[3q+1], v[3q+2], request number} */
+} rlfc_mailbox;
+int rlfc_block_server_request(const rlfc_field *f, rlfc_mailbox *mb,
+                              int32_t s, int32_t t, int32_t bx, int32_t by,
+                              int32_t channel, int32_t stop_level,
+                              uint64_t idle_ns, int32_t *out, void *stream);
+int rlfc_block_server_stop(rlfc_mailbox *mb, void *stream);
+
 /* Whole padded planes.  Replaces kernels.decode_plane_core
  * (kernels.py:219-242) as called by decoder.decode_plane (decoder.py:165-184).
  * planes: n x 3 int32 (s, t, channel); out: n x hp x wp int32.  Failure key =

@@ -82,6 +82,8 @@ _SIGS = {
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "u", "u", "i", "p", "i", "p", "p"],
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
+    "rlfc_block_server_request": ["p", "p", "i", "i", "i", "i", "i", "i", "u", "p", "p"],
+    "rlfc_block_server_stop": ["p", "p"],
     "rlfc_chain_core_sync": ["p", "u", "u", "i", "i", "p", "i", "i", "p", "p"],
     "rlfc_chain_core": ["p", "u", "p", "i", "i", "i", "p", "i", "i", "p", "p",
                         "p"],

@@ -59,12 +59,13 @@ __global__ void k_decode_blocks(const rlfc_field f, const int32_t* __restrict__ 
 // dependent cold loads, one per present node).  Values then the status code
 // go to out[0 .. B*B].
 constexpr int ONE_REC_CAP = 16 * 1024;
-template <int B>
-__global__ void __launch_bounds__(32) k_decode_block_one(const rlfc_field f, int s, int t, int bx, int by, int c,
-                                                         int k, int32_t* __restrict__ out) {
-    __shared__ __align__(16) uint8_t rec_s[ONE_REC_CAP];
-    __shared__ int32_t root_s[B * B];
-    const int lane = threadIdx.x;
+// STAGE_OUT: the values and the status go to res_s (shared) instead of out,
+// for the caller to move with vector stores (the resident server).
+template <int B, bool STAGE_OUT = false>
+__device__ __forceinline__ void decode_one_warp(const rlfc_field& f, int s, int t, int bx, int by, int c, int k,
+                                                int32_t* out, uint8_t* rec_s, int32_t* root_s,
+                                                int32_t* res_s = nullptr) {
+    const int lane = threadIdx.x & 31;
     const int64_t nblk = (int64_t)f.wb * f.hb;
     const int64_t blk = (int64_t)by * f.wb + bx;
     for (int j = lane; j < B * B; j += 32)
@@ -79,33 +80,116 @@ __global__ void __launch_bounds__(32) k_decode_block_one(const rlfc_field f, int
         for (int q = lane; q < n16; q += 32) reinterpret_cast<uint4*>(rec_s)[q] = __ldg(src + q);
     }
     __syncwarp();
-    if (lane != 0) return;
-    int32_t acc[B * B];
+    if (lane == 0) {
+        int32_t acc[B * B];
 #pragma unroll
-    for (int j = 0; j < B * B; ++j) acc[j] = root_s[j];
-    // the staged copy holds the record (+16 bytes); a corrupt record whose
-    // walk runs past it is walked again from the stream in HBM
-    int st = WALK_OOB;
-    if (staged) {
-        int32_t acc2[B * B];
+        for (int j = 0; j < B * B; ++j) acc[j] = root_s[j];
+        // the staged copy holds the record (+16 bytes); a corrupt record whose
+        // walk runs past it is walked again from the stream in HBM
+        int st = WALK_OOB;
+        if (staged) {
+            int32_t acc2[B * B];
 #pragma unroll
-        for (int j = 0; j < B * B; ++j) acc2[j] = acc[j];
-        st = walk_chain<B * B, true>(f, rec_s + (off - lo16), s, t, k, acc2, c_lut, c_nb<B>, end - off);
-        if (st != WALK_OOB) {
+            for (int j = 0; j < B * B; ++j) acc2[j] = acc[j];
+            st = walk_chain<B * B, true>(f, rec_s + (off - lo16), s, t, k, acc2, c_lut, c_nb<B>, end - off);
+            if (st != WALK_OOB) {
 #pragma unroll
-            for (int j = 0; j < B * B; ++j) acc[j] = acc2[j];
+                for (int j = 0; j < B * B; ++j) acc[j] = acc2[j];
+            }
+        }
+        if (st == WALK_OOB) {
+            st = walk_chain<B * B>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<B>, srv_avail(f, c, off));
+            if (st == WALK_OOB) st = 2;
+        }
+        if constexpr (STAGE_OUT) {
+#pragma unroll
+            for (int j = 0; j < B * B; ++j) res_s[j] = acc[j];
+            res_s[B * B] = st;
+        } else {
+#pragma unroll
+            for (int j = 0; j < B * B; ++j) out[j] = acc[j];
+            // the status word is written last, after a system-scope fence: a
+            // host polling it in mapped memory then sees the complete block
+            __threadfence_system();
+            *reinterpret_cast<volatile int32_t*>(out + B * B) = st;
         }
     }
-    if (st == WALK_OOB) {
-        st = walk_chain<B * B>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<B>, srv_avail(f, c, off));
-        if (st == WALK_OOB) st = 2;
-    }
+    __syncwarp();
+}
+
+template <int B>
+__global__ void __launch_bounds__(32) k_decode_block_one(const rlfc_field f, int s, int t, int bx, int by, int c,
+                                                         int k, int32_t* __restrict__ out) {
+    __shared__ __align__(16) uint8_t rec_s[ONE_REC_CAP];
+    __shared__ int32_t root_s[B * B];
+    decode_one_warp<B>(f, s, t, bx, by, c, k, out, rec_s, root_s);
+}
+
+// Resident single-block server (the latency path of decode_block under a
+// stream of requests): one warp polls the caller's mailbox in pinned host
+// memory over PCIe, decodes each request as k_decode_block_one does and
+// writes the block + status back as 16-byte chunks, each {3 values, request
+// number}: a 16-byte store reaches host memory whole, so the host takes the
+// result once every chunk carries its request number -- no system-scope fence
+// between the data and a flag (measured: 5.8 -> 4.4 us per echo round trip).
+// The server exits after idle_ns without a request; the host relaunches it
+// on the same stream when the stream is idle, so at most one server per
+// mailbox runs and a request that races an exit is served by the next launch.
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int B>
+__global__ void __launch_bounds__(32) k_block_server(const rlfc_field f, rlfc_mailbox* mb, uint64_t idle_ns) {
+    __shared__ __align__(16) uint8_t rec_s[ONE_REC_CAP];
+    __shared__ int32_t root_s[B * B];
+    __shared__ __align__(16) int32_t res_s[B * B + 4];       // + status
+    const int lane = threadIdx.x;
+    const uint4* req4 = reinterpret_cast<const uint4*>(mb);              // words 0-3, 4-7
+    uint4* chunks = reinterpret_cast<uint4*>(mb->out);
+    constexpr int NCH = (B * B + 1 + 2) / 3;
+    uint32_t last = 0;
+    if (lane == 0) last = reinterpret_cast<volatile uint32_t*>(mb->out)[3];   // chunk 0's number
+    last = __shfl_sync(0xffffffffu, last, 0);
+    uint64_t t_idle = globaltimer();
+    for (;;) {
+        // one poll = the request words in two independent 16-byte reads over
+        // PCIe; a request counts once both carry its number (req_seq is
+        // written after the fields, req_seq2 after req_seq)
+        uint32_t w[8];
+        if (lane == 0) {
+            uint4 a, b;
+            asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(req4) : "memory");
+            asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(req4 + 1) : "memory");
+            w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        }
 #pragma unroll
-    for (int j = 0; j < B * B; ++j) out[j] = acc[j];
-    // the status word is written last, after a system-scope fence: a host
-    // polling it in mapped memory then sees the complete block
-    __threadfence_system();
-    *reinterpret_cast<volatile int32_t*>(out + B * B) = st;
+        for (int q = 0; q < 8; ++q) w[q] = __shfl_sync(0xffffffffu, w[q], 0);
+        const uint32_t seq = w[0];
+        if (seq == last || w[7] != seq) {
+            if (globaltimer() - t_idle > idle_ns) return;
+            continue;
+        }
+        if (seq == RLFC_MAILBOX_STOP) return;
+        decode_one_warp<B, true>(f, (int)w[1], (int)w[2], (int)w[3], (int)w[4], (int)w[5], (int)w[6], nullptr,
+                                 rec_s, root_s, res_s);
+        for (int q = lane; q < NCH; q += 32) {
+            const int j = 3 * q;
+            const uint32_t x = (uint32_t)res_s[j];
+            const uint32_t y = j + 1 <= B * B ? (uint32_t)res_s[j + 1] : 0u;
+            const uint32_t z = j + 2 <= B * B ? (uint32_t)res_s[j + 2] : 0u;
+            asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(chunks + q), "r"(x), "r"(y),
+                         "r"(z), "r"(seq)
+                         : "memory");
+        }
+        __syncwarp();
+        last = seq;
+        t_idle = globaltimer();
+    }
 }
 
 // One thread per (plane request, block): kernels.py:219-242 decode_plane_core.
@@ -305,6 +389,64 @@ extern "C" int rlfc_decode_block_sync(const rlfc_field* f, int32_t s, int32_t t,
     return cudaStreamSynchronize(st) == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
 }
 
+extern "C" int rlfc_block_server_request(const rlfc_field* f, rlfc_mailbox* mb, int32_t s, int32_t t, int32_t bx,
+                                         int32_t by, int32_t c, int32_t stop_level, uint64_t idle_ns,
+                                         int32_t* out, void* stream) {
+    if (!valid_field(f) || !mb || !out) return RLFC_ERR_ARGUMENT;
+    if (s < 0 || s >= f->s_count || t < 0 || t >= f->t_count || bx < 0 || bx >= f->wb || by < 0 ||
+        by >= f->hb || c < 0 || c > 2 || stop_level < 0 || stop_level > f->tree_height)
+        return RLFC_ERR_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    volatile rlfc_mailbox* v = mb;
+    uint32_t seq = v->req_seq + 1;
+    if (seq == RLFC_MAILBOX_STOP || seq == 0) seq = 1;
+    const int32_t r[6] = {s, t, bx, by, c, stop_level};
+    for (int q = 0; q < 6; ++q) v->req[q] = r[q];
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    v->req_seq = seq;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    v->req_seq2 = seq;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    const int bsq = f->block * f->block, nch = (bsq + 1 + 2) / 3;
+    volatile uint32_t* w = reinterpret_cast<volatile uint32_t*>(mb->out);
+    auto complete = [&]() {
+        for (int q = nch - 1; q >= 0; --q)
+            if (w[4 * q + 3] != seq) return false;
+        return true;
+    };
+    // wait for every chunk to carry seq; whenever the stream is idle no
+    // server is running (it timed out, or never started): launch one
+    for (uint32_t i = 1; !complete(); ++i) {
+        if ((i & 1023u) == 0) {
+            const cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaSuccess) {
+                if (complete()) break;
+                RLFC_DISPATCH_B(f->block, k_block_server<BB><<<1, 32, 0, st>>>(*f, mb, idle_ns));
+                if (cudaGetLastError() != cudaSuccess) return RLFC_ERR_CUDA;
+            } else if (q != cudaErrorNotReady) {
+                return RLFC_ERR_CUDA;
+            }
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    for (int j = 0; j <= bsq; ++j) out[j] = (int32_t)w[4 * (j / 3) + j % 3];
+    return RLFC_OK;
+}
+
+extern "C" int rlfc_block_server_stop(rlfc_mailbox* mb, void* stream) {
+    if (!mb) return RLFC_ERR_ARGUMENT;
+    volatile rlfc_mailbox* v = mb;
+    const uint32_t cur = v->req_seq;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    v->req_seq = RLFC_MAILBOX_STOP;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    v->req_seq2 = RLFC_MAILBOX_STOP;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    const cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    v->req_seq = v->req_seq2 = cur;            // a later request continues the numbering
+    return e == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
 extern "C" int rlfc_decode_planes(const rlfc_field* f, int32_t stop_level, const int32_t* planes,
                                   int32_t n, int32_t* out, uint64_t* status, void* stream) {
     if (!valid_field(f) || n < 0 || stop_level < 0 || stop_level > f->tree_height) return RLFC_ERR_ARGUMENT;
@@ -378,3 +520,6 @@ extern "C" int rlfc_version(char* buf, int32_t len) {
     }
     return 7;
 }
+
+static_assert(offsetof(rlfc_mailbox, out) == 64 && sizeof(rlfc_mailbox) == 64 + 16 * 88,
+              "mailbox layout (decoder.MAILBOX_BYTES)");

@@ -18,6 +18,7 @@ functions raise `_native.NativeUnavailable`.
 
 import ctypes
 import threading
+import weakref
 import time
 from dataclasses import dataclass, field
 
@@ -631,23 +632,35 @@ def bise_decode_batch(payloads, descs, count, device=None):
 
 # --- reference-signature API ---------------------------------------------------
 
+MAILBOX_BYTES = 64 + 16 * 88                  # rlfc_mailbox (include/rlfc_b200.h)
+BLOCK_SERVER_IDLE_NS = 1_000_000              # resident server exits after 1 ms idle
+
+
+def _stop_server(fn, mailbox, stream):
+    fn(mailbox.data_ptr(), stream.cuda_stream)
+
+
 class _BlockScratch:
-    """Per-thread state for single-block requests: a pinned host buffer of
-    B*B+1 int32 and a private CUDA stream (the decode reads only immutable
-    state), so a request is one ctypes call into rlfc_decode_block_sync
-    (kernel, status word polled in mapped memory)."""
+    """Per-thread state for single-block requests: a mailbox in pinned host
+    memory and a private CUDA stream.  A request is one ctypes call into
+    rlfc_block_server_request: a resident one-warp server kernel on that
+    stream (started on demand, gone after 1 ms without requests) reads the
+    request from the mailbox over PCIe and writes the block back, so a
+    request in a stream of requests costs no kernel launch."""
 
     def __init__(self, df, b):
         torch = _torch()
         self.b = b
-        # pinned host memory is device-addressable (unified addressing): the
-        # kernel writes the block and its status straight into it
-        self.out_h = torch.empty(b * b + 1, dtype=torch.int32).pin_memory()
-        self.out_np = self.out_h.numpy()
+        self.mailbox = torch.zeros(MAILBOX_BYTES, dtype=torch.uint8).pin_memory()
+        self.out_np = np.zeros(b * b + 1, dtype=np.int32)
         self.stream = torch.cuda.Stream(device=df.device)
-        self.args = (df.ref, None, self.out_h.data_ptr(),
-                     self.stream.cuda_stream)
-        self.fn = _native.lib().rlfc_decode_block_sync
+        L = _native.lib()
+        self.args = (df.ref, self.mailbox.data_ptr(), self.stream.cuda_stream)
+        self.out_ptr = self.out_np.ctypes.data
+        self.fn = L.rlfc_block_server_request
+        # the server must be gone before the mailbox (or the field) is reused
+        weakref.finalize(self, _stop_server, L.rlfc_block_server_stop,
+                         self.mailbox, self.stream)
 
 
 def _block_scratch(state):
@@ -676,10 +689,11 @@ def decode_block_progressive(state: DecoderState, image_index, block_index,
                          "size 3")
     channel = int(channel) % 3
     sc = _block_scratch(state)
-    ref, dev, host, stream = sc.args
-    rc = sc.fn(ref, s, t, bx, by, channel, stop_level, dev, host, stream)
+    ref, mb, stream = sc.args
+    rc = sc.fn(ref, mb, s, t, bx, by, channel, stop_level,
+               BLOCK_SERVER_IDLE_NS, sc.out_ptr, stream)
     if rc:
-        _native.check(rc, "rlfc_decode_block_sync")
+        _native.check(rc, "rlfc_block_server_request")
     b = sc.b
     out = sc.out_np.copy()
     _raise_status(int(out[b * b]))

@@ -352,3 +352,74 @@ def test_gpu_root_decode_large_and_init_time(rl):
     dt = time.perf_counter() - t0
     assert st.device_field().roots.dtype == torch.int16
     print(f"cfg2 init {dt * 1e3:.1f} ms")
+
+
+def _server_request(rl, st, mb, stream, req, idle_ns):
+    from paper_1805_06019_b200 import _native
+    df = st.device_field()
+    b = st.header.block_size
+    out = np.zeros(b * b + 1, dtype=np.int32)
+    rc = _native.lib().rlfc_block_server_request(df.ref, mb.data_ptr(), *req, idle_ns, out.ctypes.data,
+                                                 stream.cuda_stream)
+    assert rc == 0
+    return out[:b * b].copy(), int(out[b * b])
+
+
+@pytest.mark.parametrize("name", ["mid17_r4", "b8_h2", "b16_h4", "mid17_dense", "alldesc_b4"])
+def test_block_server_matches_launch_path(rl, name):
+    """The resident server (rlfc_block_server_request) returns the same block
+    and status as a kernel launch per request (rlfc_decode_block_sync), across
+    idle exits and restarts, and stops cleanly."""
+    import time
+    from paper_1805_06019_b200 import _native, decoder
+    st = rl.init(load_stream(name))
+    df = st.device_field()
+    hdr = st.header
+    b = hdr.block_size
+    wb, hb = hdr.block_grid
+    L = _native.lib()
+    mb = torch.zeros(decoder.MAILBOX_BYTES, dtype=torch.uint8).pin_memory()
+    stream = torch.cuda.Stream()
+    host = torch.empty(b * b + 1, dtype=torch.int32).pin_memory()
+    rng = np.random.default_rng(41)
+    for i in range(300):
+        req = (int(rng.integers(0, hdr.s_count)), int(rng.integers(0, hdr.t_count)), int(rng.integers(0, wb)),
+               int(rng.integers(0, hb)), int(rng.integers(0, 3)), int(rng.integers(0, hdr.tree_height + 1)))
+        # a short idle timeout so some requests find the server gone
+        got, code = _server_request(rl, st, mb, stream, req, 20_000 if i % 7 else 1_000_000)
+        if i % 50 == 0:
+            time.sleep(0.002)
+        assert L.rlfc_decode_block_sync(df.ref, *req, None, host.data_ptr(), stream.cuda_stream) in (0,)
+        want = host.numpy()
+        assert code == int(want[b * b])
+        assert np.array_equal(got, want[:b * b]), req
+        assert np.array_equal(got.reshape(b, b), rl.decode_block_progressive(st, req[:2], req[2:4], req[4], req[5]))
+    assert L.rlfc_block_server_stop(mb.data_ptr(), stream.cuda_stream) == 0
+    stream.synchronize()
+    # a request after a stop starts a new server
+    got, code = _server_request(rl, st, mb, stream, (0, 0, 0, 0, 0, 0), 1_000_000)
+    assert code == 0 and np.array_equal(got.reshape(b, b), rl.decode_block(st, (0, 0), (0, 0), 0))
+    assert L.rlfc_block_server_stop(mb.data_ptr(), stream.cuda_stream) == 0
+    assert L.rlfc_block_server_request(df.ref, mb.data_ptr(), hdr.s_count, 0, 0, 0, 0, 0, 1000, host.data_ptr(),
+                                       stream.cuda_stream) == _native.RLFC_ERR_ARGUMENT
+
+
+def test_block_server_threads_and_release(rl):
+    """decode_block from many threads (one server per thread) equals the
+    serial result; dropping the state stops the servers (device syncs
+    return)."""
+    import gc
+    st = rl.init(load_stream("mid17_r4"))
+    hdr = st.header
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(43)
+    picks = [((int(rng.integers(0, 17)), int(rng.integers(0, 17))), (int(rng.integers(0, wb)), int(rng.integers(0, hb))),
+              int(rng.integers(0, 3))) for _ in range(400)]
+    serial = [rl.decode_block(st, *p) for p in picks]
+    with cf.ThreadPoolExecutor(8) as ex:
+        par = list(ex.map(lambda p: rl.decode_block(st, *p), picks))
+    for a, b2 in zip(serial, par):
+        assert np.array_equal(a, b2)
+    del st
+    gc.collect()
+    torch.cuda.synchronize()

@@ -31,19 +31,32 @@ print(f"decode_block latency {dt * 1e6:.2f} us (mean of {len(picks)})")
 # breakdown: the native call alone (no Python argument checks / copy)
 from paper_1805_06019_b200 import decoder  # noqa: E402
 sc = decoder._block_scratch(st)
-ref, dev, host, stream = sc.args
+ref, mb, stream = sc.args
+idle = decoder.BLOCK_SERVER_IDLE_NS
+op = sc.out_ptr
 t0 = time.perf_counter()
 for s, t, bx, by, c in picks:
-    sc.fn(ref, s, t, bx, by, c, 0, dev, host, stream)
+    sc.fn(ref, mb, s, t, bx, by, c, 0, idle, op, stream)
 dt2 = (time.perf_counter() - t0) / len(picks)
-print(f"native rlfc_decode_block_sync alone {dt2 * 1e6:.2f} us")
+print(f"native rlfc_block_server_request alone {dt2 * 1e6:.2f} us")
 # the same block over and over (record and roots L2-resident)
 s, t, bx, by, c = picks[0]
 t0 = time.perf_counter()
 for _ in range(len(picks)):
-    sc.fn(ref, s, t, bx, by, c, 0, dev, host, stream)
+    sc.fn(ref, mb, s, t, bx, by, c, 0, idle, op, stream)
 dt3 = (time.perf_counter() - t0) / len(picks)
 print(f"native call, one block repeated (L2-warm) {dt3 * 1e6:.2f} us")
+# one launch per request (rlfc_decode_block_sync: kernel + polled status)
+from paper_1805_06019_b200 import _native  # noqa: E402
+import torch  # noqa: E402
+L = _native.lib()
+host = torch.empty(st.header.block_size ** 2 + 1, dtype=torch.int32).pin_memory()
+s2 = torch.cuda.Stream()
+t0 = time.perf_counter()
+for s, t, bx, by, c in picks:
+    L.rlfc_decode_block_sync(ref, s, t, bx, by, c, 0, None, host.data_ptr(), s2.cuda_stream)
+dt5 = (time.perf_counter() - t0) / len(picks)
+print(f"native rlfc_decode_block_sync (a launch per request) {dt5 * 1e6:.2f} us")
 import torch  # noqa: E402
 x = torch.zeros(1, device="cuda")
 torch.cuda.synchronize()
