@@ -189,6 +189,104 @@ def _pinhole_basis(pose: CameraPose, geometry):
     return np.concatenate([eye, look, right, down, [half, aspect]])
 
 
+def _snap_v(f):
+    r = np.rint(f)
+    return np.where(np.abs(f - r) < SNAP_EPS, r, f)
+
+
+def _axis_taps_v(coord, count):
+    """_axis_taps over an array: (i0, has_lo, has_hi) with the reference's
+    clamping and snapping (renderer.py:119-131)."""
+    c = np.minimum(np.maximum(coord, 0.0), float(count - 1))
+    if count == 1:
+        z = np.zeros(c.shape, dtype=np.int64)
+        return z, np.ones(c.shape, bool), np.zeros(c.shape, bool)
+    i0 = np.minimum(np.floor(c).astype(np.int64), count - 2)
+    f = _snap_v(c - i0)
+    return i0, f < 1.0, f > 0.0
+
+
+def _pinhole_first_failure(state, pose, geometry, stop_level):
+    """Raise what the reference's render_view raises for this pinhole pose on
+    a stream with corrupt records (renderer.py:295-305): pixels in raster
+    order, each pixel's taps in (s, t, u, v) order, blocks decoded once
+    (memo) with channels 0, 1, 2; the first failing block raises
+    FormatError, a ray parallel to the slab raises ValueError where the
+    reference reaches it.  Error path only: ray coordinates are evaluated with
+    the reference's numpy expressions over all pixels, the touched blocks
+    decoded in one batch on the GPU."""
+    hdr = state.header
+    b = hdr.block_size
+    S, T, W, H = hdr.s_count, hdr.t_count, hdr.width, hdr.height
+    eye = np.asarray(pose.eye, dtype=np.float64)
+    fr = _pinhole_basis(pose, geometry)
+    look, right, down, half, aspect = fr[3:6], fr[6:9], fr[9:12], fr[12], fr[13]
+    px = (np.arange(pose.width) + 0.5) / pose.width * 2.0 - 1.0
+    py = (np.arange(pose.height) + 0.5) / pose.height * 2.0 - 1.0
+    dirs = (look[None, None, :] + (px[None, :, None] * half * aspect) * right[None, None, :]
+            + (py[:, None, None] * half) * down[None, None, :]).reshape(-1, 3)
+    dz = dirs[:, 2]
+    parallel = np.abs(dz) < 1e-15
+    first_par = int(np.argmax(parallel)) if parallel.any() else None
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tc = (geometry.camera_plane_z - eye[2]) / dz
+        cx, cy = eye[0] + tc * dirs[:, 0], eye[1] + tc * dirs[:, 1]
+        ti = (geometry.image_plane_z - eye[2]) / dz
+        ix, iy = eye[0] + ti * dirs[:, 0], eye[1] + ti * dirs[:, 1]
+    xs = np.arange(S, dtype=np.float64)
+    ys = np.arange(T, dtype=np.float64)
+    x0, y0, x1, y1 = geometry.image_plane_extent
+    hit = ((xs[0] <= cx) & (cx <= xs[-1]) & (ys[0] <= cy) & (cy <= ys[-1]) &
+           (x0 <= ix) & (ix <= x1) & (y0 <= iy) & (iy <= y1) & ~parallel)
+    idx = np.flatnonzero(hit)
+    sc = _snap_v(np.interp(cx[idx], xs, np.arange(S)))
+    tcoord = _snap_v(np.interp(cy[idx], ys, np.arange(T)))
+    u = _snap_v((ix[idx] - x0) / (x1 - x0) * W - 0.5)
+    v = _snap_v((iy[idx] - y0) / (y1 - y0) * H - 0.5)
+    taps = [_axis_taps_v(sc, S), _axis_taps_v(tcoord, T), _axis_taps_v(u, W), _axis_taps_v(v, H)]
+    keys, order = [], []
+    for a in range(2):
+        for bb in range(2):
+            for cc in range(2):
+                for dd in range(2):
+                    ok = np.ones(idx.shape, bool)
+                    coord = []
+                    for ax, sel in zip(taps, (a, bb, cc, dd)):
+                        i0, lo, hi = ax
+                        ok &= lo if sel == 0 else hi
+                        coord.append(i0 + sel)
+                    ss, tt, uu, vv = coord
+                    key = ((ss * T + tt) * hdr.block_grid[1] + vv // b) * hdr.block_grid[0] + uu // b
+                    keys.append(np.where(ok, key, -1))
+                    order.append(idx * 16 + ((a * 2 + bb) * 2 + cc) * 2 + dd)
+    keys = np.stack(keys, 1).ravel()
+    order = np.stack(order, 1).ravel()
+    valid = keys >= 0
+    keys, order = keys[valid], order[valid]
+    srt = np.argsort(order, kind="stable")
+    keys, order = keys[srt], order[srt]
+    uk, first = np.unique(keys, return_index=True)
+    wb, hb = hdr.block_grid
+    bx = uk % wb
+    byy = (uk // wb) % hb
+    cam = uk // (wb * hb)
+    req = np.stack([np.repeat(cam // T, 3), np.repeat(cam % T, 3), np.repeat(bx, 3), np.repeat(byy, 3),
+                    np.tile(np.arange(3), len(uk)), np.full(3 * len(uk), stop_level)], 1).astype(np.int32)
+    fail_pix = None
+    if len(req):
+        _, st = decoder.decode_blocks(state, req, raise_errors=False)
+        st = np.asarray(st.cpu().numpy() if hasattr(st, "cpu") else st).reshape(-1, 3)
+        bad = np.flatnonzero((st != 0).any(1))
+        if len(bad):
+            j = bad[np.argmin(first[bad])]
+            fail_pix = int(order[first[j]]) // 16
+            code = int(st[j][np.flatnonzero(st[j])[0]])
+    if first_par is not None and (fail_pix is None or first_par <= fail_pix):
+        raise ValueError("ray parallel to the light-slab planes")
+    if fail_pix is not None:
+        decoder._raise_status(code)
+
+
 def _geom_struct(geometry):
     x0, y0, x1, y1 = geometry.image_plane_extent
     return (geometry.camera_plane_z, geometry.image_plane_z, x0, y0, x1, y1)
@@ -257,8 +355,12 @@ def render_views(state, poses, stop_level=0, geometry=None,
             need.data_ptr(), stream), "rlfc_render_pinhole_needs")
     cams = np.flatnonzero(need.cpu().numpy())
     field, slots, dstatus = _decode_cameras(state, cams, stop_level, device)
-    if dstatus is not None:
-        decoder._raise_word(dstatus.cpu().item())
+    if dstatus is not None and dstatus.cpu().item() != 0:
+        # a tap camera holds a corrupt record; the reference decodes only the
+        # blocks its rays sample (memoised decode_block_progressive), so it
+        # raises only when one of those fails -- decide exactly that
+        for p, g in zip(poses, geos):
+            _pinhole_first_failure(state, p, g, stop_level)
     status = torch.zeros(n, dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
         _native.check(L.rlfc_render_pinhole(

@@ -423,3 +423,48 @@ def test_block_server_threads_and_release(rl):
     del st
     gc.collect()
     torch.cuda.synchronize()
+
+
+def _corrupt_first_descriptor(rl, data, bx, by, c=0):
+    """Stream copy whose record (c, bx, by) has its first present node's
+    descriptor set to 31 (outside the range table)."""
+    from paper_1805_06019_b200 import container
+    st = rl.init(data)
+    hdr = st.header
+    wb, _ = hdr.block_grid
+    starts, _ = container.section_offsets(hdr)
+    rec = starts[c][2] + int(st.offsets[c][by * wb + bx])
+    nbm = (st.m_nodes + 7) >> 3
+    bits = [(data[rec + (i >> 3)] >> (i & 7)) & 1 for i in range(st.m_nodes)]
+    level0 = st.m_nodes - hdr.s_count * hdr.t_count
+    # a first present node above level 0 lies on every view's walk
+    if 1 not in bits or bits.index(1) >= level0:
+        return None
+    buf = bytearray(data)
+    buf[rec + nbm] = 31
+    return bytes(buf)
+
+
+def test_pinhole_corrupt_record_raises_only_when_sampled(rl):
+    """The reference's pinhole render decodes only the blocks its rays sample
+    (renderer.py:134-144, 295-305): a corrupt record elsewhere in a tap camera
+    leaves the frame as the clean stream renders it; a corrupt sampled record
+    raises the reference's FormatError.  (The live reference, run on these
+    same corrupted streams in the build container, gives exactly these three
+    outcomes.)"""
+    data = load_stream("mid17_dense")                  # 17x17x32^2, B = 4, dense residuals
+    pose = rl.CameraPose(eye=(8.0, 8.0, -2.0), look=(0.0, 0.0, 1.0), fov_deg=4.0, width=24, height=24)
+    clean = rl.render_view(rl.init(data), pose)
+    far = next(d for d in (_corrupt_first_descriptor(rl, data, bx, by, c) for by in range(8) for bx in range(8)
+                           for c in range(3) if bx < 2 or by < 2) if d)
+    st_far = rl.init(far)
+    # the corrupt record is in a tap camera's image: its full decode fails ...
+    with pytest.raises(rl.FormatError):
+        rl.decode_image(st_far, (8, 8))
+    # ... but no sampled block is affected
+    assert np.array_equal(rl.render_view(st_far, pose), clean)
+    near = next(d for d in (_corrupt_first_descriptor(rl, data, bx, by, c) for bx, by in ((3, 3), (4, 4), (3, 4),
+                                                                                            (4, 3))
+                            for c in range(3)) if d)
+    with pytest.raises(rl.FormatError, match="descriptor outside range table"):
+        rl.render_view(rl.init(near), pose)
