@@ -759,12 +759,21 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     constexpr int EPT = PAY_CHUNK / THREADS;                   // entries per thread
     // entry j of chunk cc for this thread (j = tid + q * THREADS); slots
     // outside the band are skipped
-    auto load_entries = [&](uint64_t v, uint2* e4, uint32_t* sl) {
+    // the raw entries of a chunk are fetched two chunks ahead (fetch), so
+    // their latency hides behind a chunk's decode; process filters them
+    auto fetch = [&](uint64_t v, uint2* r) {
         const uint64_t cc = chunk_of(v);
 #pragma unroll
         for (int q = 0; q < EPT; ++q) {
             const uint64_t i = cc * PAY_CHUNK + tid + q * THREADS;
-            uint2 e = i < ntot ? __ldg(w.sorted + i) : make_uint2(0u, SKIP);
+            r[q] = i < ntot ? __ldg(w.sorted + i) : make_uint2(0u, SKIP);
+        }
+    };
+    auto process = [&](uint64_t v, const uint2* r, uint2* e4, uint32_t* sl) {
+        const uint64_t cc = chunk_of(v);
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) {
+            uint2 e = r[q];
             const uint64_t slot = cc * PAY_CHUNK + ((e.y >> 7) & (PAY_CHUNK - 1));
             const int c = (int)(e.y >> 5) & 3;
             const uint64_t lc = c == 0 ? lo[0] : c == 1 ? lo[1] : lo[2];
@@ -818,13 +827,20 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     bool staged = false;
     uint32_t lo16 = 0;
     if (tid == 0) {
-        range[0][0] = ~0u;
-        range[0][1] = 0u;
-        range[0][2] = 0u;
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+            range[b2][0] = ~0u;
+            range[b2][1] = 0u;
+            range[b2][2] = 0u;
+        }
     }
     __syncthreads();
+    uint2 rawn[EPT];                                         // chunk v + gridDim.x
     if (v < n) {
-        load_entries(v, ent, sl);
+        uint2 r0[EPT];
+        fetch(v, r0);
+        if (v + gridDim.x < n) fetch(v + gridDim.x, rawn);
+        process(v, r0, ent, sl);
         reduce_range(ent, 0);
     }
     __syncthreads();
@@ -832,23 +848,27 @@ __global__ void __launch_bounds__(THREADS) k_payloads(const __grid_constant__ rl
     asm volatile("cp.async.commit_group;" ::: "memory");
     for (int it = 0; v < n; v += gridDim.x, ++it) {
         const int q = it & 1;
-        if (tid == 0) {
-            range[q ^ 1][0] = ~0u;
-            range[q ^ 1][1] = 0u;
-            range[q ^ 1][2] = 0u;
-        }
-        __syncthreads();
+        // range[q ^ 1] was reset in the previous iteration (or the prologue)
+        // behind at least one barrier: no barrier here
         const bool has_next = v + gridDim.x < n;
         uint2 entn[EPT];
         uint32_t sln[EPT];
         if (has_next) {
-            load_entries(v + gridDim.x, entn, sln);
+            process(v + gridDim.x, rawn, entn, sln);
+            if (v + 2 * (uint64_t)gridDim.x < n) fetch(v + 2 * (uint64_t)gridDim.x, rawn);
             reduce_range(entn, q ^ 1);
         }
         __syncthreads();
         uint32_t lo16n = 0;
         bool stagedn = false;
         if (has_next) stagedn = stage_issue(q ^ 1, lo16n);
+        if (tid == 0) {
+            // range[q] was read by the previous iteration's stage_issue
+            // (before the barrier above); the next iteration fills it
+            range[q][0] = ~0u;
+            range[q][1] = 0u;
+            range[q][2] = 0u;
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 1;" ::: "memory");     // this chunk's copies
         __syncthreads();
