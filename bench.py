@@ -293,10 +293,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook for the N > 1 code path on a one-GPU box: every rank on
+    # cuda:0, gloo instead of NCCL (NCCL refuses two ranks on one device);
+    # its numbers are not a scaling measurement
+    one_dev = os.environ.get("BENCH_TEST_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     scaling = args.scaling or ("strong" if world > 1 else "weak")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -406,7 +415,9 @@ def main():
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": dict(workload_config(), bpp=round(st["bpp"], 4),
                            present_frac=round(st["present_frac"], 5),
-                           kernel=kern, bands=[list(b) for b in bands] if world > 1 else [[0, hb]]),
+                           kernel=kern, bands=[list(b) for b in bands] if world > 1 else [[0, hb]],
+                           **({"test_hook": "BENCH_TEST_ONE_DEVICE: all ranks on cuda:0 over gloo, "
+                                            "not a scaling measurement"} if one_dev else {})),
             "parity": parity,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s",

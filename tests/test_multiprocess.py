@@ -97,3 +97,27 @@ def test_two_ranks_gpu_band_decode(name):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_device():
+    """bench.py's N > 1 path end to end (relaunch under torchrun, strong
+    scaling over balanced bands, all_gather_into_tensor of the bands, sha256
+    parity against the reference golden, max-over-ranks timing) with both
+    ranks on cuda:0 over gloo (BENCH_TEST_ONE_DEVICE): the code the driver's
+    multi-GPU run executes, minus NCCL."""
+    import json
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, BENCH_TEST_ONE_DEVICE="1")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup",
+                        "3", "--no-render", "--no-cpu-baseline"], cwd=ROOT, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["parity"]["decode"] == "bit-exact"
+    assert len(line["config"]["bands"]) == 2 and line["config"]["bands"][0][0] == 0
+    assert line["value"] is not None and "test_hook" in line["config"]
