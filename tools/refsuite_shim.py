@@ -23,6 +23,9 @@ import os
 import sys
 
 ROUTE = os.environ.get("REFSUITE_ROUTE", "api")
+# "encoder": rlfc.encoder resolves to tools/refsuite_gpu_encoder.py, this
+# package's encoder with the RKV/SRV trees built on the GPU; the reference's
+# decoder then reads those streams
 _API = {
     "rlfc.decoder": "paper_1805_06019_b200.decoder",
     "rlfc.renderer": "paper_1805_06019_b200.renderer",
@@ -50,6 +53,8 @@ class _Alias(importlib.abc.MetaPathFinder, importlib.abc.Loader):
 # suites' conftest.py (which imports rlfc)
 if ROUTE == "api":
     sys.meta_path.insert(0, _Alias(_API))
+elif ROUTE == "encoder":
+    sys.meta_path.insert(0, _Alias({"rlfc.encoder": "refsuite_gpu_encoder"}))
 
 
 def pytest_configure(config):
@@ -58,6 +63,10 @@ def pytest_configure(config):
         import paper_1805_06019_b200
         assert rlfc.decoder is paper_1805_06019_b200.decoder
         assert rlfc.renderer is paper_1805_06019_b200.renderer
+    elif ROUTE == "encoder":
+        import rlfc
+        import refsuite_gpu_encoder
+        assert rlfc.encoder is refsuite_gpu_encoder
     elif ROUTE == "kernels":
         import rlfc.kernels as K
         from paper_1805_06019_b200 import kernels_b200 as G

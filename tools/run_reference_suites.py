@@ -1,5 +1,6 @@
 """Run the reference's own decoder / renderer / acceptance suites against
-this package (tools/refsuite_shim.py), under both integration routes.
+this package (tools/refsuite_shim.py): both integration routes, and the
+producer route (streams built by the GPU encoder, read by the reference).
 
     python tools/run_reference_suites.py --stage     # here: copy the tests
     python tools/run_reference_suites.py             # on a GPU box
@@ -26,6 +27,9 @@ SUITES = {
     # Route 2: everything that reaches the kernel module's decode entry points
     "kernels": ["test_decoder.py", "test_renderer.py", "test_acceptance.py", "test_service.py",
                 "test_bise.py", "test_kernels.py"],
+    # the producer side: every stream the suites encode comes from the GPU
+    # tree construction; the reference decodes and checks them
+    "encoder": ["test_encoder.py", "test_decoder.py", "test_container.py", "test_acceptance.py"],
 }
 
 
@@ -72,14 +76,14 @@ def run(route, out_dir):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--stage", action="store_true")
-    ap.add_argument("--route", choices=["api", "kernels", "both"], default="both")
+    ap.add_argument("--route", choices=["api", "kernels", "encoder", "all"], default="all")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out"))
     a = ap.parse_args()
     if a.stage:
         stage()
         return
     os.makedirs(a.out, exist_ok=True)
-    routes = ["api", "kernels"] if a.route == "both" else [a.route]
+    routes = ["api", "kernels", "encoder"] if a.route == "all" else [a.route]
     for r in routes:
         run(r, a.out)
 
