@@ -336,6 +336,27 @@ int rlfc_render_slab(const uint8_t *rgb_field, const int32_t *slots,
                      int32_t n, int32_t ow, int32_t oh, uint8_t *out,
                      void *stream);
 
+/* A batch of slab poses in one call (renderer.render_views, renderer.py:
+ * 279-305 per pose): tap cameras (floor and ceil of each clamped eye
+ * coordinate), slot table and camera rows are built on the host, staged with
+ * the HOST arrays poses (n x 4 doubles: s, t, has_focal, focal), geoms and bg
+ * in stage_host (pinned, rlfc_render_staging_bytes bytes) and sent to
+ * stage_dev (device, same size) with one copy; the staged decode in slot
+ * mode (workspace as for rlfc_decode_field_staged, else the fused decode)
+ * fills field (device, field_cap images of H*W*3), k_render_slab renders into
+ * out (device, n*oh*ow*3); the call returns after the stream has drained,
+ * with the decode status word in *status_word (0 = success). */
+int rlfc_render_slab_batch(const rlfc_field *f, int32_t stop_level, void *ws,
+                           uint64_t ws_bytes, uint64_t present,
+                           int32_t n_flagged, const double *poses,
+                           const rlfc_render_geom *geoms, const uint8_t *bg,
+                           int32_t n, int32_t ow, int32_t oh, uint8_t *field,
+                           int32_t field_cap, uint8_t *out,
+                           uint8_t *stage_host, uint8_t *stage_dev,
+                           uint64_t stage_bytes, uint64_t *status_word,
+                           void *stream);
+uint64_t rlfc_render_staging_bytes(const rlfc_field *f, int32_t n);
+
 /* Pinhole-pose rendering (renderer.py:279-305 with ray_to_lf_coords
  * renderer.py:87-116 and sample_quadrilinear renderer.py:147-169).
  * frames: n x 14 doubles (eye[3], look[3], right[3], down[3], half, aspect)

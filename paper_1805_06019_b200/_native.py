@@ -89,6 +89,9 @@ _SIGS = {
                         "p"],
     "rlfc_plane_core": ["p", "u", "p", "i", "i", "i", "i", "p", "i", "i", "p",
                         "p", "p", "p"],
+    "rlfc_render_slab_batch": ["p", "i", "p", "u", "u", "i", "p", "p", "p", "i", "i", "i", "p", "i", "p",
+                               "p", "p", "u", "p", "p"],
+    "rlfc_render_staging_bytes": ["p", "i"],
     "rlfc_render_slab": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
                          "i", "i", "p", "p"],
     "rlfc_render_pinhole": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
@@ -109,6 +112,7 @@ _SIGS = {
 _CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64,
        "u": ctypes.c_uint64}
 EXPORTS = tuple(_SIGS)
+_RESTYPE = {"rlfc_render_staging_bytes": ctypes.c_uint64}
 
 
 def load_library(path=CUDA_LIB):
@@ -123,7 +127,7 @@ def load_library(path=CUDA_LIB):
         raise NativeUnavailable(f"cannot load {path}: {exc}") from exc
     for name, sig in _SIGS.items():
         fn = getattr(L, name)
-        fn.restype = ctypes.c_int
+        fn.restype = _RESTYPE.get(name, ctypes.c_int)
         fn.argtypes = [_CT[c] for c in sig]
     return L
 

@@ -6,7 +6,9 @@
 // __ddiv_rn), so nvcc can never contract a*b+c into an FMA -- numpy does not
 // either -- and the operation order is numpy's.
 #include <cuda_runtime.h>
+#include <cmath>
 #include <cstdio>
+#include <cstring>
 
 #include "../../include/rlfc_b200.h"
 
@@ -317,4 +319,83 @@ extern "C" int rlfc_render_pinhole_needs(int32_t S, int32_t T, int32_t W, int32_
     dim3 grid((unsigned)(((int64_t)ow * oh + threads - 1) / threads), (unsigned)n);
     k_pinhole_needs<<<grid, threads, 0, (cudaStream_t)stream>>>(S, T, W, H, frames, geoms, ow, oh, need);
     return launch_status();
+}
+
+// ---- one call per batch of slab poses (host runtime) ------------------------------------
+// renderer.render_views for SlabPose batches without Python in the loop: the
+// tap-camera set (floor and ceil of each clamped eye coordinate, a superset
+// of renderer.py:119-131 _axis_taps), the slot table and camera rows are
+// built here, staged with the poses, geometries and backgrounds in one
+// pinned buffer and sent with one copy; the staged decode (slot mode) and
+// k_render_slab follow on the same stream; the decode status word comes back
+// with one small copy and the call returns after the stream has drained.
+extern "C" int rlfc_render_slab_batch(const rlfc_field* f, int32_t stop_level, void* ws, uint64_t ws_bytes,
+                                      uint64_t present, int32_t n_flagged, const double* poses,
+                                      const rlfc_render_geom* geoms, const uint8_t* bg, int32_t n, int32_t ow,
+                                      int32_t oh, uint8_t* field, int32_t field_cap, uint8_t* out,
+                                      uint8_t* stage_host, uint8_t* stage_dev, uint64_t stage_bytes,
+                                      uint64_t* status_word, void* stream) {
+    if (!f || !poses || !geoms || !bg || !field || !out || !stage_host || !stage_dev || !status_word || n < 1 ||
+        n > 65535 || ow < 1 || oh < 1)
+        return RLFC_ERR_ARGUMENT;
+    const int S = f->s_count, T = f->t_count, W = f->width, H = f->height;
+    auto al = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
+    const uint64_t o_stat = 0, o_pose = 16, o_geom = al(o_pose + 32ull * n), o_slot = al(o_geom + 48ull * n),
+                   o_rows = al(o_slot + 4ull * S * T), o_bg = al(o_rows + 4ull * T), total = al(o_bg + 3ull * n);
+    if (total > stage_bytes) return RLFC_ERR_ARGUMENT;
+    int32_t* slots = reinterpret_cast<int32_t*>(stage_host + o_slot);
+    for (int i = 0; i < S * T; ++i) slots[i] = -1;
+    auto cell = [](double x, int cnt, int hi) {
+        const double c = fmin(fmax(x, 0.0), (double)(cnt - 1));
+        return hi ? (int)ceil(c) : (int)floor(c);
+    };
+    for (int v = 0; v < n; ++v)
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) slots[cell(poses[4 * v], S, a) * T + cell(poses[4 * v + 1], T, b)] = 0;
+    int ncam = 0, nrows = 0;
+    int32_t* rows = reinterpret_cast<int32_t*>(stage_host + o_rows);
+    for (int t = 0; t < T; ++t) {
+        bool any = false;
+        for (int s = 0; s < S; ++s)
+            if (slots[s * T + t] == 0) any = true;
+        if (any) rows[nrows++] = t;
+    }
+    for (int i = 0; i < S * T; ++i)
+        if (slots[i] == 0) slots[i] = ncam++;
+    if (ncam > field_cap) return RLFC_ERR_ARGUMENT;
+    std::memset(stage_host + o_stat, 0, 16);
+    std::memcpy(stage_host + o_pose, poses, 32ull * n);
+    std::memcpy(stage_host + o_geom, geoms, 48ull * n);
+    std::memcpy(stage_host + o_bg, bg, 3ull * n);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(stage_dev, stage_host, total, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return RLFC_ERR_CUDA;
+    uint64_t* dstat = reinterpret_cast<uint64_t*>(stage_dev + o_stat);
+    const int32_t* dslots = reinterpret_cast<const int32_t*>(stage_dev + o_slot);
+    const int64_t img = (int64_t)H * W * 3;
+    int rc = RLFC_ERR_ARGUMENT;
+    if (ws)
+        rc = rlfc_decode_field_staged(f, stop_level, dslots, 0, f->hb, field, img, (int64_t)W * 3, ws, ws_bytes,
+                                      present, n_flagged, reinterpret_cast<const int32_t*>(stage_dev + o_rows),
+                                      nrows, dstat, stream);
+    if (rc == RLFC_ERR_ARGUMENT)
+        rc = rlfc_decode_field(f, stop_level, dslots, 0, f->hb, field, img, (int64_t)W * 3, dstat, stream);
+    if (rc != RLFC_OK) return rc;
+    rc = rlfc_render_slab(field, dslots, S, T, W, H, reinterpret_cast<const double*>(stage_dev + o_pose),
+                          reinterpret_cast<const rlfc_render_geom*>(stage_dev + o_geom), stage_dev + o_bg, n, ow,
+                          oh, out, stream);
+    if (rc != RLFC_OK) return rc;
+    if (cudaMemcpyAsync(stage_host + o_stat, dstat, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return RLFC_ERR_CUDA;
+    std::memcpy(status_word, stage_host + o_stat, 8);
+    return RLFC_OK;
+}
+
+extern "C" uint64_t rlfc_render_staging_bytes(const rlfc_field* f, int32_t n) {
+    if (!f || n < 1) return 0;
+    auto al = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
+    const uint64_t o_geom = al(16 + 32ull * n), o_slot = al(o_geom + 48ull * n),
+                   o_rows = al(o_slot + 4ull * f->s_count * f->t_count), o_bg = al(o_rows + 4ull * f->t_count);
+    return al(o_bg + 3ull * n);
 }

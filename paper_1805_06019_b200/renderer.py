@@ -339,9 +339,10 @@ def render_views(state, poses, stop_level=0, geometry=None,
         focal = np.where(pose_arr[:, 2] != 0.0, pose_arr[:, 3], gstruct[:, 1])
         if np.any(focal == gstruct[:, 0]):
             raise ValueError("focal plane coincides with the camera plane")
-        cams = _slab_camera_set(pose_arr[:, 0], pose_arr[:, 1], S, T)
-        return _render_slab_batch(state, df, stop_level, cams, pose_arr,
-                                  gstruct, bgs, ow, oh, out, stream)
+        return _render_slab_batch(state, df, stop_level, pose_arr,
+                                  np.ascontiguousarray(gstruct),
+                                  np.ascontiguousarray(bgs, dtype=np.uint8),
+                                  ow, oh, out, stream)
     d_geom = torch.from_numpy(gstruct).to(dev)
     d_bg = torch.from_numpy(bgs).to(dev)
     if geos is None:
@@ -374,10 +375,8 @@ def render_views(state, poses, stop_level=0, geometry=None,
 
 
 class _Staging:
-    """Per-thread, per-device staging of a slab render's small inputs (status
-    word, poses, geometries, slot table, camera rows, backgrounds): one pinned
-    host buffer and one device buffer, so a call makes a single host-to-device
-    copy and reads its status back with a single small copy."""
+    """Per-thread, per-device staging buffers of rlfc_render_slab_batch: one
+    pinned host buffer and one device buffer (grown on demand)."""
 
     def __init__(self, dev):
         self.dev = dev
@@ -388,11 +387,10 @@ class _Staging:
         if nbytes > self.cap:
             cap = max(4096, 1 << (nbytes - 1).bit_length())
             self.host = torch.empty(cap, dtype=torch.uint8).pin_memory()
-            self.hnp = self.host.numpy()
             self.devbuf = torch.empty(cap, dtype=torch.uint8, device=self.dev)
-            self.stat = torch.empty(8, dtype=torch.uint8).pin_memory()
+            self.status = np.zeros(1, dtype=np.uint64)
             self.cap = cap
-        return self.host, self.hnp, self.devbuf
+        return self.host, self.devbuf
 
 
 _tls = threading.local()
@@ -408,78 +406,31 @@ def _staging(dev):
     return st
 
 
-def _render_slab_batch(state, df, stop_level, cams, pose_arr, gstruct, bgs,
-                       ow, oh, out, stream):
-    """Decode the batch's tap cameras (staged path in slot mode) and render
-    every slab pose in one k_render_slab launch."""
-    import torch
-    with torch.cuda.device(df.device):
-        return _render_slab_on(state, df, stop_level, cams, pose_arr, gstruct,
-                               bgs, ow, oh, out, stream)
-
-
-def _render_slab_on(state, df, stop_level, cams, pose_arr, gstruct, bgs, ow,
-                    oh, out, stream):
+def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
+                       out, stream):
+    """Every slab pose of the batch in one native call
+    (rlfc_render_slab_batch): tap cameras decoded by the staged path in slot
+    mode, then one k_render_slab launch."""
     import torch
     hdr = state.header
-    S, T, W, H = hdr.s_count, hdr.t_count, hdr.width, hdr.height
     n = pose_arr.shape[0]
-    ncam = len(cams)
-    rows = sorted({int(c) % T for c in cams})
-    al = lambda x: (x + 15) & ~15                                 # noqa: E731
-    o_pose = 16
-    o_geom = al(o_pose + 32 * n)
-    o_slot = al(o_geom + 48 * n)
-    o_rows = al(o_slot + 4 * S * T)
-    o_bg = al(o_rows + 4 * len(rows))
-    total = al(o_bg + 3 * n)
-    stg = _staging(df.device)
-    host, hnp, dbuf = stg.buffers(total)
-    hnp[:16] = 0
-    hnp[o_pose:o_pose + 32 * n].view(np.float64)[:] = pose_arr.ravel()
-    hnp[o_geom:o_geom + 48 * n].view(np.float64)[:] = gstruct.ravel()
-    slots = hnp[o_slot:o_slot + 4 * S * T].view(np.int32)
-    slots[:] = -1
-    slots[np.asarray(cams, dtype=np.int64)] = np.arange(ncam, dtype=np.int32)
-    hnp[o_rows:o_rows + 4 * len(rows)].view(np.int32)[:] = rows
-    hnp[o_bg:o_bg + 3 * n] = bgs.ravel()
-    dbuf[:total].copy_(host[:total], non_blocking=True)
-    base = dbuf.data_ptr()
-    field = torch.empty((ncam, H, W, 3), dtype=torch.uint8, device=df.device)
     L = _native.lib()
-    hb = hdr.block_grid[1]
-    ws = df.staged_workspace(stream)
-    rc = _native.RLFC_ERR_ARGUMENT
-    if ws is not None:
+    nbytes = int(L.rlfc_render_staging_bytes(df.ref, n))
+    stg = _staging(df.device)
+    host, dbuf = stg.buffers(nbytes)
+    field = torch.empty((min(hdr.s_count * hdr.t_count, 4 * n), hdr.height, hdr.width, 3),
+                        dtype=torch.uint8, device=df.device)
+    with torch.cuda.device(df.device):
+        ws = df.staged_workspace(stream)
+        args = (None, 0, 0, 0) if ws is None else (ws[0].data_ptr(), ws[1], ws[2], ws[3])
         with df.enqueue_lock:
-            rc = L.rlfc_decode_field_staged(
-                df.ref, stop_level, base + o_slot, 0, hb, field.data_ptr(),
-                H * W * 3, W * 3, ws[0].data_ptr(), ws[1], ws[2], ws[3],
-                base + o_rows, len(rows), base, stream)
-    if rc == _native.RLFC_ERR_ARGUMENT:
-        rc = L.rlfc_decode_field(df.ref, stop_level, base + o_slot, 0, hb,
-                                 field.data_ptr(), H * W * 3, W * 3, base,
-                                 stream)
-    _native.check(rc, "rlfc_decode_field")
-    _native.check(L.rlfc_render_slab(
-        field.data_ptr(), base + o_slot, S, T, W, H, base + o_pose,
-        base + o_geom, base + o_bg, n, ow, oh, out.data_ptr(), stream),
-        "rlfc_render_slab")
-    stg.stat.copy_(dbuf[:8], non_blocking=True)
-    torch.cuda.current_stream(df.device).synchronize()
-    decoder._raise_word(int(stg.stat.numpy().view(np.int64)[0]))
+            rc = L.rlfc_render_slab_batch(
+                df.ref, stop_level, *args, pose_arr.ctypes.data, gstruct.ctypes.data, bgs.ctypes.data, n, ow,
+                oh, field.data_ptr(), field.shape[0], out.data_ptr(), host.data_ptr(), dbuf.data_ptr(),
+                stg.cap, stg.status.ctypes.data, stream)
+    _native.check(rc, "rlfc_render_slab_batch")
+    decoder._raise_word(int(stg.status[0]))
     return out
-
-
-def _slab_camera_set(ps, pt, S, T):
-    """Serial indices s*T + t of every camera a batch of slab poses can tap:
-    floor and ceil of the clamped eye position along each axis, a superset
-    of renderer.py:119-131 _axis_taps (which may drop a zero-weight tap)."""
-    cs = np.clip(ps, 0.0, S - 1.0)
-    ct = np.clip(pt, 0.0, T - 1.0)
-    sx = np.stack([np.floor(cs), np.ceil(cs)]).astype(np.int64)
-    ty = np.stack([np.floor(ct), np.ceil(ct)]).astype(np.int64)
-    return np.unique((sx[:, None, :] * T + ty[None, :, :]).ravel())
 
 
 def _decode_cameras(state, cams, stop_level, device):

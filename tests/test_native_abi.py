@@ -10,7 +10,7 @@ from conftest import ROOT
 def declared_functions():
     text = open(os.path.join(ROOT, "include", "rlfc_b200.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\bint\s+(rlfc_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(?:int|uint64_t)\s+(rlfc_\w+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
