@@ -2,8 +2,11 @@
 from the record bitmaps (measurement only): dirty (view, block) units, units
 with several present chain levels, units per blend tile (block row, camera
 row, 64-pixel chunk)."""
-import sys, numpy as np
 import os
+import sys
+
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 from paper_1805_06019_b200 import container
@@ -25,7 +28,6 @@ for c in range(3):
     offs = np.frombuffer(data, dtype='<u8', count=nblk, offset=off_start)
     srv0 = starts[c][2]
     idx = srv0 + offs.astype(np.int64)
-    bm = np.stack([np.frombuffer(data, dtype=np.uint8, count=1, offset=int(i))[0:0] for i in idx[:1]]) if False else None
     raw = np.frombuffer(data, dtype=np.uint8)
     bytes_ = raw[idx[:, None] + np.arange(nbm)[None, :]]
     bits = np.unpackbits(bytes_, axis=1, bitorder='little')[:, :M]
