@@ -592,7 +592,6 @@ __global__ void __launch_bounds__(CT, CPS) k_seg_dir(const __grid_constant__ Par
             asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        const uint8_t* buf = smem + P.off_buf + q * P.buf_bytes;
         const uint64_t* bptr = bptrs + q * MAXL;
         DSTAMP(1);
 
@@ -871,31 +870,7 @@ __global__ void k_fixup(const __grid_constant__ rlfc_field f, const int32_t* fla
 }
 
 // ---- host helpers ---------------------------------------------------------------------
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = []() -> EncodeTiledFn {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return nullptr;
-        return reinterpret_cast<EncodeTiledFn>(p);
-    }();
-    return fn;
-}
-
-static bool encode_map(CUtensorMap* map, CUtensorMapDataType dt, cuuint32_t rank, void* base, const cuuint64_t* dims,
-                       const cuuint64_t* strides, const cuuint32_t* box) {
-    EncodeTiledFn enc = encode_fn();
-    if (!enc) return false;
-    const cuuint32_t estr[5] = {1u, 1u, 1u, 1u, 1u};
-    return enc(map, dt, rank, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 static Geo geo_of(const rlfc_field& f) {
     Geo g{};
