@@ -468,3 +468,22 @@ def test_pinhole_corrupt_record_raises_only_when_sampled(rl):
                             for c in range(3)) if d)
     with pytest.raises(rl.FormatError, match="descriptor outside range table"):
         rl.render_view(rl.init(near), pose)
+
+
+def test_slab_render_corrupt_tap_camera_raises(rl):
+    """Slab renders decode whole tap cameras (renderer.py:212-218, 233-276), so
+    a corrupt record anywhere in one raises the reference's FormatError -- in
+    the single-call API and in the native batch path (rlfc_render_slab_batch).
+    (The live reference raises "descriptor outside range table" for both
+    poses on this stream.)"""
+    data = load_stream("mid17_dense")
+    far = next(d for d in (_corrupt_first_descriptor(rl, data, bx, by, c) for by in range(8) for bx in range(8)
+                           for c in range(3) if bx < 2 or by < 2) if d)
+    st = rl.init(far)
+    for pose in (rl.SlabPose(8.0, 8.0, 16, 16), rl.SlabPose(3.5, 12.25, 16, 16, focal_z=0.9)):
+        with pytest.raises(rl.FormatError, match="descriptor outside range table"):
+            rl.render_view(st, pose)
+    with pytest.raises(rl.FormatError, match="descriptor outside range table"):
+        rl.render_views(st, [rl.SlabPose(8.0, 8.0, 16, 16), rl.SlabPose(1.0, 2.0, 16, 16)])
+    # the clean stream renders the same batch without error
+    rl.render_views(rl.init(data), [rl.SlabPose(8.0, 8.0, 16, 16), rl.SlabPose(1.0, 2.0, 16, 16)])
