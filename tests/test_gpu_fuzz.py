@@ -1,0 +1,105 @@
+"""Seeded configuration fuzz over the format's parameter space (GPU).
+
+Random small fields -- grid sizes 1..24, odd image sizes (some wider than
+two 64-pixel blend chunks), B in {2, 4, 8, 16}, tree heights 1..5,
+quantiser shifts 0..8 (int16 and int32 residuals), pixel /
+block thresholds from lossless to coarse, both filters, RAW and PNG roots --
+are synthesised and encoded twice: by the native C++ producer and by the GPU
+tree construction, which must agree byte for byte (the producer is pinned to
+the reference encoder by tests/test_producer.py).  Every decode kernel, image
+subsets, block-row bands, random blocks and a slab render are then compared
+with the C oracle (pinned to the reference by tests/test_oracle_golden.py) at
+several stop levels.  Integer outputs bit-exact, renders bit-exact.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+MAXST = int(os.environ.get("FUZZ_MAXST", "24"))
+MAXH = int(os.environ.get("FUZZ_MAXH", "5"))
+MAXSHIFT = int(os.environ.get("FUZZ_MAXSHIFT", "8"))
+
+
+def _configs(n=64, seed=2026):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        B = int(rng.choice([2, 4, 8, 16], p=[0.15, 0.45, 0.25, 0.15]))
+        h = int(rng.integers(1, MAXH + 1))
+        big = i % 4 == 3                       # every fourth: wide images (several 64-pixel blend chunks)
+        S, T = int(rng.integers(1, MAXST + 1)), int(rng.integers(1, MAXST + 1))
+        W = int(rng.integers(130, 300)) if big else int(rng.integers(max(2, B // 2), 72))
+        H = int(rng.integers(max(2, B // 2), 72))
+        shift = int(rng.integers(0, MAXSHIFT + 1))
+        tp = int(rng.choice([0, 1, 2, 4, 8, 16, 32]))
+        tb = int(rng.choice([0, 10, 80, 300, 1000]))
+        filt = str(rng.choice(["gaussian", "uniform"]))
+        codec = str(rng.choice(["raw", "png"]))
+        out.append(dict(spec=dict(s_count=S, t_count=T, width=W, height=H, seed=int(rng.integers(0, 1000))),
+                        params=dict(tree_height=h, block_size=B, quant_shift=shift, pixel_threshold=tp,
+                                    block_threshold=tb, filter=filt, root_codec=codec)))
+    return out
+
+
+# extended hunts: FUZZ_N=1000 FUZZ_SEED=7 python -m pytest tests/test_gpu_fuzz.py
+CONFIGS = _configs(int(os.environ.get("FUZZ_N", "64")), int(os.environ.get("FUZZ_SEED", "2026")))
+
+
+@pytest.fixture(scope="module")
+def rl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1805_06019_b200 as rl
+    return rl
+
+
+@pytest.mark.parametrize("i", range(len(CONFIGS)))
+def test_config_fuzz(rl, i):
+    from oracle import oracle
+    from paper_1805_06019_b200 import decoder, encoder, lightfield, producer
+    cfg = CONFIGS[i]
+    p = dict(cfg["params"])
+    p["filter"] = encoder.FilterSpec(kind=p["filter"])
+    params = encoder.EncodingParams(**p)
+    lf = lightfield.synthesize_lightfield(lightfield.SyntheticSpec(**cfg["spec"]))
+    data, present = producer.encode(lf, params)
+    gdata, gpresent = producer.encode_gpu(lf, params)
+    assert gdata == data and tuple(gpresent) == tuple(present), cfg
+    st = rl.init(data)
+    orc = oracle.OracleState(data)
+    hdr = st.header
+    S, T, h = hdr.s_count, hdr.t_count, hdr.tree_height
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(100 + i)
+    for k in sorted({0, h // 2, h}):
+        want, code = orc.decode_all(k)
+        assert code == 0
+        for kernel in ("auto", "dir", "fused", "simple"):
+            got, _ = decoder.decode_field(st, k, kernel=kernel)
+            assert np.array_equal(got.cpu().numpy(), want), (cfg, k, kernel)
+        # a subset of views (slot mode) over a block-row band
+        n_img = int(rng.integers(1, S * T + 1))
+        picks = [tuple(map(int, divmod(int(j), T))) for j in rng.choice(S * T, n_img, replace=False)]
+        lo = int(rng.integers(0, hb))
+        hi = int(rng.integers(lo + 1, hb + 1))
+        got, _ = decoder.decode_field(st, k, images=picks, rows=(lo, hi))
+        r0, r1 = lo * hdr.block_size, min(hi * hdr.block_size, hdr.height)
+        for j, (s, t) in enumerate(picks):
+            assert np.array_equal(got[j].cpu().numpy(), want[s, t, r0:r1]), (cfg, k, (s, t), (lo, hi))
+    req = np.stack([rng.integers(0, S, 64), rng.integers(0, T, 64), rng.integers(0, wb, 64),
+                    rng.integers(0, hb, 64), rng.integers(0, 3, 64), rng.integers(0, h + 1, 64)], 1)
+    out, _ = rl.decode_blocks(st, req)
+    out = out.cpu().numpy()
+    for r, blk in zip(req, out):
+        want, code = orc.decode_block(*map(int, r))
+        assert code == 0 and np.array_equal(blk, want), (cfg, r)
+    s, t = float(rng.uniform(0, S - 1)), float(rng.uniform(0, T - 1))
+    focal = [None, 0.9, 1.12][i % 3]
+    k = int(rng.integers(0, h + 1))
+    img = rl.render_view(st, rl.SlabPose(s, t, 24, 20, focal_z=focal), stop_level=k)
+    assert np.array_equal(img, orc.render_slab(s, t, 24, 20, focal_z=focal, stop_level=k)), (cfg, s, t, focal, k)
