@@ -7,7 +7,7 @@ block thresholds from lossless to coarse, both filters, RAW and PNG roots --
 are synthesised and encoded twice: by the native C++ producer and by the GPU
 tree construction, which must agree byte for byte (the producer is pinned to
 the reference encoder by tests/test_producer.py).  Every decode kernel, image
-subsets, block-row bands, random blocks and a slab render are then compared
+subsets, block-row bands, random blocks, a slab and a pinhole render are then compared
 with the C oracle (pinned to the reference by tests/test_oracle_golden.py) at
 several stop levels.  Integer outputs bit-exact, renders bit-exact.
 """
@@ -103,3 +103,9 @@ def test_config_fuzz(rl, i):
     k = int(rng.integers(0, h + 1))
     img = rl.render_view(st, rl.SlabPose(s, t, 24, 20, focal_z=focal), stop_level=k)
     assert np.array_equal(img, orc.render_slab(s, t, 24, 20, focal_z=focal, stop_level=k)), (cfg, s, t, focal, k)
+    eye = (float(rng.uniform(-1, S)), float(rng.uniform(-1, T)), -float(rng.uniform(1, 4)))
+    look = (float(rng.uniform(-0.2, 0.2)), float(rng.uniform(-0.2, 0.2)), 1.0)
+    img = rl.render_view(st, rl.CameraPose(eye=eye, look=look, fov_deg=40.0, width=16, height=12), stop_level=k)
+    want = orc.render_pinhole(eye, look, 40.0, 16, 12, stop_level=k)
+    want = want[0] if isinstance(want, tuple) else want
+    assert np.array_equal(img, want), (cfg, eye, look, k)
