@@ -659,6 +659,42 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
     return bad;
 }
 
+// decode16 for one request (k_blocks_indexed): the windows read straight
+// from the SRV words in memory, digits from the global LUT, dequantisation
+// by arithmetic, accumulated into acc (kernels.py:128-159, 202-211).
+template <int MODE>
+__device__ __forceinline__ bool decode16_acc(const uint32_t* sw, uint32_t bit0, uint32_t b, const uint16_t* dlut,
+                                             int shift, int32_t* acc) {
+    const uint32_t lm = (1u << b) - 1u;
+    bool bad = false;
+    if (MODE == MODE_BITS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint64_t w = win64(sw, bit0 + 4u * (uint32_t)q * b);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[4 * q + i] += deq((uint32_t)(w >> ((uint32_t)i * b)) & lm, shift);
+        }
+    } else {
+        constexpr int G = MODE == MODE_TRIT ? 5 : 3, PB = MODE == MODE_TRIT ? 8 : 7;
+        constexpr uint32_t DB = MODE == MODE_TRIT ? 2u : 3u, DMASK = MODE == MODE_TRIT ? 3u : 7u;
+        constexpr uint32_t PMAX = MODE == MODE_TRIT ? 242u : 124u;
+        const uint32_t gbits = PB + G * b;
+#pragma unroll
+        for (int g = 0; g * G < 16; ++g) {
+            const uint64_t w = win64(sw, bit0 + (uint32_t)g * gbits);
+            const uint32_t pk = (uint32_t)w & ((1u << PB) - 1u);
+            bad |= pk > PMAX;
+            const uint32_t dg = __ldg(dlut + (pk <= PMAX ? pk : 0u));
+#pragma unroll
+            for (int i = 0; i < G && g * G + i < 16; ++i) {
+                const uint32_t low = (uint32_t)(w >> (PB + (uint32_t)i * b)) & lm;
+                acc[g * G + i] += deq((((dg >> (DB * i)) & DMASK) << b) | low, shift);
+            }
+        }
+    }
+    return bad;
+}
+
 // Payload decode over the prepared index.  Slots form chunks of PAY_CHUNK
 // consecutive payloads (consecutive nodes of consecutive records: one
 // contiguous SRV byte range per channel), and rlfc_staged_prepare stores each
@@ -1235,10 +1271,25 @@ __global__ void k_blocks_indexed(const __grid_constant__ rlfc_field f, Ws w, con
     const int64_t nblk = (int64_t)f.wb * f.hb, nrec = 3 * nblk;
     const int64_t blk = (int64_t)by * f.wb + bx, ri = (int64_t)c * nblk + blk;
     int32_t acc[BSQ];
+    if (B == 4 && f.roots_i16) {
+        // the block's four root rows: one aligned 8-byte load each
+        const int h = f.tree_height;
+        const int16_t* r0 = reinterpret_cast<const int16_t*>(f.roots) +
+                            ((((int64_t)(s >> h) * f.rsy + (t >> h)) * 3 + c) * f.hp + by * B) * f.wp + bx * B;
 #pragma unroll
-    for (int yy = 0; yy < B; ++yy)
+        for (int yy = 0; yy < B; ++yy) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(r0 + (int64_t)yy * f.wp));
+            acc[yy * B] = (int32_t)(int16_t)(v.x & 0xFFFFu);
+            acc[yy * B + 1] = (int32_t)v.x >> 16;
+            acc[yy * B + 2] = (int32_t)(int16_t)(v.y & 0xFFFFu);
+            acc[yy * B + 3] = (int32_t)v.y >> 16;
+        }
+    } else {
 #pragma unroll
-        for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+        for (int yy = 0; yy < B; ++yy)
+#pragma unroll
+            for (int xx = 0; xx < B; ++xx) acc[yy * B + xx] = root_sample(f, s, t, c, by * B + yy, bx * B + xx);
+    }
     int st = 0;
     if (__ldg(w.rec_flag + ri)) {
         const uint64_t off = f.offsets[c][blk];
@@ -1269,14 +1320,32 @@ __global__ void k_blocks_indexed(const __grid_constant__ rlfc_field f, Ws w, con
         // chain order h-1 .. k, as the reference decodes its targets
 #pragma unroll
         for (int l = MAXH - 1; l >= 0; --l) {
-            if ((ent[l].y & 31u) < (uint32_t)NUM_DESC && !st)
-                st = decode_payload_acc<BSQ>(f.srv[c] + ent[l].x, (int)(ent[l].y & 31u), f.quant_shift, acc, g_lut);
+            const uint32_t d = ent[l].y & 31u;
+            if (d >= (uint32_t)NUM_DESC || st) continue;
+            if constexpr (BSQ == 16) {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + ent[l].x);
+                const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+                const uint32_t bit0 = (uint32_t)(a & 3u) * 8u, b = (uint32_t)desc_bits((int)d);
+                const int m = desc_mode((int)d);
+                const bool bad = m == MODE_BITS   ? decode16_acc<MODE_BITS>(sw, bit0, b, nullptr, f.quant_shift, acc)
+                                 : m == MODE_TRIT ? decode16_acc<MODE_TRIT>(sw, bit0, b, g_lut.trit, f.quant_shift, acc)
+                                                  : decode16_acc<MODE_QUINT>(sw, bit0, b, g_lut.quint, f.quant_shift, acc);
+                st = bad ? 1 : 0;
+            } else {
+                st = decode_payload_acc<BSQ>(f.srv[c] + ent[l].x, (int)d, f.quant_shift, acc, g_lut);
+            }
         }
     }
     status[i] = st;
     int32_t* o = out + (int64_t)i * BSQ;
+    if constexpr (BSQ % 4 == 0) {
 #pragma unroll
-    for (int j = 0; j < BSQ; ++j) o[j] = acc[j];
+        for (int j = 0; j < BSQ; j += 4)
+            *reinterpret_cast<int4*>(o + j) = make_int4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < BSQ; ++j) o[j] = acc[j];
+    }
 }
 
 __global__ void k_flag_list(const uint32_t* rec_flag, int64_t nrec, uint32_t* flist) {

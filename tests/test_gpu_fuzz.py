@@ -91,13 +91,15 @@ def test_config_fuzz(rl, i):
         r0, r1 = lo * hdr.block_size, min(hi * hdr.block_size, hdr.height)
         for j, (s, t) in enumerate(picks):
             assert np.array_equal(got[j].cpu().numpy(), want[s, t, r0:r1]), (cfg, k, (s, t), (lo, hi))
-    req = np.stack([rng.integers(0, S, 64), rng.integers(0, T, 64), rng.integers(0, wb, 64),
-                    rng.integers(0, hb, 64), rng.integers(0, 3, 64), rng.integers(0, h + 1, 64)], 1)
-    out, _ = rl.decode_blocks(st, req)
-    out = out.cpu().numpy()
-    for r, blk in zip(req, out):
-        want, code = orc.decode_block(*map(int, r))
-        assert code == 0 and np.array_equal(blk, want), (cfg, r)
+    # 64 requests take the per-request walk, 4096 the prepared-index path
+    for nreq in (64, 4096):
+        req = np.stack([rng.integers(0, S, nreq), rng.integers(0, T, nreq), rng.integers(0, wb, nreq),
+                        rng.integers(0, hb, nreq), rng.integers(0, 3, nreq), rng.integers(0, h + 1, nreq)], 1)
+        out, _ = rl.decode_blocks(st, req)
+        out = out.cpu().numpy()
+        for r, blk in zip(req, out):
+            want, code = orc.decode_block(*map(int, r))
+            assert code == 0 and np.array_equal(blk, want), (cfg, nreq, r)
     s, t = float(rng.uniform(0, S - 1)), float(rng.uniform(0, T - 1))
     focal = [None, 0.9, 1.12][i % 3]
     k = int(rng.integers(0, h + 1))
