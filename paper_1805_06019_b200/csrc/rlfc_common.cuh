@@ -176,6 +176,24 @@ __device__ __forceinline__ uint32_t bitmap_word(const uint8_t* rec, int n0) {
     return load_bits32<GEN>(rec, (uint64_t)n0);
 }
 
+// Node size (descriptor + payload bytes) for B*B = 16 values from three
+// 64-bit immediates (5 bits per descriptor): no memory access in a walk's
+// dependent chain (k_index, walk_chain).
+constexpr uint64_t nb16_word(int w) {
+    uint64_t v = 0;
+    for (int i = 0; i < 12; ++i) {
+        const int d = w * 12 + i;
+        if (d < NUM_DESC) v |= (uint64_t)(1 + payload_bytes(d, 16)) << (5 * i);
+    }
+    return v;
+}
+__device__ __forceinline__ uint32_t node_bytes16(int d) {
+    constexpr uint64_t W0 = nb16_word(0), W1 = nb16_word(1), W2 = nb16_word(2);
+    const uint64_t w = d < 12 ? W0 : d < 24 ? W1 : W2;
+    const int i = d < 12 ? d : d < 24 ? d - 12 : d - 24;
+    return (uint32_t)(w >> (5 * i)) & 31u;
+}
+
 // Serial index of image (s, t)'s level-l ancestor (container.py:122-145).
 __device__ __forceinline__ int chain_node(const rlfc_field& f, int l, int s, int t) {
     return f.level_base[l] + (t >> l) * f.level_sx[l] + (s >> l);
@@ -219,14 +237,15 @@ __device__ int walk_chain(const rlfc_field& f, const uint8_t* rec, int s, int t,
             if (cursor >= avail) return WALK_OOB;
             int desc = rec[cursor];
             if (desc >= NUM_DESC) return 2;
-            if (cursor + nb.v[desc] > avail) return WALK_OOB;
+            const uint32_t nbytes = BSQ == 16 ? node_bytes16(desc) : (uint32_t)nb.v[desc];
+            if (cursor + nbytes > avail) return WALK_OOB;
             if (target == node) {
                 int st = decode_payload_acc<BSQ, GEN>(rec + cursor + 1, desc, f.quant_shift, acc, lut);
                 if (st) return st;
                 if (++ti == nt) return 0;
                 target = chain_node(f, h - 1 - ti, s, t);
             }
-            cursor += nb.v[desc];
+            cursor += nbytes;
         }
     }
     return 0;

@@ -267,24 +267,6 @@ __global__ void __launch_bounds__(256) k_scan_apply(uint32_t* v, int64_t n, cons
     }
 }
 
-// Node size (descriptor + payload bytes) for B*B = 16 values from three
-// 64-bit immediates (5 bits per descriptor): no memory access in the walk's
-// dependent chain.
-constexpr uint64_t nb16_word(int w) {
-    uint64_t v = 0;
-    for (int i = 0; i < 12; ++i) {
-        const int d = w * 12 + i;
-        if (d < NUM_DESC) v |= (uint64_t)(1 + payload_bytes(d, 16)) << (5 * i);
-    }
-    return v;
-}
-__device__ __forceinline__ uint32_t node_bytes16(int d) {
-    constexpr uint64_t W0 = nb16_word(0), W1 = nb16_word(1), W2 = nb16_word(2);
-    const uint64_t w = d < 12 ? W0 : d < 24 ? W1 : W2;
-    const int i = d < 12 ? d : d < 24 ? d - 12 : d - 24;
-    return (uint32_t)(w >> (5 * i)) & 31u;
-}
-
 // ---- pass 1: index -----------------------------------------------------------------
 // Records whose bitmap fits IDX_MAXW - 4 aligned words (bitmap_bytes <= 64,
 // e.g. M = 395 -> 50 bytes) load it once with aligned 16-byte loads, all in
