@@ -743,6 +743,19 @@ def decode_block_traced(state: DecoderState, image_index, block_index,
     return block, ranges
 
 
+def _to_host(t):
+    """Device tensor -> numpy through pinned memory (torch's caching host
+    allocator): the copy runs at PCIe speed instead of through the driver's
+    pageable staging, and the returned array owns the pinned block."""
+    torch = _torch()
+    if t.numel() * t.element_size() > (256 << 20):
+        return t.cpu().numpy()                 # big results: no pinned-cache growth
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
+
+
 def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
     """One image channel plane at padded dims, int32 (decoder.py:165-184)."""
     _check_indices(state, s, t)
@@ -756,7 +769,7 @@ def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
     if stop_level == state.header.tree_height:
         h = state.header.tree_height
         return state.root_planes[s >> h, t >> h, channel].copy()
-    return decode_planes(state, [(s, t, channel)], stop_level)[0].cpu().numpy()
+    return _to_host(decode_planes(state, [(s, t, channel)], stop_level)[0])
 
 
 def decode_image(state: DecoderState, image_index, stop_level=0):
@@ -764,7 +777,7 @@ def decode_image(state: DecoderState, image_index, stop_level=0):
     s, t = image_index
     _check_indices(state, s, t)
     out, _ = decode_field(state, stop_level, images=[(s, t)])
-    return out[0].cpu().numpy()
+    return _to_host(out[0])
 
 
 def decode_all(state: DecoderState, stop_level=0) -> LightFieldGrid:

@@ -459,5 +459,5 @@ def render_view(state, pose, stop_level=0, geometry: PlaneGeometry = None,
     """Render one view as uint8 RGB (reference renderer.py:279-305)."""
     if not isinstance(pose, (SlabPose, CameraPose)):
         raise TypeError(f"unknown pose type {type(pose).__name__}")
-    return render_views(state, [pose], stop_level, geometry,
-                        background)[0].cpu().numpy()
+    return decoder._to_host(render_views(state, [pose], stop_level, geometry,
+                                         background)[0])
