@@ -113,11 +113,27 @@ int rlfc_decode_block_sync(const rlfc_field *f, int32_t s, int32_t t,
  * request, or the server exited after idle_ns ns without work) and returns
  * once the result is complete in the mailbox, copied to out: out[0 .. B*B)
  * the block, out[B*B] the status (0 / 1 / 2, kernels.py:165-171).  The result
- * arrives as 16-byte chunks {3 values, request number}.  Out-of-range
+ * arrives as 16-byte chunks {3 values, request number}.  index (nullable) is
+ * used by servers launched while it is given.  Out-of-range
  * requests return RLFC_ERR_ARGUMENT.  rlfc_block_server_stop makes a running
  * server exit and waits for it (before the mailbox or the field is
  * released). */
 #define RLFC_MAILBOX_STOP 0xFFFFFFFFu
+/* Read-only view of a prepared record index (rlfc_staged_index_view): the
+ * bitmap words and word slot ranks ([nwp][nrec], word-major), the anomaly
+ * flags and the payload entries (payload offset, descriptor) of a workspace
+ * prepared by rlfc_staged_prepare.  The block server decodes a B = 4 request
+ * of an unflagged record from it (one lane per chain level) instead of
+ * walking the record. */
+typedef struct rlfc_index_view {
+    const uint32_t *bm, *rk, *rec_flag, *entries;
+    int64_t nrec;
+    int32_t nwp, _pad;
+    uint64_t cap;
+} rlfc_index_view;
+int rlfc_staged_index_view(const rlfc_field *f, void *workspace,
+                           uint64_t workspace_bytes, uint64_t present_total,
+                           rlfc_index_view *out);
 typedef struct rlfc_mailbox {
     uint32_t req_seq;      /* host: request number (written after req) */
     int32_t req[6];        /* s, t, bx, by, channel, stop_level */
@@ -128,7 +144,8 @@ typedef struct rlfc_mailbox {
 int rlfc_block_server_request(const rlfc_field *f, rlfc_mailbox *mb,
                               int32_t s, int32_t t, int32_t bx, int32_t by,
                               int32_t channel, int32_t stop_level,
-                              uint64_t idle_ns, int32_t *out, void *stream);
+                              uint64_t idle_ns, const rlfc_index_view *index,
+                              int32_t *out, void *stream);
 int rlfc_block_server_stop(rlfc_mailbox *mb, void *stream);
 
 /* Whole padded planes.  Replaces kernels.decode_plane_core

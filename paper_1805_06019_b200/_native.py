@@ -82,7 +82,8 @@ _SIGS = {
     "rlfc_decode_field_staged": ["p", "i", "p", "i", "i", "p", "q", "q", "p",
                                  "u", "u", "i", "p", "i", "p", "p"],
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
-    "rlfc_block_server_request": ["p", "p", "i", "i", "i", "i", "i", "i", "u", "p", "p"],
+    "rlfc_block_server_request": ["p", "p", "i", "i", "i", "i", "i", "i", "u", "p", "p", "p"],
+    "rlfc_staged_index_view": ["p", "p", "u", "u", "p"],
     "rlfc_block_server_stop": ["p", "p"],
     "rlfc_chain_core_sync": ["p", "u", "u", "i", "i", "p", "i", "i", "p", "p"],
     "rlfc_chain_core": ["p", "u", "p", "i", "i", "i", "p", "i", "i", "p", "p",
@@ -109,6 +110,14 @@ _SIGS = {
     "rlfc_root_planes": ["p", "i", "i", "i", "i", "i", "i", "p", "p", "p"],
     "rlfc_version": ["p", "i"],
 }
+class IndexView(ctypes.Structure):
+    """rlfc_index_view (include/rlfc_b200.h)."""
+    _fields_ = [("bm", ctypes.c_void_p), ("rk", ctypes.c_void_p),
+                ("rec_flag", ctypes.c_void_p), ("entries", ctypes.c_void_p),
+                ("nrec", ctypes.c_int64), ("nwp", ctypes.c_int32),
+                ("_pad", ctypes.c_int32), ("cap", ctypes.c_uint64)]
+
+
 _CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64,
        "u": ctypes.c_uint64}
 EXPORTS = tuple(_SIGS)

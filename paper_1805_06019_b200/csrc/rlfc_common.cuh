@@ -194,6 +194,59 @@ __device__ __forceinline__ uint32_t node_bytes16(int d) {
     return (uint32_t)(w >> (5 * i)) & 31u;
 }
 
+// ---- closed-form BISE windows (B = 4, 16 values) -------------------------------------
+// kernels.py:202-211 dequantisation in 32-bit wrap arithmetic: identical to
+// the reference's int64 result truncated into its int32 accumulator.
+__device__ __forceinline__ int32_t deq(uint32_t z, int shift) {
+    if (shift >= 32) return dequant(z, shift);
+    const uint32_t mag = (((z + 1u) >> 1) << shift) + ((1u << shift) >> 1);
+    const uint32_t v = (z & 1u) ? 0u - mag : mag;
+    return z ? (int32_t)v : 0;
+}
+
+// 64 bits of the aligned words sw from bit pos (generic: shared or global).
+__device__ __forceinline__ uint64_t win64(const uint32_t* sw, uint32_t pos) {
+    const uint32_t wi = pos >> 5, o = pos & 31u;
+    const uint32_t a = sw[wi], b = sw[wi + 1], c = sw[wi + 2];
+    return (uint64_t)__funnelshift_r(a, b, o) | (uint64_t)__funnelshift_r(b, c, o) << 32;
+}
+
+// decode16 for one request (k_blocks_indexed, k_block_server): the windows read straight
+// from the SRV words in memory, digits from the global LUT, dequantisation
+// by arithmetic, accumulated into acc (kernels.py:128-159, 202-211).
+template <int MODE>
+__device__ __forceinline__ bool decode16_acc(const uint32_t* sw, uint32_t bit0, uint32_t b, const uint16_t* dlut,
+                                             int shift, int32_t* acc) {
+    const uint32_t lm = (1u << b) - 1u;
+    bool bad = false;
+    if (MODE == MODE_BITS) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint64_t w = win64(sw, bit0 + 4u * (uint32_t)q * b);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[4 * q + i] += deq((uint32_t)(w >> ((uint32_t)i * b)) & lm, shift);
+        }
+    } else {
+        constexpr int G = MODE == MODE_TRIT ? 5 : 3, PB = MODE == MODE_TRIT ? 8 : 7;
+        constexpr uint32_t DB = MODE == MODE_TRIT ? 2u : 3u, DMASK = MODE == MODE_TRIT ? 3u : 7u;
+        constexpr uint32_t PMAX = MODE == MODE_TRIT ? 242u : 124u;
+        const uint32_t gbits = PB + G * b;
+#pragma unroll
+        for (int g = 0; g * G < 16; ++g) {
+            const uint64_t w = win64(sw, bit0 + (uint32_t)g * gbits);
+            const uint32_t pk = (uint32_t)w & ((1u << PB) - 1u);
+            bad |= pk > PMAX;
+            const uint32_t dg = __ldg(dlut + (pk <= PMAX ? pk : 0u));
+#pragma unroll
+            for (int i = 0; i < G && g * G + i < 16; ++i) {
+                const uint32_t low = (uint32_t)(w >> (PB + (uint32_t)i * b)) & lm;
+                acc[g * G + i] += deq((((dg >> (DB * i)) & DMASK) << b) | low, shift);
+            }
+        }
+    }
+    return bad;
+}
+
 // Serial index of image (s, t)'s level-l ancestor (container.py:122-145).
 __device__ __forceinline__ int chain_node(const rlfc_field& f, int l, int s, int t) {
     return f.level_base[l] + (t >> l) * f.level_sx[l] + (s >> l);

@@ -16,6 +16,7 @@
 namespace rlfc {
 
 __constant__ DigitLut c_lut = make_digit_lut();
+__device__ const DigitLut g_lut_ix = make_digit_lut();     // global copy: read with ld.global.nc
 
 template <int B>
 __constant__ NodeBytes c_nb = make_node_bytes<B * B>();
@@ -141,8 +142,64 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// B = 4 request of an unflagged record from the prepared index: lane l
+// decodes the level-l chain payload (bitmap word + rank -> slot -> entry ->
+// closed-form BISE windows), the warp sums the levels, lane j adds root
+// sample j.  A record without an anomaly flag passed the prepare-time
+// validation decode, so the status is 0.
+__device__ __forceinline__ void decode_one_indexed4(const rlfc_field& f, const rlfc_index_view& ix, int s, int t,
+                                                    int bx, int by, int c, int k, int32_t* res_s) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t ri = (int64_t)c * nblk + (int64_t)by * f.wb + bx;
+    int32_t root = 0;
+    if (lane < 16) root = root_sample(f, s, t, c, by * 4 + lane / 4, bx * 4 + lane % 4);
+    int32_t acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0;
+    if (lane >= k && lane < f.tree_height) {
+        const int nd = chain_node(f, lane, s, t);
+        const uint32_t word = __ldg(ix.bm + (int64_t)(nd >> 5) * ix.nrec + ri);
+        const uint32_t rank = __ldg(ix.rk + (int64_t)(nd >> 5) * ix.nrec + ri);
+        const uint32_t bit = (uint32_t)nd & 31u;
+        if ((word >> bit) & 1u) {
+            const uint64_t slot = (uint64_t)rank + (uint64_t)__popc(word & ((1u << bit) - 1u));
+            if (slot < ix.cap) {
+                const uint32_t ex = __ldg(ix.entries + 2 * slot), ey = __ldg(ix.entries + 2 * slot + 1);
+                const uint32_t d = ey & 31u;
+                if (d < (uint32_t)NUM_DESC) {
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + ex);
+                    const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+                    const uint32_t bit0 = (uint32_t)(a & 3u) * 8u, b = (uint32_t)desc_bits((int)d);
+                    const int m = desc_mode((int)d);
+                    if (m == MODE_BITS) decode16_acc<MODE_BITS>(sw, bit0, b, nullptr, f.quant_shift, acc);
+                    else if (m == MODE_TRIT) decode16_acc<MODE_TRIT>(sw, bit0, b, g_lut_ix.trit, f.quant_shift, acc);
+                    else decode16_acc<MODE_QUINT>(sw, bit0, b, g_lut_ix.quint, f.quant_shift, acc);
+                }
+            }
+        }
+    }
+    // levels live in lanes 0..7: butterfly within each group of 8, then
+    // every lane takes lane 0's sums
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        int32_t v = acc[j];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        acc[j] = __shfl_sync(0xffffffffu, v, 0);
+    }
+    int32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) mine = lane == j ? acc[j] : mine;
+    if (lane < 16) res_s[lane] = root + mine;
+    if (lane == 16) res_s[16] = 0;
+    __syncwarp();
+}
+
 template <int B>
-__global__ void __launch_bounds__(32) k_block_server(const rlfc_field f, rlfc_mailbox* mb, uint64_t idle_ns) {
+__global__ void __launch_bounds__(32) k_block_server(const rlfc_field f, rlfc_mailbox* mb, uint64_t idle_ns,
+                                                     const rlfc_index_view ix) {
     __shared__ __align__(16) uint8_t rec_s[ONE_REC_CAP];
     __shared__ int32_t root_s[B * B];
     __shared__ __align__(16) int32_t res_s[B * B + 4];       // + status
@@ -175,8 +232,20 @@ __global__ void __launch_bounds__(32) k_block_server(const rlfc_field f, rlfc_ma
             continue;
         }
         if (seq == RLFC_MAILBOX_STOP) return;
-        decode_one_warp<B, true>(f, (int)w[1], (int)w[2], (int)w[3], (int)w[4], (int)w[5], (int)w[6], nullptr,
-                                 rec_s, root_s, res_s);
+        bool done = false;
+        if constexpr (B == 4) {
+            if (ix.bm) {
+                const int64_t ri = ((int64_t)w[5] * f.hb + (int64_t)w[4]) * f.wb + (int64_t)w[3];
+                if (!__ldg(ix.rec_flag + ri)) {
+                    decode_one_indexed4(f, ix, (int)w[1], (int)w[2], (int)w[3], (int)w[4], (int)w[5], (int)w[6],
+                                        res_s);
+                    done = true;
+                }
+            }
+        }
+        if (!done)
+            decode_one_warp<B, true>(f, (int)w[1], (int)w[2], (int)w[3], (int)w[4], (int)w[5], (int)w[6], nullptr,
+                                     rec_s, root_s, res_s);
         for (int q = lane; q < NCH; q += 32) {
             const int j = 3 * q;
             const uint32_t x = (uint32_t)res_s[j];
@@ -391,7 +460,7 @@ extern "C" int rlfc_decode_block_sync(const rlfc_field* f, int32_t s, int32_t t,
 
 extern "C" int rlfc_block_server_request(const rlfc_field* f, rlfc_mailbox* mb, int32_t s, int32_t t, int32_t bx,
                                          int32_t by, int32_t c, int32_t stop_level, uint64_t idle_ns,
-                                         int32_t* out, void* stream) {
+                                         const rlfc_index_view* index, int32_t* out, void* stream) {
     if (!valid_field(f) || !mb || !out) return RLFC_ERR_ARGUMENT;
     if (s < 0 || s >= f->s_count || t < 0 || t >= f->t_count || bx < 0 || bx >= f->wb || by < 0 ||
         by >= f->hb || c < 0 || c > 2 || stop_level < 0 || stop_level > f->tree_height)
@@ -421,7 +490,9 @@ extern "C" int rlfc_block_server_request(const rlfc_field* f, rlfc_mailbox* mb, 
             const cudaError_t q = cudaStreamQuery(st);
             if (q == cudaSuccess) {
                 if (complete()) break;
-                RLFC_DISPATCH_B(f->block, k_block_server<BB><<<1, 32, 0, st>>>(*f, mb, idle_ns));
+                rlfc_index_view ix{};
+                if (index) ix = *index;
+                RLFC_DISPATCH_B(f->block, k_block_server<BB><<<1, 32, 0, st>>>(*f, mb, idle_ns, ix));
                 if (cudaGetLastError() != cudaSuccess) return RLFC_ERR_CUDA;
             } else if (q != cudaErrorNotReady) {
                 return RLFC_ERR_CUDA;

@@ -482,15 +482,6 @@ struct BitReader {
     }
 };
 
-// kernels.py:202-211 dequantisation in 32-bit wrap arithmetic: identical to
-// the reference's int64 result truncated into its int32 accumulator.
-__device__ __forceinline__ int32_t deq(uint32_t z, int shift) {
-    if (shift >= 32) return dequant(z, shift);
-    const uint32_t mag = (((z + 1u) >> 1) << shift) + ((1u << shift) >> 1);
-    const uint32_t v = (z & 1u) ? 0u - mag : mag;
-    return z ? (int32_t)v : 0;
-}
-
 template <typename VT>
 __device__ __forceinline__ void store4(VT* p, const int32_t* v);
 template <>
@@ -580,11 +571,6 @@ __device__ __forceinline__ bool decode_payload(const uint8_t* p, const uint16_t*
 // 64-bit window at its closed-form bit offset (every group but the last is
 // full), so all reads of a payload are independent;
 // dequantisation is a table lookup (z < 2048 for every descriptor).
-__device__ __forceinline__ uint64_t win64(const uint32_t* sw, uint32_t pos) {
-    const uint32_t wi = pos >> 5, o = pos & 31u;
-    const uint32_t a = sw[wi], b = sw[wi + 1], c = sw[wi + 2];
-    return (uint64_t)__funnelshift_r(a, b, o) | (uint64_t)__funnelshift_r(b, c, o) << 32;
-}
 
 // 16-byte store with an L2 eviction-priority policy (createpolicy)
 __device__ __forceinline__ void st16_hint(void* p, uint32_t x, uint32_t y, uint32_t z, uint32_t w, uint64_t pol) {
@@ -637,42 +623,6 @@ __device__ __forceinline__ bool decode16(const uint32_t* sw, uint32_t bit0, uint
     } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) store4<VT>(out + 4 * q, v + 4 * q);
-    }
-    return bad;
-}
-
-// decode16 for one request (k_blocks_indexed): the windows read straight
-// from the SRV words in memory, digits from the global LUT, dequantisation
-// by arithmetic, accumulated into acc (kernels.py:128-159, 202-211).
-template <int MODE>
-__device__ __forceinline__ bool decode16_acc(const uint32_t* sw, uint32_t bit0, uint32_t b, const uint16_t* dlut,
-                                             int shift, int32_t* acc) {
-    const uint32_t lm = (1u << b) - 1u;
-    bool bad = false;
-    if (MODE == MODE_BITS) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint64_t w = win64(sw, bit0 + 4u * (uint32_t)q * b);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[4 * q + i] += deq((uint32_t)(w >> ((uint32_t)i * b)) & lm, shift);
-        }
-    } else {
-        constexpr int G = MODE == MODE_TRIT ? 5 : 3, PB = MODE == MODE_TRIT ? 8 : 7;
-        constexpr uint32_t DB = MODE == MODE_TRIT ? 2u : 3u, DMASK = MODE == MODE_TRIT ? 3u : 7u;
-        constexpr uint32_t PMAX = MODE == MODE_TRIT ? 242u : 124u;
-        const uint32_t gbits = PB + G * b;
-#pragma unroll
-        for (int g = 0; g * G < 16; ++g) {
-            const uint64_t w = win64(sw, bit0 + (uint32_t)g * gbits);
-            const uint32_t pk = (uint32_t)w & ((1u << PB) - 1u);
-            bad |= pk > PMAX;
-            const uint32_t dg = __ldg(dlut + (pk <= PMAX ? pk : 0u));
-#pragma unroll
-            for (int i = 0; i < G && g * G + i < 16; ++i) {
-                const uint32_t low = (uint32_t)(w >> (PB + (uint32_t)i * b)) & lm;
-                acc[g * G + i] += deq((((dg >> (DB * i)) & DMASK) << b) | low, shift);
-            }
-        }
     }
     return bad;
 }
@@ -2156,6 +2106,23 @@ extern "C" int rlfc_staged_prepare(const rlfc_field* f, void* workspace, uint64_
     if (cudaStreamSynchronize(s) != cudaSuccess) return RLFC_ERR_CUDA;
     if (n_flagged) *n_flagged = (int32_t)nf;
     return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
+extern "C" int rlfc_staged_index_view(const rlfc_field* f, void* workspace, uint64_t workspace_bytes,
+                                      uint64_t present_total, rlfc_index_view* out) {
+    if (!f || !workspace || !out) return RLFC_ERR_ARGUMENT;
+    if (!staged::in_envelope(*f)) return RLFC_ERR_ARGUMENT;
+    staged::Ws w;
+    if (staged::carve(*f, workspace, present_total, &w) > workspace_bytes) return RLFC_ERR_ARGUMENT;
+    out->bm = w.bm;
+    out->rk = w.rk;
+    out->rec_flag = w.rec_flag;
+    out->entries = reinterpret_cast<const uint32_t*>(w.entries);
+    out->nrec = 3ll * f->wb * f->hb;
+    out->nwp = w.nwp;
+    out->_pad = 0;
+    out->cap = w.cap;
+    return RLFC_OK;
 }
 
 extern "C" int rlfc_decode_blocks_indexed(const rlfc_field* f, void* workspace, uint64_t workspace_bytes,

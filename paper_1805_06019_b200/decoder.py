@@ -657,6 +657,28 @@ class _BlockScratch:
         L = _native.lib()
         self.args = (df.ref, self.mailbox.data_ptr(), self.stream.cuda_stream)
         self.out_ptr = self.out_np.ctypes.data
+        # the prepared record index of the field (any workspace: its index
+        # part is read-only after prepare): B = 4 requests skip the record
+        # walk (one lane per chain level)
+        self.index = None
+        if b == 4:
+            with df._ws_lock:
+                have = next(iter(df._ws.values()), None)
+            ws = None
+            if have is not None:
+                ws = (have[0], df._ws_bytes, df._present)
+            else:
+                got = df.staged_workspace(torch.cuda.current_stream(df.device).cuda_stream)
+                if got is not None:
+                    ws = got[:3]
+                    torch.cuda.current_stream(df.device).synchronize()
+            if ws is not None:
+                view = _native.IndexView()
+                if L.rlfc_staged_index_view(df.ref, ws[0].data_ptr(), ws[1], ws[2],
+                                            ctypes.byref(view)) == _native.RLFC_OK:
+                    self.index = view
+                    self._ws_ref = ws[0]
+        self.index_ptr = ctypes.addressof(self.index) if self.index is not None else None
         self.fn = L.rlfc_block_server_request
         # the server must be gone before the mailbox (or the field) is reused
         weakref.finalize(self, _stop_server, L.rlfc_block_server_stop,
@@ -691,7 +713,7 @@ def decode_block_progressive(state: DecoderState, image_index, block_index,
     sc = _block_scratch(state)
     ref, mb, stream = sc.args
     rc = sc.fn(ref, mb, s, t, bx, by, channel, stop_level,
-               BLOCK_SERVER_IDLE_NS, sc.out_ptr, stream)
+               BLOCK_SERVER_IDLE_NS, sc.index_ptr, sc.out_ptr, stream)
     if rc:
         _native.check(rc, "rlfc_block_server_request")
     b = sc.b

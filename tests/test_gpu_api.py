@@ -354,22 +354,24 @@ def test_gpu_root_decode_large_and_init_time(rl):
     print(f"cfg2 init {dt * 1e3:.1f} ms")
 
 
-def _server_request(rl, st, mb, stream, req, idle_ns):
+def _server_request(rl, st, mb, stream, req, idle_ns, index=None):
     from paper_1805_06019_b200 import _native
     df = st.device_field()
     b = st.header.block_size
     out = np.zeros(b * b + 1, dtype=np.int32)
-    rc = _native.lib().rlfc_block_server_request(df.ref, mb.data_ptr(), *req, idle_ns, out.ctypes.data,
+    rc = _native.lib().rlfc_block_server_request(df.ref, mb.data_ptr(), *req, idle_ns, index, out.ctypes.data,
                                                  stream.cuda_stream)
     assert rc == 0
     return out[:b * b].copy(), int(out[b * b])
 
 
-@pytest.mark.parametrize("name", ["mid17_r4", "b8_h2", "b16_h4", "mid17_dense", "alldesc_b4"])
+@pytest.mark.parametrize("name", ["mid17_r4", "b8_h2", "b16_h4", "mid17_dense", "alldesc_b4", "grid32"])
 def test_block_server_matches_launch_path(rl, name):
     """The resident server (rlfc_block_server_request) returns the same block
-    and status as a kernel launch per request (rlfc_decode_block_sync), across
-    idle exits and restarts, and stops cleanly."""
+    and status as a kernel launch per request (rlfc_decode_block_sync), with
+    the record walk and (B = 4) with the prepared index, across idle exits
+    and restarts, and stops cleanly."""
+    import ctypes
     import time
     from paper_1805_06019_b200 import _native, decoder
     st = rl.init(load_stream(name))
@@ -378,29 +380,38 @@ def test_block_server_matches_launch_path(rl, name):
     b = hdr.block_size
     wb, hb = hdr.block_grid
     L = _native.lib()
-    mb = torch.zeros(decoder.MAILBOX_BYTES, dtype=torch.uint8).pin_memory()
-    stream = torch.cuda.Stream()
+    modes = [None]
+    if b == 4:
+        ws = df.staged_workspace(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        view = _native.IndexView()
+        assert L.rlfc_staged_index_view(df.ref, ws[0].data_ptr(), ws[1], ws[2], ctypes.byref(view)) == 0
+        modes.append(ctypes.addressof(view))
     host = torch.empty(b * b + 1, dtype=torch.int32).pin_memory()
-    rng = np.random.default_rng(41)
-    for i in range(300):
-        req = (int(rng.integers(0, hdr.s_count)), int(rng.integers(0, hdr.t_count)), int(rng.integers(0, wb)),
-               int(rng.integers(0, hb)), int(rng.integers(0, 3)), int(rng.integers(0, hdr.tree_height + 1)))
-        # a short idle timeout so some requests find the server gone
-        got, code = _server_request(rl, st, mb, stream, req, 20_000 if i % 7 else 1_000_000)
-        if i % 50 == 0:
-            time.sleep(0.002)
-        assert L.rlfc_decode_block_sync(df.ref, *req, None, host.data_ptr(), stream.cuda_stream) in (0,)
-        want = host.numpy()
-        assert code == int(want[b * b])
-        assert np.array_equal(got, want[:b * b]), req
-        assert np.array_equal(got.reshape(b, b), rl.decode_block_progressive(st, req[:2], req[2:4], req[4], req[5]))
-    assert L.rlfc_block_server_stop(mb.data_ptr(), stream.cuda_stream) == 0
-    stream.synchronize()
-    # a request after a stop starts a new server
-    got, code = _server_request(rl, st, mb, stream, (0, 0, 0, 0, 0, 0), 1_000_000)
-    assert code == 0 and np.array_equal(got.reshape(b, b), rl.decode_block(st, (0, 0), (0, 0), 0))
-    assert L.rlfc_block_server_stop(mb.data_ptr(), stream.cuda_stream) == 0
-    assert L.rlfc_block_server_request(df.ref, mb.data_ptr(), hdr.s_count, 0, 0, 0, 0, 0, 1000, host.data_ptr(),
+    for index in modes:
+        mb = torch.zeros(decoder.MAILBOX_BYTES, dtype=torch.uint8).pin_memory()
+        stream = torch.cuda.Stream()
+        rng = np.random.default_rng(41)
+        for i in range(300):
+            req = (int(rng.integers(0, hdr.s_count)), int(rng.integers(0, hdr.t_count)), int(rng.integers(0, wb)),
+                   int(rng.integers(0, hb)), int(rng.integers(0, 3)), int(rng.integers(0, hdr.tree_height + 1)))
+            # a short idle timeout so some requests find the server gone
+            got, code = _server_request(rl, st, mb, stream, req, 20_000 if i % 7 else 1_000_000, index)
+            if i % 50 == 0:
+                time.sleep(0.002)
+            assert L.rlfc_decode_block_sync(df.ref, *req, None, host.data_ptr(), stream.cuda_stream) in (0,)
+            want = host.numpy()
+            assert code == int(want[b * b]), (index, req)
+            assert np.array_equal(got, want[:b * b]), (index, req)
+            assert np.array_equal(got.reshape(b, b),
+                                  rl.decode_block_progressive(st, req[:2], req[2:4], req[4], req[5]))
+        assert L.rlfc_block_server_stop(mb.data_ptr(), stream.cuda_stream) == 0
+        stream.synchronize()
+        # a request after a stop starts a new server
+        got, code = _server_request(rl, st, mb, stream, (0, 0, 0, 0, 0, 0), 1_000_000, index)
+        assert code == 0 and np.array_equal(got.reshape(b, b), rl.decode_block(st, (0, 0), (0, 0), 0))
+        assert L.rlfc_block_server_stop(mb.data_ptr(), stream.cuda_stream) == 0
+    assert L.rlfc_block_server_request(df.ref, mb.data_ptr(), hdr.s_count, 0, 0, 0, 0, 0, 1000, None, host.data_ptr(),
                                        stream.cuda_stream) == _native.RLFC_ERR_ARGUMENT
 
 

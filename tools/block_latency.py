@@ -36,14 +36,14 @@ idle = decoder.BLOCK_SERVER_IDLE_NS
 op = sc.out_ptr
 t0 = time.perf_counter()
 for s, t, bx, by, c in picks:
-    sc.fn(ref, mb, s, t, bx, by, c, 0, idle, op, stream)
+    sc.fn(ref, mb, s, t, bx, by, c, 0, idle, sc.index_ptr, op, stream)
 dt2 = (time.perf_counter() - t0) / len(picks)
 print(f"native rlfc_block_server_request alone {dt2 * 1e6:.2f} us")
 # the same block over and over (record and roots L2-resident)
 s, t, bx, by, c = picks[0]
 t0 = time.perf_counter()
 for _ in range(len(picks)):
-    sc.fn(ref, mb, s, t, bx, by, c, 0, idle, op, stream)
+    sc.fn(ref, mb, s, t, bx, by, c, 0, idle, sc.index_ptr, op, stream)
 dt3 = (time.perf_counter() - t0) / len(picks)
 print(f"native call, one block repeated (L2-warm) {dt3 * 1e6:.2f} us")
 # one launch per request (rlfc_decode_block_sync: kernel + polled status)
