@@ -147,6 +147,19 @@ int rlfc_block_server_request(const rlfc_field *f, rlfc_mailbox *mb,
                               uint64_t idle_ns, const rlfc_index_view *index,
                               int32_t *out, void *stream);
 int rlfc_block_server_stop(rlfc_mailbox *mb, void *stream);
+/* rlfc_block_server_request with its arguments in one caller-owned struct
+ * (the host fills req per call): one pointer crosses the FFI boundary. */
+typedef struct rlfc_block_call {
+    const rlfc_field *f;
+    rlfc_mailbox *mb;
+    const rlfc_index_view *index;
+    void *stream;
+    uint64_t idle_ns;
+    int32_t *out;
+    int32_t req[6]; /* s, t, bx, by, channel, stop_level */
+    int32_t _pad[2];
+} rlfc_block_call;
+int rlfc_block_server_call(const rlfc_block_call *call);
 
 /* Whole padded planes.  Replaces kernels.decode_plane_core
  * (kernels.py:219-242) as called by decoder.decode_plane (decoder.py:165-184).

@@ -84,6 +84,7 @@ _SIGS = {
     "rlfc_bise_decode": ["p", "p", "p", "i", "i", "p", "p", "p"],
     "rlfc_block_server_request": ["p", "p", "i", "i", "i", "i", "i", "i", "u", "p", "p", "p"],
     "rlfc_staged_index_view": ["p", "p", "u", "u", "p"],
+    "rlfc_block_server_call": ["p"],
     "rlfc_block_server_stop": ["p", "p"],
     "rlfc_chain_core_sync": ["p", "u", "u", "i", "i", "p", "i", "i", "p", "p"],
     "rlfc_chain_core": ["p", "u", "p", "i", "i", "i", "p", "i", "i", "p", "p",
@@ -116,6 +117,13 @@ class IndexView(ctypes.Structure):
                 ("rec_flag", ctypes.c_void_p), ("entries", ctypes.c_void_p),
                 ("nrec", ctypes.c_int64), ("nwp", ctypes.c_int32),
                 ("_pad", ctypes.c_int32), ("cap", ctypes.c_uint64)]
+
+
+class BlockCall(ctypes.Structure):
+    """rlfc_block_call (include/rlfc_b200.h)."""
+    _fields_ = [("f", ctypes.c_void_p), ("mb", ctypes.c_void_p), ("index", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p), ("idle_ns", ctypes.c_uint64), ("out", ctypes.c_void_p),
+                ("req", ctypes.c_int32 * 6), ("_pad", ctypes.c_int32 * 2)]
 
 
 _CT = {"p": ctypes.c_void_p, "i": ctypes.c_int32, "q": ctypes.c_int64,

@@ -504,6 +504,13 @@ extern "C" int rlfc_block_server_request(const rlfc_field* f, rlfc_mailbox* mb, 
     return RLFC_OK;
 }
 
+extern "C" int rlfc_block_server_call(const rlfc_block_call* call) {
+    if (!call) return RLFC_ERR_ARGUMENT;
+    return rlfc_block_server_request(call->f, call->mb, call->req[0], call->req[1], call->req[2], call->req[3],
+                                     call->req[4], call->req[5], call->idle_ns, call->index, call->out,
+                                     call->stream);
+}
+
 extern "C" int rlfc_block_server_stop(rlfc_mailbox* mb, void* stream) {
     if (!mb) return RLFC_ERR_ARGUMENT;
     volatile rlfc_mailbox* v = mb;

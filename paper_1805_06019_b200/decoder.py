@@ -17,6 +17,7 @@ functions raise `_native.NativeUnavailable`.
 """
 
 import ctypes
+import struct
 import threading
 import weakref
 import time
@@ -633,6 +634,8 @@ def bise_decode_batch(payloads, descs, count, device=None):
 # --- reference-signature API ---------------------------------------------------
 
 MAILBOX_BYTES = 64 + 16 * 88                  # rlfc_mailbox (include/rlfc_b200.h)
+_REQ = struct.Struct("<6i")                    # rlfc_block_call.req
+_REQ_OFF = 48
 BLOCK_SERVER_IDLE_NS = 1_000_000              # resident server exits after 1 ms idle
 
 
@@ -679,6 +682,14 @@ class _BlockScratch:
                     self.index = view
                     self._ws_ref = ws[0]
         self.index_ptr = ctypes.addressof(self.index) if self.index is not None else None
+        # the whole call in one struct: per request only req changes
+        self.call = _native.BlockCall(ctypes.addressof(df.cfield), self.mailbox.data_ptr(), self.index_ptr,
+                                      self.stream.cuda_stream, BLOCK_SERVER_IDLE_NS, self.out_ptr)
+        self.call_ptr = ctypes.addressof(self.call)
+        hdr = df.header
+        self.dims = (hdr.s_count, hdr.t_count) + tuple(hdr.block_grid) + (hdr.tree_height,)
+        self.bsq = b * b
+        self.call_fn = L.rlfc_block_server_call
         self.fn = L.rlfc_block_server_request
         # the server must be gone before the mailbox (or the field) is reused
         weakref.finalize(self, _stop_server, L.rlfc_block_server_stop,
@@ -702,24 +713,28 @@ def decode_block_progressive(state: DecoderState, image_index, block_index,
     """One B x B block summing SRV levels >= stop_level (decoder.py:81-106)."""
     s, t = image_index
     bx, by = block_index
-    _check_indices(state, s, t, bx, by)
-    _check_level(state, stop_level)
+    sc = _block_scratch(state)
+    S, T, wb, hb, h = sc.dims
+    if not (0 <= s < S and 0 <= t < T):
+        _check_indices(state, s, t, bx, by)
+    if not (0 <= bx < wb and 0 <= by < hb):
+        _check_indices(state, s, t, bx, by)
+    if not 0 <= stop_level <= h:
+        _check_level(state, stop_level)
     # the reference indexes root_planes[..., channel] and srv[channel]
     # (decoder.py:73-78, 99-101): Python indexing, so -3..-1 alias 0..2
     if not -3 <= channel < 3:
         raise IndexError(f"index {channel} is out of bounds for axis 2 with "
                          "size 3")
-    channel = int(channel) % 3
-    sc = _block_scratch(state)
-    ref, mb, stream = sc.args
-    rc = sc.fn(ref, mb, s, t, bx, by, channel, stop_level,
-               BLOCK_SERVER_IDLE_NS, sc.index_ptr, sc.out_ptr, stream)
+    _REQ.pack_into(sc.call, _REQ_OFF, s, t, bx, by, int(channel) % 3, stop_level)
+    rc = sc.call_fn(sc.call_ptr)
     if rc:
         _native.check(rc, "rlfc_block_server_request")
-    b = sc.b
-    out = sc.out_np.copy()
-    _raise_status(int(out[b * b]))
-    return out[:b * b].reshape(b, b)
+    bsq = sc.bsq
+    code = int(sc.out_np[bsq])
+    if code:
+        _raise_status(code)
+    return sc.out_np[:bsq].reshape(sc.b, sc.b).copy()
 
 
 def decode_block(state: DecoderState, image_index, block_index, channel):
