@@ -351,7 +351,7 @@ def _png_idat(blob, width, height):
 
 
 def parse_roots_device(data, header: RlfcHeader, device, threads=None):
-    """Root planes decoded on the GPU (container.py:175-195 for PNG roots):
+    """Root planes decoded on the GPU (container.py:175-195; PNG and RAW roots):
     the host walks the sections and inflates each plane's IDAT stream on a
     thread pool; the PNG scanline filters are undone by rlfc_png_unfilter
     and the channel bias removed by rlfc_root_planes straight into the
@@ -363,12 +363,12 @@ def parse_roots_device(data, header: RlfcHeader, device, threads=None):
     from concurrent.futures import ThreadPoolExecutor
     import torch
     from . import _native
-    if header.root_codec_id != CODEC_PNG:
+    if header.root_codec_id not in (CODEC_PNG, CODEC_RAW):
         return None
     wp, hp = header.padded_dims
     rsx, rsy = level_dims(header.s_count, header.t_count, header.tree_height)
     starts, _ = section_offsets(header)
-    blobs = []
+    spans = []
     for c in range(3):
         pos = starts[c][0]
         end = pos + header.section_lengths[c][0]
@@ -378,10 +378,26 @@ def parse_roots_device(data, header: RlfcHeader, device, threads=None):
             (n,) = struct.unpack_from("<I", data, pos)
             if pos + 4 + n > end:
                 return None
-            blobs.append(bytes(data[pos + 4:pos + 4 + n]))
+            spans.append((pos + 4, n))
             pos += 4 + n
         if pos != end:
             return None
+    L = _native.lib()
+    dev = torch.device(device)
+    if header.root_codec_id == CODEC_RAW:
+        # little-endian 16-bit samples as stored (container.py:175-195): one
+        # pinned copy, one upload, the bias removed on the device
+        if any(n != wp * hp * 2 for _, n in spans):
+            return None                    # decode_root raises the reference's error
+        host = torch.empty((len(spans), hp * wp), dtype=torch.int16).pin_memory()
+        hv = host.numpy().view(np.uint8).reshape(len(spans), -1)
+        mv = memoryview(data)
+        for i, (a, n) in enumerate(spans):
+            hv[i] = np.frombuffer(mv[a:a + n], dtype=np.uint8)
+        with torch.cuda.device(dev):
+            samples = host.to(dev, non_blocking=True)
+        return _root_planes_device(L, samples, len(spans), rsx, rsy, hp, wp, dev)
+    blobs = [bytes(data[a:a + n]) for a, n in spans]
     stride = hp * (1 + 2 * wp)
 
     def inflate(b):
@@ -399,8 +415,6 @@ def parse_roots_device(data, header: RlfcHeader, device, threads=None):
         raws = list(ex.map(inflate, blobs))
     if any(r is None for r in raws):
         return None
-    L = _native.lib()
-    dev = torch.device(device)
     host = torch.empty((len(raws), stride), dtype=torch.uint8).pin_memory()
     hv = host.numpy()
     for i, r in enumerate(raws):
@@ -412,16 +426,26 @@ def parse_roots_device(data, header: RlfcHeader, device, threads=None):
         bad = torch.zeros(1, dtype=torch.int32, device=dev)
         _native.check(L.rlfc_png_unfilter(raw_d.data_ptr(), stride, len(raws), wp, hp, samples.data_ptr(),
                                           hp * wp, bad.data_ptr(), stream), "rlfc_png_unfilter")
-        roots = torch.empty((rsx, rsy, 3, hp, wp), dtype=torch.int16, device=dev)
-        mm = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=dev)
-        _native.check(L.rlfc_root_planes(samples.data_ptr(), len(raws), rsx, rsy, hp, wp, 1, roots.data_ptr(),
-                                         mm.data_ptr(), stream), "rlfc_root_planes")
-        lo, hi = mm.cpu().tolist()
         if bad.item():
             return None
+    return _root_planes_device(L, samples, len(raws), rsx, rsy, hp, wp, dev)
+
+
+def _root_planes_device(L, samples, nplanes, rsx, rsy, hp, wp, dev):
+    """Bias removal + scatter into the (rsx, rsy, 3, Hp, Wp) root tensor
+    (rlfc_root_planes): int16 when every sample fits, else int32."""
+    import torch
+    from . import _native
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        roots = torch.empty((rsx, rsy, 3, hp, wp), dtype=torch.int16, device=dev)
+        mm = torch.tensor([1 << 30, -(1 << 30)], dtype=torch.int32, device=dev)
+        _native.check(L.rlfc_root_planes(samples.data_ptr(), nplanes, rsx, rsy, hp, wp, 1, roots.data_ptr(),
+                                         mm.data_ptr(), stream), "rlfc_root_planes")
+        lo, hi = mm.cpu().tolist()
         if lo < -32768 or hi > 32767:
             roots = torch.empty((rsx, rsy, 3, hp, wp), dtype=torch.int32, device=dev)
-            _native.check(L.rlfc_root_planes(samples.data_ptr(), len(raws), rsx, rsy, hp, wp, 0, roots.data_ptr(),
+            _native.check(L.rlfc_root_planes(samples.data_ptr(), nplanes, rsx, rsy, hp, wp, 0, roots.data_ptr(),
                                              None, stream), "rlfc_root_planes")
     return roots
 

@@ -312,20 +312,20 @@ def test_concurrent_decodes_on_one_stream(rl):
                 assert np.array_equal(out[i], full[s, t])
 
 
-@pytest.mark.parametrize("name", ["kat8_default", "mid17_r4", "cfg1_h3_r4", "mid17_dense", "alldesc_b4"])
+@pytest.mark.parametrize("name", ["kat8_default", "mid17_r4", "cfg1_h3_r4", "mid17_dense", "alldesc_b4",
+                                  "kat8_lossless", "b16_h4", "uniform_5x3"])
 def test_gpu_root_decode_matches_pillow(rl, name):
-    """PNG root views inflated on host threads and unfiltered on the GPU
-    (container.parse_roots_device) equal Pillow's planes (the reference's
-    decoder, container.py:175-195), bias removed; non-PNG or irregular
-    streams return None (Pillow path)."""
+    """Root views decoded on the GPU (container.parse_roots_device: PNG roots
+    inflated on host threads and unfiltered on the device, RAW roots uploaded
+    as stored) equal the host decode (Pillow / frombuffer, the reference's
+    container.py:175-195), bias removed; a RAW root of the wrong length
+    returns None (the host path then raises the reference's error)."""
     from paper_1805_06019_b200 import container
     data = load_stream(name)
     hdr = container.parse_header(data)
     want = container.parse_roots(data, hdr)
     got = container.parse_roots_device(data, hdr, "cuda")
-    if hdr.root_codec_id != container.CODEC_PNG:
-        assert got is None
-        return
+    assert got is not None
     assert np.array_equal(got.cpu().numpy().astype(np.int32), want)
     st = rl.init(data)
     assert np.array_equal(st.root_planes, want)
