@@ -669,6 +669,8 @@ def run_cfg5(args):
     import paper_1805_06019_b200 as rl
     from paper_1805_06019_b200 import decoder
     data = make_stream_cfg5()
+    torch.zeros(1, device="cuda")                   # CUDA context outside the init timing
+    torch.cuda.synchronize()
     t0 = time.time()
     state = rl.init(data)
     init_s = time.time() - t0
