@@ -17,6 +17,7 @@ functions raise `_native.NativeUnavailable`.
 """
 
 import ctypes
+import os
 import struct
 import threading
 import weakref
@@ -786,11 +787,70 @@ def _to_host(t):
     pageable staging, and the returned array owns the pinned block."""
     torch = _torch()
     if t.numel() * t.element_size() > (256 << 20):
-        return t.cpu().numpy()                 # big results: no pinned-cache growth
+        return _to_host_big(t)                 # big results: no pinned-cache growth
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     h.copy_(t, non_blocking=True)
     torch.cuda.current_stream(t.device).synchronize()
     return h.numpy()
+
+
+_BOUNCE = 64 << 20
+_bounce_tls = threading.local()
+
+
+def _to_host_big(t):
+    """Large device tensor -> fresh (pageable) numpy array: chunks go through
+    a ring of three pinned bounce buffers at PCIe speed while host threads
+    copy the previous chunk into place (page faults of the fresh array spread
+    over the threads).  A plain pageable .cpu() of cfg2's 909 MB field took
+    426 ms."""
+    from concurrent.futures import ThreadPoolExecutor
+    torch = _torch()
+    src = t.contiguous().view(torch.uint8).reshape(-1)
+    n = src.numel()
+    out = np.empty(n, dtype=np.uint8)
+    ring = getattr(_bounce_tls, "ring", None)
+    if ring is None:
+        ring = _bounce_tls.ring = [torch.empty(_BOUNCE, dtype=torch.uint8).pin_memory() for _ in range(3)]
+        _bounce_tls.pool = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+    pool = _bounce_tls.pool
+    stream = torch.cuda.Stream(device=t.device)
+    stream.wait_stream(torch.cuda.current_stream(t.device))
+    chunks = [(a, min(n, a + _BOUNCE)) for a in range(0, n, _BOUNCE)]
+    events = []
+    pending = []
+
+    def issue(i):
+        a, b = chunks[i]
+        with torch.cuda.stream(stream):
+            ring[i % 3][:b - a].copy_(src[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        events.append(ev)
+
+    def drain(i):
+        a, b = chunks[i]
+        events[i].synchronize()
+        buf = ring[i % 3].numpy()
+        parts = 8
+        step = -(-(b - a) // parts)
+        futs = [pool.submit(np.copyto, out[a + j:min(b, a + j + step)], buf[j:min(b - a, j + step)])
+                for j in range(0, b - a, step)]
+        return futs
+
+    for i in range(min(2, len(chunks))):
+        issue(i)
+    for i in range(len(chunks)):
+        futs = drain(i)
+        for f in pending:
+            f.result()
+        pending = futs
+        if i + 2 < len(chunks):
+            # ring slot (i + 2) % 3 was drained two steps ago (its copies done)
+            issue(i + 2)
+    for f in pending:
+        f.result()
+    return out.view(np.dtype(str(t.dtype).replace("torch.", ""))).reshape(tuple(t.shape))
 
 
 def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
@@ -822,7 +882,7 @@ def decode_all(state: DecoderState, stop_level=0) -> LightFieldGrid:
     hdr = state.header
     out, _ = decode_field(state, stop_level)
     return LightFieldGrid(hdr.s_count, hdr.t_count, hdr.width, hdr.height,
-                          out.cpu().numpy(),
+                          _to_host(out),
                           grid_positions(hdr.s_count, hdr.t_count),
                           default_geometry(hdr.s_count, hdr.t_count))
 

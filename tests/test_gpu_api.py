@@ -498,3 +498,16 @@ def test_slab_render_corrupt_tap_camera_raises(rl):
         rl.render_views(st, [rl.SlabPose(8.0, 8.0, 16, 16), rl.SlabPose(1.0, 2.0, 16, 16)])
     # the clean stream renders the same batch without error
     rl.render_views(rl.init(data), [rl.SlabPose(8.0, 8.0, 16, 16), rl.SlabPose(1.0, 2.0, 16, 16)])
+
+
+def test_large_results_reach_host_exactly(rl):
+    """Results over 256 MB come back through the pinned bounce ring
+    (decoder._to_host_big): byte-identical, shape and dtype kept, for
+    sizes that are not a multiple of the 64 MB chunk."""
+    from paper_1805_06019_b200 import decoder
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for shape, dtype in (((300 << 20) + 12345,), torch.uint8), (((70 << 20) + 7, 2), torch.int32):
+        t = torch.randint(0, 255, shape, dtype=dtype, device="cuda", generator=g)
+        got = decoder._to_host(t)
+        assert got.shape == tuple(t.shape) and got.dtype == t.cpu().numpy().dtype
+        assert np.array_equal(got, t.cpu().numpy())
