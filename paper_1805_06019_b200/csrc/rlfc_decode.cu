@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <climits>
 
 #include "rlfc_common.cuh"
@@ -484,9 +485,14 @@ extern "C" int rlfc_block_server_request(const rlfc_field* f, rlfc_mailbox* mb, 
         return true;
     };
     // wait for every chunk to carry seq; whenever the stream is idle no
-    // server is running (it timed out, or never started): launch one
+    // server is running (it timed out, or never started): launch one.  A
+    // request unanswered for 30 s (a wedged device) returns an error
+    // instead of spinning forever.
+    const auto t_start = std::chrono::steady_clock::now();
     for (uint32_t i = 1; !complete(); ++i) {
         if ((i & 1023u) == 0) {
+            if ((i & 0xFFFFFu) == 0 && std::chrono::steady_clock::now() - t_start > std::chrono::seconds(30))
+                return RLFC_ERR_CUDA;
             const cudaError_t q = cudaStreamQuery(st);
             if (q == cudaSuccess) {
                 if (complete()) break;
