@@ -511,3 +511,43 @@ def test_large_results_reach_host_exactly(rl):
         got = decoder._to_host(t)
         assert got.shape == tuple(t.shape) and got.dtype == t.cpu().numpy().dtype
         assert np.array_equal(got, t.cpu().numpy())
+
+
+def test_mixed_concurrent_api_calls(rl):
+    """The service pattern (service.py:1-6): many threads calling
+    decode_block, decode_image, decode_plane and render_view on one shared
+    state at once return exactly the serial results (block servers, staged
+    workspaces and render staging are per thread / per stream)."""
+    st = rl.init(load_stream("mid17_r4"))
+    hdr = st.header
+    wb, hb = hdr.block_grid
+    rng = np.random.default_rng(77)
+    jobs = []
+    for i in range(160):
+        kind = i % 4
+        if kind == 0:
+            jobs.append(("block", (int(rng.integers(0, 17)), int(rng.integers(0, 17))),
+                         (int(rng.integers(0, wb)), int(rng.integers(0, hb))), int(rng.integers(0, 3)),
+                         int(rng.integers(0, hdr.tree_height + 1))))
+        elif kind == 1:
+            jobs.append(("image", (int(rng.integers(0, 17)), int(rng.integers(0, 17))), int(rng.integers(0, 4))))
+        elif kind == 2:
+            jobs.append(("plane", int(rng.integers(0, 17)), int(rng.integers(0, 17)), int(rng.integers(0, 3))))
+        else:
+            jobs.append(("view", float(rng.uniform(0, 16)), float(rng.uniform(0, 16)),
+                         [None, 0.9, 1.12][i % 3]))
+
+    def run(job):
+        if job[0] == "block":
+            return rl.decode_block_progressive(st, job[1], job[2], job[3], job[4])
+        if job[0] == "image":
+            return rl.decode_image(st, job[1], stop_level=job[2])
+        if job[0] == "plane":
+            return rl.decode_plane(st, job[1], job[2], job[3])
+        return rl.render_view(st, rl.SlabPose(job[1], job[2], 48, 40, focal_z=job[3]))
+
+    serial = [run(j) for j in jobs]
+    with cf.ThreadPoolExecutor(8) as ex:
+        par = list(ex.map(run, jobs))
+    for j, a, b in zip(jobs, serial, par):
+        assert np.array_equal(a, b), j
