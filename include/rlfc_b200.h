@@ -387,6 +387,21 @@ int rlfc_render_slab_batch(const rlfc_field *f, int32_t stop_level, void *ws,
                            void *stream);
 uint64_t rlfc_render_staging_bytes(const rlfc_field *f, int32_t n);
 
+/* One image in one call (decoder.decode_image, decoder.py:187-194): the
+ * slot table and camera row are staged in stage_host (pinned, at least
+ * 32 + 4*S*T bytes) and sent to stage_dev with one copy; the staged decode
+ * in slot mode (workspace as for rlfc_decode_field_staged, else the fused
+ * decode) fills rgb_dev (H*W*3), which is copied into rgb_host (pinned);
+ * returns after the stream drained, with the decode status word in
+ * *status_word. */
+int rlfc_decode_image_host(const rlfc_field *f, int32_t stop_level, void *ws,
+                           uint64_t ws_bytes, uint64_t present,
+                           int32_t n_flagged, int32_t s, int32_t t,
+                           uint8_t *rgb_dev, uint8_t *rgb_host,
+                           uint8_t *stage_host, uint8_t *stage_dev,
+                           uint64_t stage_bytes, uint64_t *status_word,
+                           void *stream);
+
 /* Pinhole-pose rendering (renderer.py:279-305 with ray_to_lf_coords
  * renderer.py:87-116 and sample_quadrilinear renderer.py:147-169).
  * frames: n x 14 doubles (eye[3], look[3], right[3], down[3], half, aspect)

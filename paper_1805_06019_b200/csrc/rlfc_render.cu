@@ -399,3 +399,44 @@ extern "C" uint64_t rlfc_render_staging_bytes(const rlfc_field* f, int32_t n) {
                    o_rows = al(o_slot + 4ull * f->s_count * f->t_count), o_bg = al(o_rows + 4ull * f->t_count);
     return al(o_bg + 3ull * n);
 }
+
+// ---- one image in one call (host runtime) ----------------------------------------------
+// decoder.decode_image (decoder.py:187-194) without Python in the loop: the
+// slot table (one view) and its camera row are staged with the status word
+// in one pinned buffer and sent with one copy; the staged decode in slot mode
+// (else the fused decode) fills rgb_dev, the image and the status come back
+// with two copies on the same stream, and the call returns after it drained.
+extern "C" int rlfc_decode_image_host(const rlfc_field* f, int32_t stop_level, void* ws, uint64_t ws_bytes,
+                                      uint64_t present, int32_t n_flagged, int32_t s, int32_t t, uint8_t* rgb_dev,
+                                      uint8_t* rgb_host, uint8_t* stage_host, uint8_t* stage_dev,
+                                      uint64_t stage_bytes, uint64_t* status_word, void* stream) {
+    if (!f || !rgb_dev || !rgb_host || !stage_host || !stage_dev || !status_word) return RLFC_ERR_ARGUMENT;
+    const int S = f->s_count, T = f->t_count, W = f->width, H = f->height;
+    if (s < 0 || s >= S || t < 0 || t >= T || stop_level < 0 || stop_level > f->tree_height) return RLFC_ERR_ARGUMENT;
+    const uint64_t o_slot = 16, o_rows = (o_slot + 4ull * S * T + 15) & ~15ull, total = o_rows + 16;
+    if (total > stage_bytes) return RLFC_ERR_ARGUMENT;
+    std::memset(stage_host, 0, 16);
+    int32_t* slots = reinterpret_cast<int32_t*>(stage_host + o_slot);
+    for (int i = 0; i < S * T; ++i) slots[i] = -1;
+    slots[s * T + t] = 0;
+    reinterpret_cast<int32_t*>(stage_host + o_rows)[0] = t;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(stage_dev, stage_host, total, cudaMemcpyHostToDevice, st) != cudaSuccess) return RLFC_ERR_CUDA;
+    uint64_t* dstat = reinterpret_cast<uint64_t*>(stage_dev);
+    const int32_t* dslots = reinterpret_cast<const int32_t*>(stage_dev + o_slot);
+    const int64_t img = (int64_t)H * W * 3;
+    int rc = RLFC_ERR_ARGUMENT;
+    if (ws)
+        rc = rlfc_decode_field_staged(f, stop_level, dslots, 0, f->hb, rgb_dev, img, (int64_t)W * 3, ws, ws_bytes,
+                                      present, n_flagged, reinterpret_cast<const int32_t*>(stage_dev + o_rows), 1,
+                                      dstat, stream);
+    if (rc == RLFC_ERR_ARGUMENT)
+        rc = rlfc_decode_field(f, stop_level, dslots, 0, f->hb, rgb_dev, img, (int64_t)W * 3, dstat, stream);
+    if (rc != RLFC_OK) return rc;
+    if (cudaMemcpyAsync(rgb_host, rgb_dev, img, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(stage_host, dstat, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return RLFC_ERR_CUDA;
+    std::memcpy(status_word, stage_host, 8);
+    return RLFC_OK;
+}

@@ -869,12 +869,45 @@ def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
     return _to_host(decode_planes(state, [(s, t, channel)], stop_level)[0])
 
 
+_img_tls = threading.local()
+
+
 def decode_image(state: DecoderState, image_index, stop_level=0):
-    """One camera image as true-dims RGB8 (decoder.py:187-194)."""
+    """One camera image as true-dims RGB8 (decoder.py:187-194): one native
+    call (rlfc_decode_image_host) stages the slot table, decodes and brings
+    the image back into a pinned array the result owns."""
+    torch = _torch()
     s, t = image_index
     _check_indices(state, s, t)
-    out, _ = decode_field(state, stop_level, images=[(s, t)])
-    return _to_host(out[0])
+    _check_level(state, stop_level)
+    hdr = state.header
+    df = state.device_field()
+    L = _native.lib()
+    key = df.device.index
+    bufs = getattr(_img_tls, "bufs", None)
+    if bufs is None:
+        bufs = _img_tls.bufs = {}
+    need = 32 + 4 * hdr.s_count * hdr.t_count
+    b = bufs.get(key)
+    if b is None or b[0].numel() < need:
+        cap = max(4096, 1 << (need - 1).bit_length())
+        b = bufs[key] = (torch.empty(cap, dtype=torch.uint8).pin_memory(),
+                         torch.empty(cap, dtype=torch.uint8, device=df.device),
+                         np.zeros(1, dtype=np.uint64))
+    host_stage, dev_stage, word = b
+    img = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, device=df.device)
+    res = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, pin_memory=True)
+    with torch.cuda.device(df.device):
+        stream = _stream()
+        ws = df.staged_workspace(stream)
+        args = (None, 0, 0, 0) if ws is None else (ws[0].data_ptr(), ws[1], ws[2], ws[3])
+        with df.enqueue_lock:
+            rc = L.rlfc_decode_image_host(df.ref, stop_level, *args, int(s), int(t), img.data_ptr(),
+                                          res.data_ptr(), host_stage.data_ptr(), dev_stage.data_ptr(),
+                                          host_stage.numel(), word.ctypes.data, stream)
+    _native.check(rc, "rlfc_decode_image_host")
+    _raise_word(int(word[0]))
+    return res.numpy()
 
 
 def decode_all(state: DecoderState, stop_level=0) -> LightFieldGrid:
