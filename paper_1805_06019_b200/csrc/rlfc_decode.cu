@@ -607,3 +607,34 @@ extern "C" int rlfc_version(char* buf, int32_t len) {
 
 static_assert(offsetof(rlfc_mailbox, out) == 64 && sizeof(rlfc_mailbox) == 64 + 16 * 88,
               "mailbox layout (decoder.MAILBOX_BYTES)");
+
+// One padded plane in one call (decoder.decode_plane, decoder.py:165-184):
+// the request and a zero status word go up in one copy, k_decode_planes
+// runs, the plane and the status come back, the call returns drained.
+extern "C" int rlfc_decode_plane_host(const rlfc_field* f, int32_t stop_level, int32_t s, int32_t t, int32_t c,
+                                      int32_t* plane_dev, int32_t* plane_host, uint8_t* stage_host,
+                                      uint8_t* stage_dev, uint64_t* status_word, void* stream) {
+    if (!valid_field(f) || !plane_dev || !plane_host || !stage_host || !stage_dev || !status_word)
+        return RLFC_ERR_ARGUMENT;
+    if (s < 0 || s >= f->s_count || t < 0 || t >= f->t_count || c < 0 || c > 2 || stop_level < 0 ||
+        stop_level > f->tree_height)
+        return RLFC_ERR_ARGUMENT;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(stage_host, 0, 32);
+    int32_t* req = reinterpret_cast<int32_t*>(stage_host + 16);
+    req[0] = s;
+    req[1] = t;
+    req[2] = c;
+    if (cudaMemcpyAsync(stage_dev, stage_host, 32, cudaMemcpyHostToDevice, st) != cudaSuccess) return RLFC_ERR_CUDA;
+    uint64_t* dstat = reinterpret_cast<uint64_t*>(stage_dev);
+    const int rc = rlfc_decode_planes(f, stop_level, reinterpret_cast<const int32_t*>(stage_dev + 16), 1, plane_dev,
+                                      dstat, stream);
+    if (rc != RLFC_OK) return rc;
+    if (cudaMemcpyAsync(plane_host, plane_dev, (size_t)f->hp * f->wp * 4, cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(stage_host, dstat, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return RLFC_ERR_CUDA;
+    std::memcpy(status_word, stage_host, 8);
+    return RLFC_OK;
+}

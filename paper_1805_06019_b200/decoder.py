@@ -866,10 +866,41 @@ def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
     if stop_level == state.header.tree_height:
         h = state.header.tree_height
         return state.root_planes[s >> h, t >> h, channel].copy()
-    return _to_host(decode_planes(state, [(s, t, channel)], stop_level)[0])
+    # one native call: request staged, k_decode_planes, pinned result
+    torch = _torch()
+    hdr = state.header
+    df = state.device_field()
+    wp, hp = hdr.padded_dims
+    host_stage, dev_stage, word = _image_buffers(df, 64)
+    plane = torch.empty((hp, wp), dtype=torch.int32, device=df.device)
+    res = torch.empty((hp, wp), dtype=torch.int32, pin_memory=True)
+    with torch.cuda.device(df.device):
+        rc = _native.lib().rlfc_decode_plane_host(
+            df.ref, stop_level, int(s), int(t), channel, plane.data_ptr(), res.data_ptr(),
+            host_stage.data_ptr(), dev_stage.data_ptr(), word.ctypes.data, _stream())
+    _native.check(rc, "rlfc_decode_plane_host")
+    _raise_word(int(word[0]))
+    return res.numpy()
 
 
 _img_tls = threading.local()
+
+
+def _image_buffers(df, need):
+    """Per-thread, per-device staging of the one-call image / plane decodes:
+    (pinned host buffer, device buffer, status word), grown on demand."""
+    torch = _torch()
+    key = df.device.index
+    bufs = getattr(_img_tls, "bufs", None)
+    if bufs is None:
+        bufs = _img_tls.bufs = {}
+    b = bufs.get(key)
+    if b is None or b[0].numel() < need:
+        cap = max(4096, 1 << (need - 1).bit_length())
+        b = bufs[key] = (torch.empty(cap, dtype=torch.uint8).pin_memory(),
+                         torch.empty(cap, dtype=torch.uint8, device=df.device),
+                         np.zeros(1, dtype=np.uint64))
+    return b
 
 
 def decode_image(state: DecoderState, image_index, stop_level=0):
@@ -883,18 +914,7 @@ def decode_image(state: DecoderState, image_index, stop_level=0):
     hdr = state.header
     df = state.device_field()
     L = _native.lib()
-    key = df.device.index
-    bufs = getattr(_img_tls, "bufs", None)
-    if bufs is None:
-        bufs = _img_tls.bufs = {}
-    need = 32 + 4 * hdr.s_count * hdr.t_count
-    b = bufs.get(key)
-    if b is None or b[0].numel() < need:
-        cap = max(4096, 1 << (need - 1).bit_length())
-        b = bufs[key] = (torch.empty(cap, dtype=torch.uint8).pin_memory(),
-                         torch.empty(cap, dtype=torch.uint8, device=df.device),
-                         np.zeros(1, dtype=np.uint64))
-    host_stage, dev_stage, word = b
+    host_stage, dev_stage, word = _image_buffers(df, 32 + 4 * hdr.s_count * hdr.t_count)
     img = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, device=df.device)
     res = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, pin_memory=True)
     with torch.cuda.device(df.device):
