@@ -384,7 +384,8 @@ int rlfc_render_slab(const uint8_t *rgb_field, const int32_t *slots,
  * stage_dev (device, same size) with one copy; the staged decode in slot
  * mode (workspace as for rlfc_decode_field_staged, else the fused decode)
  * fills field (device, field_cap images of H*W*3), k_render_slab renders into
- * out (device, n*oh*ow*3); the call returns after the stream has drained,
+ * out (device, n*oh*ow*3), copied into out_host (pinned, nullable); the call
+ * returns after the stream has drained,
  * with the decode status word in *status_word (0 = success). */
 int rlfc_render_slab_batch(const rlfc_field *f, int32_t stop_level, void *ws,
                            uint64_t ws_bytes, uint64_t present,
@@ -393,8 +394,8 @@ int rlfc_render_slab_batch(const rlfc_field *f, int32_t stop_level, void *ws,
                            int32_t n, int32_t ow, int32_t oh, uint8_t *field,
                            int32_t field_cap, uint8_t *out,
                            uint8_t *stage_host, uint8_t *stage_dev,
-                           uint64_t stage_bytes, uint64_t *status_word,
-                           void *stream);
+                           uint64_t stage_bytes, uint8_t *out_host,
+                           uint64_t *status_word, void *stream);
 uint64_t rlfc_render_staging_bytes(const rlfc_field *f, int32_t n);
 
 /* One image in one call (decoder.decode_image, decoder.py:187-194): the

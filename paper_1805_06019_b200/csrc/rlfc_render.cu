@@ -334,7 +334,7 @@ extern "C" int rlfc_render_slab_batch(const rlfc_field* f, int32_t stop_level, v
                                       const rlfc_render_geom* geoms, const uint8_t* bg, int32_t n, int32_t ow,
                                       int32_t oh, uint8_t* field, int32_t field_cap, uint8_t* out,
                                       uint8_t* stage_host, uint8_t* stage_dev, uint64_t stage_bytes,
-                                      uint64_t* status_word, void* stream) {
+                                      uint8_t* out_host, uint64_t* status_word, void* stream) {
     if (!f || !poses || !geoms || !bg || !field || !out || !stage_host || !stage_dev || !status_word || n < 1 ||
         n > 65535 || ow < 1 || oh < 1)
         return RLFC_ERR_ARGUMENT;
@@ -385,6 +385,8 @@ extern "C" int rlfc_render_slab_batch(const rlfc_field* f, int32_t stop_level, v
                           reinterpret_cast<const rlfc_render_geom*>(stage_dev + o_geom), stage_dev + o_bg, n, ow,
                           oh, out, stream);
     if (rc != RLFC_OK) return rc;
+    if (out_host && cudaMemcpyAsync(out_host, out, (size_t)n * oh * ow * 3, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return RLFC_ERR_CUDA;
     if (cudaMemcpyAsync(stage_host + o_stat, dstat, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
         cudaStreamSynchronize(st) != cudaSuccess)
         return RLFC_ERR_CUDA;

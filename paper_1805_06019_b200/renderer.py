@@ -293,7 +293,7 @@ def _geom_struct(geometry):
 
 
 def render_views(state, poses, stop_level=0, geometry=None,
-                 background=(0, 0, 0), device=None, out=None):
+                 background=(0, 0, 0), device=None, out=None, _host=None):
     """Render a batch of same-size poses; returns a CUDA uint8 tensor
     (n, height, width, 3).  geometry / background: one for all poses or one
     per pose."""
@@ -342,7 +342,7 @@ def render_views(state, poses, stop_level=0, geometry=None,
         return _render_slab_batch(state, df, stop_level, pose_arr,
                                   np.ascontiguousarray(gstruct),
                                   np.ascontiguousarray(bgs, dtype=np.uint8),
-                                  ow, oh, out, stream)
+                                  ow, oh, out, stream, _host)
     d_geom = torch.from_numpy(gstruct).to(dev)
     d_bg = torch.from_numpy(bgs).to(dev)
     if geos is None:
@@ -407,7 +407,7 @@ def _staging(dev):
 
 
 def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
-                       out, stream):
+                       out, stream, out_host=None):
     """Every slab pose of the batch in one native call
     (rlfc_render_slab_batch): tap cameras decoded by the staged path in slot
     mode, then one k_render_slab launch."""
@@ -427,7 +427,7 @@ def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
             rc = L.rlfc_render_slab_batch(
                 df.ref, stop_level, *args, pose_arr.ctypes.data, gstruct.ctypes.data, bgs.ctypes.data, n, ow,
                 oh, field.data_ptr(), field.shape[0], out.data_ptr(), host.data_ptr(), dbuf.data_ptr(),
-                stg.cap, stg.status.ctypes.data, stream)
+                stg.cap, None if out_host is None else out_host.data_ptr(), stg.status.ctypes.data, stream)
     _native.check(rc, "rlfc_render_slab_batch")
     decoder._raise_word(int(stg.status[0]))
     return out
@@ -459,5 +459,12 @@ def render_view(state, pose, stop_level=0, geometry: PlaneGeometry = None,
     """Render one view as uint8 RGB (reference renderer.py:279-305)."""
     if not isinstance(pose, (SlabPose, CameraPose)):
         raise TypeError(f"unknown pose type {type(pose).__name__}")
+    if isinstance(pose, SlabPose):
+        # the native batch call also brings the view back into a pinned
+        # array the result owns (one stream drain per call)
+        import torch
+        host = torch.empty((1, pose.height, pose.width, 3), dtype=torch.uint8, pin_memory=True)
+        render_views(state, [pose], stop_level, geometry, background, _host=host)
+        return host.numpy()[0]
     return decoder._to_host(render_views(state, [pose], stop_level, geometry,
                                          background)[0])
