@@ -200,6 +200,39 @@ def test_corrupt_fuzz(rl, i):
                 if wcode == 0:
                     assert np.array_equal(got.cpu().numpy(), want), (cfg, trial, k, kernel)
         S, T = hdr.s_count, hdr.t_count
+        # single images (decoder.py:187-194: planes of channels 0, 1, 2, the
+        # first failing one raises) and single planes, through the one-call
+        # host paths
+        for _ in range(3):
+            s, t = int(rng.integers(0, S)), int(rng.integers(0, T))
+            k = int(rng.integers(0, hdr.tree_height))
+            codes = [orc.decode_plane(s, t, cc, k)[1] for cc in range(3)]
+            want_code = next((x for x in codes if x), 0)
+            try:
+                img = rl.decode_image(st, (s, t), stop_level=k)
+                got_code = 0
+            except rl.FormatError as e:
+                got_code = 2 if "descriptor" in str(e) else 1
+                img = None
+            if got_code != want_code:
+                assert got_code == 2 and any(
+                    _walk_past_end(bad, hdr, cc, s, t, bx, by, k)
+                    for cc in range(3) for by in range(hb) for bx in range(wb)), (cfg, trial, s, t, k)
+            elif want_code == 0:
+                want_img, _ = orc.decode_all(k)
+                assert np.array_equal(img, want_img[s, t]), (cfg, trial, s, t, k)
+            cc = int(rng.integers(0, 3))
+            wplane, wcode = orc.decode_plane(s, t, cc, k)
+            try:
+                plane = rl.decode_plane(st, s, t, cc, stop_level=k)
+                pcode = 0
+            except rl.FormatError as e:
+                pcode = 2 if "descriptor" in str(e) else 1
+            if pcode != wcode:
+                assert pcode == 2 and any(_walk_past_end(bad, hdr, cc, s, t, bx, by, k)
+                                          for by in range(hb) for bx in range(wb)), (cfg, trial, s, t, cc, k)
+            elif wcode == 0:
+                assert np.array_equal(plane, wplane), (cfg, trial, s, t, cc, k)
         req = np.stack([rng.integers(0, S, 32), rng.integers(0, T, 32), rng.integers(0, wb, 32),
                         rng.integers(0, hb, 32), np.full(32, c), rng.integers(0, hdr.tree_height + 1, 32)], 1)
         out, status = rl.decode_blocks(st, req, raise_errors=False)
