@@ -16,6 +16,7 @@ the GPU (decoder.py).
 import io
 import os
 import struct
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -350,6 +351,22 @@ def _png_idat(blob, width, height):
     return b"".join(idat)
 
 
+_POOL = None
+_POOL_LOCK = threading.Lock()
+
+
+def _inflate_pool():
+    """Process-wide thread pool for the root-view inflates (zlib releases
+    the GIL); created once, so an init does not pay thread start-up."""
+    global _POOL
+    from concurrent.futures import ThreadPoolExecutor
+    with _POOL_LOCK:
+        if _POOL is None:
+            _POOL = ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1),
+                                       thread_name_prefix="rlfc-inflate")
+        return _POOL
+
+
 def parse_roots_device(data, header: RlfcHeader, device, threads=None):
     """Root planes decoded on the GPU (container.py:175-195; PNG and RAW roots):
     the host walks the sections and inflates each plane's IDAT stream on a
@@ -410,9 +427,11 @@ def parse_roots_device(data, header: RlfcHeader, device, threads=None):
             return None
         return raw if len(raw) == stride else None
 
-    nthreads = threads or min(32, os.cpu_count() or 1)
-    with ThreadPoolExecutor(max_workers=nthreads) as ex:
-        raws = list(ex.map(inflate, blobs))
+    if threads:
+        with ThreadPoolExecutor(max_workers=threads) as ex:
+            raws = list(ex.map(inflate, blobs))
+    else:
+        raws = list(_inflate_pool().map(inflate, blobs))
     if any(r is None for r in raws):
         return None
     host = torch.empty((len(raws), stride), dtype=torch.uint8).pin_memory()
