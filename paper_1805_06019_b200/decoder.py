@@ -425,7 +425,14 @@ def decode_blocks(state, requests, device=None, raise_errors=True):
     status = torch.zeros(n, dtype=torch.int32, device=df.device)
     with torch.cuda.device(df.device):
         stream = _stream()
-        ws = df.staged_workspace(stream) if n >= 4096 else None
+        # the prepared index pays from ~4k requests on; smaller batches use
+        # it too once the field has one (its index part is read-only)
+        if n >= 4096:
+            ws = df.staged_workspace(stream)
+        else:
+            with df._ws_lock:
+                have = next(iter(df._ws.values()), None)
+            ws = None if have is None else (have[0], df._ws_bytes, df._present)
         rc = _native.RLFC_ERR_ARGUMENT
         if ws is not None:
             # large batches: the prepared record index (no record walks)
