@@ -1049,6 +1049,7 @@ struct BlendParams {
     int nwp;
     int TW, NB, nchunks, nstrip;
     int store_mode;              // 2: TMA tensor stores, 1: per-row bulk copies, 0: byte stores
+    int store_keep;              // 1: output stores with the normal L2 policy, 0: evict-first
     int tma_in;                  // 1: staging and raw roots arrive by TMA tensor loads
     int roots_vec;               // root rows are 16-byte aligned in HBM (manual path)
     const int32_t* trows;        // camera rows to decode (grid.y indexes it), or null = all
@@ -1720,11 +1721,15 @@ __global__ void __launch_bounds__(BT, NL == 1 ? RLFC_BLEND_MINB : RLFC_DENSE_MIN
     const int nrows_band = min(by * B + B, f.height) - by * B;   // rows of this block row
     if (P.store_mode == 2) {
         if (tid == 0) {
-            // the output streams through L2 once: evict it first so the
-            // record tables, residuals and root colours the other tiles
-            // gather stay resident
+            // the output streams through L2 once: for B > 4 evict it first
+            // so the record tables, residuals and root colours the other
+            // tiles gather stay resident; B = 4 tiles measured faster with
+            // the normal policy (P.store_keep)
             uint64_t pol = 0;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+            if (P.store_keep)
+                asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+            else
+                asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
             for (int st = 0; st < P.nstrip; ++st) {
                 const int x0 = (bx0 * B + st * STRIP) * 3;
                 if (x0 >= f.width * 3) break;
@@ -1904,6 +1909,14 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     memset(&rgb_map, 0, sizeof(rgb_map));
     memset(&root_map, 0, sizeof(root_map));
     P.store_mode = aligned ? 1 : 0;
+    // output L2 policy (TMA stores), measured at cfg2: B = 4 tiles are
+    // faster with the normal policy (R4 0.419 vs 0.431 ms, R3 and R6 equal),
+    // B = 8 and 16 with evict-first (R2 0.294 vs 0.307 ms, R1 0.168 vs
+    // 0.176 ms)
+#ifndef RLFC_STORE_KEEP_B
+#define RLFC_STORE_KEEP_B 4
+#endif
+    P.store_keep = B <= RLFC_STORE_KEEP_B ? 1 : 0;
     const int nrows = min(by_hi * B, f.height) - by_lo * B;
     if (aligned && !slots && S <= 256) {
         const cuuint64_t dims[4] = {(cuuint64_t)f.width * 3, (cuuint64_t)nrows, (cuuint64_t)f.t_count,
