@@ -42,6 +42,11 @@ def _torch():
     return torch
 
 
+def _get_device():
+    """The calling thread's current CUDA device index (CUDA initialised)."""
+    return _torch()._C._cuda_getDevice()
+
+
 class DeviceField:
     """One stream resident in one GPU's HBM plus its `rlfc_field` descriptor.
 
@@ -708,7 +713,14 @@ def _block_scratch(state):
     """The calling thread's single-block scratch for this state's field on
     the current device.  It lives on the DeviceField (keyed by thread), so it
     is released with the state; nothing module-level holds the state."""
-    df = state.device_field()
+    # the uploaded field of the current device without the lock and device
+    # object of device_field() (a dict read is atomic; a field exists only
+    # once CUDA is initialised, so the raw device query is safe); first use
+    # uploads
+    devs = state._devices
+    df = devs.get(_get_device()) if devs else None
+    if df is None:
+        df = state.device_field()
     key = threading.get_ident()
     sc = df.block_scratch.get(key)
     if sc is None:

@@ -66,3 +66,20 @@ for _ in range(len(picks)):
     torch.cuda.synchronize()
 dt4 = (time.perf_counter() - t0) / len(picks)
 print(f"torch one-kernel launch + synchronize {dt4 * 1e6:.2f} us")
+
+# the Python side of decode_block alone: the native call replaced by a no-op
+def _py_cost(label, fn, n=20000):
+    t0 = time.perf_counter()
+    for _ in range(n):
+        fn()
+    print(f"{label} {(time.perf_counter() - t0) / n * 1e6:.3f} us")
+
+
+_py_cost("torch.cuda.current_device()", torch.cuda.current_device)
+_py_cost("state.device_field()", st.device_field)
+_py_cost("decoder._block_scratch(state)", lambda: decoder._block_scratch(st))
+real = sc.call_fn
+sc.call_fn = lambda p: 0
+s, t, bx, by, c = picks[0]
+_py_cost("decode_block with a no-op native call", lambda: rl.decode_block(st, (s, t), (bx, by), c))
+sc.call_fn = real
