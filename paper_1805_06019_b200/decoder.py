@@ -47,6 +47,17 @@ def _get_device():
     return _torch()._C._cuda_getDevice()
 
 
+def _field_on(state, device=None):
+    """state.device_field(device) without its lock and device object when
+    the field of the current device is already uploaded (a dict read is
+    atomic; a field exists only once CUDA is initialised)."""
+    if device is None and state._devices:
+        df = state._devices.get(_get_device())
+        if df is not None:
+            return df
+    return state.device_field(device)
+
+
 class DeviceField:
     """One stream resident in one GPU's HBM plus its `rlfc_field` descriptor.
 
@@ -713,14 +724,7 @@ def _block_scratch(state):
     """The calling thread's single-block scratch for this state's field on
     the current device.  It lives on the DeviceField (keyed by thread), so it
     is released with the state; nothing module-level holds the state."""
-    # the uploaded field of the current device without the lock and device
-    # object of device_field() (a dict read is atomic; a field exists only
-    # once CUDA is initialised, so the raw device query is safe); first use
-    # uploads
-    devs = state._devices
-    df = devs.get(_get_device()) if devs else None
-    if df is None:
-        df = state.device_field()
+    df = _field_on(state)
     key = threading.get_ident()
     sc = df.block_scratch.get(key)
     if sc is None:

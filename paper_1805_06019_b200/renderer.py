@@ -322,13 +322,15 @@ def render_views(state, poses, stop_level=0, geometry=None,
     else:
         one = default_geometry(S, T) if geometry is None else geometry
         geos = None
-        gstruct = np.tile(np.array(_geom_struct(one), dtype=np.float64), (n, 1))
+        gstruct = np.empty((n, 6), dtype=np.float64)
+        gstruct[:] = _geom_struct(one)
     bgs = np.asarray(background, dtype=np.uint8).reshape(-1, 3)
-    bgs = np.broadcast_to(bgs, (n, 3)).copy() if bgs.shape[0] == 1 else bgs
-    df = state.device_field(device)
+    if bgs.shape[0] == 1 and n > 1:
+        bgs = np.repeat(bgs, n, axis=0)
+    df = decoder._field_on(state, device)
     dev = df.device
     L = _native.lib()
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    stream = torch._C._cuda_getCurrentRawStream(dev.index)
     if out is None:
         out = torch.empty((n, oh, ow, 3), dtype=torch.uint8, device=dev)
     if kinds == {SlabPose}:
@@ -336,11 +338,15 @@ def render_views(state, poses, stop_level=0, geometry=None,
                               float(p.focal_z or 0.0)) for p in poses],
                             dtype=np.float64)
         # renderer.py:175-176: a focal plane on the camera plane is rejected
-        focal = np.where(pose_arr[:, 2] != 0.0, pose_arr[:, 3], gstruct[:, 1])
-        if np.any(focal == gstruct[:, 0]):
+        if n <= 8:
+            bad = any((p.focal_z if p.focal_z is not None else g[1]) == g[0]
+                      for p, g in zip(poses, gstruct.tolist()))
+        else:
+            focal = np.where(pose_arr[:, 2] != 0.0, pose_arr[:, 3], gstruct[:, 1])
+            bad = bool(np.any(focal == gstruct[:, 0]))
+        if bad:
             raise ValueError("focal plane coincides with the camera plane")
-        return _render_slab_batch(state, df, stop_level, pose_arr,
-                                  np.ascontiguousarray(gstruct),
+        return _render_slab_batch(state, df, stop_level, pose_arr, gstruct,
                                   np.ascontiguousarray(bgs, dtype=np.uint8),
                                   ow, oh, out, stream, _host)
     d_geom = torch.from_numpy(gstruct).to(dev)
@@ -378,9 +384,25 @@ class _Staging:
     """Per-thread, per-device staging buffers of rlfc_render_slab_batch: one
     pinned host buffer and one device buffer (grown on demand)."""
 
+    # camera fields up to this size are kept between calls (the batch call
+    # is synchronous, so the next call may reuse the scratch)
+    FIELD_KEEP_BYTES = 64 << 20
+
     def __init__(self, dev):
         self.dev = dev
         self.cap = 0
+        self.field = None
+
+    def camera_field(self, shape):
+        import torch
+        nbytes = shape[0] * shape[1] * shape[2] * shape[3]
+        f = self.field
+        if f is not None and tuple(f.shape) == shape:
+            return f
+        f = torch.empty(shape, dtype=torch.uint8, device=self.dev)
+        if nbytes <= self.FIELD_KEEP_BYTES:
+            self.field = f
+        return f
 
     def buffers(self, nbytes):
         import torch
@@ -418,9 +440,12 @@ def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
     nbytes = int(L.rlfc_render_staging_bytes(df.ref, n))
     stg = _staging(df.device)
     host, dbuf = stg.buffers(nbytes)
-    field = torch.empty((min(hdr.s_count * hdr.t_count, 4 * n), hdr.height, hdr.width, 3),
-                        dtype=torch.uint8, device=df.device)
-    with torch.cuda.device(df.device):
+    field = stg.camera_field((min(hdr.s_count * hdr.t_count, 4 * n), hdr.height, hdr.width, 3))
+    switch = decoder._get_device() != df.device.index
+    if switch:
+        prev = torch.cuda.current_device()
+        torch.cuda.set_device(df.device)
+    try:
         ws = df.staged_workspace(stream)
         args = (None, 0, 0, 0) if ws is None else (ws[0].data_ptr(), ws[1], ws[2], ws[3])
         with df.enqueue_lock:
@@ -428,6 +453,9 @@ def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
                 df.ref, stop_level, *args, pose_arr.ctypes.data, gstruct.ctypes.data, bgs.ctypes.data, n, ow,
                 oh, field.data_ptr(), field.shape[0], out.data_ptr(), host.data_ptr(), dbuf.data_ptr(),
                 stg.cap, None if out_host is None else out_host.data_ptr(), stg.status.ctypes.data, stream)
+    finally:
+        if switch:
+            torch.cuda.set_device(prev)
     _native.check(rc, "rlfc_render_slab_batch")
     decoder._raise_word(int(stg.status[0]))
     return out
