@@ -585,13 +585,37 @@ def e2e_measure(state, band, args, rl):
     dt = (time.perf_counter() - t0) / steps
     hdr = state.header
     px = hdr.s_count * hdr.t_count * hdr.width * res.rows_px
+    # this box's pinned-copy bandwidth: the PCIe floor of the step (the
+    # D2H of the RGB field dominates; the bands overlap H2D, decode and D2H)
+    bw = pcie_bandwidth()
+    floor_ms = max(res.d2h_bytes / bw["d2h_gbs"], res.h2d_bytes / bw["h2d_gbs"]) / 1e6
     return {"value": px / dt / 1e9, "unit": "Gpix/s",
             "h2d_bytes_per_step": res.h2d_bytes,
             "d2h_bytes_per_step": res.d2h_bytes,
             "ms_per_step": dt * 1e3,
+            "pcie": dict(bw, floor_ms=floor_ms, frac_of_floor=floor_ms / (dt * 1e3)),
             "path": "decoder.HostPipeline: pinned H2D of SRV+offsets+roots, "
                     "staged decode, pinned D2H of RGB; 8 block-row bands "
                     "pipelined over three CUDA streams (PCIe D2H-bound)"}
+
+
+def pcie_bandwidth(nbytes=256 << 20, reps=8):
+    """Pinned host <-> device copy bandwidth (GB/s) of one 256 MB buffer."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, fn in (("h2d_gbs", lambda: d.copy_(h, non_blocking=True)),
+                     ("d2h_gbs", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        out[name] = reps * nbytes / (time.perf_counter() - t0) / 1e9
+    del h, d
+    return out
 
 
 def random_access_measure(state, rl):
