@@ -644,12 +644,14 @@ def random_access_measure(state, rl):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    picks = req[:200]
-    for p in picks[:10]:
-        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    # Python ints, as a caller holds them (no numpy scalar conversions in
+    # the timed loop)
+    picks = [((s, t), (bx, by), c) for s, t, bx, by, c, _ in req[:2000].tolist()]
+    for a in picks[:10]:
+        rl.decode_block(state, *a)
     t0 = time.perf_counter()
-    for p in picks:
-        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    for a in picks:
+        rl.decode_block(state, *a)
     lat = (time.perf_counter() - t0) / len(picks)
     return {"blocks_per_s": n / (ms * 1e-3), "batch": n, "ms_per_batch": ms,
             "decode_block_latency_us": lat * 1e6,
@@ -704,13 +706,14 @@ def run_cfg5(args):
     picks = np.stack([rng.integers(0, hdr.s_count, 10000), rng.integers(0, hdr.t_count, 10000),
                       rng.integers(0, wb, 10000), rng.integers(0, hb, 10000),
                       rng.integers(0, 3, 10000)], 1)
-    for p in picks[:50]:
-        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
+    calls = [((s, t), (bx, by), c) for s, t, bx, by, c in picks.tolist()]
+    for a in calls[:50]:
+        rl.decode_block(state, *a)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for p in picks:
-        rl.decode_block(state, (int(p[0]), int(p[1])), (int(p[2]), int(p[3])), int(p[4]))
-    lat_us = (time.perf_counter() - t0) / len(picks) * 1e6
+    for a in calls:
+        rl.decode_block(state, *a)
+    lat_us = (time.perf_counter() - t0) / len(calls) * 1e6
     n = 1_000_000
     req = np.stack([rng.integers(0, hdr.s_count, n), rng.integers(0, hdr.t_count, n),
                     rng.integers(0, wb, n), rng.integers(0, hb, n),

@@ -42,6 +42,15 @@ def _torch():
     return torch
 
 
+def _host_bytes(arr):
+    """A CPU uint8 tensor viewing a (possibly read-only) host byte array
+    without copying it; only ever read (the source of an upload)."""
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return _torch().from_numpy(np.asarray(arr, dtype=np.uint8).reshape(-1))
+
+
 def _get_device():
     """The calling thread's current CUDA device index (CUDA initialised)."""
     return _torch()._C._cuda_getDevice()
@@ -78,9 +87,14 @@ class DeviceField:
         self.srv = []
         self.offsets = []
         for c in range(3):
-            buf = torch.zeros(len(srv[c]) + SRV_TAIL_PAD, dtype=torch.uint8)
-            buf[:len(srv[c])] = torch.from_numpy(np.asarray(srv[c]).copy())
-            self.srv.append(buf.to(self.device))
+            # straight from the stream bytes into HBM (no host copies of the
+            # section), then the zero tail on the device
+            n = len(srv[c])
+            buf = torch.empty(n + SRV_TAIL_PAD, dtype=torch.uint8, device=self.device)
+            buf[n:].zero_()
+            if n:
+                buf[:n].copy_(_host_bytes(srv[c]))
+            self.srv.append(buf)
             off = np.ascontiguousarray(offsets[c]).view(np.int64)
             self.offsets.append(torch.from_numpy(off.copy()).to(self.device))
         if roots_dev is not None and roots_dev.device == self.device:
