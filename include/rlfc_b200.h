@@ -171,13 +171,18 @@ int rlfc_decode_planes(const rlfc_field *f, int32_t stop_level,
 
 /* One padded plane in one call (decoder.decode_plane, decoder.py:165-184):
  * request and status staged through stage_host / stage_dev (pinned / device,
- * 32 bytes each), k_decode_planes into plane_dev (hp*wp int32), copied into
- * plane_host (pinned); returns drained, the status word in *status_word. */
+ * 32 bytes each), the plane decoded into plane_dev (hp*wp int32), copied into
+ * plane_host (pinned); returns drained, the status word in *status_word.
+ * With a prepared record index (rlfc_staged_index_view; B = 4, nullable)
+ * every block of an unflagged record is summed from the index
+ * (k_plane_indexed4); otherwise, and for flagged records, the record walk of
+ * k_decode_planes. */
 int rlfc_decode_plane_host(const rlfc_field *f, int32_t stop_level,
                            int32_t s, int32_t t, int32_t channel,
                            int32_t *plane_dev, int32_t *plane_host,
                            uint8_t *stage_host, uint8_t *stage_dev,
-                           uint64_t *status_word, void *stream);
+                           uint64_t *status_word,
+                           const rlfc_index_view *index, void *stream);
 
 /* Fused full-field decode: every (s, t) image with image_slots[s*T + t] >= 0
  * (image_slots NULL = all images, slot = s*T + t), block rows

@@ -94,7 +94,7 @@ _SIGS = {
     "rlfc_render_slab_batch": ["p", "i", "p", "u", "u", "i", "p", "p", "p", "i", "i", "i", "p", "i", "p",
                                "p", "p", "u", "p", "p", "p"],
     "rlfc_render_staging_bytes": ["p", "i"],
-    "rlfc_decode_plane_host": ["p", "i", "i", "i", "i", "p", "p", "p", "p", "p", "p"],
+    "rlfc_decode_plane_host": ["p", "i", "i", "i", "i", "p", "p", "p", "p", "p", "p", "p"],
     "rlfc_decode_image_host": ["p", "i", "p", "u", "u", "i", "i", "i", "p", "p", "p", "p", "u", "p", "p"],
     "rlfc_render_slab": ["p", "p", "i", "i", "i", "i", "p", "p", "p", "i",
                          "i", "i", "p", "p"],

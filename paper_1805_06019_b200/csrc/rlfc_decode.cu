@@ -289,6 +289,87 @@ __global__ void k_decode_planes(const rlfc_field f, int stop_level, const int32_
         for (int xx = 0; xx < B; ++xx) o[(int64_t)(by * B + yy) * f.wp + bx * B + xx] = acc[yy * B + xx];
 }
 
+// One padded plane from the prepared record index (B = 4,
+// decoder.decode_plane, decoder.py:165-184): one thread per block adds the
+// present chain levels >= k to its root samples (integer sums, so the level
+// order is free: each level is one bitmap word, one rank and one entry load,
+// all issued before any payload is decoded). Blocks of records that prepare
+// flagged take the reference-order record walk and report its key, as
+// k_decode_planes does. Rows leave as 16-byte stores.
+__global__ void __launch_bounds__(256) k_plane_indexed4(const rlfc_field f, const rlfc_index_view ix, int k, int s,
+                                                        int t, int c, int32_t* __restrict__ out, uint64_t* status) {
+    constexpr int MAXL = 8;
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk >= nblk) return;
+    const int bx = (int)(blk % f.wb), by = (int)(blk / f.wb);
+    const int64_t ri = (int64_t)c * nblk + blk;
+    const int h = f.tree_height;
+    int32_t acc[16];
+    if (f.roots_i16) {
+        const int16_t* r0 = reinterpret_cast<const int16_t*>(f.roots) +
+                            ((((int64_t)(s >> h) * f.rsy + (t >> h)) * 3 + c) * f.hp + by * 4) * f.wp + bx * 4;
+#pragma unroll
+        for (int yy = 0; yy < 4; ++yy) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(r0 + (int64_t)yy * f.wp));
+            acc[yy * 4] = (int32_t)(int16_t)(v.x & 0xFFFFu);
+            acc[yy * 4 + 1] = (int32_t)v.x >> 16;
+            acc[yy * 4 + 2] = (int32_t)(int16_t)(v.y & 0xFFFFu);
+            acc[yy * 4 + 3] = (int32_t)v.y >> 16;
+        }
+    } else {
+#pragma unroll
+        for (int yy = 0; yy < 4; ++yy)
+#pragma unroll
+            for (int xx = 0; xx < 4; ++xx) acc[yy * 4 + xx] = root_sample(f, s, t, c, by * 4 + yy, bx * 4 + xx);
+    }
+    int st = 0;
+    if (__ldg(ix.rec_flag + ri)) {
+        const uint64_t off = f.offsets[c][blk];
+        st = walk_chain<16>(f, f.srv[c] + off, s, t, k, acc, c_lut, c_nb<4>, srv_avail(f, c, off));
+        if (st == WALK_OOB) st = 2;
+    } else {
+        uint32_t words[MAXL], ranks[MAXL];
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+            words[l] = ranks[l] = 0u;
+            if (l >= k && l < h) {
+                const int nd = chain_node(f, l, s, t);
+                words[l] = __ldg(ix.bm + (int64_t)(nd >> 5) * ix.nrec + ri);
+                ranks[l] = __ldg(ix.rk + (int64_t)(nd >> 5) * ix.nrec + ri);
+            }
+        }
+        uint2 ent[MAXL];
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+            ent[l] = make_uint2(0u, 31u);
+            if (l >= k && l < h) {
+                const uint32_t bit = (uint32_t)chain_node(f, l, s, t) & 31u;
+                const uint64_t slot = (uint64_t)ranks[l] + (uint64_t)__popc(words[l] & ((1u << bit) - 1u));
+                if (((words[l] >> bit) & 1u) && slot < ix.cap)
+                    ent[l] = make_uint2(__ldg(ix.entries + 2 * slot), __ldg(ix.entries + 2 * slot + 1));
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < MAXL; ++l) {
+            const uint32_t d = ent[l].y & 31u;
+            if (d >= (uint32_t)NUM_DESC) continue;
+            const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + ent[l].x);
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+            const uint32_t bit0 = (uint32_t)(a & 3u) * 8u, b = (uint32_t)desc_bits((int)d);
+            const int m = desc_mode((int)d);
+            if (m == MODE_BITS) decode16_acc<MODE_BITS>(sw, bit0, b, nullptr, f.quant_shift, acc);
+            else if (m == MODE_TRIT) decode16_acc<MODE_TRIT>(sw, bit0, b, g_lut_ix.trit, f.quant_shift, acc);
+            else decode16_acc<MODE_QUINT>(sw, bit0, b, g_lut_ix.quint, f.quant_shift, acc);
+        }
+    }
+    if (st) report(status, (uint64_t)blk, st);
+#pragma unroll
+    for (int yy = 0; yy < 4; ++yy)
+        *reinterpret_cast<int4*>(out + (int64_t)(by * 4 + yy) * f.wp + bx * 4) =
+            make_int4(acc[yy * 4], acc[yy * 4 + 1], acc[yy * 4 + 2], acc[yy * 4 + 3]);
+}
+
 // One thread per (image, block) of a band: three channel chains, inverse lift,
 // clamp, RGB8 store of the true-dims crop (decoder.py:187-194).
 template <int B>
@@ -613,7 +694,8 @@ static_assert(offsetof(rlfc_mailbox, out) == 64 && sizeof(rlfc_mailbox) == 64 + 
 // runs, the plane and the status come back, the call returns drained.
 extern "C" int rlfc_decode_plane_host(const rlfc_field* f, int32_t stop_level, int32_t s, int32_t t, int32_t c,
                                       int32_t* plane_dev, int32_t* plane_host, uint8_t* stage_host,
-                                      uint8_t* stage_dev, uint64_t* status_word, void* stream) {
+                                      uint8_t* stage_dev, uint64_t* status_word, const rlfc_index_view* index,
+                                      void* stream) {
     if (!valid_field(f) || !plane_dev || !plane_host || !stage_host || !stage_dev || !status_word)
         return RLFC_ERR_ARGUMENT;
     if (s < 0 || s >= f->s_count || t < 0 || t >= f->t_count || c < 0 || c > 2 || stop_level < 0 ||
@@ -627,9 +709,17 @@ extern "C" int rlfc_decode_plane_host(const rlfc_field* f, int32_t stop_level, i
     req[2] = c;
     if (cudaMemcpyAsync(stage_dev, stage_host, 32, cudaMemcpyHostToDevice, st) != cudaSuccess) return RLFC_ERR_CUDA;
     uint64_t* dstat = reinterpret_cast<uint64_t*>(stage_dev);
-    const int rc = rlfc_decode_planes(f, stop_level, reinterpret_cast<const int32_t*>(stage_dev + 16), 1, plane_dev,
-                                      dstat, stream);
-    if (rc != RLFC_OK) return rc;
+    if (index && index->bm && f->block == 4 && f->tree_height <= 8 && (reinterpret_cast<uintptr_t>(plane_dev) & 15) == 0) {
+        // the prepared record index (k_plane_indexed4): no record walks
+        const int64_t nblk = (int64_t)f->wb * f->hb;
+        k_plane_indexed4<<<(unsigned)((nblk + 255) / 256), 256, 0, st>>>(*f, *index, stop_level, s, t, c, plane_dev,
+                                                                          dstat);
+        if (cudaGetLastError() != cudaSuccess) return RLFC_ERR_CUDA;
+    } else {
+        const int rc = rlfc_decode_planes(f, stop_level, reinterpret_cast<const int32_t*>(stage_dev + 16), 1,
+                                          plane_dev, dstat, stream);
+        if (rc != RLFC_OK) return rc;
+    }
     if (cudaMemcpyAsync(plane_host, plane_dev, (size_t)f->hp * f->wp * 4, cudaMemcpyDeviceToHost, st) !=
             cudaSuccess ||
         cudaMemcpyAsync(stage_host, dstat, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||

@@ -140,6 +140,7 @@ class DeviceField:
         self._present = None
         self._dir = None
         self.block_scratch = {}      # thread id -> _BlockScratch
+        self._index_view = None      # rlfc_index_view (index_view()), False: none
 
     def directory(self):
         """The device record directory (rlfc_b200.h rlfc_dir: tile-major
@@ -191,6 +192,36 @@ class DeviceField:
             self._dir = Directory(d, blobs, blob_off, flagged, root_rgb,
                                   tables, build_ms)
             return self._dir
+
+    def index_view(self):
+        """The prepared record index as an rlfc_index_view (B = 4), from any
+        staged workspace of this field (its index part is read-only after
+        prepare; the view keeps that workspace alive), or None."""
+        v = self._index_view
+        if v is not None:
+            return v or None
+        torch = _torch()
+        with self._ws_lock:
+            have = next(iter(self._ws.values()), None)
+        ws = None
+        if have is not None:
+            ws = (have[0], self._ws_bytes, self._present)
+        else:
+            with torch.cuda.device(self.device):
+                cur = torch.cuda.current_stream(self.device)
+                got = self.staged_workspace(cur.cuda_stream)
+                if got is not None:
+                    ws = got[:3]
+                    cur.synchronize()
+        view = False
+        if ws is not None:
+            iv = _native.IndexView()
+            if _native.lib().rlfc_staged_index_view(self.ref, ws[0].data_ptr(), ws[1], ws[2],
+                                                    ctypes.byref(iv)) == _native.RLFC_OK:
+                iv._ws_ref = ws[0]
+                view = iv
+        self._index_view = view
+        return view or None
 
     def staged_workspace(self, stream_handle):
         """(tensor, bytes, present_total, n_flagged) for the staged decode on one CUDA
@@ -701,24 +732,7 @@ class _BlockScratch:
         # the prepared record index of the field (any workspace: its index
         # part is read-only after prepare): B = 4 requests skip the record
         # walk (one lane per chain level)
-        self.index = None
-        if b == 4:
-            with df._ws_lock:
-                have = next(iter(df._ws.values()), None)
-            ws = None
-            if have is not None:
-                ws = (have[0], df._ws_bytes, df._present)
-            else:
-                got = df.staged_workspace(torch.cuda.current_stream(df.device).cuda_stream)
-                if got is not None:
-                    ws = got[:3]
-                    torch.cuda.current_stream(df.device).synchronize()
-            if ws is not None:
-                view = _native.IndexView()
-                if L.rlfc_staged_index_view(df.ref, ws[0].data_ptr(), ws[1], ws[2],
-                                            ctypes.byref(view)) == _native.RLFC_OK:
-                    self.index = view
-                    self._ws_ref = ws[0]
+        self.index = df.index_view() if b == 4 else None
         self.index_ptr = ctypes.addressof(self.index) if self.index is not None else None
         # the whole call in one struct: per request only req changes
         self.call = _native.BlockCall(ctypes.addressof(df.cfield), self.mailbox.data_ptr(), self.index_ptr,
@@ -906,15 +920,18 @@ def decode_plane(state: DecoderState, s, t, channel, stop_level=0):
     # one native call: request staged, k_decode_planes, pinned result
     torch = _torch()
     hdr = state.header
-    df = state.device_field()
+    # the current device's field (device_field() default): no device switch
+    df = _field_on(state)
     wp, hp = hdr.padded_dims
     host_stage, dev_stage, word = _image_buffers(df, 64)
     plane = torch.empty((hp, wp), dtype=torch.int32, device=df.device)
     res = torch.empty((hp, wp), dtype=torch.int32, pin_memory=True)
-    with torch.cuda.device(df.device):
-        rc = _native.lib().rlfc_decode_plane_host(
-            df.ref, stop_level, int(s), int(t), channel, plane.data_ptr(), res.data_ptr(),
-            host_stage.data_ptr(), dev_stage.data_ptr(), word.ctypes.data, _stream())
+    iv = df.index_view() if hdr.block_size == 4 else None
+    rc = _native.lib().rlfc_decode_plane_host(
+        df.ref, stop_level, int(s), int(t), channel, plane.data_ptr(), res.data_ptr(),
+        host_stage.data_ptr(), dev_stage.data_ptr(), word.ctypes.data,
+        None if iv is None else ctypes.byref(iv),
+        torch._C._cuda_getCurrentRawStream(df.device.index))
     _native.check(rc, "rlfc_decode_plane_host")
     _raise_word(int(word[0]))
     return res.numpy()
@@ -949,19 +966,19 @@ def decode_image(state: DecoderState, image_index, stop_level=0):
     _check_indices(state, s, t)
     _check_level(state, stop_level)
     hdr = state.header
-    df = state.device_field()
+    # the current device's field (device_field() default): no device switch
+    df = _field_on(state)
     L = _native.lib()
     host_stage, dev_stage, word = _image_buffers(df, 32 + 4 * hdr.s_count * hdr.t_count)
     img = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, device=df.device)
     res = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, pin_memory=True)
-    with torch.cuda.device(df.device):
-        stream = _stream()
-        ws = df.staged_workspace(stream)
-        args = (None, 0, 0, 0) if ws is None else (ws[0].data_ptr(), ws[1], ws[2], ws[3])
-        with df.enqueue_lock:
-            rc = L.rlfc_decode_image_host(df.ref, stop_level, *args, int(s), int(t), img.data_ptr(),
-                                          res.data_ptr(), host_stage.data_ptr(), dev_stage.data_ptr(),
-                                          host_stage.numel(), word.ctypes.data, stream)
+    stream = torch._C._cuda_getCurrentRawStream(df.device.index)
+    ws = df.staged_workspace(stream)
+    args = (None, 0, 0, 0) if ws is None else (ws[0].data_ptr(), ws[1], ws[2], ws[3])
+    with df.enqueue_lock:
+        rc = L.rlfc_decode_image_host(df.ref, stop_level, *args, int(s), int(t), img.data_ptr(),
+                                      res.data_ptr(), host_stage.data_ptr(), dev_stage.data_ptr(),
+                                      host_stage.numel(), word.ctypes.data, stream)
     _native.check(rc, "rlfc_decode_image_host")
     _raise_word(int(word[0]))
     return res.numpy()

@@ -22,3 +22,5 @@ tm("render_views b1 k0", lambda: rl.render_views(st, one))
 tm("render_views b1 kh", lambda: rl.render_views(st, one, stop_level=h))
 tm("render_view b1 k0 (host result)", lambda: rl.render_view(st, one[0]))
 tm("decode_block", lambda: rl.decode_block(st, (3, 4), (10, 20), 1), n=5000)
+tm("decode_image", lambda: rl.decode_image(st, (3, 4)), n=300)
+tm("decode_plane", lambda: rl.decode_plane(st, 3, 4, 1), n=300)
