@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "../../include/rlfc_b200.h"
+#include "rlfc_field.cuh"
 
 namespace rlfc {
 
@@ -341,7 +342,8 @@ extern "C" int rlfc_render_slab_batch(const rlfc_field* f, int32_t stop_level, v
     const int S = f->s_count, T = f->t_count, W = f->width, H = f->height;
     auto al = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
     const uint64_t o_stat = 0, o_pose = 16, o_geom = al(o_pose + 32ull * n), o_slot = al(o_geom + 48ull * n),
-                   o_rows = al(o_slot + 4ull * S * T), o_bg = al(o_rows + 4ull * T), total = al(o_bg + 3ull * n);
+                   o_rows = al(o_slot + 4ull * S * T), o_bg = al(o_rows + 4ull * T), o_sel = al(o_bg + 3ull * n),
+                   total = al(o_sel + 4ull * (1 + rlfc::SEL_NODES_MAX));
     if (total > stage_bytes) return RLFC_ERR_ARGUMENT;
     int32_t* slots = reinterpret_cast<int32_t*>(stage_host + o_slot);
     for (int i = 0; i < S * T; ++i) slots[i] = -1;
@@ -360,9 +362,19 @@ extern "C" int rlfc_render_slab_batch(const rlfc_field* f, int32_t stop_level, v
             if (slots[s * T + t] == 0) any = true;
         if (any) rows[nrows++] = t;
     }
+    int32_t views[4 * 64];
+    int nviews = 0;
     for (int i = 0; i < S * T; ++i)
-        if (slots[i] == 0) slots[i] = ncam++;
+        if (slots[i] == 0) {
+            if (nviews < 4 * 64) views[nviews] = i;
+            ++nviews;
+            slots[i] = ncam++;
+        }
     if (ncam > field_cap) return RLFC_ERR_ARGUMENT;
+    // the slot-mode node list, built here (no k_sel_nodes launch)
+    uint32_t* sel = reinterpret_cast<uint32_t*>(stage_host + o_sel);
+    const int sel_n = nviews <= 4 * 64 ? rlfc::sel_nodes_host(*f, stop_level, views, nviews, sel)
+                                       : (int)(sel[0] = rlfc::SEL_NODES_MAX + 1);
     std::memset(stage_host + o_stat, 0, 16);
     std::memcpy(stage_host + o_pose, poses, 32ull * n);
     std::memcpy(stage_host + o_geom, geoms, 48ull * n);
@@ -375,9 +387,10 @@ extern "C" int rlfc_render_slab_batch(const rlfc_field* f, int32_t stop_level, v
     const int64_t img = (int64_t)H * W * 3;
     int rc = RLFC_ERR_ARGUMENT;
     if (ws)
-        rc = rlfc_decode_field_staged(f, stop_level, dslots, 0, f->hb, field, img, (int64_t)W * 3, ws, ws_bytes,
-                                      present, n_flagged, reinterpret_cast<const int32_t*>(stage_dev + o_rows),
-                                      nrows, dstat, stream);
+        rc = rlfc::decode_field_staged_sel(f, stop_level, dslots, 0, f->hb, field, img, (int64_t)W * 3, ws, ws_bytes,
+                                           present, n_flagged, reinterpret_cast<const int32_t*>(stage_dev + o_rows),
+                                           nrows, dstat, stream, reinterpret_cast<const uint32_t*>(stage_dev + o_sel),
+                                           sel_n);
     if (rc == RLFC_ERR_ARGUMENT)
         rc = rlfc_decode_field(f, stop_level, dslots, 0, f->hb, field, img, (int64_t)W * 3, dstat, stream);
     if (rc != RLFC_OK) return rc;
@@ -398,8 +411,9 @@ extern "C" uint64_t rlfc_render_staging_bytes(const rlfc_field* f, int32_t n) {
     if (!f || n < 1) return 0;
     auto al = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
     const uint64_t o_geom = al(16 + 32ull * n), o_slot = al(o_geom + 48ull * n),
-                   o_rows = al(o_slot + 4ull * f->s_count * f->t_count), o_bg = al(o_rows + 4ull * f->t_count);
-    return al(o_bg + 3ull * n);
+                   o_rows = al(o_slot + 4ull * f->s_count * f->t_count), o_bg = al(o_rows + 4ull * f->t_count),
+                   o_sel = al(o_bg + 3ull * n);
+    return al(o_sel + 4ull * (1 + rlfc::SEL_NODES_MAX));
 }
 
 // ---- one image in one call (host runtime) ----------------------------------------------
@@ -415,13 +429,16 @@ extern "C" int rlfc_decode_image_host(const rlfc_field* f, int32_t stop_level, v
     if (!f || !rgb_dev || !rgb_host || !stage_host || !stage_dev || !status_word) return RLFC_ERR_ARGUMENT;
     const int S = f->s_count, T = f->t_count, W = f->width, H = f->height;
     if (s < 0 || s >= S || t < 0 || t >= T || stop_level < 0 || stop_level > f->tree_height) return RLFC_ERR_ARGUMENT;
-    const uint64_t o_slot = 16, o_rows = (o_slot + 4ull * S * T + 15) & ~15ull, total = o_rows + 16;
+    const uint64_t o_slot = 16, o_rows = (o_slot + 4ull * S * T + 15) & ~15ull, o_sel = o_rows + 16,
+                   total = o_sel + 4ull * (1 + rlfc::SEL_NODES_MAX);
     if (total > stage_bytes) return RLFC_ERR_ARGUMENT;
     std::memset(stage_host, 0, 16);
     int32_t* slots = reinterpret_cast<int32_t*>(stage_host + o_slot);
     for (int i = 0; i < S * T; ++i) slots[i] = -1;
     slots[s * T + t] = 0;
     reinterpret_cast<int32_t*>(stage_host + o_rows)[0] = t;
+    const int32_t view = s * T + t;
+    const int sel_n = rlfc::sel_nodes_host(*f, stop_level, &view, 1, reinterpret_cast<uint32_t*>(stage_host + o_sel));
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemcpyAsync(stage_dev, stage_host, total, cudaMemcpyHostToDevice, st) != cudaSuccess) return RLFC_ERR_CUDA;
     uint64_t* dstat = reinterpret_cast<uint64_t*>(stage_dev);
@@ -429,9 +446,10 @@ extern "C" int rlfc_decode_image_host(const rlfc_field* f, int32_t stop_level, v
     const int64_t img = (int64_t)H * W * 3;
     int rc = RLFC_ERR_ARGUMENT;
     if (ws)
-        rc = rlfc_decode_field_staged(f, stop_level, dslots, 0, f->hb, rgb_dev, img, (int64_t)W * 3, ws, ws_bytes,
-                                      present, n_flagged, reinterpret_cast<const int32_t*>(stage_dev + o_rows), 1,
-                                      dstat, stream);
+        rc = rlfc::decode_field_staged_sel(f, stop_level, dslots, 0, f->hb, rgb_dev, img, (int64_t)W * 3, ws,
+                                           ws_bytes, present, n_flagged,
+                                           reinterpret_cast<const int32_t*>(stage_dev + o_rows), 1, dstat, stream,
+                                           reinterpret_cast<const uint32_t*>(stage_dev + o_sel), sel_n);
     if (rc == RLFC_ERR_ARGUMENT)
         rc = rlfc_decode_field(f, stop_level, dslots, 0, f->hb, rgb_dev, img, (int64_t)W * 3, dstat, stream);
     if (rc != RLFC_OK) return rc;

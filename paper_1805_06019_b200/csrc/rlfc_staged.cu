@@ -41,11 +41,13 @@
 //   RGB8 root colours | word-major bitmap words and word ranks.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
 #include "rlfc_common.cuh"
+#include "rlfc_field.cuh"
 
 namespace rlfc {
 namespace staged {
@@ -54,7 +56,7 @@ constexpr int MAXH = 8;
 constexpr int MAXS = 64;
 constexpr int THREADS = 256;
 constexpr uint32_t SKIP = 31;       // entry descriptor: slot not decoded
-constexpr int SEL_MAX = 64;         // slot-mode decodes needing at most this many chain nodes decode only those
+constexpr int SEL_MAX = SEL_NODES_MAX;         // slot-mode decodes needing at most this many chain nodes decode only those
 constexpr int STRIP = 64;           // pixels per TMA box column (192 bytes)
 
 __device__ const DigitLut g_lut = make_digit_lut();
@@ -932,7 +934,7 @@ __global__ void __launch_bounds__(256) k_sel_nodes(const __grid_constant__ rlfc_
 
 template <int BSQ, typename VT>
 __global__ void __launch_bounds__(THREADS) k_payloads_sel(const __grid_constant__ rlfc_field f, Ws w, int by_lo,
-                                                          int by_hi) {
+                                                          int by_hi, const uint32_t* __restrict__ sel) {
     constexpr int G8 = 8;                                  // nodes per round
     __shared__ uint16_t lut[243 + 125];
     __shared__ VT dq[BSQ == 16 ? 2048 : 1];
@@ -941,14 +943,14 @@ __global__ void __launch_bounds__(THREADS) k_payloads_sel(const __grid_constant_
     __shared__ uint32_t qs[THREADS * G8];                  // slot,
     __shared__ uint32_t qr[THREADS * G8];                  // record
     __shared__ int qn;
-    const uint32_t cnt = __ldg(w.sel);
+    const uint32_t cnt = __ldg(sel);
     if (cnt > (uint32_t)SEL_MAX || cnt == 0) return;
     const int tid = threadIdx.x;
     const int shift = f.quant_shift;
     for (int i = tid; i < 243 + 125; i += THREADS) lut[i] = i < 243 ? g_lut.trit[i] : g_lut.quint[i - 243];
     if (BSQ == 16)
         for (int z = tid; z < 2048; z += THREADS) dq[z] = (VT)deq((uint32_t)z, shift);
-    for (int i = tid; i < (int)cnt; i += THREADS) nodes[i] = __ldg(w.sel + 1 + i);
+    for (int i = tid; i < (int)cnt; i += THREADS) nodes[i] = __ldg(sel + 1 + i);
     // one thread per record finds the round's present nodes (bitmap word and
     // slot rank loads issued together); the CTA then decodes the compacted
     // payloads with every lane busy (present nodes are sparse: decoding in
@@ -1856,7 +1858,8 @@ static void run_payloads(const rlfc_field& f, const Ws& w, int by_lo, int by_hi,
 template <int B, typename VT, typename RT>
 static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, int by_hi, uint8_t* rgb,
                   int64_t img_stride, int64_t row_stride, const Ws& w, int n_flagged, uint64_t* status,
-                  cudaStream_t stream, bool build_units = false, const int32_t* trows = nullptr, int ntrows = 0) {
+                  cudaStream_t stream, bool build_units = false, const int32_t* trows = nullptr, int ntrows = 0,
+                  const uint32_t* sel_dev = nullptr, int sel_n = -1) {
     constexpr int BSQ = B * B;
     const bool tma_ok = w.root_rgb && (reinterpret_cast<uintptr_t>(f.roots) & 15) == 0 &&
                         ((f.wp * (int)sizeof(RT)) % 16) == 0 && encode_fn() != nullptr;
@@ -1966,15 +1969,23 @@ static int launch(const rlfc_field& f, int k, const int32_t* slots, int by_lo, i
     if (k < h && !P.build_units) {
         // a slot-mode decode of few views decodes only their chain nodes;
         // the full pass then exits at once (and runs when there are more)
-        const bool sel = slots != nullptr && w.sel != nullptr;
+        // (a caller that built the node list on the host passes it in
+        // device memory with its count: no k_sel_nodes, and no launch of the
+        // full pass when the list is in use)
+        const bool sel = slots != nullptr && (w.sel != nullptr || sel_dev != nullptr);
+        const uint32_t* selp = sel_dev ? sel_dev : w.sel;
+        const bool host_sel = sel && sel_dev != nullptr;
+        bool full = true;
         if (sel) {
-            k_sel_nodes<<<1, 256, 0, stream>>>(f, slots, k, w.sel);
+            if (!host_sel) k_sel_nodes<<<1, 256, 0, stream>>>(f, slots, k, w.sel);
             const int64_t nrb = 3ll * (by_hi - by_lo) * f.wb;
-            if (nrb > 0)
+            const bool use = !host_sel || (sel_n > 0 && sel_n <= SEL_MAX);
+            if (nrb > 0 && use)
                 k_payloads_sel<BSQ, VT><<<(unsigned)((nrb + THREADS - 1) / THREADS), THREADS, 0, stream>>>(
-                    f, w, by_lo, by_hi);
+                    f, w, by_lo, by_hi, selp);
+            if (host_sel) full = !use;
         }
-        run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream, sel ? w.sel : nullptr);
+        if (full) run_payloads<BSQ, VT>(f, w, by_lo, by_hi, sms, stream, sel && !host_sel ? w.sel : nullptr);
     }
     // dense streams (many units with several present levels): the variant
     // holding three levels per unit in registers
@@ -2162,6 +2173,43 @@ extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level,
                                         int64_t row_stride, void* workspace, uint64_t workspace_bytes,
                                         uint64_t present_total, int32_t n_flagged, const int32_t* t_rows,
                                         int32_t n_trows, uint64_t* status, void* stream) {
+    return rlfc::decode_field_staged_sel(f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride, row_stride,
+                                         workspace, workspace_bytes, present_total, n_flagged, t_rows, n_trows,
+                                         status, stream, nullptr, -1);
+}
+
+namespace rlfc {
+int sel_nodes_host(const rlfc_field& f, int k, const int32_t* views, int nviews, uint32_t* out) {
+    // the distinct chain nodes at levels >= k of the given views (serial
+    // indices), ascending (k_sel_nodes on the host): out[0] = count, or
+    // SEL_MAX + 1 when there are more
+    uint32_t nodes[staged::SEL_MAX];
+    int n = 0;
+    for (int i = 0; i < nviews; ++i) {
+        const int s = views[i] / f.t_count, t = views[i] % f.t_count;
+        for (int l = k; l < f.tree_height; ++l) {
+            const uint32_t nd = (uint32_t)(f.level_base[l] + (t >> l) * f.level_sx[l] + (s >> l));
+            bool seen = false;
+            for (int j = 0; j < n && !seen; ++j) seen = nodes[j] == nd;
+            if (seen) continue;
+            if (n == staged::SEL_MAX) {
+                out[0] = staged::SEL_MAX + 1;
+                return staged::SEL_MAX + 1;
+            }
+            nodes[n++] = nd;
+        }
+    }
+    std::sort(nodes, nodes + n);
+    out[0] = (uint32_t)n;
+    for (int j = 0; j < n; ++j) out[1 + j] = nodes[j];
+    return n;
+}
+
+int decode_field_staged_sel(const rlfc_field* f, int32_t stop_level, const int32_t* image_slots, int32_t by_lo,
+                            int32_t by_hi, uint8_t* rgb, int64_t img_stride, int64_t row_stride, void* workspace,
+                            uint64_t workspace_bytes, uint64_t present_total, int32_t n_flagged,
+                            const int32_t* t_rows, int32_t n_trows, uint64_t* status, void* stream,
+                            const uint32_t* sel_dev, int sel_n) {
     if (!f || !rgb || !status || !workspace) return RLFC_ERR_ARGUMENT;
     if (stop_level < 0 || stop_level > f->tree_height || by_lo < 0 || by_hi > f->hb || by_lo > by_hi)
         return RLFC_ERR_ARGUMENT;
@@ -2175,15 +2223,19 @@ extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level,
 #define RLFC_STAGED(B_)                                                                                            \
     if (small && r16)                                                                                              \
         return staged::launch<B_, int16_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows);                                     \
+                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows,  \
+                                                    sel_dev, sel_n);                                     \
     if (small)                                                                                                     \
         return staged::launch<B_, int16_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows);                                     \
+                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows,  \
+                                                    sel_dev, sel_n);                                     \
     if (r16)                                                                                                       \
         return staged::launch<B_, int32_t, int16_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,   \
-                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows);                                     \
+                                                    row_stride, w, n_flagged, status, s, false, t_rows, n_trows,  \
+                                                    sel_dev, sel_n);                                     \
     return staged::launch<B_, int32_t, int32_t>(*f, stop_level, image_slots, by_lo, by_hi, rgb, img_stride,       \
-                                                row_stride, w, n_flagged, status, s, false, t_rows, n_trows);
+                                                row_stride, w, n_flagged, status, s, false, t_rows, n_trows,  \
+                                                    sel_dev, sel_n);
     switch (f->block) {
         case 4: { RLFC_STAGED(4) }
         case 8: { RLFC_STAGED(8) }
@@ -2192,3 +2244,4 @@ extern "C" int rlfc_decode_field_staged(const rlfc_field* f, int32_t stop_level,
     }
 #undef RLFC_STAGED
 }
+}  // namespace rlfc

@@ -969,7 +969,7 @@ def decode_image(state: DecoderState, image_index, stop_level=0):
     # the current device's field (device_field() default): no device switch
     df = _field_on(state)
     L = _native.lib()
-    host_stage, dev_stage, word = _image_buffers(df, 32 + 4 * hdr.s_count * hdr.t_count)
+    host_stage, dev_stage, word = _image_buffers(df, 48 + 4 * hdr.s_count * hdr.t_count + 4 * 65)
     img = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, device=df.device)
     res = torch.empty((hdr.height, hdr.width, 3), dtype=torch.uint8, pin_memory=True)
     stream = torch._C._cuda_getCurrentRawStream(df.device.index)
