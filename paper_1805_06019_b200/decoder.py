@@ -141,6 +141,7 @@ class DeviceField:
         self._dir = None
         self.block_scratch = {}      # thread id -> _BlockScratch
         self._index_view = None      # rlfc_index_view (index_view()), False: none
+        self.render_field = None     # renderer's tap-camera scratch (under enqueue_lock)
 
     def directory(self):
         """The device record directory (rlfc_b200.h rlfc_dir: tile-major

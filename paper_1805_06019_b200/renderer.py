@@ -384,25 +384,9 @@ class _Staging:
     """Per-thread, per-device staging buffers of rlfc_render_slab_batch: one
     pinned host buffer and one device buffer (grown on demand)."""
 
-    # camera fields up to this size are kept between calls (the batch call
-    # is synchronous, so the next call may reuse the scratch)
-    FIELD_KEEP_BYTES = 64 << 20
-
     def __init__(self, dev):
         self.dev = dev
         self.cap = 0
-        self.field = None
-
-    def camera_field(self, shape):
-        import torch
-        nbytes = shape[0] * shape[1] * shape[2] * shape[3]
-        f = self.field
-        if f is not None and tuple(f.shape) == shape:
-            return f
-        f = torch.empty(shape, dtype=torch.uint8, device=self.dev)
-        if nbytes <= self.FIELD_KEEP_BYTES:
-            self.field = f
-        return f
 
     def buffers(self, nbytes):
         import torch
@@ -428,6 +412,24 @@ def _staging(dev):
     return st
 
 
+# tap-camera fields up to this size stay allocated on their DeviceField
+# between batch calls: the calls on one field run under its enqueue lock and
+# return drained, so the next call may reuse the scratch
+_FIELD_KEEP_BYTES = 64 << 20
+
+
+def _camera_field(df, shape):
+    """The decoded tap cameras' scratch (caller holds df.enqueue_lock)."""
+    import torch
+    f = getattr(df, "render_field", None)
+    if f is not None and tuple(f.shape) == shape:
+        return f
+    f = torch.empty(shape, dtype=torch.uint8, device=df.device)
+    if shape[0] * shape[1] * shape[2] * shape[3] <= _FIELD_KEEP_BYTES:
+        df.render_field = f
+    return f
+
+
 def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
                        out, stream, out_host=None):
     """Every slab pose of the batch in one native call
@@ -440,7 +442,7 @@ def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
     nbytes = int(L.rlfc_render_staging_bytes(df.ref, n))
     stg = _staging(df.device)
     host, dbuf = stg.buffers(nbytes)
-    field = stg.camera_field((min(hdr.s_count * hdr.t_count, 4 * n), hdr.height, hdr.width, 3))
+    shape = (min(hdr.s_count * hdr.t_count, 4 * n), hdr.height, hdr.width, 3)
     switch = decoder._get_device() != df.device.index
     if switch:
         prev = torch.cuda.current_device()
@@ -449,6 +451,7 @@ def _render_slab_batch(state, df, stop_level, pose_arr, gstruct, bgs, ow, oh,
         ws = df.staged_workspace(stream)
         args = (None, 0, 0, 0) if ws is None else (ws[0].data_ptr(), ws[1], ws[2], ws[3])
         with df.enqueue_lock:
+            field = _camera_field(df, shape)
             rc = L.rlfc_render_slab_batch(
                 df.ref, stop_level, *args, pose_arr.ctypes.data, gstruct.ctypes.data, bgs.ctypes.data, n, ow,
                 oh, field.data_ptr(), field.shape[0], out.data_ptr(), host.data_ptr(), dbuf.data_ptr(),
