@@ -847,7 +847,11 @@ def _to_host(t):
 
 
 _BOUNCE = 64 << 20
-_bounce_tls = threading.local()
+# one process-wide ring of pinned bounce buffers and copy pool: large
+# results are PCIe-bound, so concurrent callers take turns (_bounce_lock)
+# instead of each pinning its own 192 MB
+_bounce = {}
+_bounce_lock = threading.Lock()
 
 
 def _to_host_big(t):
@@ -861,11 +865,16 @@ def _to_host_big(t):
     src = t.contiguous().view(torch.uint8).reshape(-1)
     n = src.numel()
     out = np.empty(n, dtype=np.uint8)
-    ring = getattr(_bounce_tls, "ring", None)
-    if ring is None:
-        ring = _bounce_tls.ring = [torch.empty(_BOUNCE, dtype=torch.uint8).pin_memory() for _ in range(3)]
-        _bounce_tls.pool = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
-    pool = _bounce_tls.pool
+    with _bounce_lock:
+        if not _bounce:
+            _bounce["ring"] = [torch.empty(_BOUNCE, dtype=torch.uint8).pin_memory() for _ in range(3)]
+            _bounce["pool"] = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+        return _to_host_ring(t, src, n, out, _bounce["ring"], _bounce["pool"])
+
+
+def _to_host_ring(t, src, n, out, ring, pool):
+    """_to_host_big's pipeline over the shared ring (caller holds _bounce_lock)."""
+    torch = _torch()
     stream = torch.cuda.Stream(device=t.device)
     stream.wait_stream(torch.cuda.current_stream(t.device))
     chunks = [(a, min(n, a + _BOUNCE)) for a in range(0, n, _BOUNCE)]
