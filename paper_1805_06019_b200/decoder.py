@@ -51,9 +51,15 @@ def _host_bytes(arr):
         return _torch().from_numpy(np.asarray(arr, dtype=np.uint8).reshape(-1))
 
 
+_cuda_get_device = None
+
+
 def _get_device():
     """The calling thread's current CUDA device index (CUDA initialised)."""
-    return _torch()._C._cuda_getDevice()
+    global _cuda_get_device
+    if _cuda_get_device is None:
+        _cuda_get_device = _torch()._C._cuda_getDevice
+    return _cuda_get_device()
 
 
 def _field_on(state, device=None):
@@ -726,6 +732,7 @@ class _BlockScratch:
         self.b = b
         self.mailbox = torch.zeros(MAILBOX_BYTES, dtype=torch.uint8).pin_memory()
         self.out_np = np.zeros(b * b + 1, dtype=np.int32)
+        self.out_block = self.out_np[:b * b].reshape(b, b)
         self.stream = torch.cuda.Stream(device=df.device)
         L = _native.lib()
         self.args = (df.ref, self.mailbox.data_ptr(), self.stream.cuda_stream)
@@ -783,17 +790,15 @@ def decode_block_progressive(state: DecoderState, image_index, block_index,
     rc = sc.call_fn(sc.call_ptr)
     if rc:
         _native.check(rc, "rlfc_block_server_request")
-    bsq = sc.bsq
-    code = int(sc.out_np[bsq])
+    code = sc.out_np.item(sc.bsq)
     if code:
         _raise_status(code)
-    return sc.out_np[:bsq].reshape(sc.b, sc.b).copy()
+    return sc.out_block.copy()
 
 
 def decode_block(state: DecoderState, image_index, block_index, channel):
     """Fully decode one block of one channel plane (decoder.py:109-112)."""
-    return decode_block_progressive(state, image_index, block_index, channel,
-                                    stop_level=0)
+    return decode_block_progressive(state, image_index, block_index, channel, 0)
 
 
 def decode_block_traced(state: DecoderState, image_index, block_index,
