@@ -1188,6 +1188,30 @@ __global__ void k_fixup(const __grid_constant__ rlfc_field f, const uint32_t* fl
 // and descriptor, and only the chain payloads are read and BISE-decoded -- no
 // walk over the record's earlier nodes.  Records with a stream anomaly take
 // the reference-order walk.  Out-of-range requests report code 3.
+// One BISE mode's payloads of a lane's chain (levels in pm) added into acc,
+// one per round; the entry of the round's level is picked by predicated
+// selects (no dynamic register indexing).
+template <int MODE>
+__device__ __forceinline__ bool indexed_mode_rounds(const rlfc_field& f, int c, const uint2 (&ent)[MAXH], uint32_t pm,
+                                                    int32_t* acc) {
+    bool bad = false;
+    while (pm) {
+        const int l = __ffs(pm) - 1;
+        pm &= pm - 1u;
+        uint2 e = make_uint2(0u, 0u);
+#pragma unroll
+        for (int ll = 0; ll < MAXH; ++ll)
+            if (ll == l) e = ent[ll];
+        const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + e.x);
+        const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+        const uint32_t bit0 = (uint32_t)(a & 3u) * 8u, b = (uint32_t)desc_bits((int)(e.y & 31u));
+        bad |= decode16_acc<MODE>(sw, bit0, b,
+                                  MODE == MODE_BITS ? nullptr : MODE == MODE_TRIT ? g_lut.trit : g_lut.quint,
+                                  f.quant_shift, acc);
+    }
+    return bad;
+}
+
 template <int B>
 __global__ void k_blocks_indexed(const __grid_constant__ rlfc_field f, Ws w, const int32_t* __restrict__ req, int n,
                                  int32_t* __restrict__ out, int32_t* __restrict__ status) {
@@ -1252,21 +1276,35 @@ __global__ void k_blocks_indexed(const __grid_constant__ rlfc_field f, Ws w, con
                     ent[l] = __ldg(w.entries + ranks[l] + __popc(words[l] & ((1u << bit) - 1u)));
             }
         }
-        // chain order h-1 .. k, as the reference decodes its targets
+        if constexpr (BSQ == 16) {
+            // mode-major: a lane decodes its present levels one BISE mode at
+            // a time, so each round of a warp runs one mode's code for every
+            // lane that has a payload of that mode (level-major rounds ran a
+            // body per (level, mode) pair present anywhere in the warp). The
+            // level sums are integer additions, so their order is free; an
+            // unflagged record has no corrupt pack (prepare validated it).
+            uint32_t pm[3] = {0u, 0u, 0u};
 #pragma unroll
-        for (int l = MAXH - 1; l >= 0; --l) {
-            const uint32_t d = ent[l].y & 31u;
-            if (d >= (uint32_t)NUM_DESC || st) continue;
-            if constexpr (BSQ == 16) {
-                const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + ent[l].x);
-                const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-                const uint32_t bit0 = (uint32_t)(a & 3u) * 8u, b = (uint32_t)desc_bits((int)d);
-                const int m = desc_mode((int)d);
-                const bool bad = m == MODE_BITS   ? decode16_acc<MODE_BITS>(sw, bit0, b, nullptr, f.quant_shift, acc)
-                                 : m == MODE_TRIT ? decode16_acc<MODE_TRIT>(sw, bit0, b, g_lut.trit, f.quant_shift, acc)
-                                                  : decode16_acc<MODE_QUINT>(sw, bit0, b, g_lut.quint, f.quant_shift, acc);
-                st = bad ? 1 : 0;
-            } else {
+            for (int l = 0; l < MAXH; ++l) {
+                const uint32_t d = ent[l].y & 31u;
+                if (d < (uint32_t)NUM_DESC) {
+                    const int m = desc_mode((int)d);
+                    pm[0] |= (m == MODE_BITS ? 1u : 0u) << l;
+                    pm[1] |= (m == MODE_TRIT ? 1u : 0u) << l;
+                    pm[2] |= (m == MODE_QUINT ? 1u : 0u) << l;
+                }
+            }
+            bool bad = false;
+            bad |= indexed_mode_rounds<MODE_BITS>(f, c, ent, pm[0], acc);
+            bad |= indexed_mode_rounds<MODE_TRIT>(f, c, ent, pm[1], acc);
+            bad |= indexed_mode_rounds<MODE_QUINT>(f, c, ent, pm[2], acc);
+            st = bad ? 1 : 0;
+        } else {
+            // chain order h-1 .. k, as the reference decodes its targets
+#pragma unroll
+            for (int l = MAXH - 1; l >= 0; --l) {
+                const uint32_t d = ent[l].y & 31u;
+                if (d >= (uint32_t)NUM_DESC || st) continue;
                 st = decode_payload_acc<BSQ>(f.srv[c] + ent[l].x, (int)d, f.quant_shift, acc, g_lut);
             }
         }
