@@ -296,6 +296,24 @@ __global__ void k_decode_planes(const rlfc_field f, int stop_level, const int32_
 // all issued before any payload is decoded). Blocks of records that prepare
 // flagged take the reference-order record walk and report its key, as
 // k_decode_planes does. Rows leave as 16-byte stores.
+template <int MODE>
+__device__ __forceinline__ void plane_mode_rounds(const rlfc_field& f, int c, const uint2 (&ent)[8], uint32_t pm,
+                                                  int32_t* acc) {
+    while (pm) {
+        const int l = __ffs(pm) - 1;
+        pm &= pm - 1u;
+        uint2 e = make_uint2(0u, 0u);
+#pragma unroll
+        for (int ll = 0; ll < 8; ++ll)
+            if (ll == l) e = ent[ll];
+        const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + e.x);
+        const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+        decode16_acc<MODE>(sw, (uint32_t)(a & 3u) * 8u, (uint32_t)desc_bits((int)(e.y & 31u)),
+                           MODE == MODE_BITS ? nullptr : MODE == MODE_TRIT ? g_lut_ix.trit : g_lut_ix.quint,
+                           f.quant_shift, acc);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_plane_indexed4(const rlfc_field f, const rlfc_index_view ix, int k, int s,
                                                         int t, int c, int32_t* __restrict__ out, uint64_t* status) {
     constexpr int MAXL = 8;
@@ -350,18 +368,22 @@ __global__ void __launch_bounds__(256) k_plane_indexed4(const rlfc_field f, cons
                     ent[l] = make_uint2(__ldg(ix.entries + 2 * slot), __ldg(ix.entries + 2 * slot + 1));
             }
         }
+        // mode-major (as k_blocks_indexed): one BISE mode's payloads per
+        // round, so a warp runs each mode's body once per round
+        uint32_t pm[3] = {0u, 0u, 0u};
 #pragma unroll
         for (int l = 0; l < MAXL; ++l) {
             const uint32_t d = ent[l].y & 31u;
-            if (d >= (uint32_t)NUM_DESC) continue;
-            const uintptr_t a = reinterpret_cast<uintptr_t>(f.srv[c] + ent[l].x);
-            const uint32_t* sw = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-            const uint32_t bit0 = (uint32_t)(a & 3u) * 8u, b = (uint32_t)desc_bits((int)d);
-            const int m = desc_mode((int)d);
-            if (m == MODE_BITS) decode16_acc<MODE_BITS>(sw, bit0, b, nullptr, f.quant_shift, acc);
-            else if (m == MODE_TRIT) decode16_acc<MODE_TRIT>(sw, bit0, b, g_lut_ix.trit, f.quant_shift, acc);
-            else decode16_acc<MODE_QUINT>(sw, bit0, b, g_lut_ix.quint, f.quant_shift, acc);
+            if (d < (uint32_t)NUM_DESC) {
+                const int m = desc_mode((int)d);
+                pm[0] |= (m == MODE_BITS ? 1u : 0u) << l;
+                pm[1] |= (m == MODE_TRIT ? 1u : 0u) << l;
+                pm[2] |= (m == MODE_QUINT ? 1u : 0u) << l;
+            }
         }
+        plane_mode_rounds<MODE_BITS>(f, c, ent, pm[0], acc);
+        plane_mode_rounds<MODE_TRIT>(f, c, ent, pm[1], acc);
+        plane_mode_rounds<MODE_QUINT>(f, c, ent, pm[2], acc);
     }
     if (st) report(status, (uint64_t)blk, st);
 #pragma unroll
