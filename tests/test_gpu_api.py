@@ -551,3 +551,40 @@ def test_mixed_concurrent_api_calls(rl):
         par = list(ex.map(run, jobs))
     for j, a, b in zip(jobs, serial, par):
         assert np.array_equal(a, b), j
+
+
+def test_plane_host_indexed_equals_walk(rl):
+    """rlfc_decode_plane_host with the prepared index (k_plane_indexed4) and
+    without it (the record walk of k_decode_planes): identical planes and
+    status words at every stop level and channel, on a clean B = 4 stream and
+    on one with a corrupt record (flagged at prepare: the indexed kernel walks
+    it and reports the same failure key)."""
+    import ctypes
+    from paper_1805_06019_b200 import _native, decoder
+    data = load_stream("mid17_dense")
+    bad = next(d for d in (_corrupt_first_descriptor(rl, data, bx, by, c) for by in range(8) for bx in range(8)
+                           for c in range(3)) if d)
+    L = _native.lib()
+    for stream_bytes in (data, bad):
+        st = rl.init(stream_bytes)
+        df = st.device_field()
+        iv = df.index_view()
+        assert iv is not None
+        hdr = st.header
+        wp, hp = hdr.padded_dims
+        host_stage, dev_stage, word = decoder._image_buffers(df, 64)
+        plane = torch.empty((hp, wp), dtype=torch.int32, device=df.device)
+        stream = torch.cuda.current_stream().cuda_stream
+        for k in range(hdr.tree_height):
+            for c in range(3):
+                for s, t in [(0, 0), (16, 16), (5, 11)]:
+                    got = []
+                    for index in (ctypes.byref(iv), None):
+                        res = torch.empty((hp, wp), dtype=torch.int32, pin_memory=True)
+                        assert L.rlfc_decode_plane_host(df.ref, k, s, t, c, plane.data_ptr(), res.data_ptr(),
+                                                        host_stage.data_ptr(), dev_stage.data_ptr(),
+                                                        word.ctypes.data, index, stream) == 0
+                        got.append((res.numpy().copy(), int(word[0])))
+                    assert got[0][1] == got[1][1]
+                    if got[0][1] == 0:
+                        assert np.array_equal(got[0][0], got[1][0])
