@@ -392,6 +392,106 @@ __global__ void __launch_bounds__(256) k_plane_indexed4(const rlfc_field f, cons
             make_int4(acc[yy * 4], acc[yy * 4 + 1], acc[yy * 4 + 2], acc[yy * 4 + 3]);
 }
 
+// One camera image from the prepared record index (B = 4,
+// decoder.decode_image, decoder.py:187-194): one thread per block sums the
+// three channels' present chain levels >= k onto their roots (mode-major, as
+// k_plane_indexed4), inverts the YCoCg-R lift, clamps and stores RGB8 rows
+// of the true-dims crop. Records that prepare flagged take the record walk;
+// the first failing channel reports the key k_decode_field_simple uses.
+__global__ void __launch_bounds__(128) k_image_indexed4(const rlfc_field f, const rlfc_index_view ix, int k, int s,
+                                                        int t, uint8_t* __restrict__ rgb, int64_t row_stride,
+                                                        uint64_t* status) {
+    const int64_t nblk = (int64_t)f.wb * f.hb;
+    const int64_t blk = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk >= nblk) return;
+    const int bx = (int)(blk % f.wb), by = (int)(blk / f.wb);
+    const int h = f.tree_height, img = s * f.t_count + t;
+    int32_t acc[3][16];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (f.roots_i16) {
+            const int16_t* r0 = reinterpret_cast<const int16_t*>(f.roots) +
+                                ((((int64_t)(s >> h) * f.rsy + (t >> h)) * 3 + c) * f.hp + by * 4) * f.wp + bx * 4;
+#pragma unroll
+            for (int yy = 0; yy < 4; ++yy) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(r0 + (int64_t)yy * f.wp));
+                acc[c][yy * 4] = (int32_t)(int16_t)(v.x & 0xFFFFu);
+                acc[c][yy * 4 + 1] = (int32_t)v.x >> 16;
+                acc[c][yy * 4 + 2] = (int32_t)(int16_t)(v.y & 0xFFFFu);
+                acc[c][yy * 4 + 3] = (int32_t)v.y >> 16;
+            }
+        } else {
+#pragma unroll
+            for (int yy = 0; yy < 4; ++yy)
+#pragma unroll
+                for (int xx = 0; xx < 4; ++xx)
+                    acc[c][yy * 4 + xx] = root_sample(f, s, t, c, by * 4 + yy, bx * 4 + xx);
+        }
+        const int64_t ri = (int64_t)c * nblk + blk;
+        if (__ldg(ix.rec_flag + ri)) {
+            const uint64_t off = f.offsets[c][blk];
+            int st = walk_chain<16>(f, f.srv[c] + off, s, t, k, acc[c], c_lut, c_nb<4>, srv_avail(f, c, off));
+            if (st == WALK_OOB) st = 2;
+            if (st) {
+                report(status, (((uint64_t)img * 3 + c) * f.hb + by) * f.wb + bx, st);
+                return;
+            }
+        } else {
+            uint2 ent[8];
+            uint32_t pm[3] = {0u, 0u, 0u};
+#pragma unroll
+            for (int l = 0; l < 8; ++l) {
+                ent[l] = make_uint2(0u, 31u);
+                if (l >= k && l < h) {
+                    const int nd = chain_node(f, l, s, t);
+                    const uint32_t word = __ldg(ix.bm + (int64_t)(nd >> 5) * ix.nrec + ri);
+                    const uint32_t rank = __ldg(ix.rk + (int64_t)(nd >> 5) * ix.nrec + ri);
+                    const uint32_t bit = (uint32_t)nd & 31u;
+                    const uint64_t slot = (uint64_t)rank + (uint64_t)__popc(word & ((1u << bit) - 1u));
+                    if (((word >> bit) & 1u) && slot < ix.cap)
+                        ent[l] = make_uint2(__ldg(ix.entries + 2 * slot), __ldg(ix.entries + 2 * slot + 1));
+                }
+                const uint32_t d = ent[l].y & 31u;
+                if (d < (uint32_t)NUM_DESC) {
+                    const int m = desc_mode((int)d);
+                    pm[0] |= (m == MODE_BITS ? 1u : 0u) << l;
+                    pm[1] |= (m == MODE_TRIT ? 1u : 0u) << l;
+                    pm[2] |= (m == MODE_QUINT ? 1u : 0u) << l;
+                }
+            }
+            plane_mode_rounds<MODE_BITS>(f, c, ent, pm[0], acc[c]);
+            plane_mode_rounds<MODE_TRIT>(f, c, ent, pm[1], acc[c]);
+            plane_mode_rounds<MODE_QUINT>(f, c, ent, pm[2], acc[c]);
+        }
+    }
+#pragma unroll
+    for (int yy = 0; yy < 4; ++yy) {
+        const int y = by * 4 + yy;
+        if (y >= f.height) break;
+        uint8_t* orow = rgb + (int64_t)y * row_stride;
+#pragma unroll
+        for (int xx = 0; xx < 4; ++xx) {
+            const int x = bx * 4 + xx;
+            if (x >= f.width) break;
+            uint32_t r, g, b;
+            const int j = yy * 4 + xx;
+            ycocg_to_rgb8(acc[0][j], acc[1][j], acc[2][j], r, g, b);
+            orow[3 * x] = (uint8_t)r;
+            orow[3 * x + 1] = (uint8_t)g;
+            orow[3 * x + 2] = (uint8_t)b;
+        }
+    }
+}
+
+int image_indexed_launch(const rlfc_field* f, const rlfc_index_view* ix, int32_t k, int32_t s, int32_t t,
+                         uint8_t* rgb, int64_t row_stride, uint64_t* status, void* stream) {
+    if (!f || !ix || !ix->bm || f->block != 4 || f->tree_height > 8) return RLFC_ERR_ARGUMENT;
+    const int64_t nblk = (int64_t)f->wb * f->hb;
+    k_image_indexed4<<<(unsigned)((nblk + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, *ix, k, s, t, rgb,
+                                                                                      row_stride, status);
+    return cudaGetLastError() == cudaSuccess ? RLFC_OK : RLFC_ERR_CUDA;
+}
+
 // One thread per (image, block) of a band: three channel chains, inverse lift,
 // clamp, RGB8 store of the true-dims crop (decoder.py:187-194).
 template <int B>

@@ -24,4 +24,8 @@ int decode_field_staged_sel(const rlfc_field* f, int32_t stop_level, const int32
 // SEL_NODES_MAX + 1 when there are more. out holds 1 + SEL_NODES_MAX words.
 constexpr int SEL_NODES_MAX = 64;
 int sel_nodes_host(const rlfc_field& f, int k, const int32_t* views, int nviews, uint32_t* out);
+// One camera image (B = 4) from the prepared record index (k_image_indexed4);
+// RLFC_ERR_ARGUMENT outside its envelope.
+int image_indexed_launch(const rlfc_field* f, const rlfc_index_view* ix, int32_t k, int32_t s, int32_t t,
+                         uint8_t* rgb, int64_t row_stride, uint64_t* status, void* stream);
 }  // namespace rlfc

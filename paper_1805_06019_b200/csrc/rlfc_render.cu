@@ -445,7 +445,11 @@ extern "C" int rlfc_decode_image_host(const rlfc_field* f, int32_t stop_level, v
     const int32_t* dslots = reinterpret_cast<const int32_t*>(stage_dev + o_slot);
     const int64_t img = (int64_t)H * W * 3;
     int rc = RLFC_ERR_ARGUMENT;
-    if (ws)
+    // B = 4: one kernel over the prepared record index (k_image_indexed4)
+    rlfc_index_view iv;
+    if (ws && f->block == 4 && rlfc_staged_index_view(f, ws, ws_bytes, present, &iv) == RLFC_OK)
+        rc = rlfc::image_indexed_launch(f, &iv, stop_level, s, t, rgb_dev, (int64_t)W * 3, dstat, stream);
+    if (rc == RLFC_ERR_ARGUMENT && ws)
         rc = rlfc::decode_field_staged_sel(f, stop_level, dslots, 0, f->hb, rgb_dev, img, (int64_t)W * 3, ws,
                                            ws_bytes, present, n_flagged,
                                            reinterpret_cast<const int32_t*>(stage_dev + o_rows), 1, dstat, stream,
